@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: BERT-large encoder layer fwd+bwd (BASELINE.json config "L": B=8, J=K=512,
+H=16, P=64, I=1024, U=4096, bf16) per GPU, data-parallel over N GPUs (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, NCCL)
+
+A step = one forward + backward of the layer over one batch of synthetic input already
+resident in HBM (+ the NCCL SUM all-reduce of the parameter gradients when N > 1).
+Rank 0 prints one JSON line.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BERT-large encoder layer fwd+bwd tokens/s"
+UNIT = "tokens/s"
+WORKLOAD = "L: BERT-large encoder layer B=8/GPU J=K=512 H=16 P=64 I=1024 U=4096 p=0.1 GELU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-samples", type=int, default=2)
+    ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx.append(float(r[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, r[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ oracle timing
+def time_oracle(dims, samples: int, dtype: str):
+    """The fp64 CPU oracle as it stands, on one sequence (B=1 slice) per sample."""
+    import numpy as np  # noqa: F401
+    from oracle import encoder as E
+    from synth import make_inputs, make_params
+    d1 = dims.with_batch(1)
+    prm = make_params(d1, dtype, "bench")
+    inp = make_inputs(d1, dtype)
+    cfg = E.Cfg(act=E.ACT_GELU_ERF)
+    ts = []
+    for _ in range(samples):
+        t0 = time.perf_counter()
+        Y, sv = E.encoder_layer_forward(inp["X"], prm, d1.H, cfg)
+        E.encoder_layer_backward(inp["dY"], inp["X"], prm, d1.H, cfg, sv)
+        ts.append(time.perf_counter() - t0)
+    return ts
+
+
+def cpu_cores():
+    for v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS"):
+        if os.environ.get(v):
+            return int(os.environ[v])
+    return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the fp64 oracle timed on the host cores (rank 0 only)."""
+    from synth import CONFIGS
+    if rank != 0:
+        return
+    dims = CONFIGS["L"]
+    J = dims.J
+    if args.warmup:
+        time_oracle(dims, min(args.warmup, 1), args.dtype)
+    ts = time_oracle(dims, args.steps, args.dtype)
+    total = sum(ts)
+    value = args.steps * J / total
+    sample = f"1 sequence (B=1 slice of config L) fwd+bwd per step, fp64 numpy oracle"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2007_00072_b200 import _abi, dp, tally
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    from synth import CONFIGS, make_inputs, make_params
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    dims_global = CONFIGS["L"].with_batch(CONFIGS["L"].B * world)
+    boff, B = dp.shard(dims_global.B, world, rank)
+    dims = CONFIGS["L"].with_batch(B)
+    es = 2 if args.dtype == "bf16" else 4
+    tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
+
+    cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff)
+    layer = EncoderLayer(dims, args.dtype, cfg)
+    layer.set_params(make_params(dims, args.dtype, "bench"))
+    inp = make_inputs(dims_global, args.dtype)
+    X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
+    dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
+    Y = torch.empty_like(X)
+    dX = torch.empty_like(X)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    lib = _abi.load()
+    nops = lib.enc_num_ops()
+    names = [lib.enc_op_name(i).decode() for i in range(nops)]
+    ms_buf = (_abi.c_float * nops)()
+
+    def step():
+        layer.forward(X, None, Y)
+        layer.backward(X, dY, dX)
+        if world > 1:
+            dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # per-operator breakdown pass (all ops timed; not the timed region)
+    lib.enc_set_timing(layer.ctx.ptr, (1 << nops) - 1)
+    per_op = {n: [] for n in names}
+    for _ in range(3):
+        if not args.no_flush:
+            flush.zero_()
+        step()
+        torch.cuda.synchronize()
+        _abi.check("enc_op_times", lib.enc_op_times(layer.ctx.ptr, ms_buf))
+        for i, n in enumerate(names):
+            per_op[n].append(ms_buf[i])
+    per_op = {n: statistics.median(v) for n, v in per_op.items()}
+    fused = tally.fused_bytes(dims, es)
+    flops = tally.gemm_flops(dims)
+    dominant = max(per_op, key=per_op.get)
+    dom_id = names.index(dominant)
+    lib.enc_set_timing(layer.ctx.ptr, 1 << dom_id)
+
+    # ---------------- timed region
+    sampler = ClockSampler(local)
+    sampler.start()
+    barrier()
+    launches0 = lib.enc_launch_count(layer.ctx.ptr)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    dom_ms = []
+    t_wall = time.perf_counter()
+    for k in range(args.steps):
+        if not args.no_flush:
+            flush.zero_()
+        ev[k][0].record()
+        step()
+        ev[k][1].record()
+        torch.cuda.synchronize()
+        _abi.check("enc_op_times", lib.enc_op_times(layer.ctx.ptr, ms_buf))
+        dom_ms.append(ms_buf[dom_id])
+    barrier()
+    t_wall = time.perf_counter() - t_wall
+    launches = lib.enc_launch_count(layer.ctx.ptr) - launches0
+    clocks = sampler.stop()
+    step_ms = sum(a.elapsed_time(b) for a, b in ev)
+    step_ms = dp.max_over_ranks(step_ms, dev)
+    ms_per_step = step_ms / args.steps
+    tokens = dims_global.B * dims_global.J
+    value = tokens / (ms_per_step * 1e-3)
+
+    # ---------------- roofline of the dominant kernel
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        peak_src = "measured"
+    except OSError:
+        peak_src = "fallback"
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    tc_peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    dom_avg_ms = statistics.mean(dom_ms)
+    if dominant in fused:
+        ach = fused[dominant] / (dom_avg_ms * 1e-3) / 1e9
+        roof = {"kernel": dominant, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                "algorithmic_bytes": fused[dominant], "peak_source": peak_src}
+    else:
+        ach = flops[dominant] / (dom_avg_ms * 1e-3) / 1e12
+        if args.dtype == "fp32":
+            tc_peak = tc_peak / 2.0 * 0.5   # no TF32: fp32 runs on CUDA cores (context only)
+        roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": tc_peak,
+                "unit": "TFLOP/s", "frac": ach / tc_peak, "traffic": None,
+                "algorithmic_flops": flops[dominant], "peak_source": peak_src + " (sustained)"}
+    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_path):
+        try:
+            roof["traffic"] = json.load(open(traffic_path)).get(dominant)
+        except (OSError, ValueError):
+            pass
+
+    # ---------------- end to end through the C ABI with host buffers
+    Xh = X.cpu().pin_memory()
+    dYh = dY.cpu().pin_memory()
+    Yh = torch.empty_like(Xh).pin_memory()
+    dXh = torch.empty_like(Xh).pin_memory()
+    lib.enc_set_timing(layer.ctx.ptr, 0)
+    for _ in range(2):
+        layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+        if world > 1:
+            dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+    e1.record()
+    barrier()
+    e2e_ms = dp.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
+    e2e = {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT,
+           "h2d_bytes_per_step": 2 * X.numel() * es, "d2h_bytes_per_step": 2 * X.numel() * es,
+           "ms_per_step": e2e_ms}
+
+    if args.breakdown and rank == 0:
+        for n in names:
+            extra = ""
+            if n in fused:
+                extra = f"{fused[n] / (per_op[n] * 1e-3) / 1e9:8.0f} GB/s"
+            elif n in flops:
+                extra = f"{flops[n] / (per_op[n] * 1e-3) / 1e12:8.1f} TF/s"
+            print(f"  {n:14s} {per_op[n] * 1e3:9.1f} us  {extra}", file=sys.stderr)
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            ts = time_oracle(CONFIGS["L"], args.cpu_samples, args.dtype)
+            cpu = {"value": CONFIGS["L"].J * len(ts) / sum(ts), "unit": UNIT,
+                   "cores": cpu_cores(), "kind": "oracle",
+                   "sample": f"{len(ts)} x one sequence (B=1 slice of config L) fwd+bwd, "
+                             f"fp64 numpy oracle, {sum(ts):.1f} s"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": WORKLOAD, "global_batch": dims_global.B, "seq_len": dims.J,
+                       "parallelism": f"dp{world}",
+                       "l2": "flushed (512 MB write) between steps" if not args.no_flush
+                       else "not flushed", "graph": "eager launches"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "wall_s_timed_region": t_wall,
+            "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return line
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,738 @@
+// C ABI of libencoder.so (include/encoder.h): argument validation, the enc_ctx, buffer
+// layouts, and the encoder-layer forward/backward orchestration (operator order of Table
+// A.1).  Everything runs on `stream`; nothing synchronises.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <new>
+
+#include "../../include/encoder.h"
+#include "gemm.h"
+#include "kernels.h"
+
+using namespace enc;
+
+struct enc_ctx {
+  int device = 0;
+  int num_sms = 148;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  size_t blas_ws_bytes = 0;
+  float* red = nullptr;      // column-reduction partials
+  size_t red_floats = 0;
+  // optional per-operator CUDA-event timing (enc_set_timing / enc_op_times)
+  uint64_t timing_mask = 0;
+  cudaEvent_t ev0[ENC_NUM_OPS] = {};
+  cudaEvent_t ev1[ENC_NUM_OPS] = {};
+  bool recorded[ENC_NUM_OPS] = {};
+  uint64_t launches = 0;     // kernels this library launched (excluding cuBLAS)
+};
+
+namespace {
+const char* kOpNames[ENC_NUM_OPS] = {
+    "gemm_qkv", "aib_fwd", "gemm_qk", "bsb_fwd", "gemm_av", "gemm_out", "bdrln_fwd1",
+    "gemm_l1", "bad_fwd", "gemm_l2", "bdrln_fwd2", "bdrln_bwd2", "gemm_l2_dx", "gemm_l2_dw",
+    "bad_bwd", "gemm_l1_dx", "gemm_l1_dw", "bdrln_bwd1", "gemm_out_dx", "gemm_out_dw",
+    "gemm_av_da", "gemm_av_dv", "bsb_bwd", "gemm_qk_dq", "gemm_qk_dk", "aib_bwd",
+    "gemm_qkv_dx", "gemm_qkv_dw"};
+
+// Records CUDA events around one operator on `st` when its bit is set in timing_mask.
+struct OpTimer {
+  enc_ctx* c;
+  int op;
+  cudaStream_t st;
+  bool on;
+  OpTimer(enc_ctx* c_, int op_, cudaStream_t st_, int launches)
+      : c(c_), op(op_), st(st_), on((c_->timing_mask >> op_) & 1ull) {
+    c->launches += launches;
+    if (on) cudaEventRecord(c->ev0[op], st);
+  }
+  ~OpTimer() {
+    if (on) {
+      cudaEventRecord(c->ev1[op], st);
+      c->recorded[op] = true;
+    }
+  }
+};
+}  // namespace
+
+static thread_local int g_last_cuda = 0;
+
+static int cuda_fail(cudaError_t e) {
+  g_last_cuda = (int)e;
+  return ENC_ECUDA;
+}
+#define CK(x)                                  \
+  do {                                         \
+    cudaError_t _e = (x);                      \
+    if (_e != cudaSuccess) return cuda_fail(_e); \
+  } while (0)
+#define CB(x)                                           \
+  do {                                                  \
+    cublasStatus_t _s = (x);                            \
+    if (_s != CUBLAS_STATUS_SUCCESS) return ENC_ECUBLAS; \
+  } while (0)
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+static size_t esize(int dtype) { return dtype == ENC_BF16 ? 2 : 4; }
+static bool valid_dtype(int dtype) { return dtype == ENC_BF16 || dtype == ENC_FP32; }
+static bool valid_p(float p) { return p >= 0.f && p < 1.f && p == p; }
+
+extern "C" {
+
+const char* enc_strerror(int code) {
+  switch (code) {
+    case ENC_OK: return "ok";
+    case ENC_EINVAL: return "invalid argument (dimension, p, or K != J / W != P / I != H*P)";
+    case ENC_EALIGN: return "misaligned pointer (16 B) or dimension not a multiple of 8";
+    case ENC_EDTYPE: return "unknown dtype";
+    case ENC_ECUDA: return "CUDA error (see enc_last_cuda_error)";
+    case ENC_ECUBLAS: return "cuBLAS error";
+    case ENC_EUNSUPPORTED: return "shape outside the compiled kernel variants";
+    case ENC_ENULL: return "required pointer is NULL";
+    default: return "unknown error";
+  }
+}
+
+int enc_last_cuda_error(void) { return g_last_cuda; }
+
+const char* enc_version(void) { return "paper_2007_00072_b200 0.1 sm_100a"; }
+
+int enc_create(enc_ctx** out, int device) {
+  if (!out) return ENC_ENULL;
+  *out = nullptr;
+  int prev = 0;
+  CK(cudaGetDevice(&prev));
+  CK(cudaSetDevice(device));
+  enc_ctx* c = new (std::nothrow) enc_ctx();
+  if (!c) return ENC_EINVAL;
+  c->device = device;
+  cudaError_t e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) { delete c; cudaSetDevice(prev); return cuda_fail(e); }
+  if (cublasCreate(&c->blas) != CUBLAS_STATUS_SUCCESS) { delete c; cudaSetDevice(prev); return ENC_ECUBLAS; }
+  c->blas_ws_bytes = 32u << 20;
+  c->red_floats = (64u << 20) / sizeof(float);
+  e = cudaMalloc(&c->blas_ws, c->blas_ws_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->red, c->red_floats * sizeof(float));
+  if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
+  if (cublasSetWorkspace(c->blas, c->blas_ws, c->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS ||
+      cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
+    enc_destroy(c);
+    cudaSetDevice(prev);
+    return ENC_ECUBLAS;
+  }
+  for (int i = 0; i < ENC_NUM_OPS && e == cudaSuccess; ++i) {
+    e = cudaEventCreate(&c->ev0[i]);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1[i]);
+  }
+  if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
+  cudaSetDevice(prev);
+  *out = c;
+  return ENC_OK;
+}
+
+int enc_num_ops(void) { return ENC_NUM_OPS; }
+
+const char* enc_op_name(int op) { return (op >= 0 && op < ENC_NUM_OPS) ? kOpNames[op] : ""; }
+
+int enc_set_timing(enc_ctx* c, uint64_t op_mask) {
+  if (!c) return ENC_ENULL;
+  c->timing_mask = op_mask;
+  for (int i = 0; i < ENC_NUM_OPS; ++i) c->recorded[i] = false;
+  return ENC_OK;
+}
+
+int enc_op_times(enc_ctx* c, float* ms) {
+  if (!c || !ms) return ENC_ENULL;
+  for (int i = 0; i < ENC_NUM_OPS; ++i) {
+    ms[i] = -1.f;
+    if (!c->recorded[i]) continue;
+    CK(cudaEventSynchronize(c->ev1[i]));
+    CK(cudaEventElapsedTime(&ms[i], c->ev0[i], c->ev1[i]));
+  }
+  return ENC_OK;
+}
+
+uint64_t enc_launch_count(const enc_ctx* c) { return c ? c->launches : 0; }
+
+void enc_destroy(enc_ctx* c) {
+  if (!c) return;
+  for (int i = 0; i < ENC_NUM_OPS; ++i) {
+    if (c->ev0[i]) cudaEventDestroy(c->ev0[i]);
+    if (c->ev1[i]) cudaEventDestroy(c->ev1[i]);
+  }
+  if (c->blas) cublasDestroy(c->blas);
+  if (c->blas_ws) cudaFree(c->blas_ws);
+  if (c->red) cudaFree(c->red);
+  delete c;
+}
+
+}  // extern "C"
+
+static ReduceWs ws_of(const enc_ctx* c) { return ReduceWs{c->red, c->red_floats, c->num_sms}; }
+
+// ------------------------------------------------------------------ dims validation
+static int check_dims(const enc_dims* d, int dtype) {
+  if (!d) return ENC_ENULL;
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (d->B < 0 || d->J <= 0 || d->H <= 0 || d->P <= 0 || d->U <= 0) return ENC_EINVAL;
+  if (d->K != d->J || d->W != d->P || d->I != d->H * d->P) return ENC_EINVAL;
+  if (d->I % 8 || d->U % 8 || d->K % 8 || d->P % 8) return ENC_EALIGN;
+  if (!rowop_supported(d->K) || !rowop_supported(d->I)) return ENC_EUNSUPPORTED;
+  return ENC_OK;
+}
+
+static int check_cfg(const enc_cfg* c) {
+  if (!c) return ENC_ENULL;
+  if (!valid_p(c->p_attn) || !valid_p(c->p_hidden) || !valid_p(c->p_ffn)) return ENC_EINVAL;
+  if (c->act < ENC_ACT_GELU_ERF || c->act > ENC_ACT_RELU) return ENC_EINVAL;
+  if (!(c->ln_eps >= 0.f)) return ENC_EINVAL;
+  if (c->batch_offset < 0) return ENC_EINVAL;
+  return ENC_OK;
+}
+
+#define CHECK_PTRS(...)                                        \
+  do {                                                         \
+    const void* _ps[] = {__VA_ARGS__};                         \
+    for (const void* _p : _ps) {                               \
+      if (!_p) return ENC_ENULL;                               \
+      if (!aligned16(_p)) return ENC_EALIGN;                   \
+    }                                                          \
+  } while (0)
+
+// ------------------------------------------------------------------ buffer layouts
+namespace {
+enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_N };
+enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y1, F_Y2, F_N };
+enum BwdId { B_PTR, B_DY2, B_DA1, B_DH, B_DX1, B_DYO, B_DC, B_DA, B_DS, B_DQ, B_DK, B_DV, B_DQKV, B_N };
+
+struct Layout {
+  size_t off[16];
+  size_t total;
+};
+
+static size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Layout make_layout(const size_t* sizes, int n) {
+  Layout L;
+  size_t o = 0;
+  for (int i = 0; i < n; ++i) {
+    L.off[i] = o;
+    o += al(sizes[i]);
+  }
+  L.total = o;
+  return L;
+}
+
+struct Sizes {
+  size_t BJI, BJU, BHJK, BJ3I, BJ, ptr;
+};
+static Sizes sizes_of(const enc_dims* d, int dtype) {
+  const size_t es = esize(dtype);
+  const size_t BJ = (size_t)d->B * d->J;
+  Sizes s;
+  s.BJI = BJ * d->I * es;
+  s.BJU = BJ * d->U * es;
+  s.BHJK = (size_t)d->B * d->H * d->J * d->K * es;
+  s.BJ3I = BJ * 3 * d->I * es;
+  s.BJ = BJ * sizeof(float);
+  s.ptr = (size_t)5 * d->B * d->H * sizeof(void*);
+  return s;
+}
+static Layout saved_layout(const enc_dims* d, int dtype) {
+  const Sizes s = sizes_of(d, dtype);
+  const size_t sz[S_N] = {s.BJI, s.BJI, s.BJI, s.BHJK, s.BHJK, s.BJI, s.BJI,
+                          s.BJI, s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ};
+  return make_layout(sz, S_N);
+}
+static Layout fwd_layout(const enc_dims* d, int dtype) {
+  const Sizes s = sizes_of(d, dtype);
+  const size_t sz[F_N] = {s.ptr, s.BJ3I, s.BHJK, s.BJI, s.BJU, s.BJI};
+  return make_layout(sz, F_N);
+}
+static Layout bwd_layout(const enc_dims* d, int dtype) {
+  const Sizes s = sizes_of(d, dtype);
+  const size_t sz[B_N] = {s.ptr, s.BJI,  s.BJU, s.BJU, s.BJI, s.BJI, s.BJI,
+                          s.BHJK, s.BHJK, s.BJI, s.BJI, s.BJI, s.BJ3I};
+  return make_layout(sz, B_N);
+}
+static inline char* at(void* base, size_t off) { return (char*)base + off; }
+}  // namespace
+
+extern "C" {
+
+int enc_layer_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* scratch_bytes) {
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (saved_bytes) *saved_bytes = saved_layout(d, dtype).total;
+  if (scratch_bytes) {
+    const size_t f = fwd_layout(d, dtype).total, b = bwd_layout(d, dtype).total;
+    *scratch_bytes = f > b ? f : b;
+  }
+  return ENC_OK;
+}
+
+int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (!saved || !v) return ENC_ENULL;
+  const Layout L = saved_layout(d, dtype);
+  v->Q = at(saved, L.off[S_Q]);
+  v->K = at(saved, L.off[S_K]);
+  v->V = at(saved, L.off[S_V]);
+  v->P = at(saved, L.off[S_P]);
+  v->A = at(saved, L.off[S_A]);
+  v->C = at(saved, L.off[S_C]);
+  v->X1 = at(saved, L.off[S_X1]);
+  v->xhat1 = at(saved, L.off[S_XH1]);
+  v->h = at(saved, L.off[S_H]);
+  v->A1 = at(saved, L.off[S_A1]);
+  v->xhat2 = at(saved, L.off[S_XH2]);
+  v->rstd1 = (float*)at(saved, L.off[S_R1]);
+  v->rstd2 = (float*)at(saved, L.off[S_R2]);
+  return ENC_OK;
+}
+
+// ------------------------------------------------------------------ per-operator ABI
+int enc_dropout_mask(int64_t n, int64_t index0, float p, uint64_t seed, uint64_t subseq,
+                     uint8_t* keep, enc_stream_t stream) {
+  if (n < 0 || index0 < 0 || !valid_p(p)) return ENC_EINVAL;
+  if (n > 0 && !keep) return ENC_ENULL;
+  CK(launch_dropout_mask(n, index0, make_philox_key(p, seed, subseq), keep, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
+static int check_bjhp(int dtype, int B, int J, int H, int P) {
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (B < 0 || J <= 0 || H <= 0 || P <= 0) return ENC_EINVAL;
+  if (P % 8) return ENC_EALIGN;
+  return ENC_OK;
+}
+
+int enc_aib_fwd(enc_ctx* ctx, int dtype, int B, int J, int H, int P, const void* qkv,
+                const float* bqkv, void* q, void* k, void* v, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjhp(dtype, B, J, H, P);
+  if (r) return r;
+  CHECK_PTRS(qkv, bqkv, q, k, v);
+  {
+    OpTimer _t(ctx, ENC_OP_AIB_FWD, (cudaStream_t)stream, 1);
+    CK(launch_aib_fwd(dtype, B, J, H, P, qkv, bqkv, q, k, v, (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_aib_bwd(enc_ctx* ctx, int dtype, int B, int J, int H, int P, const void* dq,
+                const void* dk, const void* dv, void* dqkv, float* dbqkv, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjhp(dtype, B, J, H, P);
+  if (r) return r;
+  CHECK_PTRS(dq, dk, dv, dqkv, dbqkv);
+  {
+    OpTimer _t(ctx, ENC_OP_AIB_BWD, (cudaStream_t)stream, 2);
+    CK(launch_aib_bwd(dtype, B, J, H, P, dq, dk, dv, dqkv, dbqkv, ws_of(ctx), (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+static int check_bhjk(int dtype, int B, int H, int J, int K, float p) {
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (B < 0 || H <= 0 || J <= 0 || K <= 0 || !valid_p(p)) return ENC_EINVAL;
+  if (K % 8) return ENC_EALIGN;
+  if (!rowop_supported(K)) return ENC_EUNSUPPORTED;
+  return ENC_OK;
+}
+
+int enc_bsb_fwd(enc_ctx* ctx, int dtype, int B, int H, int J, int K, float scale, const void* S,
+                const float* mask_bias, float p, uint64_t seed, uint64_t subseq,
+                int64_t batch_offset, void* P, void* A, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bhjk(dtype, B, H, J, K, p);
+  if (r) return r;
+  if (batch_offset < 0) return ENC_EINVAL;
+  CHECK_PTRS(S, P, A);
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  {
+    OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
+    CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias, make_philox_key(p, seed, subseq),
+                      batch_offset, P, A, (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_bsb_bwd(enc_ctx* ctx, int dtype, int B, int H, int J, int K, float scale, const void* dA,
+                const void* P, float p, uint64_t seed, uint64_t subseq, int64_t batch_offset,
+                void* dS, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bhjk(dtype, B, H, J, K, p);
+  if (r) return r;
+  if (batch_offset < 0) return ENC_EINVAL;
+  CHECK_PTRS(dA, P, dS);
+  {
+    OpTimer _t(ctx, ENC_OP_BSB_BWD, (cudaStream_t)stream, 1);
+    CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, P, make_philox_key(p, seed, subseq),
+                      batch_offset, dS, (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+static int check_bjn(int dtype, int B, int J, int N, float p, bool rowop) {
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (B < 0 || J <= 0 || N <= 0 || !valid_p(p)) return ENC_EINVAL;
+  if (N % 8) return ENC_EALIGN;
+  if (rowop && !rowop_supported(N)) return ENC_EUNSUPPORTED;
+  return ENC_OK;
+}
+
+int enc_bdrln_fwd(enc_ctx* ctx, int dtype, int B, int J, int I, const void* Y, const float* bias,
+                  const void* R, const float* gamma, const float* beta, float eps, float p,
+                  uint64_t seed, uint64_t subseq, int64_t batch_offset, void* out, void* xhat,
+                  float* rstd, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjn(dtype, B, J, I, p, true);
+  if (r) return r;
+  if (batch_offset < 0 || !(eps >= 0.f)) return ENC_EINVAL;
+  CHECK_PTRS(Y, bias, R, gamma, beta, out, xhat, rstd);
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_FWD1, (cudaStream_t)stream, 1);
+    CK(launch_bdrln_fwd(dtype, B, J, I, Y, bias, R, gamma, beta, eps,
+                        make_philox_key(p, seed, subseq), batch_offset, out, xhat, rstd,
+                        (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_bdrln_bwd(enc_ctx* ctx, int dtype, int B, int J, int I, const void* dOut,
+                  const void* xhat, const float* rstd, const float* gamma, float p,
+                  uint64_t seed, uint64_t subseq, int64_t batch_offset, void* dz, void* dYpre,
+                  float* dgamma, float* dbeta, float* dbias, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjn(dtype, B, J, I, p, true);
+  if (r) return r;
+  if (batch_offset < 0) return ENC_EINVAL;
+  CHECK_PTRS(dOut, xhat, rstd, gamma, dz, dYpre, dgamma, dbeta, dbias);
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, (cudaStream_t)stream, 2);
+    CK(launch_bdrln_bwd(dtype, B, J, I, dOut, xhat, rstd, gamma, make_philox_key(p, seed, subseq),
+                        batch_offset, dz, dYpre, dgamma, dbeta, dbias, ws_of(ctx),
+                        (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_bad_fwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* Y1, const float* b1,
+                int act, float p, uint64_t seed, uint64_t subseq, int64_t batch_offset, void* h,
+                void* A1, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjn(dtype, B, J, U, p, false);
+  if (r) return r;
+  if (batch_offset < 0 || act < 0 || act > 2) return ENC_EINVAL;
+  CHECK_PTRS(Y1, b1, h, A1);
+  {
+    OpTimer _t(ctx, ENC_OP_BAD_FWD, (cudaStream_t)stream, 1);
+    CK(launch_bad_fwd(dtype, B, J, U, Y1, b1, act, make_philox_key(p, seed, subseq), batch_offset,
+                      h, A1, (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_bad_bwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* dA1, const void* h,
+                int act, float p, uint64_t seed, uint64_t subseq, int64_t batch_offset, void* dh,
+                float* db1, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_bjn(dtype, B, J, U, p, false);
+  if (r) return r;
+  if (batch_offset < 0 || act < 0 || act > 2) return ENC_EINVAL;
+  CHECK_PTRS(dA1, h, dh, db1);
+  {
+    OpTimer _t(ctx, ENC_OP_BAD_BWD, (cudaStream_t)stream, 2);
+    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, act, make_philox_key(p, seed, subseq), batch_offset,
+                      dh, db1, ws_of(ctx), (cudaStream_t)stream));
+  }
+  return ENC_OK;
+}
+
+int enc_bei(enc_ctx* ctx, int dtype, int64_t n, const void* a, const void* b, void* out,
+            enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (n < 0) return ENC_EINVAL;
+  if (n % 8) return ENC_EALIGN;
+  CHECK_PTRS(a, b, out);
+  CK(launch_bei(dtype, n, a, b, out, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
+// ------------------------------------------------------------------ whole layer
+static int check_params(const enc_params* p) {
+  if (!p) return ENC_ENULL;
+  CHECK_PTRS(p->Wqkv, p->Wo, p->W1, p->W2, p->bqkv, p->bo, p->b1, p->b2, p->g1, p->be1, p->g2,
+             p->be2);
+  return ENC_OK;
+}
+
+int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                          const enc_params* prm, const void* X, const float* mask_bias, void* Y,
+                          void* saved, void* scratch, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if ((r = check_cfg(cfg))) return r;
+  if ((r = check_params(prm))) return r;
+  CHECK_PTRS(X, Y, saved, scratch);
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if (d->B == 0) return ENC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CB(cublasSetStream(ctx->blas, st));
+  const int B = d->B, J = d->J, K = d->K, H = d->H, P = d->P, I = d->I, U = d->U;
+  const int BJ = B * J, BH = B * H;
+  const size_t es = esize(dtype);
+  const Layout SL = saved_layout(d, dtype), FL = fwd_layout(d, dtype);
+  void *Q = at(saved, SL.off[S_Q]), *Kt = at(saved, SL.off[S_K]), *V = at(saved, SL.off[S_V]);
+  void *Pm = at(saved, SL.off[S_P]), *A = at(saved, SL.off[S_A]), *C = at(saved, SL.off[S_C]);
+  void *X1 = at(saved, SL.off[S_X1]), *xh1 = at(saved, SL.off[S_XH1]);
+  void *h = at(saved, SL.off[S_H]), *A1 = at(saved, SL.off[S_A1]);
+  void* xh2 = at(saved, SL.off[S_XH2]);
+  float *r1 = (float*)at(saved, SL.off[S_R1]), *r2 = (float*)at(saved, SL.off[S_R2]);
+  void** ptr = (void**)at(scratch, FL.off[F_PTR]);
+  void *QKV = at(scratch, FL.off[F_QKV]), *S = at(scratch, FL.off[F_S]);
+  void *Yo = at(scratch, FL.off[F_YO]), *Y1 = at(scratch, FL.off[F_Y1]);
+  void* Y2 = at(scratch, FL.off[F_Y2]);
+  const uint64_t l4 = 4ull * cfg->layer_id;
+  const float scale = 1.0f / sqrtf((float)P);  // DESIGN.md R3
+  const int64_t boff = cfg->batch_offset;
+
+  // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
+               QKV, 3 * I));
+  }
+  // AIB (:550)
+  {
+    OpTimer _t(ctx, ENC_OP_AIB_FWD, st, 1);
+    CK(launch_aib_fwd(dtype, B, J, H, P, QKV, prm->bqkv, Q, Kt, V, st));
+  }
+  // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QK, st, 0);
+    CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P, Kt, P,
+                       (long long)K * P, 0.f, S, K, (long long)J * K, BH));
+  }
+  // BSB (:552)
+  {
+    OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
+    CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias,
+                      make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+  }
+  // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
+    CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
+    CB(gemm_rm_batched(ctx->blas, dtype, false, false, J, P, K, 1.f, (const void* const*)ptr, K,
+                       (const void* const*)(ptr + BH), P, 0.f, (void* const*)(ptr + 2 * BH), I, BH));
+  }
+  // Out (:554)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_OUT, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, I, I, 1.f, C, I, prm->Wo, I, 0.f, Yo, I));
+  }
+  // BDRLN site 1 (:555-558)
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_FWD1, st, 1);
+    CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st));
+  }
+  // Linear (:559)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, Y1, U));
+  }
+  // BAD (:560-562)
+  {
+    OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 1);
+    CK(launch_bad_fwd(dtype, B, J, U, Y1, prm->b1, cfg->act,
+                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, h, A1, st));
+  }
+  // Linear (:563)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L2, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, I, U, 1.f, A1, U, prm->W2, U, 0.f, Y2, I));
+  }
+  // BDRLN site 2 (:564-567)
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_FWD2, st, 1);
+    CK(launch_bdrln_fwd(dtype, B, J, I, Y2, prm->b2, X1, prm->g2, prm->be2, cfg->ln_eps,
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st));
+  }
+  return ENC_OK;
+}
+
+int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                           const enc_params* prm, const void* X, const void* saved,
+                           const void* dY, void* dX, const enc_grads* g, void* scratch,
+                           enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if ((r = check_cfg(cfg))) return r;
+  if ((r = check_params(prm))) return r;
+  if (!g) return ENC_ENULL;
+  CHECK_PTRS(X, saved, dY, dX, scratch, g->dWqkv, g->dWo, g->dW1, g->dW2, g->dbqkv, g->dbo, g->db1,
+             g->db2, g->dg1, g->dbe1, g->dg2, g->dbe2);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = d->B, J = d->J, K = d->K, H = d->H, P = d->P, I = d->I, U = d->U;
+  const int BJ = B * J, BH = B * H;
+  const size_t es = esize(dtype);
+  const ReduceWs ws = ws_of(ctx);
+  if (B == 0) {
+    const size_t n[12] = {(size_t)3 * I * I, (size_t)I * I, (size_t)U * I, (size_t)I * U,
+                          (size_t)3 * I, (size_t)I, (size_t)U, (size_t)I, (size_t)I, (size_t)I,
+                          (size_t)I, (size_t)I};
+    float* p[12] = {g->dWqkv, g->dWo, g->dW1, g->dW2, g->dbqkv, g->dbo,
+                    g->db1,   g->db2, g->dg1, g->dbe1, g->dg2, g->dbe2};
+    for (int i = 0; i < 12; ++i) CK(cudaMemsetAsync(p[i], 0, n[i] * sizeof(float), st));
+    return ENC_OK;
+  }
+  CB(cublasSetStream(ctx->blas, st));
+  const Layout SL = saved_layout(d, dtype), BL = bwd_layout(d, dtype);
+  void* sv = (void*)saved;
+  void *Q = at(sv, SL.off[S_Q]), *Kt = at(sv, SL.off[S_K]), *V = at(sv, SL.off[S_V]);
+  void *Pm = at(sv, SL.off[S_P]), *A = at(sv, SL.off[S_A]), *C = at(sv, SL.off[S_C]);
+  void *X1 = at(sv, SL.off[S_X1]), *xh1 = at(sv, SL.off[S_XH1]);
+  void *h = at(sv, SL.off[S_H]), *A1 = at(sv, SL.off[S_A1]), *xh2 = at(sv, SL.off[S_XH2]);
+  float *r1 = (float*)at(sv, SL.off[S_R1]), *r2 = (float*)at(sv, SL.off[S_R2]);
+  void** ptr = (void**)at(scratch, BL.off[B_PTR]);
+  void *dY2 = at(scratch, BL.off[B_DY2]), *dA1 = at(scratch, BL.off[B_DA1]);
+  void *dh = at(scratch, BL.off[B_DH]), *dX1 = at(scratch, BL.off[B_DX1]);
+  void *dYo = at(scratch, BL.off[B_DYO]), *dC = at(scratch, BL.off[B_DC]);
+  void *dA = at(scratch, BL.off[B_DA]), *dS = at(scratch, BL.off[B_DS]);
+  void *dQ = at(scratch, BL.off[B_DQ]), *dK = at(scratch, BL.off[B_DK]);
+  void *dV = at(scratch, BL.off[B_DV]), *dQKV = at(scratch, BL.off[B_DQKV]);
+  const uint64_t l4 = 4ull * cfg->layer_id;
+  const float scale = 1.0f / sqrtf((float)P);
+  const int64_t boff = cfg->batch_offset;
+  const int F32 = ENC_FP32;
+
+  // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_BWD2, st, 2);
+    CK(launch_bdrln_bwd(dtype, B, J, I, dY, xh2, r2, prm->g2,
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, dX1, dY2, g->dg2,
+                        g->dbe2, g->db2, ws, st));
+  }
+  // Linear2 dX (:573), dW (:574)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, U, I, 1.f, dY2, I, prm->W2, U, 0.f, dA1, U));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U));
+  }
+  // BAD-bwd (:576-578)
+  {
+    OpTimer _t(ctx, ENC_OP_BAD_BWD, st, 2);
+    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, cfg->act,
+                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, ws, st));
+  }
+  // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L1_DX, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, U, 1.f, dh, U, prm->W1, I, 1.f, dX1, I));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I));
+  }
+  // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo
+  {
+    OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, st, 2);
+    CK(launch_bdrln_bwd(dtype, B, J, I, dX1, xh1, r1, prm->g1,
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, dX, dYo, g->dg1,
+                        g->dbe1, g->dbo, ws, st));
+  }
+  // Out dX (:586), dW (:587)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_OUT_DX, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, I, 1.f, dYo, I, prm->Wo, I, 0.f, dC, I));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I));
+  }
+  // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, 1);
+    CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, dC, dA, dV, ptr, st));
+    CB(gemm_rm_batched(ctx->blas, dtype, false, true, J, K, P, 1.f, (const void* const*)(ptr + 2 * BH),
+                       I, (const void* const*)(ptr + BH), P, 0.f, (void* const*)(ptr + 3 * BH), K, BH));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, 0);
+    CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
+                       (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH), P, BH));
+  }
+  // BSB-bwd (:590)
+  {
+    OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
+    CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
+                      make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
+  }
+  // QK^T dX1 (:591): dQ = dS K;  dX2 (:592): dK = dS^T Q
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DQ, st, 0);
+    CB(gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, dS, K, (long long)J * K, Kt, P,
+                       (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, 0);
+    CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,
+                       (long long)J * P, 0.f, dK, P, (long long)K * P, BH));
+  }
+  // AIB-bwd (:595)
+  {
+    OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
+    CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, ws, st));
+  }
+  // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, 3 * I, 1.f, dQKV, 3 * I, prm->Wqkv, I,
+               1.f, dX, I));
+  }
+  {
+    OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, st, 0);
+    CB(gemm_rm(ctx->blas, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
+               g->dWqkv, I));
+  }
+  return ENC_OK;
+}
+
+int encoder_layer_step_host(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                            const enc_params* prm, const void* X_host, const void* dY_host,
+                            void* Y_host, void* dX_host, void* X_dev, void* dY_dev, void* Y_dev,
+                            void* dX_dev, const float* mask_bias, const enc_grads* g, void* saved,
+                            void* scratch, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (!X_host || !dY_host || !Y_host || !dX_host) return ENC_ENULL;
+  CHECK_PTRS(X_dev, dY_dev, Y_dev, dX_dev);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
+  CK(cudaMemcpyAsync(X_dev, X_host, bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dY_dev, dY_host, bytes, cudaMemcpyHostToDevice, st));
+  r = encoder_layer_forward(ctx, d, dtype, cfg, prm, X_dev, mask_bias, Y_dev, saved, scratch, stream);
+  if (r) return r;
+  r = encoder_layer_backward(ctx, d, dtype, cfg, prm, X_dev, saved, dY_dev, dX_dev, g, scratch, stream);
+  if (r) return r;
+  CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(dX_host, dX_dev, bytes, cudaMemcpyDeviceToHost, st));
+  return ENC_OK;
+}
+
+}  // extern "C"

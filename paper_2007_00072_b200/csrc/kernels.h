@@ -1,0 +1,82 @@
+// Host-side launchers of the fused sm_100a kernels (internal to libencoder.so).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+// Chunks-per-lane dispatch for the warp-per-row operators: a row of n elements has
+// nc = n/8 chunks, lane l owns chunks l, l+32, ...; CPL = ceil(nc/32) rounded up to a
+// compiled variant (rows up to 4096 elements).
+#define ENC_CPL_DISPATCH(nc, ...)                         \
+  do {                                                     \
+    const int _cpl = ((nc) + 31) / 32;                     \
+    if (_cpl <= 1) { constexpr int CPL = 1; __VA_ARGS__; }        \
+    else if (_cpl <= 2) { constexpr int CPL = 2; __VA_ARGS__; }   \
+    else if (_cpl <= 4) { constexpr int CPL = 4; __VA_ARGS__; }   \
+    else if (_cpl <= 8) { constexpr int CPL = 8; __VA_ARGS__; }   \
+    else { constexpr int CPL = 16; __VA_ARGS__; }                 \
+  } while (0)
+
+namespace enc {
+
+// Deterministic column-reduction workspace (owned by enc_ctx).
+struct ReduceWs {
+  float* partials;       // device, capacity `cap_floats`
+  size_t cap_floats;
+  int num_sms;
+};
+
+PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq);
+
+// dtype: 0 = bf16, 1 = fp32 (enc_dtype).  All return cudaSuccess or the launch error;
+// shape support is checked by the caller (api.cu) through *_supported().
+bool rowop_supported(int n_per_row);  // BSB (K), BDRLN (I): chunks-per-lane variants
+
+cudaError_t launch_dropout_mask(int64_t n, int64_t index0, const PhiloxKey& pk, uint8_t* keep,
+                                cudaStream_t st);
+
+cudaError_t launch_aib_fwd(int dtype, int B, int J, int H, int P, const void* qkv,
+                           const float* bqkv, void* q, void* k, void* v, cudaStream_t st);
+cudaError_t launch_aib_bwd(int dtype, int B, int J, int H, int P, const void* dq,
+                           const void* dk, const void* dv, void* dqkv, float* dbqkv,
+                           const ReduceWs& ws, cudaStream_t st);
+
+cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
+                           const float* mask_bias, const PhiloxKey& pk, int64_t batch_offset,
+                           void* P, void* A, cudaStream_t st);
+cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, const void* dA,
+                           const void* P, const PhiloxKey& pk, int64_t batch_offset, void* dS,
+                           cudaStream_t st);
+
+cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, const float* bias,
+                             const void* R, const float* gamma, const float* beta, float eps,
+                             const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
+                             float* rstd, cudaStream_t st);
+cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, const void* xhat,
+                             const float* rstd, const float* gamma, const PhiloxKey& pk,
+                             int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
+                             float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st);
+
+cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
+                           int act, const PhiloxKey& pk, int64_t batch_offset, void* h,
+                           void* A1, cudaStream_t st);
+cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, const void* h,
+                           int act, const PhiloxKey& pk, int64_t batch_offset, void* dh,
+                           float* db1, const ReduceWs& ws, cudaStream_t st);
+
+cudaError_t launch_bei(int dtype, int64_t n, const void* a, const void* b, void* out,
+                       cudaStream_t st);
+
+// Deterministic finalize: out_q[j] = sum_{r < R} partials[r*ncols + q*nper + j] in
+// ascending r order (fixed tree), q = 0..nq-1 with nq*nper = ncols.
+cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int nper,
+                                   float* out0, float* out1, float* out2, cudaStream_t st);
+
+// Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
+// dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.
+cudaError_t launch_make_attn_ptrs(int B, int H, int J, int P, size_t esize, const void* A,
+                                  const void* V, const void* C, const void* dA,
+                                  const void* dV, void** table, cudaStream_t st);
+
+}  // namespace enc

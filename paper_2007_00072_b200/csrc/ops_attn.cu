@@ -1,0 +1,348 @@
+// Attention-side fused operators: AIB / AIB-bwd (paper `aib`/`baib`),
+// BSB / BSB-bwd (paper `sm`/`bs`), the dropout-mask test hook and the
+// pointer tables of the two-level-strided attention GEMMs.
+//
+// BSB maps one score row (K elements) to one warp: the row lives in registers (CPL
+// chunks of 8 per lane), the max and sum are warp-shuffle all-reductions, so S is read
+// once and P, A written once -- the algorithmic 6*K bytes/row (bf16).  Dropout keep
+// bits are regenerated with one Philox4x32-10 call per 8-element chunk.
+#include <math.h>
+
+#include "kernels.h"
+
+namespace enc {
+
+PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq) {
+  PhiloxKey k;
+  const double T = floor((double)p * 65536.0 + 0.5);   // fp64 on the host (R5)
+  k.T = (uint32_t)T;
+  k.scale = (float)(65536.0 / (65536.0 - T));          // correctly rounded to fp32
+  k.k0 = (uint32_t)seed;
+  k.k1 = (uint32_t)(seed >> 32);
+  k.s0 = (uint32_t)subseq;
+  k.s1 = (uint32_t)(subseq >> 32);
+  return k;
+}
+
+static inline int grid_for(int64_t n, int threads, int cap) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// ------------------------------------------------------------------ dropout mask hook
+__global__ void dropout_mask_kernel(int64_t n, int64_t index0, PhiloxKey pk, uint8_t* keep) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t idx = (uint64_t)(index0 + i);
+    keep[i] = (uint8_t)((keep_bits8(idx >> 3, pk) >> (idx & 7)) & 1u);
+  }
+}
+
+cudaError_t launch_dropout_mask(int64_t n, int64_t index0, const PhiloxKey& pk, uint8_t* keep,
+                                cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  dropout_mask_kernel<<<grid_for(n, 256, 148 * 32), 256, 0, st>>>(n, index0, pk, keep);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ AIB forward
+// qkv [B*J, 3I] + bqkv -> q,k,v [B,H,J,P].  One thread per 8-element chunk; consecutive
+// threads walk a qkv row (coalesced reads) and write P/8 consecutive chunks per head
+// (a 128-byte contiguous run at P = 64, bf16).
+template <typename T>
+__global__ void __launch_bounds__(256) aib_fwd_kernel(const T* __restrict__ qkv,
+                                                      const float* __restrict__ bqkv,
+                                                      T* __restrict__ q, T* __restrict__ k,
+                                                      T* __restrict__ v, int64_t nchunks,
+                                                      int J, int H, int P) {
+  const int I = H * P;
+  const int nc3 = (3 * I) >> 3;
+  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t bj = c / nc3;
+    const int col = (int)(c - bj * nc3) << 3;
+    const int t = col / I;
+    const int rem = col - t * I;
+    const int h = rem / P;
+    const int p0 = rem - h * P;
+    const int64_t b = bj / J;
+    const int j = (int)(bj - b * J);
+    float x[8], bb[8];
+    Chunk<T>::load_cs(qkv + c * 8, x);
+    load_f32x8(bqkv + col, bb);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] += bb[i];
+    T* dst = (t == 0 ? q : (t == 1 ? k : v)) + (((b * H + h) * J + j) * P + p0);
+    Chunk<T>::store(dst, x);
+  }
+}
+
+cudaError_t launch_aib_fwd(int dtype, int B, int J, int H, int P, const void* qkv,
+                           const float* bqkv, void* q, void* k, void* v, cudaStream_t st) {
+  const int64_t n = (int64_t)B * J * (3 * H * P / 8);
+  if (n == 0) return cudaSuccess;
+  const int grid = grid_for(n, 256, 148 * 16);
+  if (dtype == 0)
+    aib_fwd_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+        (const __nv_bfloat16*)qkv, bqkv, (__nv_bfloat16*)q, (__nv_bfloat16*)k,
+        (__nv_bfloat16*)v, n, J, H, P);
+  else
+    aib_fwd_kernel<float><<<grid, 256, 0, st>>>((const float*)qkv, bqkv, (float*)q, (float*)k,
+                                                (float*)v, n, J, H, P);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ AIB backward
+// Column-parallel: thread (blockIdx.x, threadIdx.x) owns chunk column ch of dqkv; block
+// row y walks rows [y*rpb, (y+1)*rpb), gathers the chunk from dq/dk/dv, writes dqkv and
+// accumulates the bias-gradient partial in registers (no atomics: deterministic).
+template <typename T>
+__global__ void __launch_bounds__(128) aib_bwd_kernel(const T* __restrict__ dq,
+                                                      const T* __restrict__ dk,
+                                                      const T* __restrict__ dv,
+                                                      T* __restrict__ dqkv,
+                                                      float* __restrict__ partials,
+                                                      int rows, int rpb, int J, int H, int P) {
+  const int I = H * P;
+  const int nc3 = (3 * I) >> 3;
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= nc3) return;
+  const int col = ch << 3;
+  const int t = col / I;
+  const int rem = col - t * I;
+  const int h = rem / P;
+  const int p0 = rem - h * P;
+  const T* src = (t == 0 ? dq : (t == 1 ? dk : dv));
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  const int r0 = blockIdx.y * rpb;
+  const int r1 = min(rows, r0 + rpb);
+  for (int r = r0; r < r1; ++r) {
+    const int b = r / J;
+    const int j = r - b * J;
+    float x[8];
+    Chunk<T>::load_cs(src + ((((int64_t)b * H + h) * J + j) * P + p0), x);
+    Chunk<T>::store(dqkv + (int64_t)r * 3 * I + col, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] += x[i];
+  }
+  float* out = partials + (int64_t)blockIdx.y * 3 * I + col;
+  reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+cudaError_t launch_aib_bwd(int dtype, int B, int J, int H, int P, const void* dq,
+                           const void* dk, const void* dv, void* dqkv, float* dbqkv,
+                           const ReduceWs& ws, cudaStream_t st) {
+  const int I = H * P;
+  const int rows = B * J;
+  const int nc3 = 3 * I / 8;
+  if (rows == 0) return cudaMemsetAsync(dbqkv, 0, sizeof(float) * 3 * I, st);
+  dim3 block(128);
+  const int gx = (nc3 + 127) / 128;
+  int R = (4 * ws.num_sms + gx - 1) / gx;
+  const size_t cap_rows = ws.cap_floats / (size_t)(3 * I);
+  if ((size_t)R > cap_rows) R = (int)cap_rows;
+  if (R > rows) R = rows;
+  if (R < 1) R = 1;
+  const int rpb = (rows + R - 1) / R;
+  R = (rows + rpb - 1) / rpb;
+  dim3 grid(gx, R);
+  if (dtype == 0)
+    aib_bwd_kernel<__nv_bfloat16><<<grid, block, 0, st>>>(
+        (const __nv_bfloat16*)dq, (const __nv_bfloat16*)dk, (const __nv_bfloat16*)dv,
+        (__nv_bfloat16*)dqkv, ws.partials, rows, rpb, J, H, P);
+  else
+    aib_bwd_kernel<float><<<grid, block, 0, st>>>((const float*)dq, (const float*)dk,
+                                                  (const float*)dv, (float*)dqkv, ws.partials,
+                                                  rows, rpb, J, H, P);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_colsum_finalize(ws.partials, R, 3 * I, 3 * I, dbqkv, nullptr, nullptr, st);
+}
+
+// ------------------------------------------------------------------ BSB forward
+// One warp per row of K scores.  y = S*scale*log2(e) + M*log2(e); P = exp2(y - max y) /
+// sum; A = keep ? P*s : 0.  exp2 of the log2e-prescaled value equals exp(x - max x).
+constexpr float kLog2e = 1.4426950408889634f;
+
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
+                                                      const float* __restrict__ M,
+                                                      T* __restrict__ Pout,
+                                                      T* __restrict__ Aout, int64_t rows,
+                                                      int K, int HJ, float c, int64_t g0,
+                                                      PhiloxKey pk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nc = K >> 3;
+  const T* s = S + row * K;
+  const float* m = M ? M + (row / HJ) * K : nullptr;
+  float v[CPL][8];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      Chunk<T>::load_cs(s + ch * 8, v[i]);
+      if (m) {
+        float mb[8];
+        load_f32x8(m + ch * 8, mb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] = fmaf(v[i][j], c, mb[j] * kLog2e);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[i][j] *= c;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mx = fmaxf(mx, v[i][j]);
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    if (lane + 32 * i < nc) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[i][j] = exp2f(v[i][j] - mx);
+        sum += v[i][j];
+      }
+    }
+  }
+  sum = warp_sum(sum);
+  const float inv = 1.f / sum;
+  const int64_t gbase = g0 + row * nc;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      float p[8], a[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) p[j] = v[i][j] * inv;
+      Chunk<T>::store(Pout + row * K + ch * 8, p);
+      const uint32_t kb = keep_bits8((uint64_t)(gbase + ch), pk);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a[j] = ((kb >> j) & 1u) ? p[j] * pk.scale : 0.f;
+      Chunk<T>::store(Aout + row * K + ch * 8, a);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ BSB backward
+template <typename T, int CPL>
+__global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
+                                                      const T* __restrict__ Pin,
+                                                      T* __restrict__ dS, int64_t rows, int K,
+                                                      float scale, int64_t g0, PhiloxKey pk) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nc = K >> 3;
+  float dp[CPL][8], p[CPL][8];
+  float dot = 0.f;
+  const int64_t gbase = g0 + row * nc;
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      Chunk<T>::load_cs(dA + row * K + ch * 8, dp[i]);
+      Chunk<T>::load_cs(Pin + row * K + ch * 8, p[i]);
+      const uint32_t kb = keep_bits8((uint64_t)(gbase + ch), pk);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        dp[i][j] = ((kb >> j) & 1u) ? dp[i][j] * pk.scale : 0.f;
+        dot = fmaf(dp[i][j], p[i][j], dot);
+      }
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      float o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = scale * p[i][j] * (dp[i][j] - dot);
+      Chunk<T>::store(dS + row * K + ch * 8, o);
+    }
+  }
+}
+
+bool rowop_supported(int n) { return n > 0 && (n % 8) == 0 && n <= 32 * 8 * 16; }
+
+cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
+                           const float* mask_bias, const PhiloxKey& pk, int64_t batch_offset,
+                           void* P, void* A, cudaStream_t st) {
+  const int64_t rows = (int64_t)B * H * J;
+  if (rows == 0) return cudaSuccess;
+  const int nc = K / 8;
+  const int64_t g0 = batch_offset * (int64_t)H * J * nc;
+  const int grid = (int)((rows + 7) / 8);
+  const float c = scale * kLog2e;
+  ENC_CPL_DISPATCH(nc, {
+    if (dtype == 0)
+      bsb_fwd_kernel<__nv_bfloat16, CPL><<<grid, 256, 0, st>>>(
+          (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
+          H * J, c, g0, pk);
+    else
+      bsb_fwd_kernel<float, CPL><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
+                                                       (float*)A, rows, K, H * J, c, g0, pk);
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, const void* dA,
+                           const void* P, const PhiloxKey& pk, int64_t batch_offset, void* dS,
+                           cudaStream_t st) {
+  const int64_t rows = (int64_t)B * H * J;
+  if (rows == 0) return cudaSuccess;
+  const int nc = K / 8;
+  const int64_t g0 = batch_offset * (int64_t)H * J * nc;
+  const int grid = (int)((rows + 7) / 8);
+  ENC_CPL_DISPATCH(nc, {
+    if (dtype == 0)
+      bsb_bwd_kernel<__nv_bfloat16, CPL><<<grid, 256, 0, st>>>(
+          (const __nv_bfloat16*)dA, (const __nv_bfloat16*)P, (__nv_bfloat16*)dS, rows, K,
+          scale, g0, pk);
+    else
+      bsb_bwd_kernel<float, CPL><<<grid, 256, 0, st>>>((const float*)dA, (const float*)P,
+                                                       (float*)dS, rows, K, scale, g0, pk);
+  });
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ attention pointers
+// table layout: [0] A_bh, [1] V_bh, [2] C_bh, [3] dA_bh, [4] dV_bh, each B*H entries.
+// A, dA: [B,H,J,J] contiguous per (b,h); V, dV: [B,H,J,P]; C: [B,J,H,P] (row stride I).
+__global__ void make_attn_ptrs_kernel(int BH, int H, int J, int P, size_t esize, const char* A,
+                                      const char* V, const char* C, const char* dA,
+                                      const char* dV, void** table) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= BH) return;
+  const int b = i / H, h = i - (i / H) * H;
+  const size_t sJJ = (size_t)J * J * esize, sJP = (size_t)J * P * esize;
+  table[i] = (void*)(A + i * sJJ);
+  table[BH + i] = (void*)(V + i * sJP);
+  table[2 * BH + i] = (void*)(C + ((size_t)b * J * H * P + (size_t)h * P) * esize);
+  table[3 * BH + i] = (void*)(dA ? dA + i * sJJ : nullptr);
+  table[4 * BH + i] = (void*)(dV ? dV + i * sJP : nullptr);
+}
+
+cudaError_t launch_make_attn_ptrs(int B, int H, int J, int P, size_t esize, const void* A,
+                                  const void* V, const void* C, const void* dA,
+                                  const void* dV, void** table, cudaStream_t st) {
+  const int BH = B * H;
+  if (BH == 0) return cudaSuccess;
+  make_attn_ptrs_kernel<<<(BH + 255) / 256, 256, 0, st>>>(BH, H, J, P, esize, (const char*)A,
+                                                           (const char*)V, (const char*)C,
+                                                           (const char*)dA, (const char*)dV,
+                                                           table);
+  return cudaGetLastError();
+}
+
+}  // namespace enc

@@ -1,0 +1,170 @@
+"""EncoderLayer: buffer management around encoder_layer_forward / encoder_layer_backward.
+
+PyTorch supplies device memory (the caller-owned `saved`, `scratch`, parameter and
+gradient buffers of include/encoder.h) and the CUDA stream; all compute runs in
+libencoder.so.  Parameter gradients live in ONE flat fp32 buffer laid out as two
+contiguous buckets so data parallelism can all-reduce them with one collective each
+(DESIGN.md "Multi-GPU"): the FFN bucket (ready first in backward) then the attention bucket.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import check
+from .ops import Context
+
+ACTS = {"gelu": _abi.ACT_GELU_ERF, "gelu_tanh": _abi.ACT_GELU_TANH, "relu": _abi.ACT_RELU}
+TORCH_DT = {"bf16": torch.bfloat16, "fp32": torch.float32}
+ABI_DT = {"bf16": _abi.ENC_BF16, "fp32": _abi.ENC_FP32}
+
+FFN_BUCKET = ("W1", "W2", "b1", "b2", "g2", "be2")
+ATTN_BUCKET = ("Wqkv", "Wo", "bqkv", "bo", "g1", "be1")
+
+
+@dataclass
+class LayerCfg:
+    """enc_cfg (include/encoder.h); defaults follow DESIGN.md R3-R7."""
+    p_attn: float = 0.1
+    p_hidden: float = 0.1
+    p_ffn: float = 0.1
+    seed: int = 2007000072
+    layer_id: int = 0
+    batch_offset: int = 0
+    ln_eps: float = 1e-5
+    act: str = "gelu"
+
+    def to_c(self) -> _abi.enc_cfg:
+        return _abi.enc_cfg(self.p_attn, self.p_hidden, self.p_ffn, self.seed, self.layer_id,
+                            self.batch_offset, self.ln_eps, ACTS[self.act])
+
+
+def param_shapes(I: int, U: int) -> dict:
+    return {"Wqkv": (3 * I, I), "Wo": (I, I), "W1": (U, I), "W2": (I, U), "bqkv": (3 * I,),
+            "bo": (I,), "b1": (U,), "b2": (I,), "g1": (I,), "be1": (I,), "g2": (I,), "be2": (I,)}
+
+
+def c_dims(B, J, H, P, U) -> _abi.enc_dims:
+    return _abi.enc_dims(B, J, J, H, P, P, H * P, U)
+
+
+class EncoderLayer:
+    """One BERT encoder layer (post-LN) on one GPU.
+
+    dims: object with B (local batch), J, H, P, U.  dtype: 'bf16' or 'fp32'.
+    """
+
+    def __init__(self, dims, dtype: str = "bf16", cfg: LayerCfg | None = None,
+                 ctx: Context | None = None, device=None):
+        self.lib = _abi.load()
+        self.B, self.J, self.H, self.P, self.U = dims.B, dims.J, dims.H, dims.P, dims.U
+        self.I = self.H * self.P
+        self.dtype = dtype
+        self.tdt = TORCH_DT[dtype]
+        self.adt = ABI_DT[dtype]
+        self.cfg = cfg or LayerCfg()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        self.ctx = ctx or Context(self.device.index)
+        self.dims = c_dims(self.B, self.J, self.H, self.P, self.U)
+        sb, cb = ctypes.c_size_t(), ctypes.c_size_t()
+        check("enc_layer_sizes", self.lib.enc_layer_sizes(ctypes.byref(self.dims), self.adt,
+                                                          ctypes.byref(sb), ctypes.byref(cb)))
+        self.saved = torch.empty(max(sb.value, 16), dtype=torch.uint8, device=self.device)
+        self.scratch = torch.empty(max(cb.value, 16), dtype=torch.uint8, device=self.device)
+        shapes = param_shapes(self.I, self.U)
+        self.params = {}
+        for n, s in shapes.items():
+            dt = self.tdt if n.startswith("W") else torch.float32
+            self.params[n] = torch.zeros(s, dtype=dt, device=self.device)
+        # flat fp32 gradient buffer: FFN bucket, then attention bucket
+        order = FFN_BUCKET + ATTN_BUCKET
+        sizes = [int(np.prod(shapes[n])) for n in order]
+        self.grad_flat = torch.zeros(sum(sizes), dtype=torch.float32, device=self.device)
+        self.grads = {}
+        off = 0
+        for n, sz in zip(order, sizes):
+            self.grads[n] = self.grad_flat[off:off + sz].view(shapes[n])
+            off += sz
+        self.ffn_bucket = self.grad_flat[:sum(sizes[:len(FFN_BUCKET)])]
+        self.attn_bucket = self.grad_flat[sum(sizes[:len(FFN_BUCKET)]):]
+        self._refresh_structs()
+
+    # ------------------------------------------------------------------ parameters
+    def set_params(self, params: dict):
+        for n, v in params.items():
+            if n not in self.params:
+                continue
+            t = torch.as_tensor(np.asarray(v)) if not isinstance(v, torch.Tensor) else v
+            self.params[n].copy_(t.to(self.params[n].dtype))
+        self._refresh_structs()
+
+    def _refresh_structs(self):
+        self.c_params = _abi.enc_params(*[self.params[n].data_ptr() for n in _abi.PARAM_FIELDS])
+        self.c_grads = _abi.enc_grads(*[self.grads[n].data_ptr() for n in _abi.PARAM_FIELDS])
+
+    # ------------------------------------------------------------------ passes
+    def _stream(self, stream):
+        return (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
+
+    def forward(self, X: torch.Tensor, mask_bias: torch.Tensor | None = None,
+                Y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        assert X.dtype == self.tdt and X.is_contiguous() and X.is_cuda
+        if Y is None:
+            Y = torch.empty_like(X)
+        cfg = self.cfg.to_c()
+        check("encoder_layer_forward", self.lib.encoder_layer_forward(
+            self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
+            ctypes.byref(self.c_params), X.data_ptr(),
+            None if mask_bias is None else mask_bias.data_ptr(), Y.data_ptr(),
+            self.saved.data_ptr(), self.scratch.data_ptr(), self._stream(stream)))
+        return Y
+
+    def backward(self, X: torch.Tensor, dY: torch.Tensor, dX: torch.Tensor | None = None,
+                 stream=None) -> torch.Tensor:
+        assert dY.dtype == self.tdt and dY.is_contiguous() and dY.is_cuda
+        if dX is None:
+            dX = torch.empty_like(dY)
+        cfg = self.cfg.to_c()
+        check("encoder_layer_backward", self.lib.encoder_layer_backward(
+            self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
+            ctypes.byref(self.c_params), X.data_ptr(), self.saved.data_ptr(), dY.data_ptr(),
+            dX.data_ptr(), ctypes.byref(self.c_grads), self.scratch.data_ptr(),
+            self._stream(stream)))
+        return dX
+
+    def step_host(self, X_host, dY_host, Y_host, dX_host, X_dev, dY_dev, Y_dev, dX_dev,
+                  mask_bias=None, stream=None):
+        """encoder_layer_step_host: H2D inputs, fwd + bwd, D2H Y and dX (host tensors
+        should be pinned)."""
+        cfg = self.cfg.to_c()
+        check("encoder_layer_step_host", self.lib.encoder_layer_step_host(
+            self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
+            ctypes.byref(self.c_params), X_host.data_ptr(), dY_host.data_ptr(),
+            Y_host.data_ptr(), dX_host.data_ptr(), X_dev.data_ptr(), dY_dev.data_ptr(),
+            Y_dev.data_ptr(), dX_dev.data_ptr(),
+            None if mask_bias is None else mask_bias.data_ptr(), ctypes.byref(self.c_grads),
+            self.saved.data_ptr(), self.scratch.data_ptr(), self._stream(stream)))
+
+    # ------------------------------------------------------------------ inspection
+    def saved_views(self) -> dict:
+        v = _abi.enc_saved_view()
+        check("enc_saved_views", self.lib.enc_saved_views(ctypes.byref(self.dims), self.adt,
+                                                          self.saved.data_ptr(), ctypes.byref(v)))
+        B, J, H, P, I, U = self.B, self.J, self.H, self.P, self.I, self.U
+        shapes = {"Q": (B, H, J, P), "K": (B, H, J, P), "V": (B, H, J, P), "P": (B, H, J, J),
+                  "A": (B, H, J, J), "C": (B, J, I), "X1": (B, J, I), "xhat1": (B, J, I),
+                  "h": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I), "rstd1": (B, J),
+                  "rstd2": (B, J)}
+        base = self.saved.data_ptr()
+        out = {}
+        for n in _abi.SAVED_FIELDS:
+            off = getattr(v, n) - base
+            dt = torch.float32 if n.startswith("rstd") else self.tdt
+            numel = int(np.prod(shapes[n]))
+            nbytes = numel * torch.empty((), dtype=dt).element_size()
+            out[n] = self.saved[off:off + nbytes].view(dt).view(shapes[n])
+        return out

@@ -1,0 +1,115 @@
+"""Per-operator Python binding: the same names as include/encoder.h, taking torch CUDA
+tensors.  Argument marshalling only (pointers, sizes, the current CUDA stream); every
+step runs in libencoder.so.  PyTorch supplies device memory and streams only."""
+from __future__ import annotations
+
+import torch
+
+from . import _abi
+from ._abi import check
+
+_DT = {torch.bfloat16: _abi.ENC_BF16, torch.float32: _abi.ENC_FP32}
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported dtype {t.dtype}")
+    return _DT[t.dtype]
+
+
+def _p(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Context:
+    """Owns an enc_ctx (cuBLAS handle, cuBLAS workspace, reduction workspace)."""
+
+    def __init__(self, device=None):
+        lib = _abi.load()
+        dev = torch.cuda.current_device() if device is None else int(device)
+        h = _abi.c_void_p()
+        check("enc_create", lib.enc_create(_abi.ctypes.byref(h), dev))
+        self.handle = h
+        self.device = dev
+        self._lib = lib
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self._lib.enc_destroy(h)
+            self.handle = None
+
+    @property
+    def ptr(self):
+        return self.handle
+
+
+def enc_dropout_mask(n, index0, p, seed, subseq, keep: torch.Tensor, stream=None):
+    lib = _abi.load()
+    check("enc_dropout_mask", lib.enc_dropout_mask(n, index0, p, seed, subseq, _p(keep),
+                                                   _stream(stream)))
+
+
+def enc_aib_fwd(ctx, B, J, H, P, qkv, bqkv, q, k, v, stream=None):
+    check("enc_aib_fwd", _abi.load().enc_aib_fwd(ctx.ptr, _dt(qkv), B, J, H, P, _p(qkv), _p(bqkv),
+                                                 _p(q), _p(k), _p(v), _stream(stream)))
+
+
+def enc_aib_bwd(ctx, B, J, H, P, dq, dk, dv, dqkv, dbqkv, stream=None):
+    check("enc_aib_bwd", _abi.load().enc_aib_bwd(ctx.ptr, _dt(dq), B, J, H, P, _p(dq), _p(dk),
+                                                 _p(dv), _p(dqkv), _p(dbqkv), _stream(stream)))
+
+
+def enc_bsb_fwd(ctx, B, H, J, K, scale, S, mask_bias, p, seed, subseq, batch_offset, P, A,
+                stream=None):
+    check("enc_bsb_fwd", _abi.load().enc_bsb_fwd(ctx.ptr, _dt(S), B, H, J, K, scale, _p(S),
+                                                 _p(mask_bias), p, seed, subseq, batch_offset,
+                                                 _p(P), _p(A), _stream(stream)))
+
+
+def enc_bsb_bwd(ctx, B, H, J, K, scale, dA, P, p, seed, subseq, batch_offset, dS, stream=None):
+    check("enc_bsb_bwd", _abi.load().enc_bsb_bwd(ctx.ptr, _dt(dA), B, H, J, K, scale, _p(dA),
+                                                 _p(P), p, seed, subseq, batch_offset, _p(dS),
+                                                 _stream(stream)))
+
+
+def enc_bdrln_fwd(ctx, B, J, I, Y, bias, R, gamma, beta, eps, p, seed, subseq, batch_offset,
+                  out, xhat, rstd, stream=None):
+    check("enc_bdrln_fwd", _abi.load().enc_bdrln_fwd(
+        ctx.ptr, _dt(Y), B, J, I, _p(Y), _p(bias), _p(R), _p(gamma), _p(beta), eps, p, seed,
+        subseq, batch_offset, _p(out), _p(xhat), _p(rstd), _stream(stream)))
+
+
+def enc_bdrln_bwd(ctx, B, J, I, dOut, xhat, rstd, gamma, p, seed, subseq, batch_offset, dz,
+                  dYpre, dgamma, dbeta, dbias, stream=None):
+    check("enc_bdrln_bwd", _abi.load().enc_bdrln_bwd(
+        ctx.ptr, _dt(dOut), B, J, I, _p(dOut), _p(xhat), _p(rstd), _p(gamma), p, seed, subseq,
+        batch_offset, _p(dz), _p(dYpre), _p(dgamma), _p(dbeta), _p(dbias), _stream(stream)))
+
+
+def enc_bad_fwd(ctx, B, J, U, Y1, b1, act, p, seed, subseq, batch_offset, h, A1, stream=None):
+    check("enc_bad_fwd", _abi.load().enc_bad_fwd(ctx.ptr, _dt(Y1), B, J, U, _p(Y1), _p(b1), act,
+                                                 p, seed, subseq, batch_offset, _p(h), _p(A1),
+                                                 _stream(stream)))
+
+
+def enc_bad_bwd(ctx, B, J, U, dA1, h, act, p, seed, subseq, batch_offset, dh, db1, stream=None):
+    check("enc_bad_bwd", _abi.load().enc_bad_bwd(ctx.ptr, _dt(dA1), B, J, U, _p(dA1), _p(h), act,
+                                                 p, seed, subseq, batch_offset, _p(dh), _p(db1),
+                                                 _stream(stream)))
+
+
+def enc_bei(ctx, a, b, out, stream=None):
+    check("enc_bei", _abi.load().enc_bei(ctx.ptr, _dt(a), a.numel(), _p(a), _p(b), _p(out),
+                                         _stream(stream)))

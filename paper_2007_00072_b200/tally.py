@@ -1,0 +1,56 @@
+"""Flop and algorithmic-byte tally of the layer (host-side bookkeeping for bench.py and
+DESIGN.md; no compute).
+
+Algorithmic bytes = the bytes the fused operator must move given its inputs/outputs in
+HBM (masks regenerated, never stored): SURVEY.md 8(d) "Algorithmic bytes per token".
+Flops of the contractions follow Table A.1, e.g. Q,K,V = 2*3*B*J*I*I.
+"""
+from __future__ import annotations
+
+
+def _d(d):
+    B, J, H, P, U = d.B, d.J, d.H, d.P, d.U
+    return B, J, H, P, H * P, U
+
+
+def fused_bytes(d, es: int = 2, mask_bias: bool = False) -> dict:
+    """Algorithmic HBM bytes per launch of each fused operator (es = activation bytes)."""
+    B, J, H, P, I, U = _d(d)
+    BJ, BJI, BJU, BHJK = B * J, B * J * I, B * J * U, B * H * J * J
+    f = 4  # fp32
+    return {
+        "aib_fwd": 2 * BJ * 3 * I * es + 3 * I * f,
+        "bsb_fwd": 3 * BHJK * es + (B * J * f if mask_bias else 0),
+        "bdrln_fwd1": 4 * BJI * es + BJ * f + 3 * I * f,
+        "bad_fwd": 3 * BJU * es + U * f,
+        "bdrln_fwd2": 4 * BJI * es + BJ * f + 3 * I * f,
+        "bdrln_bwd2": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
+        "bad_bwd": 3 * BJU * es + U * f,
+        "bdrln_bwd1": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
+        "bsb_bwd": 3 * BHJK * es,
+        "aib_bwd": 2 * BJ * 3 * I * es + 3 * I * f,
+    }
+
+
+def gemm_flops(d) -> dict:
+    """2*M*N*K of every contraction of one fwd+bwd step (Table A.1)."""
+    B, J, H, P, I, U = _d(d)
+    BJ = B * J
+    att = 2 * B * H * J * J * P
+    return {
+        "gemm_qkv": 2 * BJ * 3 * I * I, "gemm_qk": att, "gemm_av": att,
+        "gemm_out": 2 * BJ * I * I, "gemm_l1": 2 * BJ * U * I, "gemm_l2": 2 * BJ * I * U,
+        "gemm_l2_dx": 2 * BJ * I * U, "gemm_l2_dw": 2 * BJ * I * U,
+        "gemm_l1_dx": 2 * BJ * I * U, "gemm_l1_dw": 2 * BJ * I * U,
+        "gemm_out_dx": 2 * BJ * I * I, "gemm_out_dw": 2 * BJ * I * I,
+        "gemm_av_da": att, "gemm_av_dv": att, "gemm_qk_dq": att, "gemm_qk_dk": att,
+        "gemm_qkv_dx": 2 * BJ * 3 * I * I, "gemm_qkv_dw": 2 * BJ * 3 * I * I,
+    }
+
+
+def step_fused_bytes(d, es: int = 2) -> int:
+    return sum(fused_bytes(d, es).values())
+
+
+def step_flops(d) -> int:
+    return sum(gemm_flops(d).values())
