@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=2)
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--eager", action="store_true",
+                    help="launch every step eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
 
 
@@ -221,6 +223,32 @@ def main():
     dominant = max(per_op, key=per_op.get)
     dom_id = names.index(dominant)
     lib.enc_set_timing(layer.ctx.ptr, 1 << dom_id)
+    l0 = lib.enc_launch_count(layer.ctx.ptr)
+    layer.forward(X, None, Y)
+    layer.backward(X, dY, dX)
+    per_step_launches = lib.enc_launch_count(layer.ctx.ptr) - l0
+
+    # ---------------- CUDA graph of the layer step (fwd + bwd); events of the timed op
+    # (enabled above) are captured as event-record nodes of the graph
+    run_layer = lambda: (layer.forward(X, None, Y), layer.backward(X, dY, dX))  # noqa: E731
+    if not args.eager:
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            run_layer()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            run_layer()
+        torch.cuda.synchronize()
+
+        def step():  # noqa: F811
+            graph.replay()
+            if world > 1:
+                dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
 
     # ---------------- timed region
     sampler = ClockSampler(local)
@@ -243,6 +271,8 @@ def main():
     barrier()
     t_wall = time.perf_counter() - t_wall
     launches = lib.enc_launch_count(layer.ctx.ptr) - launches0
+    if not args.eager:   # graph replays launch the captured kernels; count them per step
+        launches = per_step_launches * args.steps
     clocks = sampler.stop()
     step_ms = sum(a.elapsed_time(b) for a, b in ev)
     step_ms = dp.max_over_ranks(step_ms, dev)
@@ -327,7 +357,7 @@ def main():
             "config": {"workload": WORKLOAD, "global_batch": dims_global.B, "seq_len": dims.J,
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
-                       else "not flushed", "graph": "eager launches"},
+                       else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},

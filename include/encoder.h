@@ -106,6 +106,14 @@ typedef struct {
   float *rstd1, *rstd2;
 } enc_saved_view;
 
+/* Views into `scratch` of the backward temporaries, valid after encoder_layer_backward
+ * until the next forward/backward call on the same scratch (parity / inspection hook):
+ * dY2 (= BDRLN-bwd#2 dYpre), dX1, dYo, dC [B,J,I]; dA1, dh [B,J,U]; dA, dS [B,H,J,K];
+ * dQ, dK, dV [B,H,J,P]; dQKV [B,J,3I]. */
+typedef struct {
+  void *dY2, *dA1, *dh, *dX1, *dYo, *dC, *dA, *dS, *dQ, *dK, *dV, *dQKV;
+} enc_bwd_view;
+
 typedef struct enc_ctx enc_ctx;
 
 /* ---- context ---------------------------------------------------------------------- */
@@ -146,6 +154,8 @@ uint64_t enc_launch_count(const enc_ctx* ctx);
 int enc_layer_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* scratch_bytes);
 /* Pointers to the named tensors inside `saved` (test / inspection hook). */
 int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* out);
+/* Pointers to the backward temporaries inside `scratch` (test / inspection hook). */
+int enc_bwd_views(const enc_dims* d, int dtype, void* scratch, enc_bwd_view* out);
 
 /* Forward: X [B,J,I] -> Y [B,J,I].  mask_bias [B,K] fp32 additive attention bias
  * (BERT key-padding mask, R1) or NULL.  Steps: QKV GEMM, AIB, QK^T, BSB,

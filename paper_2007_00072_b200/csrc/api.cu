@@ -48,13 +48,22 @@ struct OpTimer {
   OpTimer(enc_ctx* c_, int op_, cudaStream_t st_, int launches)
       : c(c_), op(op_), st(st_), on((c_->timing_mask >> op_) & 1ull) {
     c->launches += launches;
-    if (on) cudaEventRecord(c->ev0[op], st);
+    if (on) record(c->ev0[op]);
   }
   ~OpTimer() {
     if (on) {
-      cudaEventRecord(c->ev1[op], st);
+      record(c->ev1[op]);
       c->recorded[op] = true;
     }
+  }
+  // inside CUDA-graph capture the event must become an event-record node of the graph
+  void record(cudaEvent_t ev) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cs);
+    if (cs == cudaStreamCaptureStatusActive)
+      cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal);
+    else
+      cudaEventRecord(ev, st);
   }
 };
 }  // namespace
@@ -182,6 +191,7 @@ static int check_dims(const enc_dims* d, int dtype) {
   if (d->K != d->J || d->W != d->P || d->I != d->H * d->P) return ENC_EINVAL;
   if (d->I % 8 || d->U % 8 || d->K % 8 || d->P % 8) return ENC_EALIGN;
   if (!rowop_supported(d->K) || !rowop_supported(d->I)) return ENC_EUNSUPPORTED;
+  if (!bdrln_bwd_supported(d->I, dtype)) return ENC_EUNSUPPORTED;
   return ENC_OK;
 }
 
@@ -293,6 +303,26 @@ int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* v
   v->xhat2 = at(saved, L.off[S_XH2]);
   v->rstd1 = (float*)at(saved, L.off[S_R1]);
   v->rstd2 = (float*)at(saved, L.off[S_R2]);
+  return ENC_OK;
+}
+
+int enc_bwd_views(const enc_dims* d, int dtype, void* scratch, enc_bwd_view* v) {
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (!scratch || !v) return ENC_ENULL;
+  const Layout L = bwd_layout(d, dtype);
+  v->dY2 = at(scratch, L.off[B_DY2]);
+  v->dA1 = at(scratch, L.off[B_DA1]);
+  v->dh = at(scratch, L.off[B_DH]);
+  v->dX1 = at(scratch, L.off[B_DX1]);
+  v->dYo = at(scratch, L.off[B_DYO]);
+  v->dC = at(scratch, L.off[B_DC]);
+  v->dA = at(scratch, L.off[B_DA]);
+  v->dS = at(scratch, L.off[B_DS]);
+  v->dQ = at(scratch, L.off[B_DQ]);
+  v->dK = at(scratch, L.off[B_DK]);
+  v->dV = at(scratch, L.off[B_DV]);
+  v->dQKV = at(scratch, L.off[B_DQKV]);
   return ENC_OK;
 }
 
@@ -412,6 +442,7 @@ int enc_bdrln_bwd(enc_ctx* ctx, int dtype, int B, int J, int I, const void* dOut
   if (!ctx) return ENC_ENULL;
   int r = check_bjn(dtype, B, J, I, p, true);
   if (r) return r;
+  if (!bdrln_bwd_supported(I, dtype)) return ENC_EUNSUPPORTED;
   if (batch_offset < 0) return ENC_EINVAL;
   CHECK_PTRS(dOut, xhat, rstd, gamma, dz, dYpre, dgamma, dbeta, dbias);
   {

@@ -14,13 +14,22 @@ namespace enc {
 constexpr int kWarp = 32;
 
 // ---------------------------------------------------------------- chunk load / store
+// Raw = the chunk's bytes as loaded (kept packed in registers until used, so all loads of
+// a row can be issued before any arithmetic: memory-level parallelism).
 template <typename T>
 struct Chunk;
 
 template <>
 struct Chunk<__nv_bfloat16> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float v[8]) {
-    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  using Raw = uint4;
+  static constexpr int kBytes = 16;
+  static __device__ __forceinline__ Raw ld(const __nv_bfloat16* p) {  // streamed once
+    return __ldcs(reinterpret_cast<const uint4*>(p));
+  }
+  static __device__ __forceinline__ Raw ld_smem(const __nv_bfloat16* p) {
+    return *reinterpret_cast<const uint4*>(p);
+  }
+  static __device__ __forceinline__ void unpack(const Raw& u, float v[8]) {
     const uint32_t w[4] = {u.x, u.y, u.z, u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -28,15 +37,8 @@ struct Chunk<__nv_bfloat16> {
       v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
     }
   }
-  // streaming load for data read exactly once
   static __device__ __forceinline__ void load_cs(const __nv_bfloat16* p, float v[8]) {
-    uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
-    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v[2 * i] = __uint_as_float(w[i] << 16);
-      v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-    }
+    unpack(ld(p), v);
   }
   static __device__ __forceinline__ uint32_t pack2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);  // round to nearest even
@@ -50,37 +52,34 @@ struct Chunk<__nv_bfloat16> {
     u.w = pack2(v[6], v[7]);
     *reinterpret_cast<uint4*>(p) = u;
   }
-  static __device__ __forceinline__ void store_cs(__nv_bfloat16* p, const float v[8]) {
-    uint4 u;
-    u.x = pack2(v[0], v[1]);
-    u.y = pack2(v[2], v[3]);
-    u.z = pack2(v[4], v[5]);
-    u.w = pack2(v[6], v[7]);
-    __stcs(reinterpret_cast<uint4*>(p), u);
-  }
 };
 
 template <>
 struct Chunk<float> {
-  static __device__ __forceinline__ void load(const float* p, float v[8]) {
-    float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  struct Raw {
+    float4 a, b;
+  };
+  static constexpr int kBytes = 32;
+  static __device__ __forceinline__ Raw ld(const float* p) {
+    Raw r;
+    r.a = __ldcs(reinterpret_cast<const float4*>(p));
+    r.b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    return r;
   }
-  static __device__ __forceinline__ void load_cs(const float* p, float v[8]) {
-    float4 a = __ldcs(reinterpret_cast<const float4*>(p));
-    float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  static __device__ __forceinline__ Raw ld_smem(const float* p) {
+    Raw r;
+    r.a = reinterpret_cast<const float4*>(p)[0];
+    r.b = reinterpret_cast<const float4*>(p)[1];
+    return r;
   }
+  static __device__ __forceinline__ void unpack(const Raw& r, float v[8]) {
+    v[0] = r.a.x; v[1] = r.a.y; v[2] = r.a.z; v[3] = r.a.w;
+    v[4] = r.b.x; v[5] = r.b.y; v[6] = r.b.z; v[7] = r.b.w;
+  }
+  static __device__ __forceinline__ void load_cs(const float* p, float v[8]) { unpack(ld(p), v); }
   static __device__ __forceinline__ void store(float* p, const float v[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
     reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
-  }
-  static __device__ __forceinline__ void store_cs(float* p, const float v[8]) {
-    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
-    __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v[4], v[5], v[6], v[7]));
   }
 };
 
@@ -94,44 +93,78 @@ __device__ __forceinline__ void load_f32x8(const float* p, float v[8]) {
 
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al. SC'11 (Random123); same ctr/key/word layout as cuRAND's
-// curand_init(seed, subseq, 4*g) + curand4() (R5).
+// curand_init(seed, subseq, 4*g) + curand4() (R5).  The ten round keys and the
+// counter half that is the same for every call of a site (ctr.zw = subsequence) are
+// folded on the host, so a call costs 19 IMAD.WIDE + 20 LOP3 (keys read from the
+// kernel-parameter constant bank).
 struct PhiloxKey {
-  uint32_t k0, k1;  // seed lo, hi
-  uint32_t s0, s1;  // subsequence lo, hi
-  uint32_t T;       // keep iff 16-bit lane >= T
-  float scale;      // 65536 / (65536 - T), correctly rounded
+  uint32_t rk0[10], rk1[10];  // round keys: seed lo/hi + r * Weyl constants
+  uint32_t a0;                // round 0: umulhi(M1, subseq lo) ^ rk0[0]
+  uint32_t l1;                // round 0: M1 * subseq lo
+  uint32_t b0;                // round 0: subseq hi ^ rk1[0]
+  uint32_t T;                 // keep iff 16-bit lane >= T
+  float scale;                // 65536 / (65536 - T), correctly rounded
 };
 
-__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+__device__ __forceinline__ uint4 philox4x32_10(uint64_t g, const PhiloxKey& pk) {
+  const uint32_t g0 = (uint32_t)g, g1 = (uint32_t)(g >> 32);
+  // round 0 with ctr = (g0, g1, s0, s1)
+  uint4 c;
+  {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, g0), lo0 = 0xD2511F53u * g0;
+    c = make_uint4(pk.a0 ^ g1, pk.l1, hi0 ^ pk.b0, lo0);
+  }
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    if (r) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
+  for (int r = 1; r < 10; ++r) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    c = make_uint4(hi1 ^ c.y ^ pk.rk0[r], lo1, hi0 ^ c.w ^ pk.rk1[r], lo0);
   }
   return c;
 }
 
-// 8 keep bits (bit i = lane i) of chunk g (= logical index >> 3).
+// 8 keep bits (bit i = lane i) of chunk g (= logical index >> 3).  Test hook only; the
+// kernels use keep_mul8, which avoids materialising the bits.
 __device__ __forceinline__ uint32_t keep_bits8(uint64_t g, const PhiloxKey& pk) {
   if (pk.T == 0) return 0xFFu;
-  const uint4 w = philox4x32_10(make_uint4((uint32_t)g, (uint32_t)(g >> 32), pk.s0, pk.s1),
-                                pk.k0, pk.k1);
+  const uint4 w = philox4x32_10(g, pk);
   const uint32_t T = pk.T;
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
   uint32_t b = 0;
-  b |= ((w.x & 0xFFFFu) >= T) << 0;
-  b |= ((w.x >> 16) >= T) << 1;
-  b |= ((w.y & 0xFFFFu) >= T) << 2;
-  b |= ((w.y >> 16) >= T) << 3;
-  b |= ((w.z & 0xFFFFu) >= T) << 4;
-  b |= ((w.z >> 16) >= T) << 5;
-  b |= ((w.w & 0xFFFFu) >= T) << 6;
-  b |= ((w.w >> 16) >= T) << 7;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    b |= ((wv[i] & 0xFFFFu) >= T) << (2 * i);
+    b |= ((wv[i] >> 16) >= T) << (2 * i + 1);
+  }
   return b;
+}
+
+// m[j] = keep_j ? scale : 0 for the 8 elements of chunk g.  Lane 2i is the low half of
+// word i, lane 2i+1 the high half.  r_hi >= T  <=>  w >= T<<16 and r_lo >= T  <=>
+// (w << 16) >= T<<16, so each decision is one compare (+ one shift for low halves).
+__device__ __forceinline__ void keep_mul8(uint64_t g, const PhiloxKey& pk, float m[8]) {
+  if (pk.T == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = 1.f;
+    return;
+  }
+  const uint4 w = philox4x32_10(g, pk);
+  const uint32_t T16 = pk.T << 16;
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    m[2 * i] = (wv[i] << 16) >= T16 ? pk.scale : 0.f;
+    m[2 * i + 1] = wv[i] >= T16 ? pk.scale : 0.f;
+  }
+}
+
+// v[j] = keep_j ? v[j] * scale : 0
+__device__ __forceinline__ void dropout8(float v[8], uint64_t g, const PhiloxKey& pk) {
+  if (pk.T == 0) return;
+  float m[8];
+  keep_mul8(g, pk, m);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] *= m[j];
 }
 
 // ---------------------------------------------------------------- warp reductions

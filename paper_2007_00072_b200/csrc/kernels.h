@@ -18,6 +18,18 @@
     else { constexpr int CPL = 16; __VA_ARGS__; }                 \
   } while (0)
 
+// Same, capped at 8 chunks per lane (rows up to 2048 elements); larger rows return
+// cudaErrorInvalidValue (the C ABI rejects them first with ENC_EUNSUPPORTED).
+#define ENC_CPL_DISPATCH8(nc, ...)                         \
+  do {                                                     \
+    const int _cpl = ((nc) + 31) / 32;                     \
+    if (_cpl <= 1) { constexpr int CPL = 1; __VA_ARGS__; }        \
+    else if (_cpl <= 2) { constexpr int CPL = 2; __VA_ARGS__; }   \
+    else if (_cpl <= 4) { constexpr int CPL = 4; __VA_ARGS__; }   \
+    else if (_cpl <= 8) { constexpr int CPL = 8; __VA_ARGS__; }   \
+    else return cudaErrorInvalidValue;                     \
+  } while (0)
+
 namespace enc {
 
 // Deterministic column-reduction workspace (owned by enc_ctx).
@@ -32,6 +44,7 @@ PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq);
 // dtype: 0 = bf16, 1 = fp32 (enc_dtype).  All return cudaSuccess or the launch error;
 // shape support is checked by the caller (api.cu) through *_supported().
 bool rowop_supported(int n_per_row);  // BSB (K), BDRLN (I): chunks-per-lane variants
+bool bdrln_bwd_supported(int I, int dtype);  // shared-memory ring fits
 
 cudaError_t launch_dropout_mask(int64_t n, int64_t index0, const PhiloxKey& pk, uint8_t* keep,
                                 cudaStream_t st);

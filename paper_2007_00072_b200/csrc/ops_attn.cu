@@ -17,10 +17,18 @@ PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq) {
   const double T = floor((double)p * 65536.0 + 0.5);   // fp64 on the host (R5)
   k.T = (uint32_t)T;
   k.scale = (float)(65536.0 / (65536.0 - T));          // correctly rounded to fp32
-  k.k0 = (uint32_t)seed;
-  k.k1 = (uint32_t)(seed >> 32);
-  k.s0 = (uint32_t)subseq;
-  k.s1 = (uint32_t)(subseq >> 32);
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    k.rk0[r] = k0;
+    k.rk1[r] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  const uint32_t s0 = (uint32_t)subseq, s1 = (uint32_t)(subseq >> 32);
+  const uint64_t m1s0 = (uint64_t)0xCD9E8D57u * s0;
+  k.a0 = (uint32_t)(m1s0 >> 32) ^ k.rk0[0];
+  k.l1 = (uint32_t)m1s0;
+  k.b0 = s1 ^ k.rk1[0];
   return k;
 }
 
@@ -59,6 +67,7 @@ __global__ void __launch_bounds__(256) aib_fwd_kernel(const T* __restrict__ qkv,
                                                       int J, int H, int P) {
   const int I = H * P;
   const int nc3 = (3 * I) >> 3;
+#pragma unroll 2
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t bj = c / nc3;
@@ -120,14 +129,29 @@ __global__ void __launch_bounds__(128) aib_bwd_kernel(const T* __restrict__ dq,
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
   const int r0 = blockIdx.y * rpb;
   const int r1 = min(rows, r0 + rpb);
-  for (int r = r0; r < r1; ++r) {
-    const int b = r / J;
-    const int j = r - b * J;
-    float x[8];
-    Chunk<T>::load_cs(src + ((((int64_t)b * H + h) * J + j) * P + p0), x);
-    Chunk<T>::store(dqkv + (int64_t)r * 3 * I + col, x);
+  constexpr int kU = 8;  // rows in flight per thread
+  for (int rb = r0; rb < r1; rb += kU) {
+    typename Chunk<T>::Raw raw[kU];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc[i] += x[i];
+    for (int u = 0; u < kU; ++u) {
+      const int r = rb + u;
+      if (r < r1) {
+        const int b = r / J;
+        const int j = r - b * J;
+        raw[u] = Chunk<T>::ld(src + ((((int64_t)b * H + h) * J + j) * P + p0));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int r = rb + u;
+      if (r < r1) {
+        float x[8];
+        Chunk<T>::unpack(raw[u], x);
+        Chunk<T>::store(dqkv + (int64_t)r * 3 * I + col, x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
+      }
+    }
   }
   float* out = partials + (int64_t)blockIdx.y * 3 * I + col;
   reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -176,19 +200,24 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
                                                       T* __restrict__ Aout, int64_t rows,
                                                       int K, int HJ, float c, int64_t g0,
                                                       PhiloxKey pk) {
+  using Cv = Chunk<T>;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int nc = K >> 3;
   const T* s = S + row * K;
   const float* m = M ? M + (row / HJ) * K : nullptr;
+  typename Cv::Raw raw[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i)
+    if (lane + 32 * i < nc) raw[i] = Cv::ld(s + (lane + 32 * i) * 8);
   float v[CPL][8];
   float mx = -INFINITY;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
     const int ch = lane + 32 * i;
     if (ch < nc) {
-      Chunk<T>::load_cs(s + ch * 8, v[i]);
+      Cv::unpack(raw[i], v[i]);
       if (m) {
         float mb[8];
         load_f32x8(m + ch * 8, mb);
@@ -221,14 +250,11 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
   for (int i = 0; i < CPL; ++i) {
     const int ch = lane + 32 * i;
     if (ch < nc) {
-      float p[8], a[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) p[j] = v[i][j] * inv;
-      Chunk<T>::store(Pout + row * K + ch * 8, p);
-      const uint32_t kb = keep_bits8((uint64_t)(gbase + ch), pk);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) a[j] = ((kb >> j) & 1u) ? p[j] * pk.scale : 0.f;
-      Chunk<T>::store(Aout + row * K + ch * 8, a);
+      for (int j = 0; j < 8; ++j) v[i][j] *= inv;
+      Cv::store(Pout + row * K + ch * 8, v[i]);
+      dropout8(v[i], (uint64_t)(gbase + ch), pk);
+      Cv::store(Aout + row * K + ch * 8, v[i]);
     }
   }
 }
@@ -239,25 +265,33 @@ __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
                                                       const T* __restrict__ Pin,
                                                       T* __restrict__ dS, int64_t rows, int K,
                                                       float scale, int64_t g0, PhiloxKey pk) {
+  using Cv = Chunk<T>;
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int nc = K >> 3;
-  float dp[CPL][8], p[CPL][8];
+  typename Cv::Raw ra[CPL], rp[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      ra[i] = Cv::ld(dA + row * K + ch * 8);
+      rp[i] = Cv::ld(Pin + row * K + ch * 8);
+    }
+  }
+  float dp[CPL][8];
   float dot = 0.f;
   const int64_t gbase = g0 + row * nc;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
     const int ch = lane + 32 * i;
     if (ch < nc) {
-      Chunk<T>::load_cs(dA + row * K + ch * 8, dp[i]);
-      Chunk<T>::load_cs(Pin + row * K + ch * 8, p[i]);
-      const uint32_t kb = keep_bits8((uint64_t)(gbase + ch), pk);
+      float p[8];
+      Cv::unpack(ra[i], dp[i]);
+      Cv::unpack(rp[i], p);
+      dropout8(dp[i], (uint64_t)(gbase + ch), pk);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        dp[i][j] = ((kb >> j) & 1u) ? dp[i][j] * pk.scale : 0.f;
-        dot = fmaf(dp[i][j], p[i][j], dot);
-      }
+      for (int j = 0; j < 8; ++j) dot = fmaf(dp[i][j], p[j], dot);
     }
   }
   dot = warp_sum(dot);
@@ -265,10 +299,11 @@ __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
   for (int i = 0; i < CPL; ++i) {
     const int ch = lane + 32 * i;
     if (ch < nc) {
-      float o[8];
+      float p[8], o[8];
+      Cv::unpack(rp[i], p);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) o[j] = scale * p[i][j] * (dp[i][j] - dot);
-      Chunk<T>::store(dS + row * K + ch * 8, o);
+      for (int j = 0; j < 8; ++j) o[j] = scale * p[j] * (dp[i][j] - dot);
+      Cv::store(dS + row * K + ch * 8, o);
     }
   }
 }

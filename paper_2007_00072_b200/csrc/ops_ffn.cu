@@ -14,11 +14,35 @@ namespace enc {
 
 enum { kActGeluErf = 0, kActGeluTanh = 1, kActRelu = 2 };
 
+// GELU-erf without erff: Abramowitz & Stegun 7.1.26, erf(x) = 1 - poly(t) e^{-x^2},
+// t = 1/(1 + p x), |error| <= 1.5e-7 (below fp32 resolution of 1 + erf).  With
+// x = |h|/sqrt(2), e^{-x^2} = e^{-h^2/2} is also the Gaussian density's exponential, so
+// GELU and GELU' share one MUFU.EX2 and one MUFU.RCP.
+struct GeluErfParts {
+  float cdf2;  // 1 + erf(h / sqrt 2)  (= 2 Phi(h))
+  float e;     // exp(-h^2 / 2)
+};
+__device__ __forceinline__ GeluErfParts gelu_erf_parts(float h) {
+  const float x = fabsf(h) * 0.70710678118654752f;
+  const float t = __frcp_rn(fmaf(0.3275911f, x, 1.f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float e = exp2f(-0.72134752044448170f * h * h);  // e^{-h^2/2}
+  const float erf_abs = fmaf(-p, e, 1.f);
+  GeluErfParts r;
+  r.cdf2 = 1.f + copysignf(erf_abs, h);
+  r.e = e;
+  return r;
+}
+
 template <int ACT>
 __device__ __forceinline__ float act_f(float h) {
-  if (ACT == kActGeluErf) return 0.5f * h * (1.f + erff(h * 0.70710678118654752f));
+  if (ACT == kActGeluErf) return 0.5f * h * gelu_erf_parts(h).cdf2;
   if (ACT == kActGeluTanh) {
-    const float u = 0.7978845608028654f * (h + 0.044715f * h * h * h);
+    const float u = 0.7978845608028654f * fmaf(0.044715f * h, h * h, h);
     return 0.5f * h * (1.f + tanhf(u));
   }
   return h > 0.f ? h : 0.f;
@@ -26,12 +50,13 @@ __device__ __forceinline__ float act_f(float h) {
 
 template <int ACT>
 __device__ __forceinline__ float act_df(float h) {
-  if (ACT == kActGeluErf)
-    return 0.5f * (1.f + erff(h * 0.70710678118654752f)) +
-           h * 0.3989422804014327f * __expf(-0.5f * h * h);
+  if (ACT == kActGeluErf) {
+    const GeluErfParts g = gelu_erf_parts(h);
+    return fmaf(h * 0.3989422804014327f, g.e, 0.5f * g.cdf2);  // Phi(h) + h phi(h)
+  }
   if (ACT == kActGeluTanh) {
     const float c = 0.7978845608028654f;
-    const float t = tanhf(c * (h + 0.044715f * h * h * h));
+    const float t = tanhf(c * fmaf(0.044715f * h, h * h, h));
     return 0.5f * (1.f + t) + 0.5f * h * (1.f - t * t) * c * (1.f + 3.f * 0.044715f * h * h);
   }
   return h > 0.f ? 1.f : 0.f;
@@ -44,28 +69,41 @@ __global__ void __launch_bounds__(256) bad_fwd_kernel(const T* __restrict__ Y1,
                                                       T* __restrict__ h_out,
                                                       T* __restrict__ A1, int64_t nchunks,
                                                       int ncU, int64_t g0, PhiloxKey pk) {
-  for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
-       c += (int64_t)gridDim.x * blockDim.x) {
-    const int col = (int)(c % ncU) << 3;
-    float y[8], b[8], a[8];
-    Chunk<T>::load_cs(Y1 + c * 8, y);
-    load_f32x8(b1 + col, b);
-    const uint32_t kb = keep_bits8((uint64_t)(g0 + c), pk);
+  constexpr int kU = 2;  // chunks in flight per thread
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c0 < nchunks;
+       c0 += kU * stride) {
+    typename Chunk<T>::Raw raw[kU];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      y[j] += b[j];
-      a[j] = ((kb >> j) & 1u) ? act_f<ACT>(y[j]) * pk.scale : 0.f;
+    for (int u = 0; u < kU; ++u)
+      if (c0 + u * stride < nchunks) raw[u] = Chunk<T>::ld(Y1 + (c0 + u * stride) * 8);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t c = c0 + u * stride;
+      if (c < nchunks) {
+        const int col = (int)(c % ncU) << 3;
+        float y[8], b[8], a[8];
+        Chunk<T>::unpack(raw[u], y);
+        load_f32x8(b1 + col, b);
+        float m[8];
+        keep_mul8((uint64_t)(g0 + c), pk, m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          y[j] += b[j];
+          a[j] = act_f<ACT>(y[j]) * m[j];
+        }
+        Chunk<T>::store(h_out + c * 8, y);
+        Chunk<T>::store(A1 + c * 8, a);
+      }
     }
-    Chunk<T>::store(h_out + c * 8, y);
-    Chunk<T>::store(A1 + c * 8, a);
   }
 }
 
-#define ENC_ACT_DISPATCH(act, ...)                                      \
-  do {                                                                   \
+#define ENC_ACT_DISPATCH(act, ...)                                                \
+  do {                                                                            \
     if ((act) == kActGeluErf) { constexpr int ACT = kActGeluErf; __VA_ARGS__; }   \
     else if ((act) == kActGeluTanh) { constexpr int ACT = kActGeluTanh; __VA_ARGS__; } \
-    else { constexpr int ACT = kActRelu; __VA_ARGS__; }                         \
+    else { constexpr int ACT = kActRelu; __VA_ARGS__; }                           \
   } while (0)
 
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
@@ -75,8 +113,8 @@ cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const
   if (n == 0) return cudaSuccess;
   const int ncU = U / 8;
   const int64_t g0 = batch_offset * (int64_t)J * ncU;
-  int64_t grid = (n + 255) / 256;
-  if (grid > 148 * 16) grid = 148 * 16;
+  int64_t grid = (n + 511) / 512;
+  if (grid > 148 * 8) grid = 148 * 8;
   ENC_ACT_DISPATCH(act, {
     if (dtype == 0)
       bad_fwd_kernel<__nv_bfloat16, ACT><<<(int)grid, 256, 0, st>>>(
@@ -104,19 +142,34 @@ __global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
   const int r0 = blockIdx.y * rpb;
   const int r1 = min(rows, r0 + rpb);
-#pragma unroll 2
-  for (int r = r0; r < r1; ++r) {
-    const int64_t off = (int64_t)r * U + col;
-    float d[8], x[8];
-    Chunk<T>::load_cs(dA1 + off, d);
-    Chunk<T>::load_cs(h + off, x);
-    const uint32_t kb = keep_bits8((uint64_t)(g0 + (int64_t)r * ncU + ch), pk);
+  constexpr int kU = 4;  // rows in flight per thread
+  for (int rb = r0; rb < r1; rb += kU) {
+    typename Chunk<T>::Raw rd[kU], rh[kU];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      d[j] = ((kb >> j) & 1u) ? d[j] * pk.scale * act_df<ACT>(x[j]) : 0.f;
-      acc[j] += d[j];
+    for (int u = 0; u < kU; ++u) {
+      if (rb + u < r1) {
+        const int64_t off = (int64_t)(rb + u) * U + col;
+        rd[u] = Chunk<T>::ld(dA1 + off);
+        rh[u] = Chunk<T>::ld(h + off);
+      }
     }
-    Chunk<T>::store(dh + off, d);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int r = rb + u;
+      if (r < r1) {
+        float d[8], x[8];
+        Chunk<T>::unpack(rd[u], d);
+        Chunk<T>::unpack(rh[u], x);
+        float m[8];
+        keep_mul8((uint64_t)(g0 + (int64_t)r * ncU + ch), pk, m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d[j] = d[j] * m[j] * act_df<ACT>(x[j]);
+          acc[j] += d[j];
+        }
+        Chunk<T>::store(dh + (int64_t)r * U + col, d);
+      }
+    }
   }
   float* out = partials + (int64_t)blockIdx.y * U + col;
   reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
@@ -131,7 +184,7 @@ cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, cons
   const int ncU = U / 8;
   const int64_t g0 = batch_offset * (int64_t)J * ncU;
   const int gx = (ncU + 127) / 128;
-  int R = (4 * ws.num_sms + gx - 1) / gx;
+  int R = (8 * ws.num_sms + gx - 1) / gx;
   const size_t cap = ws.cap_floats / (size_t)U;
   if ((size_t)R > cap) R = (int)cap;
   if (R > rows) R = rows;

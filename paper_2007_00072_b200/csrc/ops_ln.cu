@@ -11,6 +11,7 @@
 #include <math.h>
 
 #include "kernels.h"
+#include "tma.cuh"
 
 namespace enc {
 
@@ -21,11 +22,22 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
     PhiloxKey pk) {
+  using C = Chunk<T>;
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= rows) return;
   const int nc = I >> 3;
   const int64_t base = (int64_t)row * I;
+  // all loads of the row first (2*CPL 16/32-byte loads in flight per lane)
+  typename C::Raw ry[CPL], rr[CPL];
+#pragma unroll
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      ry[i] = C::ld(Y + base + ch * 8);
+      rr[i] = C::ld(R + base + ch * 8);
+    }
+  }
   float z[CPL][8];
   float sum = 0.f;
 #pragma unroll
@@ -33,13 +45,14 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
     const int ch = lane + 32 * i;
     if (ch < nc) {
       float y[8], b[8];
-      Chunk<T>::load_cs(Y + base + ch * 8, y);
-      Chunk<T>::load_cs(R + base + ch * 8, z[i]);
+      C::unpack(ry[i], y);
+      C::unpack(rr[i], z[i]);
       load_f32x8(bias + ch * 8, b);
-      const uint32_t kb = keep_bits8((uint64_t)(g0 + (int64_t)row * nc + ch), pk);
+      float m[8];
+      keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        z[i][j] += ((kb >> j) & 1u) ? (y[j] + b[j]) * pk.scale : 0.f;
+        z[i][j] = fmaf(y[j] + b[j], m[j], z[i][j]);
         sum += z[i][j];
       }
     }
@@ -71,8 +84,8 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
         xh[j] = (z[i][j] - mean) * rstd;
         o[j] = fmaf(g[j], xh[j], be[j]);
       }
-      Chunk<T>::store(out + base + ch * 8, o);
-      Chunk<T>::store(xhat + base + ch * 8, xh);
+      C::store(out + base + ch * 8, o);
+      C::store(xhat + base + ch * 8, xh);
     }
   }
   if (lane == 0) rstd_out[row] = rstd;
@@ -101,17 +114,47 @@ cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, cons
 }
 
 // ------------------------------------------------------------------ BDRLN backward
+// Persistent: one CTA of 8 warps per SM, warp w of CTA c takes rows c*8+w, +8G, ...
+// Each warp streams its rows through a 2-stage shared-memory ring filled by the bulk-copy
+// (TMA) engine -- the next row's dOut and xhat land while the current one is computed,
+// so a warp keeps two rows in flight without spending registers on them (the registers
+// hold the three column-sum accumulators instead).
 constexpr int kLnBwdWarps = 8;
+constexpr int kLnBwdMaxSmem = 200 * 1024;
 
 template <typename T, int CPL>
-__global__ void __launch_bounds__(256) bdrln_bwd_kernel(
+__global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
-    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk) {
-  extern __shared__ float red[];  // [3][I]
+    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk, int kLnBwdStages) {
+  using C = Chunk<T>;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nc = I >> 3;
+  const uint32_t row_bytes = (uint32_t)I * sizeof(T);
+  // layout: [warp][stage][2 tensors][I] T | mbar[warp][stage] | red[3][I] float
+  T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * kLnBwdStages * 2 * I;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kLnBwdWarps * kLnBwdStages * 2 * row_bytes);
+  uint64_t* bar = bars + warp * kLnBwdStages;
+  float* red = reinterpret_cast<float*>(bars + kLnBwdWarps * kLnBwdStages);
+
+  const int stride = gridDim.x * kLnBwdWarps;
+  const int first = blockIdx.x * kLnBwdWarps + warp;
+  if (lane == 0) {
+    for (int s = 0; s < kLnBwdStages; ++s) mbar_init(&bar[s], 1);  // (1 or 2 stages)
+    fence_mbar_init();
+    for (int s = 0; s < kLnBwdStages; ++s) {
+      const int r = first + s * stride;
+      if (r < rows) {
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring + (s * 2 + 0) * I, dOut + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring + (s * 2 + 1) * I, xhat + (int64_t)r * I, row_bytes, &bar[s]);
+      }
+    }
+  }
+  __syncwarp();
+
   const float inv_n = 1.f / (float)I;
   float acc_g[CPL][8], acc_b[CPL][8], acc_d[CPL][8];
 #pragma unroll
@@ -119,8 +162,32 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
 #pragma unroll
     for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
 
-  const int stride = gridDim.x * kLnBwdWarps;
-  for (int row = blockIdx.x * kLnBwdWarps + warp; row < rows; row += stride) {
+  int k = 0;
+  for (int row = first; row < rows; row += stride, ++k) {
+    const int s = k % kLnBwdStages;
+    mbar_wait(&bar[s], (uint32_t)(k / kLnBwdStages) & 1u);
+    const T* sg = ring + (s * 2 + 0) * I;
+    const T* sx = ring + (s * 2 + 1) * I;
+    typename C::Raw rg[CPL], rx[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) {
+      const int ch = lane + 32 * i;
+      if (ch < nc) {
+        rg[i] = C::ld_smem(sg + ch * 8);
+        rx[i] = C::ld_smem(sx + ch * 8);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {  // refill this stage with the row kStages ahead
+      const int nr = row + kLnBwdStages * stride;
+      if (nr < rows) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring + (s * 2 + 0) * I, dOut + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring + (s * 2 + 1) * I, xhat + (int64_t)nr * I, row_bytes, &bar[s]);
+      }
+    }
+    const float rs = __ldg(rstd + row);
     const int64_t base = (int64_t)row * I;
     float go[CPL][8], xh[CPL][8];
     float s1 = 0.f, s2 = 0.f;
@@ -129,8 +196,8 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
       const int ch = lane + 32 * i;
       if (ch < nc) {
         float gm[8];
-        Chunk<T>::load_cs(dOut + base + ch * 8, go[i]);
-        Chunk<T>::load_cs(xhat + base + ch * 8, xh[i]);
+        C::unpack(rg[i], go[i]);
+        C::unpack(rx[i], xh[i]);
         load_f32x8(gamma + ch * 8, gm);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -144,21 +211,20 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
     }
     const float mg = warp_sum(s1) * inv_n;
     const float mgx = warp_sum(s2) * inv_n;
-    const float rs = __ldg(rstd + row);
 #pragma unroll
     for (int i = 0; i < CPL; ++i) {
       const int ch = lane + 32 * i;
       if (ch < nc) {
-        float d[8], y[8];
-        const uint32_t kb = keep_bits8((uint64_t)(g0 + (int64_t)row * nc + ch), pk);
+        float d[8], y[8], m[8];
+        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           d[j] = rs * (go[i][j] - mg - xh[i][j] * mgx);
-          y[j] = ((kb >> j) & 1u) ? d[j] * pk.scale : 0.f;
+          y[j] = d[j] * m[j];
           acc_d[i][j] += y[j];
         }
-        Chunk<T>::store(dz + base + ch * 8, d);
-        Chunk<T>::store(dYpre + base + ch * 8, y);
+        C::store(dz + base + ch * 8, d);
+        C::store(dYpre + base + ch * 8, y);
       }
     }
   }
@@ -191,6 +257,23 @@ __global__ void __launch_bounds__(256) bdrln_bwd_kernel(
   for (int c = threadIdx.x; c < 3 * I; c += blockDim.x) out[c] = red[c];
 }
 
+static size_t bdrln_bwd_smem(int I, size_t es, int stages) {
+  return (size_t)kLnBwdWarps * stages * 2 * I * es + sizeof(uint64_t) * kLnBwdWarps * stages +
+         sizeof(float) * 3 * I;
+}
+
+// 2-stage ring when it fits, else 1 stage; rows up to 2048 elements (8 chunks per lane)
+static int bdrln_bwd_stages(int I, int dtype) {
+  const size_t es = dtype == 0 ? 2 : 4;
+  if (bdrln_bwd_smem(I, es, 2) <= kLnBwdMaxSmem) return 2;
+  if (bdrln_bwd_smem(I, es, 1) <= kLnBwdMaxSmem) return 1;
+  return 0;
+}
+
+bool bdrln_bwd_supported(int I, int dtype) {
+  return rowop_supported(I) && I <= 2048 && bdrln_bwd_stages(I, dtype) > 0;
+}
+
 cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, const void* xhat,
                              const float* rstd, const float* gamma, const PhiloxKey& pk,
                              int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
@@ -203,25 +286,29 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
   }
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
-  // ~2 rows per warp: enough CTAs to cover every SM, few partial rows
-  int G = (rows + 2 * kLnBwdWarps - 1) / (2 * kLnBwdWarps);
-  if (G > 2 * ws.num_sms) G = 2 * ws.num_sms;
+  int G = (rows + kLnBwdWarps - 1) / kLnBwdWarps;
+  if (G > ws.num_sms) G = ws.num_sms;
   const size_t cap = ws.cap_floats / (size_t)(3 * I);
   if ((size_t)G > cap) G = (int)cap;
   if (G < 1) G = 1;
-  const size_t smem = sizeof(float) * 3 * I;
-  ENC_CPL_DISPATCH(nc, {
-    if (dtype == 0) {
-      auto kern = bdrln_bwd_kernel<__nv_bfloat16, CPL>;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<G, 256, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat, rstd,
-                                 gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre, ws.partials,
-                                 rows, I, g0, pk);
-    } else {
-      auto kern = bdrln_bwd_kernel<float, CPL>;
-      if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      kern<<<G, 256, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
-                                 (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
+  const int stages = bdrln_bwd_stages(I, dtype);
+  if (stages == 0) return cudaErrorInvalidValue;
+  const size_t smem = bdrln_bwd_smem(I, dtype == 0 ? 2 : 4, stages);
+  ENC_CPL_DISPATCH8(nc, {
+    {
+      if (dtype == 0) {
+        auto kern = bdrln_bwd_kernel<__nv_bfloat16, CPL>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<G, kLnBwdWarps * 32, smem, st>>>(
+            (const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat, rstd, gamma,
+            (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, stages);
+      } else {
+        auto kern = bdrln_bwd_kernel<float, CPL>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<G, kLnBwdWarps * 32, smem, st>>>((const float*)dOut, (const float*)xhat, rstd,
+                                                gamma, (float*)dz, (float*)dYpre, ws.partials,
+                                                rows, I, g0, pk, stages);
+      }
     }
   });
   cudaError_t e = cudaGetLastError();

@@ -168,3 +168,22 @@ class EncoderLayer:
             nbytes = numel * torch.empty((), dtype=dt).element_size()
             out[n] = self.saved[off:off + nbytes].view(dt).view(shapes[n])
         return out
+
+    def bwd_views(self) -> dict:
+        """Backward temporaries in `scratch` (valid after backward())."""
+        v = _abi.enc_bwd_view()
+        check("enc_bwd_views", self.lib.enc_bwd_views(ctypes.byref(self.dims), self.adt,
+                                                      self.scratch.data_ptr(), ctypes.byref(v)))
+        B, J, H, P, I, U = self.B, self.J, self.H, self.P, self.I, self.U
+        shapes = {"dY2": (B, J, I), "dA1": (B, J, U), "dh": (B, J, U), "dX1": (B, J, I),
+                  "dYo": (B, J, I), "dC": (B, J, I), "dA": (B, H, J, J), "dS": (B, H, J, J),
+                  "dQ": (B, H, J, P), "dK": (B, H, J, P), "dV": (B, H, J, P),
+                  "dQKV": (B, J, 3 * I)}
+        base = self.scratch.data_ptr()
+        es = torch.empty((), dtype=self.tdt).element_size()
+        out = {}
+        for n in _abi.BWD_FIELDS:
+            off = getattr(v, n) - base
+            numel = int(np.prod(shapes[n]))
+            out[n] = self.scratch[off:off + numel * es].view(self.tdt).view(shapes[n])
+        return out

@@ -1,6 +1,13 @@
 """Whole-layer parity: encoder_layer_forward / encoder_layer_backward through the C ABI vs
-the fp64 oracle on the same seeded inputs (configs T, a small bf16 case, and the paper's
-BERT-large layer L at full size)."""
+the fp64 oracle on the same seeded inputs.
+
+* fp32 path (TF32 off): end to end against the oracle, configs T and the paper's BERT-large
+  layer L at full size, 1e-5 normwise relative (R14).
+* bf16 path: stage by stage (R14) -- every stage's GPU output against the oracle
+  stage applied to the GPU's own stored bf16 inputs of that stage (forward from the saved
+  set, backward from the saved set and the backward temporaries), so the check isolates the
+  implementation from the conditioning of bf16 storage; end-to-end bf16 errors are printed.
+"""
 import numpy as np
 import pytest
 import torch
@@ -15,7 +22,11 @@ ACT = {"gelu": E.ACT_GELU_ERF, "gelu_tanh": E.ACT_GELU_TANH, "relu": E.ACT_RELU}
 TDT = {"bf16": torch.bfloat16, "fp32": torch.float32}
 
 
-def _run(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weight_std=0.02):
+def f64(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _setup(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weight_std=0.02):
     from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
     prm = make_params(dims, dtype, "parity", weight_std=weight_std)
     inp = make_inputs(dims, dtype, key_padding=key_padding)
@@ -31,54 +42,147 @@ def _run(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weigh
     torch.cuda.synchronize()
     ocfg = E.Cfg(p_attn=p, p_hidden=p, p_ffn=p, act=ACT[act], layer_id=layer_id,
                  batch_offset=batch_offset)
+    return layer, prm, inp, ocfg, f64(Y), f64(dX)
+
+
+def _end_to_end(dims, dtype, act, key_padding, **kw):
+    layer, prm, inp, ocfg, Y, dX = _setup(dims, dtype, act, key_padding, **kw)
     Yo, sv = E.encoder_layer_forward(inp["X"], prm, dims.H, ocfg, inp["mask_bias"])
-    dXo, go, inter = E.encoder_layer_backward(inp["dY"], inp["X"], prm, dims.H, ocfg, sv)
-    f = lambda t: t.float().cpu().numpy().astype(np.float64)  # noqa: E731
-    gpu = {"Y": f(Y), "dX": f(dX)}
+    dXo, go, _ = E.encoder_layer_backward(inp["dY"], inp["X"], prm, dims.H, ocfg, sv)
+    gpu = {"Y": Y, "dX": dX}
     ref = {"Y": Yo, "dX": dXo}
     for n in go:
-        gpu["d" + n] = f(layer.grads[n])
+        gpu["d" + n] = f64(layer.grads[n])
         ref["d" + n] = go[n]
-    sv_gpu = layer.saved_views()
+    s = layer.saved_views()
     for n in ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2"):
-        gpu["saved." + n] = f(sv_gpu[n])
+        gpu["saved." + n] = f64(s[n])
         ref["saved." + n] = sv[n]
     return gpu, ref
 
 
+def _stagewise(dims, dtype, act, key_padding, **kw):
+    """(gpu, ref) pairs of every stage, the oracle fed with the GPU's stored inputs."""
+    layer, prm, inp, ocfg, Y, dX = _setup(dims, dtype, act, key_padding, **kw)
+    B, J, H, P, I = dims.B, dims.J, dims.H, dims.P, dims.I
+    sub = lambda site: 4 * ocfg.layer_id + site  # noqa: E731
+    sc, boff, seed = 1.0 / np.sqrt(P), ocfg.batch_offset, ocfg.seed
+    W = {k: np.asarray(v, np.float64) for k, v in prm.items()}
+    X = np.asarray(inp["X"], np.float64)
+    dY = np.asarray(inp["dY"], np.float64)
+    s = {k: f64(v) for k, v in layer.saved_views().items()}
+    b = {k: f64(v) for k, v in layer.bwd_views().items()}
+    g = {k: f64(v) for k, v in layer.grads.items()}
+    pairs = []
+    # ---- forward
+    QKV = X @ W["Wqkv"].T
+    Qo, Ko, Vo = E.aib_fwd(QKV, W["bqkv"], H, P)
+    pairs += [("Q", s["Q"], Qo), ("K", s["K"], Ko), ("V", s["V"], Vo)]
+    Po, Ao = E.bsb_fwd(s["Q"] @ s["K"].transpose(0, 1, 3, 2), inp["mask_bias"], sc,
+                       ocfg.p_attn, seed, sub(0), boff)
+    pairs += [("P", s["P"], Po), ("A", s["A"], Ao)]
+    Co = (s["A"] @ s["V"]).transpose(0, 2, 1, 3).reshape(B, J, I)
+    pairs += [("C", s["C"], Co)]
+    X1o, xh1o, r1o = E.bdrln_fwd(s["C"] @ W["Wo"].T, W["bo"], X, W["g1"], W["be1"],
+                                 ocfg.ln_eps, ocfg.p_hidden, seed, sub(1), boff)
+    pairs += [("X1", s["X1"], X1o), ("xhat1", s["xhat1"], xh1o)]
+    ho, A1o = E.bad_fwd(s["X1"] @ W["W1"].T, W["b1"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
+    pairs += [("h", s["h"], ho), ("A1", s["A1"], A1o)]
+    Yo, xh2o, r2o = E.bdrln_fwd(s["A1"] @ W["W2"].T, W["b2"], s["X1"], W["g2"], W["be2"],
+                                ocfg.ln_eps, ocfg.p_hidden, seed, sub(3), boff)
+    pairs += [("Y", Y, Yo), ("xhat2", s["xhat2"], xh2o)]
+    fp32_pairs = [("rstd1", s["rstd1"], r1o), ("rstd2", s["rstd2"], r2o)]
+    # ---- backward
+    dz2o, dY2o, dg2o, dbe2o, db2o = E.bdrln_bwd(dY, s["xhat2"], s["rstd2"], W["g2"],
+                                                ocfg.p_hidden, seed, sub(3), boff)
+    pairs += [("dY2", b["dY2"], dY2o), ("dg2", g["g2"], dg2o), ("dbe2", g["be2"], dbe2o),
+              ("db2", g["b2"], db2o)]
+    pairs += [("dA1", b["dA1"], b["dY2"] @ W["W2"]),
+              ("dW2", g["W2"], np.einsum("bji,bju->iu", b["dY2"], s["A1"]))]
+    dho, db1o = E.bad_bwd(b["dA1"], s["h"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
+    pairs += [("dh", b["dh"], dho), ("db1", g["b1"], db1o)]
+    pairs += [("dX1", b["dX1"], b["dh"] @ W["W1"] + dz2o),
+              ("dW1", g["W1"], np.einsum("bju,bji->ui", b["dh"], s["X1"]))]
+    dz1o, dYoo, dg1o, dbe1o, dboo = E.bdrln_bwd(b["dX1"], s["xhat1"], s["rstd1"], W["g1"],
+                                                ocfg.p_hidden, seed, sub(1), boff)
+    pairs += [("dYo", b["dYo"], dYoo), ("dg1", g["g1"], dg1o), ("dbe1", g["be1"], dbe1o),
+              ("dbo", g["bo"], dboo)]
+    pairs += [("dC", b["dC"], b["dYo"] @ W["Wo"]),
+              ("dWo", g["Wo"], np.einsum("bji,bjk->ik", b["dYo"], s["C"]))]
+    dCbh = b["dC"].reshape(B, J, H, P).transpose(0, 2, 1, 3)
+    pairs += [("dA", b["dA"], dCbh @ s["V"].transpose(0, 1, 3, 2)),
+              ("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
+    pairs += [("dS", b["dS"], E.bsb_bwd(b["dA"], s["P"], sc, ocfg.p_attn, seed, sub(0), boff))]
+    pairs += [("dQ", b["dQ"], b["dS"] @ s["K"]),
+              ("dK", b["dK"], b["dS"].transpose(0, 1, 3, 2) @ s["Q"])]
+    dQKVo, dbqkvo = E.aib_bwd(b["dQ"], b["dK"], b["dV"])
+    pairs += [("dQKV", b["dQKV"], dQKVo), ("dbqkv", g["bqkv"], dbqkvo)]
+    pairs += [("dX", dX, b["dQKV"] @ W["Wqkv"] + dz1o),
+              ("dWqkv", g["Wqkv"], np.einsum("bjo,bji->oi", b["dQKV"], X))]
+    return pairs, fp32_pairs
+
+
 @pytest.mark.parametrize("act", ["gelu", "relu", "gelu_tanh"])
 def test_layer_T_fp32(act):
-    gpu, ref = _run(CONFIGS["T"], "fp32", act, key_padding=True, weight_std=0.2)
+    gpu, ref = _end_to_end(CONFIGS["T"], "fp32", act, key_padding=True, weight_std=0.2)
     for n in gpu:
         assert_parity(n, gpu[n], ref[n], "fp32")
 
 
 def test_layer_T_fp32_batch_offset_and_layer_id():
-    gpu, ref = _run(CONFIGS["T"], "fp32", "gelu", key_padding=False, batch_offset=6,
-                    layer_id=7, weight_std=0.2)
+    gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=False, batch_offset=6,
+                           layer_id=7, weight_std=0.2)
     for n in gpu:
         assert_parity(n, gpu[n], ref[n], "fp32")
 
 
 def test_layer_T_fp32_no_dropout():
-    gpu, ref = _run(CONFIGS["T"], "fp32", "gelu", key_padding=True, p=0.0, weight_std=0.2)
+    gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=True, p=0.0,
+                           weight_std=0.2)
     for n in gpu:
         assert_parity(n, gpu[n], ref[n], "fp32")
 
 
-def test_layer_small_bf16():
-    dims = Dims(B=2, J=64, H=4, P=16, U=256)
-    gpu, ref = _run(dims, "bf16", "gelu", key_padding=True, weight_std=0.06)
+def test_layer_L_fp32_full():
+    """The paper's BERT-large layer (B=8, J=K=512, H=16, P=64, I=1024, U=4096) end to end
+    on the fp32 path at full size: every output and saved tensor within 1e-5 normwise."""
+    gpu, ref = _end_to_end(CONFIGS["L"], "fp32", "gelu", key_padding=True)
     for n in gpu:
-        assert_parity(n, gpu[n], ref[n], "bf16")
+        e = errors(gpu[n], ref[n])
+        print(f"{n:14s} max_rel {e['max_rel']:.3e}")
+    for n in gpu:
+        assert_parity(n, gpu[n], ref[n], "fp32")
 
 
-def test_layer_L_bf16_full():
-    """The paper's BERT-large layer (B=8, J=K=512, H=16, P=64, I=1024, U=4096) at full
-    size, bf16 with fp32 accumulation/statistics, vs the fp64 oracle on the same inputs."""
-    gpu, ref = _run(CONFIGS["L"], "bf16", "gelu", key_padding=False)
-    report = {n: errors(gpu[n], ref[n]) for n in gpu}
-    for n, e in sorted(report.items()):
-        print(f"{n:14s} max/rms {e['max_over_rms']:.3e} mean_rel {e['mean_rel']:.3e}")
-    for n in gpu:
-        assert_parity(n, gpu[n], ref[n], "bf16")
+@pytest.mark.parametrize("dims,act,kp", [
+    (Dims(B=2, J=64, H=4, P=16, U=256), "gelu", True),
+    (Dims(B=3, J=40, H=2, P=24, U=96), "relu", True),
+])
+def test_layer_small_bf16_stagewise(dims, act, kp):
+    pairs, f32 = _stagewise(dims, "bf16", act, kp, weight_std=0.06)
+    for n, g, o in pairs:
+        assert_parity(n, g, o, "bf16")
+    for n, g, o in f32:   # rstd of the bf16-rounded GEMM output: bf16-level agreement
+        assert_parity(n, g, o, "bf16")
+
+
+def test_layer_L_bf16_stagewise():
+    """Config L, bf16, every stage vs the oracle on the GPU's stored inputs."""
+    pairs, f32 = _stagewise(CONFIGS["L"], "bf16", "gelu", key_padding=False)
+    for n, g, o in pairs:
+        e = errors(g, o)
+        print(f"{n:8s} mixed {e['mixed']:.3e} mean_rel {e['mean_rel']:.3e}")
+    for n, g, o in pairs:
+        assert_parity(n, g, o, "bf16")
+    for n, g, o in f32:   # rstd of the bf16-rounded GEMM output: bf16-level agreement
+        assert_parity(n, g, o, "bf16")
+
+
+def test_layer_L_bf16_end_to_end_report():
+    """End-to-end bf16 errors at config L (printed; asserted only for the layer output,
+    whose LayerNorm makes it well conditioned -- DESIGN.md R14)."""
+    gpu, ref = _end_to_end(CONFIGS["L"], "bf16", "gelu", key_padding=False)
+    for n in sorted(gpu):
+        e = errors(gpu[n], ref[n])
+        print(f"{n:14s} mixed {e['mixed']:.3e} mean_rel {e['mean_rel']:.3e}")
+    assert_parity("Y", gpu["Y"], ref["Y"], "bf16")
