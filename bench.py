@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=2)
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--attn-backend", choices=["tc", "cublas"], default="tc",
+                    help="attention contractions: hand-written tcgen05 kernels or cuBLAS")
     ap.add_argument("--eager", action="store_true",
                     help="launch every step eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -180,6 +182,8 @@ def main():
     cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff)
     layer = EncoderLayer(dims, args.dtype, cfg)
     layer.set_params(make_params(dims, args.dtype, "bench"))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 0,
+                                                            int(args.attn_backend == "tc")))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
@@ -357,7 +361,9 @@ def main():
             "config": {"workload": WORKLOAD, "global_batch": dims_global.B, "seq_len": dims.J,
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
-                       else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)"},
+                       else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)",
+                       "attention_contractions": "tcgen05 (hand-written)" if args.attn_backend == "tc"
+                       else "cuBLAS"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},

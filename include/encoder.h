@@ -236,6 +236,21 @@ int enc_bad_bwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* dA1,
                 const void* h, int act, float p, uint64_t seed, uint64_t subseq,
                 int64_t batch_offset, void* dh, float* db1, enc_stream_t stream);
 
+/* Attention contractions on the hand-written tcgen05/TMEM/TMA kernels (bf16 only;
+ * J % 128 == 0, P == 64).  which: ENC_AG_QK  S[B,H,J,K] = Q K^T (Table A.1 :551),
+ * ENC_AG_AV C[B,J,H,P] = A V (:553), ENC_AG_DA dA = dC V^T (:588, dC in [B,J,H,P]),
+ * ENC_AG_DV dV = A^T dC (:589), ENC_AG_DQ dQ = dS K (:591), ENC_AG_DK dK = dS^T Q (:592);
+ * Q, K, V, dQ, dK, dV [B,H,J,P]; S, A, dA, dS [B,H,J,K].  X, Y = the two operands in the
+ * order written, Z = the result. */
+enum { ENC_AG_QK = 0, ENC_AG_AV, ENC_AG_DA, ENC_AG_DV, ENC_AG_DQ, ENC_AG_DK };
+int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const void* X,
+                  const void* Y, void* Z, enc_stream_t stream);
+
+/* Options of a context.  ENC_OPT_ATTN_TC: 1 = the layer runs its six attention
+ * contractions on the hand-written tcgen05 kernels (default when supported), 0 = cuBLAS. */
+enum { ENC_OPT_ATTN_TC = 0 };
+int enc_set_option(enc_ctx* ctx, int key, int value);
+
 /* BEI (paper `bei`): out = a + b, n elements (out may alias a). */
 int enc_bei(enc_ctx* ctx, int dtype, int64_t n, const void* a, const void* b, void* out,
             enc_stream_t stream);

@@ -98,6 +98,9 @@ _SIGS = {
     "enc_set_timing": (c_int, [c_void_p, c_uint64]),
     "enc_op_times": (c_int, [c_void_p, POINTER(c_float)]),
     "enc_launch_count": (c_uint64, [c_void_p]),
+    "enc_attn_gemm": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                              c_void_p, c_void_p]),
+    "enc_set_option": (c_int, [c_void_p, c_int, c_int]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 

@@ -7,6 +7,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <climits>
+
 #include <new>
 
 #include "../../include/encoder.h"
@@ -29,6 +31,7 @@ struct enc_ctx {
   cudaEvent_t ev1[ENC_NUM_OPS] = {};
   bool recorded[ENC_NUM_OPS] = {};
   uint64_t launches = 0;     // kernels this library launched (excluding cuBLAS)
+  int attn_tc = 1;           // ENC_OPT_ATTN_TC
 };
 
 namespace {
@@ -192,6 +195,10 @@ static int check_dims(const enc_dims* d, int dtype) {
   if (d->I % 8 || d->U % 8 || d->K % 8 || d->P % 8) return ENC_EALIGN;
   if (!rowop_supported(d->K) || !rowop_supported(d->I)) return ENC_EUNSUPPORTED;
   if (!bdrln_bwd_supported(d->I, dtype)) return ENC_EUNSUPPORTED;
+  // chunk / row indices are 32-bit inside the kernels
+  const int64_t wide = 3 * d->I > d->U ? 3 * d->I : d->U;
+  if ((int64_t)d->B * d->J * wide / 8 >= INT32_MAX || (int64_t)d->B * d->H * d->J >= INT32_MAX)
+    return ENC_EUNSUPPORTED;
   return ENC_OK;
 }
 
@@ -339,6 +346,7 @@ static int check_bjhp(int dtype, int B, int J, int H, int P) {
   if (!valid_dtype(dtype)) return ENC_EDTYPE;
   if (B < 0 || J <= 0 || H <= 0 || P <= 0) return ENC_EINVAL;
   if (P % 8) return ENC_EALIGN;
+  if ((int64_t)B * J * 3 * H * P / 8 >= INT32_MAX) return ENC_EUNSUPPORTED;
   return ENC_OK;
 }
 
@@ -373,6 +381,7 @@ static int check_bhjk(int dtype, int B, int H, int J, int K, float p) {
   if (B < 0 || H <= 0 || J <= 0 || K <= 0 || !valid_p(p)) return ENC_EINVAL;
   if (K % 8) return ENC_EALIGN;
   if (!rowop_supported(K)) return ENC_EUNSUPPORTED;
+  if ((int64_t)B * H * J >= INT32_MAX) return ENC_EUNSUPPORTED;
   return ENC_OK;
 }
 
@@ -414,6 +423,7 @@ static int check_bjn(int dtype, int B, int J, int N, float p, bool rowop) {
   if (B < 0 || J <= 0 || N <= 0 || !valid_p(p)) return ENC_EINVAL;
   if (N % 8) return ENC_EALIGN;
   if (rowop && !rowop_supported(N)) return ENC_EUNSUPPORTED;
+  if ((int64_t)B * J * N / 8 >= INT32_MAX) return ENC_EUNSUPPORTED;
   return ENC_OK;
 }
 
@@ -486,6 +496,28 @@ int enc_bad_bwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* dA1, c
   return ENC_OK;
 }
 
+int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const void* X,
+                  const void* Y, void* Z, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (which < ENC_AG_QK || which > ENC_AG_DK || B < 0 || H <= 0 || J <= 0 || P <= 0)
+    return ENC_EINVAL;
+  if (!attn_gemm_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(X, Y, Z);
+  if (B == 0) return ENC_OK;
+  CK(launch_attn_gemm(which, B, H, J, P, X, Y, Z, (cudaStream_t)stream));
+  ctx->launches += 1;
+  return ENC_OK;
+}
+
+int enc_set_option(enc_ctx* ctx, int key, int value) {
+  if (!ctx) return ENC_ENULL;
+  if (key == ENC_OPT_ATTN_TC) {
+    ctx->attn_tc = value ? 1 : 0;
+    return ENC_OK;
+  }
+  return ENC_EINVAL;
+}
+
 int enc_bei(enc_ctx* ctx, int dtype, int64_t n, const void* a, const void* b, void* out,
             enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
@@ -535,6 +567,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   const uint64_t l4 = 4ull * cfg->layer_id;
   const float scale = 1.0f / sqrtf((float)P);  // DESIGN.md R3
   const int64_t boff = cfg->batch_offset;
+  const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
 
   // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T
   {
@@ -549,9 +582,12 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   }
   // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK, st, 0);
-    CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P, Kt, P,
-                       (long long)K * P, 0.f, S, K, (long long)J * K, BH));
+    OpTimer _t(ctx, ENC_OP_GEMM_QK, st, tc_attn ? 1 : 0);
+    if (tc_attn)
+      CK(launch_attn_gemm(ENC_AG_QK, B, H, J, P, Q, Kt, S, st));
+    else
+      CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P, Kt,
+                         P, (long long)K * P, 0.f, S, K, (long long)J * K, BH));
   }
   // BSB (:552)
   {
@@ -562,9 +598,14 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
-    CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
-    CB(gemm_rm_batched(ctx->blas, dtype, false, false, J, P, K, 1.f, (const void* const*)ptr, K,
-                       (const void* const*)(ptr + BH), P, 0.f, (void* const*)(ptr + 2 * BH), I, BH));
+    if (tc_attn) {
+      CK(launch_attn_gemm(ENC_AG_AV, B, H, J, P, A, V, C, st));
+    } else {
+      CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
+      CB(gemm_rm_batched(ctx->blas, dtype, false, false, J, P, K, 1.f, (const void* const*)ptr, K,
+                         (const void* const*)(ptr + BH), P, 0.f, (void* const*)(ptr + 2 * BH), I,
+                         BH));
+    }
   }
   // Out (:554)
   {
@@ -646,6 +687,7 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   const uint64_t l4 = 4ull * cfg->layer_id;
   const float scale = 1.0f / sqrtf((float)P);
   const int64_t boff = cfg->batch_offset;
+  const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
   const int F32 = ENC_FP32;
 
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
@@ -698,14 +740,23 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, 1);
-    CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, dC, dA, dV, ptr, st));
-    CB(gemm_rm_batched(ctx->blas, dtype, false, true, J, K, P, 1.f, (const void* const*)(ptr + 2 * BH),
-                       I, (const void* const*)(ptr + BH), P, 0.f, (void* const*)(ptr + 3 * BH), K, BH));
+    if (tc_attn) {
+      CK(launch_attn_gemm(ENC_AG_DA, B, H, J, P, dC, V, dA, st));
+    } else {
+      CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, dC, dA, dV, ptr, st));
+      CB(gemm_rm_batched(ctx->blas, dtype, false, true, J, K, P, 1.f,
+                         (const void* const*)(ptr + 2 * BH), I, (const void* const*)(ptr + BH), P,
+                         0.f, (void* const*)(ptr + 3 * BH), K, BH));
+    }
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, 0);
-    CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
-                       (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH), P, BH));
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
+    if (tc_attn)
+      CK(launch_attn_gemm(ENC_AG_DV, B, H, J, P, A, dC, dV, st));
+    else
+      CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
+                         (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH),
+                         P, BH));
   }
   // BSB-bwd (:590)
   {
@@ -715,14 +766,20 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   }
   // QK^T dX1 (:591): dQ = dS K;  dX2 (:592): dK = dS^T Q
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK_DQ, st, 0);
-    CB(gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, dS, K, (long long)J * K, Kt, P,
-                       (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DQ, st, tc_attn ? 1 : 0);
+    if (tc_attn)
+      CK(launch_attn_gemm(ENC_AG_DQ, B, H, J, P, dS, Kt, dQ, st));
+    else
+      CB(gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, dS, K, (long long)J * K, Kt,
+                         P, (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, 0);
-    CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,
-                       (long long)J * P, 0.f, dK, P, (long long)K * P, BH));
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, tc_attn ? 1 : 0);
+    if (tc_attn)
+      CK(launch_attn_gemm(ENC_AG_DK, B, H, J, P, dS, Q, dK, st));
+    else
+      CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,
+                         (long long)J * P, 0.f, dK, P, (long long)K * P, BH));
   }
   // AIB-bwd (:595)
   {

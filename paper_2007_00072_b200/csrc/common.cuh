@@ -109,16 +109,18 @@ struct PhiloxKey {
 __device__ __forceinline__ uint4 philox4x32_10(uint64_t g, const PhiloxKey& pk) {
   const uint32_t g0 = (uint32_t)g, g1 = (uint32_t)(g >> 32);
   // round 0 with ctr = (g0, g1, s0, s1)
+  // one IMAD.WIDE.U32 per 32x32->64 product (hi and lo together)
   uint4 c;
   {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, g0), lo0 = 0xD2511F53u * g0;
-    c = make_uint4(pk.a0 ^ g1, pk.l1, hi0 ^ pk.b0, lo0);
+    const uint64_t p0 = (uint64_t)0xD2511F53u * g0;
+    c = make_uint4(pk.a0 ^ g1, pk.l1, (uint32_t)(p0 >> 32) ^ pk.b0, (uint32_t)p0);
   }
 #pragma unroll
   for (int r = 1; r < 10; ++r) {
-    const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
-    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
-    c = make_uint4(hi1 ^ c.y ^ pk.rk0[r], lo1, hi0 ^ c.w ^ pk.rk1[r], lo0);
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ pk.rk0[r], (uint32_t)p1,
+                   (uint32_t)(p0 >> 32) ^ c.w ^ pk.rk1[r], (uint32_t)p0);
   }
   return c;
 }

@@ -86,6 +86,13 @@ cudaError_t launch_bei(int dtype, int64_t n, const void* a, const void* b, void*
 cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int nper,
                                    float* out0, float* out1, float* out2, cudaStream_t st);
 
+// Hand-written tcgen05 attention contractions (attn_gemm.cu), bf16 in / fp32 accumulate /
+// bf16 out.  which: 0 S=Q K^T, 1 C=A V (C in [B,J,H,P]), 2 dA=dC V^T (dC in [B,J,H,P]),
+// 3 dV=A^T dC, 4 dQ=dS K, 5 dK=dS^T Q; all other operands [B,H,rows,cols].
+bool attn_gemm_supported(int J, int P);
+cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, const void* Y,
+                             void* Z, cudaStream_t st);
+
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.
 cudaError_t launch_make_attn_ptrs(int B, int H, int J, int P, size_t esize, const void* A,

@@ -70,20 +70,20 @@ __global__ void __launch_bounds__(256) aib_fwd_kernel(const T* __restrict__ qkv,
 #pragma unroll 2
   for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks;
        c += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t bj = c / nc3;
-    const int col = (int)(c - bj * nc3) << 3;
+    const int bj = (int)c / nc3;          // chunk counts < 2^31 (host-checked)
+    const int col = ((int)c - bj * nc3) << 3;
     const int t = col / I;
     const int rem = col - t * I;
     const int h = rem / P;
     const int p0 = rem - h * P;
-    const int64_t b = bj / J;
-    const int j = (int)(bj - b * J);
+    const int b = bj / J;
+    const int j = bj - b * J;
     float x[8], bb[8];
     Chunk<T>::load_cs(qkv + c * 8, x);
     load_f32x8(bqkv + col, bb);
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] += bb[i];
-    T* dst = (t == 0 ? q : (t == 1 ? k : v)) + (((b * H + h) * J + j) * P + p0);
+    T* dst = (t == 0 ? q : (t == 1 ? k : v)) + ((((int64_t)b * H + h) * J + j) * P + p0);
     Chunk<T>::store(dst, x);
   }
 }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
   if (row >= rows) return;
   const int nc = K >> 3;
   const T* s = S + row * K;
-  const float* m = M ? M + (row / HJ) * K : nullptr;
+  const float* m = M ? M + (int64_t)((int)row / HJ) * K : nullptr;  // rows < 2^31
   typename Cv::Raw raw[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i)

@@ -24,7 +24,7 @@ struct GeluErfParts {
 };
 __device__ __forceinline__ GeluErfParts gelu_erf_parts(float h) {
   const float x = fabsf(h) * 0.70710678118654752f;
-  const float t = __frcp_rn(fmaf(0.3275911f, x, 1.f));
+  const float t = __fdividef(1.f, fmaf(0.3275911f, x, 1.f));  // MUFU.RCP
   float p = fmaf(1.061405429f, t, -1.453152027f);
   p = fmaf(p, t, 1.421413741f);
   p = fmaf(p, t, -0.284496736f);
@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) bad_fwd_kernel(const T* __restrict__ Y1,
     for (int u = 0; u < kU; ++u) {
       const int64_t c = c0 + u * stride;
       if (c < nchunks) {
-        const int col = (int)(c % ncU) << 3;
+        const int col = ((int)c % ncU) << 3;  // chunk counts < 2^31 (host-checked)
         float y[8], b[8], a[8];
         Chunk<T>::unpack(raw[u], y);
         load_f32x8(b1 + col, b);

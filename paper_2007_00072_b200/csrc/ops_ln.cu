@@ -133,11 +133,13 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
   const int warp = threadIdx.x >> 5;
   const int nc = I >> 3;
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
-  // layout: [warp][stage][2 tensors][I] T | mbar[warp][stage] | red[3][I] float
-  T* ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * kLnBwdStages * 2 * I;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kLnBwdWarps * kLnBwdStages * 2 * row_bytes);
+  // layout: mbar[warp][stage] | union { ring [warp][stage][2 tensors][I] T,
+  //                                      red [warp][3][I] float (after the row loop) }
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* bar = bars + warp * kLnBwdStages;
-  float* red = reinterpret_cast<float*>(bars + kLnBwdWarps * kLnBwdStages);
+  unsigned char* body = smem_raw + 128;
+  T* ring = reinterpret_cast<T*>(body) + (size_t)warp * kLnBwdStages * 2 * I;
+  float* red = reinterpret_cast<float*>(body);
 
   const int stride = gridDim.x * kLnBwdWarps;
   const int first = blockIdx.x * kLnBwdWarps + warp;
@@ -228,38 +230,40 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
       }
     }
   }
-  // fixed-order CTA reduction: warp 0 writes, warps 1..7 add in turn
-  for (int w = 0; w < kLnBwdWarps; ++w) {
-    if (warp == w) {
+  // CTA reduction in a fixed order: every warp stores its three column-sum vectors to its
+  // own slice (no read-modify-write chains), then each thread adds the 8 slices of its
+  // columns in warp order.  The ring is dead by now (all its bulk copies were consumed).
+  __syncthreads();
+  float* mine = red + (size_t)warp * 3 * I;
 #pragma unroll
-      for (int i = 0; i < CPL; ++i) {
-        const int ch = lane + 32 * i;
-        if (ch < nc) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = ch * 8 + j;
-            if (w == 0) {
-              red[c] = acc_g[i][j];
-              red[I + c] = acc_b[i][j];
-              red[2 * I + c] = acc_d[i][j];
-            } else {
-              red[c] += acc_g[i][j];
-              red[I + c] += acc_b[i][j];
-              red[2 * I + c] += acc_d[i][j];
-            }
-          }
-        }
-      }
+  for (int i = 0; i < CPL; ++i) {
+    const int ch = lane + 32 * i;
+    if (ch < nc) {
+      float4* d0 = reinterpret_cast<float4*>(mine + ch * 8);
+      float4* d1 = reinterpret_cast<float4*>(mine + I + ch * 8);
+      float4* d2 = reinterpret_cast<float4*>(mine + 2 * I + ch * 8);
+      d0[0] = make_float4(acc_g[i][0], acc_g[i][1], acc_g[i][2], acc_g[i][3]);
+      d0[1] = make_float4(acc_g[i][4], acc_g[i][5], acc_g[i][6], acc_g[i][7]);
+      d1[0] = make_float4(acc_b[i][0], acc_b[i][1], acc_b[i][2], acc_b[i][3]);
+      d1[1] = make_float4(acc_b[i][4], acc_b[i][5], acc_b[i][6], acc_b[i][7]);
+      d2[0] = make_float4(acc_d[i][0], acc_d[i][1], acc_d[i][2], acc_d[i][3]);
+      d2[1] = make_float4(acc_d[i][4], acc_d[i][5], acc_d[i][6], acc_d[i][7]);
     }
-    __syncthreads();
   }
+  __syncthreads();
   float* out = partials + (int64_t)blockIdx.x * 3 * I;
-  for (int c = threadIdx.x; c < 3 * I; c += blockDim.x) out[c] = red[c];
+  for (int c = threadIdx.x; c < 3 * I; c += blockDim.x) {
+    float s = red[c];
+#pragma unroll
+    for (int w = 1; w < kLnBwdWarps; ++w) s += red[(size_t)w * 3 * I + c];
+    out[c] = s;
+  }
 }
 
 static size_t bdrln_bwd_smem(int I, size_t es, int stages) {
-  return (size_t)kLnBwdWarps * stages * 2 * I * es + sizeof(uint64_t) * kLnBwdWarps * stages +
-         sizeof(float) * 3 * I;
+  const size_t ring = (size_t)kLnBwdWarps * stages * 2 * I * es;
+  const size_t red = (size_t)kLnBwdWarps * 3 * I * sizeof(float);
+  return 128 + (ring > red ? ring : red);
 }
 
 // 2-stage ring when it fits, else 1 stage; rows up to 2048 elements (8 chunks per lane)
@@ -317,9 +321,11 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
 }
 
 // ------------------------------------------------------------------ column-sum finalize
-// Block (32 columns) x (16 row-slices).  Thread (x, y) sums partial rows y, y+16, ... of
-// column c in ascending order; the 16 slice sums are then added in ascending y order.
-constexpr int kFinY = 16;
+// Block = 32 columns x 32 row-slices.  Thread (x, y) sums partial rows y, y+32, ... of its
+// column (all loads issued first, ascending order), then the 32 slice sums are added in
+// ascending y order: a fixed summation order, independent of timing.
+constexpr int kFinY = 32;
+constexpr int kFinMaxPer = 16;  // partial rows per slice handled with loads in flight
 
 __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
     const float* __restrict__ partials, int R, int ncols, int nper, float* out0, float* out1,
@@ -328,8 +334,16 @@ __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
   const int c = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
   if (c < ncols) {
-#pragma unroll 8
-    for (int r = threadIdx.y; r < R; r += kFinY) s += partials[(int64_t)r * ncols + c];
+    for (int r0 = threadIdx.y; r0 < R; r0 += kFinY * kFinMaxPer) {
+      float v[kFinMaxPer];
+#pragma unroll
+      for (int u = 0; u < kFinMaxPer; ++u) {
+        const int r = r0 + u * kFinY;
+        v[u] = r < R ? __ldcg(partials + (int64_t)r * ncols + c) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kFinMaxPer; ++u) s += v[u];
+    }
   }
   sm[threadIdx.y][threadIdx.x] = s;
   __syncthreads();

@@ -113,3 +113,15 @@ def enc_bad_bwd(ctx, B, J, U, dA1, h, act, p, seed, subseq, batch_offset, dh, db
 def enc_bei(ctx, a, b, out, stream=None):
     check("enc_bei", _abi.load().enc_bei(ctx.ptr, _dt(a), a.numel(), _p(a), _p(b), _p(out),
                                          _stream(stream)))
+
+
+AG_QK, AG_AV, AG_DA, AG_DV, AG_DQ, AG_DK = range(6)
+
+
+def enc_attn_gemm(ctx, which, B, H, J, P, X, Y, Z, stream=None):
+    check("enc_attn_gemm", _abi.load().enc_attn_gemm(ctx.ptr, which, B, H, J, P, _p(X), _p(Y),
+                                                     _p(Z), _stream(stream)))
+
+
+def enc_set_option(ctx, key, value):
+    check("enc_set_option", _abi.load().enc_set_option(ctx.ptr, key, value))

@@ -155,8 +155,9 @@ def test_layer_L_fp32_full():
 
 
 @pytest.mark.parametrize("dims,act,kp", [
-    (Dims(B=2, J=64, H=4, P=16, U=256), "gelu", True),
-    (Dims(B=3, J=40, H=2, P=24, U=96), "relu", True),
+    (Dims(B=2, J=64, H=4, P=16, U=256), "gelu", True),      # cuBLAS attention path
+    (Dims(B=3, J=40, H=2, P=24, U=96), "relu", True),       # cuBLAS attention path
+    (Dims(B=2, J=256, H=4, P=64, U=1024), "gelu", True),    # tcgen05 attention path
 ])
 def test_layer_small_bf16_stagewise(dims, act, kp):
     pairs, f32 = _stagewise(dims, "bf16", act, kp, weight_std=0.06)
