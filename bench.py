@@ -39,8 +39,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=2)
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
-    ap.add_argument("--attn-backend", choices=["tc", "cublas"], default="tc",
-                    help="attention contractions: hand-written tcgen05 kernels or cuBLAS")
+    ap.add_argument("--attn-backend", choices=["fused", "tc", "cublas"], default="fused",
+                    help="attention: fused tcgen05 score kernels (QK^T+BSB, dA+BSB-bwd), "
+                         "separate tcgen05 contractions, or cuBLAS contractions")
     ap.add_argument("--eager", action="store_true",
                     help="launch every step eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -182,8 +183,10 @@ def main():
     cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff)
     layer = EncoderLayer(dims, args.dtype, cfg)
     layer.set_params(make_params(dims, args.dtype, "bench"))
-    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 0,
-                                                            int(args.attn_backend == "tc")))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(
+        layer.ctx.ptr, 0, int(args.attn_backend in ("tc", "fused"))))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(
+        layer.ctx.ptr, 1, int(args.attn_backend == "fused")))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
@@ -222,7 +225,8 @@ def main():
         for i, n in enumerate(names):
             per_op[n].append(ms_buf[i])
     per_op = {n: statistics.median(v) for n, v in per_op.items()}
-    fused = tally.fused_bytes(dims, es)
+    fused = tally.fused_bytes(dims, es, fused_attn=(args.attn_backend == "fused"
+                                                    and args.dtype == "bf16"))
     flops = tally.gemm_flops(dims)
     dominant = max(per_op, key=per_op.get)
     dom_id = names.index(dominant)
@@ -362,8 +366,9 @@ def main():
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
                        else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)",
-                       "attention_contractions": "tcgen05 (hand-written)" if args.attn_backend == "tc"
-                       else "cuBLAS"},
+                       "attention": {"fused": "fused tcgen05 QK^T+BSB / dA+BSB-bwd + tcgen05 GEMMs",
+                                     "tc": "tcgen05 GEMMs + separate BSB kernels",
+                                     "cublas": "cuBLAS GEMMs + separate BSB kernels"}[args.attn_backend]},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},

@@ -246,9 +246,26 @@ enum { ENC_AG_QK = 0, ENC_AG_AV, ENC_AG_DA, ENC_AG_DV, ENC_AG_DQ, ENC_AG_DK };
 int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const void* X,
                   const void* Y, void* Z, enc_stream_t stream);
 
-/* Options of a context.  ENC_OPT_ATTN_TC: 1 = the layer runs its six attention
- * contractions on the hand-written tcgen05 kernels (default when supported), 0 = cuBLAS. */
-enum { ENC_OPT_ATTN_TC = 0 };
+/* Fused score kernels (bf16, P == 64, J in {256, 512}): one tcgen05 kernel computes the
+ * contraction into TMEM and applies the fused normalisation in its epilogue, so the score
+ * tensor never reaches HBM.
+ *   enc_attn_fwd_fused: S = Q K^T (:551) then BSB (:552) -> P, A [B,H,J,K]
+ *   enc_attn_bwd_fused: dA = dC V^T (:588, dC in [B,J,H,P]) then BSB-bwd (:590) with the
+ *                       saved P -> dS [B,H,J,K]
+ * Same dropout / scale conventions as enc_bsb_fwd / enc_bsb_bwd. */
+int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
+                       const void* K, const float* mask_bias, float p, uint64_t seed,
+                       uint64_t subseq, int64_t batch_offset, void* P_out, void* A,
+                       enc_stream_t stream);
+int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
+                       const void* V, const void* P_in, float p, uint64_t seed, uint64_t subseq,
+                       int64_t batch_offset, void* dS, enc_stream_t stream);
+
+/* Options of a context.  ENC_OPT_ATTN_TC: 1 = the layer runs its attention contractions on
+ * the hand-written tcgen05 kernels (default when supported), 0 = cuBLAS.
+ * ENC_OPT_ATTN_FUSED: 1 = QK^T+BSB and dA+BSB-bwd run as the fused kernels above (default
+ * when supported; requires ENC_OPT_ATTN_TC), 0 = separate contraction and BSB kernels. */
+enum { ENC_OPT_ATTN_TC = 0, ENC_OPT_ATTN_FUSED = 1 };
 int enc_set_option(enc_ctx* ctx, int key, int value);
 
 /* BEI (paper `bei`): out = a + b, n elements (out may alias a). */

@@ -101,6 +101,12 @@ _SIGS = {
     "enc_attn_gemm": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
                               c_void_p, c_void_p]),
     "enc_set_option": (c_int, [c_void_p, c_int, c_int]),
+    "enc_attn_fwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
+                                   c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
+                                   c_void_p, c_void_p, c_void_p]),
+    "enc_attn_bwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
+                                   c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
+                                   c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 

@@ -32,6 +32,7 @@ struct enc_ctx {
   bool recorded[ENC_NUM_OPS] = {};
   uint64_t launches = 0;     // kernels this library launched (excluding cuBLAS)
   int attn_tc = 1;           // ENC_OPT_ATTN_TC
+  int attn_fused = 1;        // ENC_OPT_ATTN_FUSED
 };
 
 namespace {
@@ -509,10 +510,44 @@ int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const voi
   return ENC_OK;
 }
 
+int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
+                       const void* Kt, const float* mask_bias, float p, uint64_t seed,
+                       uint64_t subseq, int64_t batch_offset, void* Pout, void* A,
+                       enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(Q, Kt, Pout, A);
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if (B == 0) return ENC_OK;
+  OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
+  CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias, make_philox_key(p, seed, subseq),
+                        batch_offset, Pout, A, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
+int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
+                       const void* V, const void* Pin, float p, uint64_t seed, uint64_t subseq,
+                       int64_t batch_offset, void* dS, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(dC, V, Pin, dS);
+  if (B == 0) return ENC_OK;
+  OpTimer _t(ctx, ENC_OP_BSB_BWD, (cudaStream_t)stream, 1);
+  CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pin, make_philox_key(p, seed, subseq),
+                         batch_offset, dS, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
 int enc_set_option(enc_ctx* ctx, int key, int value) {
   if (!ctx) return ENC_ENULL;
   if (key == ENC_OPT_ATTN_TC) {
     ctx->attn_tc = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_ATTN_FUSED) {
+    ctx->attn_fused = value ? 1 : 0;
     return ENC_OK;
   }
   return ENC_EINVAL;
@@ -568,6 +603,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   const float scale = 1.0f / sqrtf((float)P);  // DESIGN.md R3
   const int64_t boff = cfg->batch_offset;
   const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
+  const bool fused_attn = tc_attn && ctx->attn_fused && attn_fused_supported(J, P);
 
   // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T
   {
@@ -580,20 +616,27 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     OpTimer _t(ctx, ENC_OP_AIB_FWD, st, 1);
     CK(launch_aib_fwd(dtype, B, J, H, P, QKV, prm->bqkv, Q, Kt, V, st));
   }
-  // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
-  {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK, st, tc_attn ? 1 : 0);
-    if (tc_attn)
-      CK(launch_attn_gemm(ENC_AG_QK, B, H, J, P, Q, Kt, S, st));
-    else
-      CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P, Kt,
-                         P, (long long)K * P, 0.f, S, K, (long long)J * K, BH));
-  }
-  // BSB (:552)
-  {
+  if (fused_attn) {
+    // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
-    CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias,
-                      make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+    CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias,
+                          make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+  } else {
+    // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
+    {
+      OpTimer _t(ctx, ENC_OP_GEMM_QK, st, tc_attn ? 1 : 0);
+      if (tc_attn)
+        CK(launch_attn_gemm(ENC_AG_QK, B, H, J, P, Q, Kt, S, st));
+      else
+        CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P,
+                           Kt, P, (long long)K * P, 0.f, S, K, (long long)J * K, BH));
+    }
+    // BSB (:552)
+    {
+      OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
+      CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias,
+                        make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+    }
   }
   // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]
   {
@@ -688,6 +731,7 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   const float scale = 1.0f / sqrtf((float)P);
   const int64_t boff = cfg->batch_offset;
   const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
+  const bool fused_attn = tc_attn && ctx->attn_fused && attn_fused_supported(J, P);
   const int F32 = ENC_FP32;
 
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
@@ -739,8 +783,10 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, 1);
-    if (tc_attn) {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, fused_attn ? 0 : 1);
+    if (fused_attn) {
+      // dA is produced inside the fused dA + BSB-bwd kernel below
+    } else if (tc_attn) {
       CK(launch_attn_gemm(ENC_AG_DA, B, H, J, P, dC, V, dA, st));
     } else {
       CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, dC, dA, dV, ptr, st));
@@ -761,8 +807,12 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // BSB-bwd (:590)
   {
     OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
-    CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
-                      make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
+    if (fused_attn)  // Gamma dX1 (:588) + BSB-bwd (:590): dA stays in TMEM
+      CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pm,
+                             make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
+    else
+      CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
+                        make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
   }
   // QK^T dX1 (:591): dQ = dS K;  dX2 (:592): dK = dS^T Q
   {

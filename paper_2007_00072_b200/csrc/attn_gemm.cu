@@ -48,8 +48,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_gemm_kernel(
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B aligned operand ring (SWIZZLE_128B atoms), then barriers; after the last MMA the
   // ring is reused as the epilogue's TMA-store staging buffers
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* base = tc::align1024(smem_raw);
   constexpr uint32_t kABytes = kBM * kBK * 2;
   constexpr uint32_t kBBytes = BN * kBK * 2;
   static_assert(STAGES * (kABytes + kBBytes) >= 4 * 2 * 4096, "staging must fit in the ring");
@@ -193,7 +192,7 @@ bool make_map(CUtensorMap* m, const void* ptr, const uint64_t dims[4], const uin
   cuuint64_t gstride[3] = {strides[0] * 2, strides[1] * 2, strides[2] * 2};
   cuuint32_t bdim[4] = {box[0], box[1], box[2], box[3]};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = cuTensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+  CUresult r = tmap_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
                                       const_cast<void*>(ptr), gdim, gstride, bdim, estr,
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

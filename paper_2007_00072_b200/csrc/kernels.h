@@ -1,5 +1,6 @@
 // Host-side launchers of the fused sm_100a kernels (internal to libencoder.so).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -92,6 +93,23 @@ cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int 
 bool attn_gemm_supported(int J, int P);
 cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, const void* Y,
                              void* Z, cudaStream_t st);
+
+// cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
+CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,
+                           void* addr, const cuuint64_t* dims, const cuuint64_t* strides,
+                           const cuuint32_t* box, const cuuint32_t* estrides,
+                           CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                           CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob);
+
+// Fused tcgen05 score kernels (attn_fused.cu): QK^T + BSB (writes P, A) and dC V^T +
+// BSB-bwd (writes dS), bf16, P == 64, J in {256, 512}.
+bool attn_fused_supported(int J, int P);
+cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
+                               const void* Kt, const float* mask_bias, const PhiloxKey& pk,
+                               int64_t batch_offset, void* Pout, void* Aout, cudaStream_t st);
+cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
+                                const void* V, const void* Pin, const PhiloxKey& pk,
+                                int64_t batch_offset, void* dS, cudaStream_t st);
 
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.

@@ -125,3 +125,20 @@ def enc_attn_gemm(ctx, which, B, H, J, P, X, Y, Z, stream=None):
 
 def enc_set_option(ctx, key, value):
     check("enc_set_option", _abi.load().enc_set_option(ctx.ptr, key, value))
+
+
+OPT_ATTN_TC, OPT_ATTN_FUSED = 0, 1
+
+
+def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
+                       Pout, A, stream=None):
+    check("enc_attn_fwd_fused", _abi.load().enc_attn_fwd_fused(
+        ctx.ptr, B, H, J, P, scale, _p(Q), _p(K), _p(mask_bias), p, seed, subseq, batch_offset,
+        _p(Pout), _p(A), _stream(stream)))
+
+
+def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batch_offset, dS,
+                       stream=None):
+    check("enc_attn_bwd_fused", _abi.load().enc_attn_bwd_fused(
+        ctx.ptr, B, H, J, P, scale, _p(dC), _p(V), _p(Pin), p, seed, subseq, batch_offset,
+        _p(dS), _stream(stream)))

@@ -13,21 +13,29 @@ def _d(d):
     return B, J, H, P, H * P, U
 
 
-def fused_bytes(d, es: int = 2, mask_bias: bool = False) -> dict:
-    """Algorithmic HBM bytes per launch of each fused operator (es = activation bytes)."""
+def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = False) -> dict:
+    """Algorithmic HBM bytes per launch of each fused operator (es = activation bytes).
+    fused_attn: BSB / BSB-bwd run fused with their contraction (QK^T + BSB reads Q, K and
+    writes P, A; dC V^T + BSB-bwd reads dC, V, P and writes dS)."""
     B, J, H, P, I, U = _d(d)
     BJ, BJI, BJU, BHJK = B * J, B * J * I, B * J * U, B * H * J * J
     f = 4  # fp32
+    if fused_attn:
+        bsb_f = 2 * BJI * es + 2 * BHJK * es + (B * J * f if mask_bias else 0)
+        bsb_b = 2 * BJI * es + 2 * BHJK * es
+    else:
+        bsb_f = 3 * BHJK * es + (B * J * f if mask_bias else 0)
+        bsb_b = 3 * BHJK * es
     return {
         "aib_fwd": 2 * BJ * 3 * I * es + 3 * I * f,
-        "bsb_fwd": 3 * BHJK * es + (B * J * f if mask_bias else 0),
+        "bsb_fwd": bsb_f,
         "bdrln_fwd1": 4 * BJI * es + BJ * f + 3 * I * f,
         "bad_fwd": 3 * BJU * es + U * f,
         "bdrln_fwd2": 4 * BJI * es + BJ * f + 3 * I * f,
         "bdrln_bwd2": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
         "bad_bwd": 3 * BJU * es + U * f,
         "bdrln_bwd1": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
-        "bsb_bwd": 3 * BHJK * es,
+        "bsb_bwd": bsb_b,
         "aib_bwd": 2 * BJ * 3 * I * es + 3 * I * f,
     }
 

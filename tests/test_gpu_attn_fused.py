@@ -1,0 +1,81 @@
+"""Parity of the fused tcgen05 score kernels against the fp64 oracle:
+  enc_attn_fwd_fused  == BSB(Q K^T)          (oracle bsb_fwd on the fp64 product)
+  enc_attn_bwd_fused  == BSB-bwd(dC V^T, P)  (oracle bsb_bwd on the fp64 product)
+Dropout keep decisions must match exactly: dropped elements are exactly zero."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import encoder as E
+from oracle import philox
+from synth import make_positive_rows, make_tensor
+from tol import assert_parity
+
+pytestmark = pytest.mark.gpu
+SEED = 2007000072
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2007_00072_b200 import ops as _ops
+    return _ops
+
+
+@pytest.fixture(scope="module")
+def ctx(ops):
+    return ops.Context(0)
+
+
+def dev(a):
+    return torch.tensor(np.ascontiguousarray(a, np.float32), device="cuda").to(torch.bfloat16)
+
+
+def host(t):
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+@pytest.mark.parametrize("B,H,J", [(1, 1, 256), (2, 3, 512), (8, 16, 512), (3, 2, 256)])
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("p", [0.1, 0.0])
+def test_fused_forward(ops, ctx, B, H, J, masked, p):
+    P = 64
+    Q = make_tensor((B, H, J, P), 21, "bf16", std=0.8)
+    K = make_tensor((B, H, J, P), 22, "bf16", std=0.8)
+    M = None
+    if masked:
+        M = np.zeros((B, J), np.float32)
+        for b in range(B):
+            M[b, J // 2 + 17 * b:] = -10000.0
+    boff, sub, scale = 5, 8, 0.125
+    Pm = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
+    A = torch.full_like(Pm, float("nan"))
+    Mt = None if M is None else torch.tensor(M, device="cuda")
+    ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, dev(Q), dev(K), Mt, p, SEED, sub, boff, Pm, A)
+    torch.cuda.synchronize()
+    S = Q.astype(np.float64) @ K.astype(np.float64).transpose(0, 1, 3, 2)
+    Po, Ao = E.bsb_fwd(S, M, scale, p, SEED, sub, boff)
+    gP, gA = host(Pm), host(A)
+    assert np.isfinite(gP).all() and np.isfinite(gA).all()
+    assert_parity("P", gP, Po, "bf16")
+    assert_parity("A", gA, Ao, "bf16")
+    keep = philox.keep_mask_tensor(S.shape, boff, p, SEED, sub)
+    assert (gA[~keep] == 0).all()
+    assert np.allclose(gP.sum(-1), 1.0, atol=2e-2)
+
+
+@pytest.mark.parametrize("B,H,J", [(1, 1, 256), (2, 3, 512), (8, 16, 512)])
+@pytest.mark.parametrize("p", [0.1, 0.0])
+def test_fused_backward(ops, ctx, B, H, J, p):
+    P = 64
+    dC = make_tensor((B, J, H, P), 31, "bf16")          # [B,J,H,P]
+    V = make_tensor((B, H, J, P), 32, "bf16")
+    Pm = make_positive_rows((B, H, J, J), 33, "bf16")
+    boff, sub, scale = 2, 4, 0.125
+    dS = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
+    ops.enc_attn_bwd_fused(ctx, B, H, J, P, scale, dev(dC), dev(V), dev(Pm), p, SEED, sub, boff, dS)
+    torch.cuda.synchronize()
+    dA = dC.astype(np.float64).transpose(0, 2, 1, 3) @ V.astype(np.float64).transpose(0, 1, 3, 2)
+    dSo = E.bsb_bwd(dA, Pm, scale, p, SEED, sub, boff)
+    g = host(dS)
+    assert np.isfinite(g).all()
+    assert_parity("dS", g, dSo, "bf16")

@@ -110,9 +110,15 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     pairs += [("dC", b["dC"], b["dYo"] @ W["Wo"]),
               ("dWo", g["Wo"], np.einsum("bji,bjk->ik", b["dYo"], s["C"]))]
     dCbh = b["dC"].reshape(B, J, H, P).transpose(0, 2, 1, 3)
-    pairs += [("dA", b["dA"], dCbh @ s["V"].transpose(0, 1, 3, 2)),
-              ("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
-    pairs += [("dS", b["dS"], E.bsb_bwd(b["dA"], s["P"], sc, ocfg.p_attn, seed, sub(0), boff))]
+    dAo = dCbh @ s["V"].transpose(0, 1, 3, 2)
+    pairs += [("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
+    if dtype == "bf16" and P == 64 and J in (256, 512):
+        # fused dC V^T + BSB-bwd kernel: dA never leaves TMEM; dS from the fp64 product
+        pairs += [("dS", b["dS"], E.bsb_bwd(dAo, s["P"], sc, ocfg.p_attn, seed, sub(0), boff))]
+    else:
+        pairs += [("dA", b["dA"], dAo)]
+        pairs += [("dS", b["dS"], E.bsb_bwd(b["dA"], s["P"], sc, ocfg.p_attn, seed, sub(0),
+                                            boff))]
     pairs += [("dQ", b["dQ"], b["dS"] @ s["K"]),
               ("dK", b["dK"], b["dS"].transpose(0, 1, 3, 2) @ s["Q"])]
     dQKVo, dbqkvo = E.aib_bwd(b["dQ"], b["dK"], b["dV"])
