@@ -265,7 +265,12 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
  * the hand-written tcgen05 kernels (default when supported), 0 = cuBLAS.
  * ENC_OPT_ATTN_FUSED: 1 = QK^T+BSB and dA+BSB-bwd run as the fused kernels above (default
  * when supported; requires ENC_OPT_ATTN_TC), 0 = separate contraction and BSB kernels. */
-enum { ENC_OPT_ATTN_TC = 0, ENC_OPT_ATTN_FUSED = 1 };
+/* ENC_OPT_GEMM_LT: 1 = the weight contractions (QKV, Out, Linear1/2, fwd/dX/dW) run through
+ * cuBLASLt with a per-shape algorithm chosen by timing every heuristic candidate on the
+ * first eager call (the paper's contraction tuning; default), 0 = cuBLAS
+ * cublasGemmEx with its default heuristic.  ENC_OPT_GEMM_AUTOTUNE: 1 = measure (default),
+ * 0 = take cuBLASLt's first heuristic candidate. */
+enum { ENC_OPT_ATTN_TC = 0, ENC_OPT_ATTN_FUSED = 1, ENC_OPT_GEMM_LT = 2, ENC_OPT_GEMM_AUTOTUNE = 3 };
 int enc_set_option(enc_ctx* ctx, int key, int value);
 
 /* BEI (paper `bei`): out = a + b, n elements (out may alias a). */

@@ -33,7 +33,19 @@ struct enc_ctx {
   uint64_t launches = 0;     // kernels this library launched (excluding cuBLAS)
   int attn_tc = 1;           // ENC_OPT_ATTN_TC
   int attn_fused = 1;        // ENC_OPT_ATTN_FUSED
+  LtCtx* lt = nullptr;       // cuBLASLt + measured algorithm cache (weight GEMMs)
+  int use_lt = 1;            // ENC_OPT_GEMM_LT
 };
+
+// weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
+static cublasStatus_t wgemm(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA,
+                            bool tB, int M, int N, int K, float alpha, const void* A, int lda,
+                            const void* B, int ldb, float beta, void* C, int ldc) {
+  if (ctx->lt && ctx->use_lt && alpha == 1.f)
+    return lt_gemm_rm(ctx->lt, in_dt, out_dt, tA, tB, M, N, K, A, lda, B, ldb, beta, C, ldc,
+                      LT_EPI_NONE, nullptr, st);
+  return gemm_rm(ctx->blas, in_dt, out_dt, tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
 
 namespace {
 const char* kOpNames[ENC_NUM_OPS] = {
@@ -142,6 +154,7 @@ int enc_create(enc_ctx** out, int device) {
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1[i]);
   }
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
+  c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
   cudaSetDevice(prev);
   *out = c;
   return ENC_OK;
@@ -177,6 +190,7 @@ void enc_destroy(enc_ctx* c) {
     if (c->ev0[i]) cudaEventDestroy(c->ev0[i]);
     if (c->ev1[i]) cudaEventDestroy(c->ev1[i]);
   }
+  if (c->lt) lt_destroy(c->lt);
   if (c->blas) cublasDestroy(c->blas);
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->red) cudaFree(c->red);
@@ -546,6 +560,14 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->attn_tc = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_GEMM_LT) {
+    ctx->use_lt = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_GEMM_AUTOTUNE) {
+    if (ctx->lt) lt_set_autotune(ctx->lt, value ? 1 : 0);
+    return ENC_OK;
+  }
   if (key == ENC_OPT_ATTN_FUSED) {
     ctx->attn_fused = value ? 1 : 0;
     return ENC_OK;
@@ -608,7 +630,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
+    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
                QKV, 3 * I));
   }
   // AIB (:550)
@@ -653,7 +675,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Out (:554)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, I, I, 1.f, C, I, prm->Wo, I, 0.f, Yo, I));
+    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, I, I, 1.f, C, I, prm->Wo, I, 0.f, Yo, I));
   }
   // BDRLN site 1 (:555-558)
   {
@@ -664,7 +686,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Linear (:559)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, Y1, U));
+    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, Y1, U));
   }
   // BAD (:560-562)
   {
@@ -675,7 +697,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Linear (:563)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L2, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, true, BJ, I, U, 1.f, A1, U, prm->W2, U, 0.f, Y2, I));
+    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, I, U, 1.f, A1, U, prm->W2, U, 0.f, Y2, I));
   }
   // BDRLN site 2 (:564-567)
   {
@@ -744,11 +766,11 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // Linear2 dX (:573), dW (:574)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, U, I, 1.f, dY2, I, prm->W2, U, 0.f, dA1, U));
+    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, U, I, 1.f, dY2, I, prm->W2, U, 0.f, dA1, U));
   }
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U));
+    CB(wgemm(ctx, st,dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U));
   }
   // BAD-bwd (:576-578)
   {
@@ -759,11 +781,11 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DX, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, U, 1.f, dh, U, prm->W1, I, 1.f, dX1, I));
+    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, U, 1.f, dh, U, prm->W1, I, 1.f, dX1, I));
   }
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I));
+    CB(wgemm(ctx, st,dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I));
   }
   // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo
   {
@@ -775,11 +797,11 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // Out dX (:586), dW (:587)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DX, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, I, 1.f, dYo, I, prm->Wo, I, 0.f, dC, I));
+    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, I, 1.f, dYo, I, prm->Wo, I, 0.f, dC, I));
   }
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I));
+    CB(wgemm(ctx, st,dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I));
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
@@ -839,12 +861,12 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, dtype, false, false, BJ, I, 3 * I, 1.f, dQKV, 3 * I, prm->Wqkv, I,
+    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, 3 * I, 1.f, dQKV, 3 * I, prm->Wqkv, I,
                1.f, dX, I));
   }
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, st, 0);
-    CB(gemm_rm(ctx->blas, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
+    CB(wgemm(ctx, st,dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
                g->dWqkv, I));
   }
   return ENC_OK;

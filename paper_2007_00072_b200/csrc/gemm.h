@@ -13,4 +13,17 @@ cublasStatus_t gemm_rm_batched(cublasHandle_t h, int dtype, bool tA, bool tB, in
                                int K, float alpha, const void* const* A, int lda,
                                const void* const* B, int ldb, float beta, void* const* C,
                                int ldc, int batch);
+
+// cuBLASLt path with measured algorithm selection (gemm_lt.cu)
+struct LtCtx;
+enum { LT_EPI_NONE = 0, LT_EPI_BIAS = 1, LT_EPI_BGRAD_A = 2 };
+LtCtx* lt_create(void* workspace, size_t workspace_bytes);
+void lt_destroy(LtCtx* c);
+void lt_set_autotune(LtCtx* c, int on);
+// Row-major C[M,N] = op(A) op(B) + beta C; epi: LT_EPI_BIAS adds bias[N] (fp32) to every row;
+// LT_EPI_BGRAD_A also writes bias[M] = sum over K of op(A) (fp32 column sums of the
+// reduction dimension).
+cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool tB, int M, int N,
+                          int K, const void* A, int lda, const void* B, int ldb, float beta,
+                          void* C, int ldc, int epi, void* bias, cudaStream_t st);
 }  // namespace enc

@@ -97,6 +97,9 @@ cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, cons
                              float* rstd, cudaStream_t st) {
   const int rows = B * J;
   if (rows == 0) return cudaSuccess;
+  if (bdrln_rg_supported(I))
+    return launch_bdrln_fwd_rg(dtype, B, J, I, Y, bias, R, gamma, beta, eps, pk, batch_offset,
+                               out, xhat, rstd, st);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const int grid = (rows + 7) / 8;
@@ -288,6 +291,9 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
     cudaMemsetAsync(dbeta, 0, sizeof(float) * I, st);
     return cudaMemsetAsync(dbias, 0, sizeof(float) * I, st);
   }
+  if (bdrln_rg_supported(I))
+    return launch_bdrln_bwd_rg(dtype, B, J, I, dOut, xhat, rstd, gamma, pk, batch_offset, dz,
+                               dYpre, dgamma, dbeta, dbias, ws, st);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   int G = (rows + kLnBwdWarps - 1) / kLnBwdWarps;

@@ -1,0 +1,378 @@
+// Row-group BDRLN kernels (forward and backward) for I % 32 == 0, I <= 2048.
+//
+// A row of I elements is shared by a group of 4 warps (each warp owns a contiguous quarter
+// of the columns, at most 2 chunks of 8 per lane), so a warp's per-row work is a quarter of
+// the one-warp-per-row kernels in ops_ln.cu and four times as many rows are in flight per
+// SM.  Persistent CTAs of 4 groups (512 threads); each group streams its rows through a
+// 2-stage shared-memory ring filled by the bulk-copy (TMA) engine one row ahead.  The
+// row statistics of the 4 quarters are combined through shared memory behind one named
+// barrier per row (forward: Chan's parallel mean / M2 combination, backward: the two
+// LayerNorm-gradient sums), always in quarter order, so results do not depend on timing.
+// The backward accumulates dgamma / dbeta / dbias column sums in registers (24 per
+// thread), reduces them over the 4 groups in fixed order and writes one partial row per CTA
+// for launch_colsum_finalize.
+#include <math.h>
+
+#include "kernels.h"
+#include "tma.cuh"
+
+namespace enc {
+namespace {
+
+constexpr int kGroups = 4;              // row groups per CTA
+constexpr int kGWarps = 4;              // warps per row group
+constexpr int kRgThreads = kGroups * kGWarps * 32;
+constexpr int kRgStages = 2;
+
+__device__ __forceinline__ void gbar(int group) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(kGWarps * 32) : "memory");
+}
+
+// shared layout: mbar[group][stage] (64 B) | red2[group][stage][4] float4 (512 B) |
+// ring[group][stage][ntens][I] T | (bwd, after the loop) colsum[group][3][I] float
+constexpr int kRgHdr = 64 + kGroups * kRgStages * kGWarps * 16;
+
+template <typename T, int NT>
+__device__ __forceinline__ T* ring_row(unsigned char* smem, int I, int g, int s, int t) {
+  return reinterpret_cast<T*>(smem + kRgHdr) + (((size_t)g * kRgStages + s) * NT + t) * I;
+}
+
+// ------------------------------------------------------------------ forward
+template <typename T, int CPW>
+__global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
+    const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
+    const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
+    T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
+    PhiloxKey pk) {
+  using C = Chunk<T>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / kGWarps, w = warp % kGWarps;
+  const int nc = I >> 3, ncq = nc / kGWarps;          // chunks per row, per quarter
+  const uint32_t row_bytes = (uint32_t)I * sizeof(T);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * kRgStages;
+  float4* red = reinterpret_cast<float4*>(smem + 64) + (size_t)g * kRgStages * kGWarps;
+  const int stride = gridDim.x * kGroups;
+  const int first = blockIdx.x * kGroups + g;
+  const bool leader = (w == 0 && lane == 0);
+  if (leader) {
+    for (int s = 0; s < kRgStages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kRgStages; ++s) {
+      const int r = first + s * stride;
+      if (r < rows) {
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), Y + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), R + (int64_t)r * I, row_bytes, &bar[s]);
+      }
+    }
+  }
+  gbar(g);
+  int k = 0;
+  for (int row = first; row < rows; row += stride, ++k) {
+    const int s = k & 1;
+    mbar_wait(&bar[s], (uint32_t)(k >> 1) & 1u);
+    const T* sy = ring_row<T, 2>(smem, I, g, s, 0);
+    const T* sr = ring_row<T, 2>(smem, I, g, s, 1);
+    float z[CPW][8];
+    float lsum = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      const int cq = lane + 32 * i;
+      if (cq < ncq) {
+        const int ch = w * ncq + cq;
+        float y[8], b[8], m[8];
+        C::unpack(C::ld_smem(sy + ch * 8), y);
+        C::unpack(C::ld_smem(sr + ch * 8), z[i]);
+        load_f32x8(bias + ch * 8, b);
+        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          z[i][j] = fmaf(y[j] + b[j], m[j], z[i][j]);
+          lsum += z[i][j];
+        }
+      }
+    }
+    // quarter mean and M2 (two passes over registers), then Chan's combination
+    const float qn = (float)(ncq * 8);
+    const float qmean = warp_sum(lsum) / qn;
+    float m2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      if (lane + 32 * i < ncq) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = z[i][j] - qmean;
+          m2 = fmaf(d, d, m2);
+        }
+      }
+    }
+    m2 = warp_sum(m2);
+    if (lane == 0) red[s * kGWarps + w] = make_float4(qmean, m2, 0.f, 0.f);
+    gbar(g);   // quarter stats visible; every warp of the group has read this ring stage
+    if (leader) {
+      const int nr = row + kRgStages * stride;
+      if (nr < rows) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), Y + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), R + (int64_t)nr * I, row_bytes, &bar[s]);
+      }
+    }
+    float mean = 0.f;
+#pragma unroll
+    for (int q = 0; q < kGWarps; ++q) mean += red[s * kGWarps + q].x;
+    mean *= 0.25f;
+    float M2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < kGWarps; ++q) {
+      const float4 st = red[s * kGWarps + q];
+      const float d = st.x - mean;
+      M2 += st.y + qn * d * d;
+    }
+    const float rstd = rsqrtf(M2 / (float)I + eps);
+    const int64_t base = (int64_t)row * I;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      const int cq = lane + 32 * i;
+      if (cq < ncq) {
+        const int ch = w * ncq + cq;
+        float gm[8], be[8], xh[8], o[8];
+        load_f32x8(gamma + ch * 8, gm);
+        load_f32x8(beta + ch * 8, be);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          xh[j] = (z[i][j] - mean) * rstd;
+          o[j] = fmaf(gm[j], xh[j], be[j]);
+        }
+        C::store(out + base + ch * 8, o);
+        C::store(xhat + base + ch * 8, xh);
+      }
+    }
+    if (leader) rstd_out[row] = rstd;
+  }
+}
+
+// ------------------------------------------------------------------ backward
+template <typename T, int CPW>
+__global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
+    const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
+    const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
+    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk) {
+  using C = Chunk<T>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = warp / kGWarps, w = warp % kGWarps;
+  const int nc = I >> 3, ncq = nc / kGWarps;
+  const uint32_t row_bytes = (uint32_t)I * sizeof(T);
+  const float inv_n = 1.f / (float)I;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * kRgStages;
+  float4* red = reinterpret_cast<float4*>(smem + 64) + (size_t)g * kRgStages * kGWarps;
+  const int stride = gridDim.x * kGroups;
+  const int first = blockIdx.x * kGroups + g;
+  const bool leader = (w == 0 && lane == 0);
+  if (leader) {
+    for (int s = 0; s < kRgStages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+    for (int s = 0; s < kRgStages; ++s) {
+      const int r = first + s * stride;
+      if (r < rows) {
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), dOut + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), xhat + (int64_t)r * I, row_bytes, &bar[s]);
+      }
+    }
+  }
+  gbar(g);
+  float acc_g[CPW][8], acc_b[CPW][8], acc_d[CPW][8];
+#pragma unroll
+  for (int i = 0; i < CPW; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
+  int k = 0;
+  for (int row = first; row < rows; row += stride, ++k) {
+    const int s = k & 1;
+    mbar_wait(&bar[s], (uint32_t)(k >> 1) & 1u);
+    const T* sg = ring_row<T, 2>(smem, I, g, s, 0);
+    const T* sx = ring_row<T, 2>(smem, I, g, s, 1);
+    float go[CPW][8], xh[CPW][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      const int cq = lane + 32 * i;
+      if (cq < ncq) {
+        const int ch = w * ncq + cq;
+        float gm[8];
+        C::unpack(C::ld_smem(sg + ch * 8), go[i]);
+        C::unpack(C::ld_smem(sx + ch * 8), xh[i]);
+        load_f32x8(gamma + ch * 8, gm);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          acc_g[i][j] = fmaf(go[i][j], xh[i][j], acc_g[i][j]);
+          acc_b[i][j] += go[i][j];
+          go[i][j] *= gm[j];
+          s1 += go[i][j];
+          s2 = fmaf(go[i][j], xh[i][j], s2);
+        }
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) red[s * kGWarps + w] = make_float4(s1, s2, 0.f, 0.f);
+    gbar(g);
+    if (leader) {
+      const int nr = row + kRgStages * stride;
+      if (nr < rows) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), dOut + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), xhat + (int64_t)nr * I, row_bytes, &bar[s]);
+      }
+    }
+    float t1 = 0.f, t2 = 0.f;
+#pragma unroll
+    for (int q = 0; q < kGWarps; ++q) {
+      const float4 st = red[s * kGWarps + q];
+      t1 += st.x;
+      t2 += st.y;
+    }
+    const float mg = t1 * inv_n, mgx = t2 * inv_n;
+    const float rs = __ldg(rstd + row);
+    const int64_t base = (int64_t)row * I;
+#pragma unroll
+    for (int i = 0; i < CPW; ++i) {
+      const int cq = lane + 32 * i;
+      if (cq < ncq) {
+        const int ch = w * ncq + cq;
+        float d[8], y[8], m[8];
+        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d[j] = rs * (go[i][j] - mg - xh[i][j] * mgx);
+          y[j] = d[j] * m[j];
+          acc_d[i][j] += y[j];
+        }
+        C::store(dz + base + ch * 8, d);
+        C::store(dYpre + base + ch * 8, y);
+      }
+    }
+  }
+  // column sums: each warp owns a column quarter; add the 4 groups in fixed order
+  __syncthreads();   // ring is dead (all its bulk copies were consumed)
+  float* colsum = reinterpret_cast<float*>(smem + kRgHdr);   // [group][3][I]
+  float* mine = colsum + (size_t)g * 3 * I;
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int cq = lane + 32 * i;
+    if (cq < ncq) {
+      const int c0 = (w * ncq + cq) * 8;
+#pragma unroll
+      for (int j = 0; j < 8; j += 4) {
+        *reinterpret_cast<float4*>(mine + c0 + j) =
+            make_float4(acc_g[i][j], acc_g[i][j + 1], acc_g[i][j + 2], acc_g[i][j + 3]);
+        *reinterpret_cast<float4*>(mine + I + c0 + j) =
+            make_float4(acc_b[i][j], acc_b[i][j + 1], acc_b[i][j + 2], acc_b[i][j + 3]);
+        *reinterpret_cast<float4*>(mine + 2 * I + c0 + j) =
+            make_float4(acc_d[i][j], acc_d[i][j + 1], acc_d[i][j + 2], acc_d[i][j + 3]);
+      }
+    }
+  }
+  __syncthreads();
+  float* outp = partials + (int64_t)blockIdx.x * 3 * I;
+  for (int c = threadIdx.x; c < 3 * I; c += kRgThreads) {
+    float v = colsum[c];
+#pragma unroll
+    for (int q = 1; q < kGroups; ++q) v += colsum[(size_t)q * 3 * I + c];
+    outp[c] = v;
+  }
+}
+
+size_t rg_smem(int I, size_t es, bool bwd) {
+  const size_t ring = (size_t)kGroups * kRgStages * 2 * I * es;
+  const size_t cols = bwd ? (size_t)kGroups * 3 * I * sizeof(float) : 0;
+  return kRgHdr + (ring > cols ? ring : cols);
+}
+
+// persistent grid: as many CTAs as can be resident (occupancy query), at most one group
+// per row
+template <typename Kern>
+int rg_grid(Kern kern, int rows, size_t smem) {
+  int dev = 0, sms = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRgThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  int G = (rows + kGroups - 1) / kGroups;
+  if (G > per_sm * sms) G = per_sm * sms;
+  return G < 1 ? 1 : G;
+}
+
+}  // namespace
+
+// quarters of whole chunks, at most 2 chunks per lane
+bool bdrln_rg_supported(int I) { return I % 32 == 0 && I <= 2048; }
+
+#define ENC_CPW_DISPATCH(ncq, ...)                             \
+  do {                                                         \
+    if ((ncq) <= 32) { constexpr int CPW = 1; __VA_ARGS__; }   \
+    else { constexpr int CPW = 2; __VA_ARGS__; }               \
+  } while (0)
+
+cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
+                                const void* R, const float* gamma, const float* beta, float eps,
+                                const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
+                                float* rstd, cudaStream_t st) {
+  const int rows = B * J;
+  const int nc = I / 8;
+  const int64_t g0 = batch_offset * (int64_t)J * nc;
+  const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false);
+  ENC_CPW_DISPATCH(nc / 4, {
+    if (dtype == 0) {
+      auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW>;
+      kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
+          (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
+          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk);
+    } else {
+      auto kern = bdrln_fwd_rg_kernel<float, CPW>;
+      kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
+          (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat, rstd,
+          rows, I, eps, g0, pk);
+    }
+  });
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut,
+                                const void* xhat, const float* rstd, const float* gamma,
+                                const PhiloxKey& pk, int64_t batch_offset, void* dz,
+                                void* dYpre, float* dgamma, float* dbeta, float* dbias,
+                                const ReduceWs& ws, cudaStream_t st) {
+  const int rows = B * J;
+  const int nc = I / 8;
+  const int64_t g0 = batch_offset * (int64_t)J * nc;
+  const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, true);
+  const int cap = (int)(ws.cap_floats / (size_t)(3 * I));
+  int G = 1;
+  ENC_CPW_DISPATCH(nc / 4, {
+    if (dtype == 0) {
+      auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW>;
+      G = rg_grid(kern, rows, smem);
+      if (G > cap) G = cap;
+      kern<<<G, kRgThreads, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
+                                        rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
+                                        ws.partials, rows, I, g0, pk);
+    } else {
+      auto kern = bdrln_bwd_rg_kernel<float, CPW>;
+      G = rg_grid(kern, rows, smem);
+      if (G > cap) G = cap;
+      kern<<<G, kRgThreads, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
+                                        (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
+    }
+  });
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_colsum_finalize(ws.partials, G, 3 * I, I, dgamma, dbeta, dbias, st);
+}
+
+}  // namespace enc
