@@ -170,10 +170,16 @@ def main():
     from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
     from synth import CONFIGS, make_inputs, make_params
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; ENC_DIST_BACKEND=gloo (test hook) lets several ranks share one GPU
+    backend = os.environ.get("ENC_DIST_BACKEND", "nccl")
+    local_dev = local % torch.cuda.device_count() if backend != "nccl" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     dims_global = CONFIGS["L"].with_batch(CONFIGS["L"].B * world)
     boff, B = dp.shard(dims_global.B, world, rank)
     dims = CONFIGS["L"].with_batch(B)
@@ -199,10 +205,18 @@ def main():
     ms_buf = (_abi.c_float * nops)()
 
     def step():
+        # data parallel: the FFN-gradient all-reduce is issued as soon as the FFN half of the
+        # backward is done and overlaps the attention half
         layer.forward(X, None, Y)
-        layer.backward(X, dY, dX)
         if world > 1:
-            dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+            layer.backward(X, dY, dX, part=layer.BWD_FFN)
+            w1 = dp.allreduce_buckets([layer.ffn_bucket], async_op=True)
+            layer.backward(X, dY, dX, part=layer.BWD_ATTN)
+            w2 = dp.allreduce_buckets([layer.attn_bucket], async_op=True)
+            for w in w1 + w2:
+                w.wait()
+        else:
+            layer.backward(X, dY, dX)
 
     def barrier():
         if world > 1:
@@ -238,28 +252,43 @@ def main():
 
     # ---------------- CUDA graph of the layer step (fwd + bwd); events of the timed op
     # (enabled above) are captured as event-record nodes of the graph
-    run_layer = lambda: (layer.forward(X, None, Y), layer.backward(X, dY, dX))  # noqa: E731
+    # two graphs for N > 1 (forward + FFN half of the backward | attention half) so the
+    # eager NCCL all-reduce of the FFN bucket overlaps the second graph
+    if world > 1:
+        parts = [lambda: (layer.forward(X, None, Y),
+                          layer.backward(X, dY, dX, part=layer.BWD_FFN)),
+                 lambda: layer.backward(X, dY, dX, part=layer.BWD_ATTN)]
+    else:
+        parts = [lambda: (layer.forward(X, None, Y), layer.backward(X, dY, dX))]
     if not args.eager:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
-            run_layer()
+            for fn in parts:
+                fn()
         torch.cuda.current_stream(dev).wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            run_layer()
+        graphs = []
+        for fn in parts:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            graphs.append(g)
         torch.cuda.synchronize()
 
         def step():  # noqa: F811
-            graph.replay()
+            graphs[0].replay()
             if world > 1:
-                dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+                w1 = dp.allreduce_buckets([layer.ffn_bucket], async_op=True)
+                graphs[1].replay()
+                w2 = dp.allreduce_buckets([layer.attn_bucket], async_op=True)
+                for w in w1 + w2:
+                    w.wait()
         for _ in range(2):
             step()
         torch.cuda.synchronize()
 
     # ---------------- timed region
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local_dev)
     sampler.start()
     barrier()
     launches0 = lib.enc_launch_count(layer.ctx.ptr)

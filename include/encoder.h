@@ -169,6 +169,15 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
                            const enc_params* prm, const void* X, const void* saved,
                            const void* dY, void* dX, const enc_grads* g, void* scratch,
                            enc_stream_t stream);
+/* The backward in two halves, for overlapping the data-parallel gradient all-reduce with
+ * the rest of the backward: ENC_BWD_FFN runs BDRLN-bwd#2 .. Linear1 dW (afterwards dW1,
+ * dW2, db1, db2, dgamma2, dbeta2 are final), ENC_BWD_ATTN the remainder (BDRLN-bwd#1 ..
+ * QKV dW).  Calling both in that order equals encoder_layer_backward. */
+enum { ENC_BWD_FFN = 1, ENC_BWD_ATTN = 2 };
+int encoder_layer_backward_part(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                                const enc_params* prm, const void* X, const void* saved,
+                                const void* dY, void* dX, const enc_grads* g, void* scratch,
+                                int part, enc_stream_t stream);
 /* End-to-end step from HOST buffers (pinned for overlap): copies X_host, dY_host to
  * X_dev, dY_dev, runs forward + backward, copies Y and dX back to Y_host, dX_host.
  * Parameter gradients stay on the device in `g`. */

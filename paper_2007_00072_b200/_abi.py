@@ -67,6 +67,10 @@ _SIGS = {
     "encoder_layer_backward": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
                                        POINTER(enc_params), c_void_p, c_void_p, c_void_p,
                                        c_void_p, POINTER(enc_grads), c_void_p, c_void_p]),
+    "encoder_layer_backward_part": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
+                                            POINTER(enc_params), c_void_p, c_void_p, c_void_p,
+                                            c_void_p, POINTER(enc_grads), c_void_p, c_int,
+                                            c_void_p]),
     "encoder_layer_step_host": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
                                         POINTER(enc_params), c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

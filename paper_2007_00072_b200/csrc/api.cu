@@ -708,11 +708,14 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   return ENC_OK;
 }
 
-int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
-                           const enc_params* prm, const void* X, const void* saved,
-                           const void* dY, void* dX, const enc_grads* g, void* scratch,
-                           enc_stream_t stream) {
+// parts: bit 0 = FFN half (BDRLN-bwd#2 .. Linear1 dW: all FFN-parameter gradients final),
+//        bit 1 = attention half (BDRLN-bwd#1 .. QKV dW)
+static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                         const enc_params* prm, const void* X, const void* saved,
+                         const void* dY, void* dX, const enc_grads* g, void* scratch,
+                         enc_stream_t stream, int parts) {
   if (!ctx) return ENC_ENULL;
+  if (parts < 1 || parts > 3) return ENC_EINVAL;
   int r = check_dims(d, dtype);
   if (r) return r;
   if ((r = check_cfg(cfg))) return r;
@@ -756,6 +759,7 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
   const bool fused_attn = tc_attn && ctx->attn_fused && attn_fused_supported(J, P);
   const int F32 = ENC_FP32;
 
+  if (parts & 1) {
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_BWD2, st, 2);
@@ -787,6 +791,8 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, st, 0);
     CB(wgemm(ctx, st,dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I));
   }
+  }  // FFN half
+  if (!(parts & 2)) return ENC_OK;
   // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, st, 2);
@@ -870,6 +876,22 @@ int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc
                g->dWqkv, I));
   }
   return ENC_OK;
+}
+
+int encoder_layer_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                           const enc_params* prm, const void* X, const void* saved,
+                           const void* dY, void* dX, const enc_grads* g, void* scratch,
+                           enc_stream_t stream) {
+  return backward_impl(ctx, d, dtype, cfg, prm, X, saved, dY, dX, g, scratch, stream, 3);
+}
+
+int encoder_layer_backward_part(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                                const enc_params* prm, const void* X, const void* saved,
+                                const void* dY, void* dX, const enc_grads* g, void* scratch,
+                                int part, enc_stream_t stream) {
+  if (part != ENC_BWD_FFN && part != ENC_BWD_ATTN) return ENC_EINVAL;
+  return backward_impl(ctx, d, dtype, cfg, prm, X, saved, dY, dX, g, scratch, stream,
+                       part == ENC_BWD_FFN ? 1 : 2);
 }
 
 int encoder_layer_step_host(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,

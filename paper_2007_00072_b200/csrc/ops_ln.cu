@@ -341,14 +341,15 @@ __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
   float s = 0.f;
   if (c < ncols) {
     for (int r0 = threadIdx.y; r0 < R; r0 += kFinY * kFinMaxPer) {
+      // unconditional loads from clamped rows (issued back to back), masked afterwards
       float v[kFinMaxPer];
 #pragma unroll
       for (int u = 0; u < kFinMaxPer; ++u) {
-        const int r = r0 + u * kFinY;
-        v[u] = r < R ? __ldcg(partials + (int64_t)r * ncols + c) : 0.f;
+        const int r = min(r0 + u * kFinY, R - 1);
+        v[u] = __ldg(partials + (int64_t)r * ncols + c);
       }
 #pragma unroll
-      for (int u = 0; u < kFinMaxPer; ++u) s += v[u];
+      for (int u = 0; u < kFinMaxPer; ++u) s += (r0 + u * kFinY < R) ? v[u] : 0.f;
     }
   }
   sm[threadIdx.y][threadIdx.x] = s;

@@ -123,17 +123,25 @@ class EncoderLayer:
             self.saved.data_ptr(), self.scratch.data_ptr(), self._stream(stream)))
         return Y
 
+    BWD_FFN, BWD_ATTN = 1, 2
+
     def backward(self, X: torch.Tensor, dY: torch.Tensor, dX: torch.Tensor | None = None,
-                 stream=None) -> torch.Tensor:
+                 stream=None, part: int | None = None) -> torch.Tensor:
+        """Whole backward, or one half (part=BWD_FFN: up to the final FFN-parameter
+        gradients, then part=BWD_ATTN: the rest) so a gradient all-reduce can overlap."""
         assert dY.dtype == self.tdt and dY.is_contiguous() and dY.is_cuda
         if dX is None:
             dX = torch.empty_like(dY)
         cfg = self.cfg.to_c()
-        check("encoder_layer_backward", self.lib.encoder_layer_backward(
-            self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
-            ctypes.byref(self.c_params), X.data_ptr(), self.saved.data_ptr(), dY.data_ptr(),
-            dX.data_ptr(), ctypes.byref(self.c_grads), self.scratch.data_ptr(),
-            self._stream(stream)))
+        args = (self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
+                ctypes.byref(self.c_params), X.data_ptr(), self.saved.data_ptr(), dY.data_ptr(),
+                dX.data_ptr(), ctypes.byref(self.c_grads), self.scratch.data_ptr())
+        if part is None:
+            check("encoder_layer_backward",
+                  self.lib.encoder_layer_backward(*args, self._stream(stream)))
+        else:
+            check("encoder_layer_backward_part",
+                  self.lib.encoder_layer_backward_part(*args, part, self._stream(stream)))
         return dX
 
     def step_host(self, X_host, dY_host, Y_host, dX_host, X_dev, dY_dev, Y_dev, dX_dev,

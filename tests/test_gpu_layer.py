@@ -193,3 +193,25 @@ def test_layer_L_bf16_end_to_end_report():
         e = errors(gpu[n], ref[n])
         print(f"{n:14s} mixed {e['mixed']:.3e} mean_rel {e['mean_rel']:.3e}")
     assert_parity("Y", gpu["Y"], ref["Y"], "bf16")
+
+
+def test_backward_halves_equal_full_backward():
+    """encoder_layer_backward_part(FFN) then (ATTN) == encoder_layer_backward, bitwise."""
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    dims = Dims(B=2, J=256, H=4, P=64, U=1024)
+    prm = make_params(dims, "bf16", "parity", weight_std=0.06)
+    inp = make_inputs(dims, "bf16", key_padding=True)
+    layer = EncoderLayer(dims, "bf16", LayerCfg())
+    layer.set_params(prm)
+    X = torch.tensor(inp["X"], device="cuda").to(torch.bfloat16)
+    dY = torch.tensor(inp["dY"], device="cuda").to(torch.bfloat16)
+    M = torch.tensor(inp["mask_bias"], device="cuda")
+    layer.forward(X, M)
+    dX_full = layer.backward(X, dY).clone()
+    g_full = layer.grad_flat.clone()
+    layer.grad_flat.zero_()
+    dX = layer.backward(X, dY, part=layer.BWD_FFN)
+    dX = layer.backward(X, dY, dX=dX, part=layer.BWD_ATTN)
+    torch.cuda.synchronize()
+    assert torch.equal(dX, dX_full)
+    assert torch.equal(layer.grad_flat, g_full)
