@@ -39,6 +39,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=2)
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--no-attn-bh", action="store_true",
+                    help="AV / dV / dQ / dK on the tiled tcgen05 kernel instead of the "
+                         "per-(b, h) streaming kernel")
     ap.add_argument("--attn-backend", choices=["fused", "tc", "cublas"], default="fused",
                     help="attention: fused tcgen05 score kernels (QK^T+BSB, dA+BSB-bwd), "
                          "separate tcgen05 contractions, or cuBLAS contractions")
@@ -193,6 +196,7 @@ def main():
         layer.ctx.ptr, 0, int(args.attn_backend in ("tc", "fused"))))
     _abi.check("enc_set_option", _abi.load().enc_set_option(
         layer.ctx.ptr, 1, int(args.attn_backend == "fused")))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 4, int(not args.no_attn_bh)))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)

@@ -250,12 +250,14 @@ int enc_bad_bwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* dA1,
  * ENC_AG_AV C[B,J,H,P] = A V (:553), ENC_AG_DA dA = dC V^T (:588, dC in [B,J,H,P]),
  * ENC_AG_DV dV = A^T dC (:589), ENC_AG_DQ dQ = dS K (:591), ENC_AG_DK dK = dS^T Q (:592);
  * Q, K, V, dQ, dK, dV [B,H,J,P]; S, A, dA, dS [B,H,J,K].  X, Y = the two operands in the
- * order written, Z = the result. */
+ * order written, Z = the result.  With ENC_OPT_ATTN_BH on (default) and J = K a multiple
+ * of 128 up to 512, AV / DV / DQ / DK run on the per-(b, h) streaming kernel (one CTA reads a
+ * whole [J x K] matrix once, outputs resident in TMEM); otherwise on the tiled kernel. */
 enum { ENC_AG_QK = 0, ENC_AG_AV, ENC_AG_DA, ENC_AG_DV, ENC_AG_DQ, ENC_AG_DK };
 int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const void* X,
                   const void* Y, void* Z, enc_stream_t stream);
 
-/* Fused score kernels (bf16, P == 64, J in {256, 512}): one tcgen05 kernel computes the
+/* Fused score kernels (bf16, P == 64, J == K == 512, the paper's sequence length): one tcgen05 kernel computes the
  * contraction into TMEM and applies the fused normalisation in its epilogue, so the score
  * tensor never reaches HBM.
  *   enc_attn_fwd_fused: S = Q K^T (:551) then BSB (:552) -> P, A [B,H,J,K]
@@ -278,8 +280,11 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
  * cuBLASLt with a per-shape algorithm chosen by timing every heuristic candidate on the
  * first eager call (the paper's contraction tuning; default), 0 = cuBLAS
  * cublasGemmEx with its default heuristic.  ENC_OPT_GEMM_AUTOTUNE: 1 = measure (default),
- * 0 = take cuBLASLt's first heuristic candidate. */
-enum { ENC_OPT_ATTN_TC = 0, ENC_OPT_ATTN_FUSED = 1, ENC_OPT_GEMM_LT = 2, ENC_OPT_GEMM_AUTOTUNE = 3 };
+ * 0 = take cuBLASLt's first heuristic candidate.  ENC_OPT_ATTN_BH: 1 = the AV / dV / dQ+dK
+ * contractions run on the per-(b, h) streaming kernel when supported (default; the layer
+ * then computes dQ and dK in one pass over dS), 0 = the tiled tcgen05 kernel. */
+enum { ENC_OPT_ATTN_TC = 0, ENC_OPT_ATTN_FUSED = 1, ENC_OPT_GEMM_LT = 2, ENC_OPT_GEMM_AUTOTUNE = 3,
+       ENC_OPT_ATTN_BH = 4 };
 int enc_set_option(enc_ctx* ctx, int key, int value);
 
 /* BEI (paper `bei`): out = a + b, n elements (out may alias a). */

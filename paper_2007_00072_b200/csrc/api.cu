@@ -33,6 +33,7 @@ struct enc_ctx {
   uint64_t launches = 0;     // kernels this library launched (excluding cuBLAS)
   int attn_tc = 1;           // ENC_OPT_ATTN_TC
   int attn_fused = 1;        // ENC_OPT_ATTN_FUSED
+  int attn_bh = 1;           // ENC_OPT_ATTN_BH
   LtCtx* lt = nullptr;       // cuBLASLt + measured algorithm cache (weight GEMMs)
   int use_lt = 1;            // ENC_OPT_GEMM_LT
 };
@@ -200,6 +201,25 @@ void enc_destroy(enc_ctx* c) {
 }  // extern "C"
 
 static ReduceWs ws_of(const enc_ctx* c) { return ReduceWs{c->red, c->red_floats, c->num_sms}; }
+
+// One attention contraction (ENC_AG_*) on the per-(b, h) streaming kernel when it applies,
+// else on the tiled tcgen05 kernel.
+static bool use_bh(const enc_ctx* ctx, int J, int P) {
+  return ctx->attn_bh && attn_bh_supported(J, P);
+}
+static cudaError_t attn_contract(const enc_ctx* ctx, int which, int B, int H, int J, int P,
+                                 const void* X, const void* Y, void* Z, cudaStream_t st) {
+  if (use_bh(ctx, J, P)) {
+    switch (which) {
+      case ENC_AG_AV: return launch_attn_av_bh(B, H, J, P, X, Y, Z, st);
+      case ENC_AG_DV: return launch_attn_dv_bh(B, H, J, P, X, Y, Z, st);
+      case ENC_AG_DQ: return launch_attn_dqdk_bh(B, H, J, P, X, Y, nullptr, Z, nullptr, st);
+      case ENC_AG_DK: return launch_attn_dqdk_bh(B, H, J, P, X, nullptr, Y, nullptr, Z, st);
+      default: break;
+    }
+  }
+  return launch_attn_gemm(which, B, H, J, P, X, Y, Z, st);
+}
 
 // ------------------------------------------------------------------ dims validation
 static int check_dims(const enc_dims* d, int dtype) {
@@ -519,7 +539,7 @@ int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const voi
   if (!attn_gemm_supported(J, P)) return ENC_EUNSUPPORTED;
   CHECK_PTRS(X, Y, Z);
   if (B == 0) return ENC_OK;
-  CK(launch_attn_gemm(which, B, H, J, P, X, Y, Z, (cudaStream_t)stream));
+  CK(attn_contract(ctx, which, B, H, J, P, X, Y, Z, (cudaStream_t)stream));
   ctx->launches += 1;
   return ENC_OK;
 }
@@ -570,6 +590,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_ATTN_FUSED) {
     ctx->attn_fused = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_ATTN_BH) {
+    ctx->attn_bh = value ? 1 : 0;
     return ENC_OK;
   }
   return ENC_EINVAL;
@@ -664,7 +688,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
     if (tc_attn) {
-      CK(launch_attn_gemm(ENC_AG_AV, B, H, J, P, A, V, C, st));
+      CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, V, C, st));
     } else {
       CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
       CB(gemm_rm_batched(ctx->blas, dtype, false, false, J, P, K, 1.f, (const void* const*)ptr, K,
@@ -826,7 +850,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
     if (tc_attn)
-      CK(launch_attn_gemm(ENC_AG_DV, B, H, J, P, A, dC, dV, st));
+      CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, dC, dV, st));
     else
       CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
                          (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH),
@@ -843,17 +867,22 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                         make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
   }
   // QK^T dX1 (:591): dQ = dS K;  dX2 (:592): dK = dS^T Q
+  const bool dqdk_one_pass = tc_attn && use_bh(ctx, J, P);
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QK_DQ, st, tc_attn ? 1 : 0);
-    if (tc_attn)
+    if (dqdk_one_pass)   // dQ and dK from one read of dS
+      CK(launch_attn_dqdk_bh(B, H, J, P, dS, Kt, Q, dQ, dK, st));
+    else if (tc_attn)
       CK(launch_attn_gemm(ENC_AG_DQ, B, H, J, P, dS, Kt, dQ, st));
     else
       CB(gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, dS, K, (long long)J * K, Kt,
                          P, (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, tc_attn ? 1 : 0);
-    if (tc_attn)
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, tc_attn && !dqdk_one_pass ? 1 : 0);
+    if (dqdk_one_pass) {
+      // computed with dQ above
+    } else if (tc_attn)
       CK(launch_attn_gemm(ENC_AG_DK, B, H, J, P, dS, Q, dK, st));
     else
       CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,

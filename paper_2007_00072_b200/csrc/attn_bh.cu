@@ -1,0 +1,322 @@
+// Per-(b, h) tcgen05 contractions over the attention-probability tensors (Table A.1
+// PAPER.md:553 "Gamma", and its backward dX1/dX2 rows :588-592):
+//
+//   AV    C[j,:]  = sum_k A[j,k]  V[k,:]        (forward, A = dropout(P))
+//   dV    dV[k,:] = sum_j A[j,k]  dC[j,:]
+//   dQdK  dQ[j,:] = sum_k dS[j,k] K[k,:]  and  dK[k,:] = sum_j dS[j,k] Q[j,:]   (one pass)
+//
+// These four contractions read a [J x K] = 512 KB bf16 matrix per (b, h) and write only
+// 64 KB, so they are HBM-bound on that read (67 MB at config L).  One CTA owns a whole
+// (b, h) pair: it streams the matrix once in 128 x 128 blocks through a TMA ring, and every
+// output row tile stays resident in TMEM until the pair is done (J/128 x 64 columns per
+// output, <= 512 columns for dQ and dK together).  dQ and dK share each dS block, so dS
+// is read once instead of twice.  The same smem block serves as a K-major operand (row
+// outputs: C, dQ) and as an MN-major operand (column outputs: dV, dK).
+//
+// Warp roles (192 threads, one CTA per SM, persistent over (b, h) pairs):
+//   warp 0     TMA producer      warp 1  TMEM allocator + MMA issuer
+//   warps 2-5  epilogue: TMEM -> bf16 -> 128-B-swizzled staging -> TMA store
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kernels.h"
+#include "tc_gemm.cuh"
+
+namespace enc {
+namespace {
+
+constexpr int kThreads = 192;
+constexpr uint32_t kXBytes = 128 * 128 * 2;  // one 128 x 128 block (two 64-column boxes)
+constexpr uint32_t kYBytes = 128 * 64 * 2;   // one 128-row x 64 operand block
+
+struct BhParams {
+  int H, nt;           // heads, J / 128
+  int units;           // B * H
+  int row_out, col_out;  // which outputs this launch computes
+  int yr_rowdim, yc_rowdim, or_rowdim, oc_rowdim;  // 4-D map dim holding the row index
+};
+
+__device__ __forceinline__ void coords(int rowdim, int inner, int row, int h, int b, int* c) {
+  c[0] = inner;
+  if (rowdim == 1) {
+    c[1] = row;
+    c[2] = h;
+  } else {
+    c[1] = h;
+    c[2] = row;
+  }
+  c[3] = b;
+}
+
+template <int STAGES>
+__global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
+    const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapYr,
+    const __grid_constant__ CUtensorMap mapYc, const __grid_constant__ CUtensorMap mapOr,
+    const __grid_constant__ CUtensorMap mapOc, BhParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = tc::align1024(smem_raw);
+  const uint32_t stage_bytes = kXBytes + (p.row_out ? kYBytes : 0) + (p.col_out ? kYBytes : 0);
+  unsigned char* stg_all = base + STAGES * stage_bytes;        // 4 warps x 2 x 4 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + 4 * 2 * 4096);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tm_full = empty + STAGES;
+  uint64_t* tm_empty = tm_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nt = p.nt;
+  const int nblk = nt * nt;
+  const uint32_t col_off = p.row_out ? nt * 64 : 0;   // TMEM column of the column outputs
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&mapX);
+    if (p.row_out) tc::prefetch_tmap(&mapYr), tc::prefetch_tmap(&mapOr);
+    if (p.col_out) tc::prefetch_tmap(&mapYc), tc::prefetch_tmap(&mapOc);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tm_full, 1);
+    mbar_init(tm_empty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int g = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const int b = u / p.H, h = u - (u / p.H) * p.H;
+        for (int blk = 0; blk < nblk; ++blk, ++g) {
+          const int jt = blk / nt, kt = blk - (blk / nt) * nt;
+          const int s = g % STAGES;
+          mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          unsigned char* sx = base + s * stage_bytes;
+          // X block rows jt*128.., columns kt*128.. as two 64-column boxes
+          tc::tma_load_4d(sx, &mapX, &full[s], kt * 128, jt * 128, h, b);
+          tc::tma_load_4d(sx + 16384, &mapX, &full[s], kt * 128 + 64, jt * 128, h, b);
+          unsigned char* sy = sx + kXBytes;
+          int c[4];
+          if (p.row_out) {   // Yr rows kt*128.. (keys)
+            coords(p.yr_rowdim, 0, kt * 128, h, b, c);
+            tc::tma_load_4d(sy, &mapYr, &full[s], c[0], c[1], c[2], c[3]);
+            sy += kYBytes;
+          }
+          if (p.col_out) {   // Yc rows jt*128.. (queries)
+            coords(p.yc_rowdim, 0, jt * 128, h, b, c);
+            tc::tma_load_4d(sy, &mapYc, &full[s], c[0], c[1], c[2], c[3]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc_r = tc::instr_desc_bf16_f32(128, 64, false, true);
+    constexpr uint32_t idesc_c = tc::instr_desc_bf16_f32(128, 64, true, true);
+    int g = 0, it = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
+      mbar_wait(tm_empty, (it & 1) ^ 1);   // epilogue released the accumulators
+      tc::fence_after_sync();
+      for (int blk = 0; blk < nblk; ++blk, ++g) {
+        const int jt = blk / nt, kt = blk - (blk / nt) * nt;
+        const int s = g % STAGES;
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        tc::fence_after_sync();
+        if (lane == 0) {
+          const uint32_t x0 = smem_u32(base + s * stage_bytes);
+          uint32_t y0 = x0 + kXBytes;
+          if (p.row_out) {
+            // out_r[jt] += X(jt,kt) Yr(kt): X K-major (rows j), Yr MN-major (rows k)
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              tc::mma_bf16(tmem + jt * 64,
+                           tc::smem_desc(x0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
+                           tc::smem_desc(y0 + ks * 2048, 8192, 1024), idesc_r,
+                           (kt | ks) != 0);
+            y0 += kYBytes;
+          }
+          if (p.col_out) {
+            // out_c[kt] += X(jt,kt)^T Yc(jt): X MN-major (M = k), Yc MN-major (rows j)
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks)
+              tc::mma_bf16(tmem + col_off + kt * 64, tc::smem_desc(x0 + ks * 2048, 16384, 1024),
+                           tc::smem_desc(y0 + ks * 2048, 8192, 1024), idesc_c,
+                           (jt | ks) != 0);
+          }
+          tc::mma_commit(&empty[s]);
+          if (blk == nblk - 1) tc::mma_commit(tm_full);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    unsigned char* stg = stg_all + q * 2 * 4096;
+    int it = 0, n = 0;
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
+      const int b = u / p.H, h = u - (u / p.H) * p.H;
+      mbar_wait(tm_full, it & 1);
+      tc::fence_after_sync();
+      const int ngroups = (p.row_out ? nt : 0) + (p.col_out ? nt : 0);
+#pragma unroll 1
+      for (int gi = 0; gi < ngroups; ++gi, ++n) {
+        const bool is_r = p.row_out && gi < nt;
+        const int t = p.row_out && !is_r ? gi - nt : gi;   // row tile of this output group
+        unsigned char* buf = stg + (n & 1) * 4096;
+        if (lane == 0) tc::bulk_wait_read<1>();
+        __syncwarp();
+        float v[64];
+        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + gi * 64;
+        tc::tmem_ld32(taddr, v);
+        tc::tmem_ld32(taddr + 32, v + 32);
+        if (gi == ngroups - 1) {   // accumulators free for the next (b, h)
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tm_empty))
+                         : "memory");
+        }
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          uint4 w;
+          w.x = Chunk<__nv_bfloat16>::pack2(v[8 * ch + 0], v[8 * ch + 1]);
+          w.y = Chunk<__nv_bfloat16>::pack2(v[8 * ch + 2], v[8 * ch + 3]);
+          w.z = Chunk<__nv_bfloat16>::pack2(v[8 * ch + 4], v[8 * ch + 5]);
+          w.w = Chunk<__nv_bfloat16>::pack2(v[8 * ch + 6], v[8 * ch + 7]);
+          *reinterpret_cast<uint4*>(buf + tc::sw128(lane, ch)) = w;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          int c[4];
+          coords(is_r ? p.or_rowdim : p.oc_rowdim, 0, t * 128 + q * 32, h, b, c);
+          tc::tma_store_4d(is_r ? &mapOr : &mapOc, buf, c[0], c[1], c[2], c[3]);
+          tc::bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) tc::bulk_wait<0>();
+    __syncwarp();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
+bool make_map(CUtensorMap* m, const void* ptr, const uint64_t d[4], const uint64_t s[3],
+              const uint32_t box[4]) {
+  cuuint64_t gdim[4] = {d[0], d[1], d[2], d[3]};
+  cuuint64_t gstr[3] = {s[0] * 2, s[1] * 2, s[2] * 2};
+  cuuint32_t bdim[4] = {box[0], box[1], box[2], box[3]};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return tmap_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), gdim,
+                           gstr, bdim, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// logical [B*H][rows][cols]; head-major [B][H][rows][cols] (rowdim 1) or token-major
+// [B][rows][H][cols] (rowdim 2); box {64 cols, box_rows rows}
+bool map_op(CUtensorMap* m, const void* ptr, bool token_major, int B, int H, int rows, int cols,
+            int box_rows, int* rowdim) {
+  uint64_t d[4], s[3];
+  uint32_t box[4];
+  if (!token_major) {
+    d[0] = cols; d[1] = rows; d[2] = H; d[3] = B;
+    s[0] = cols; s[1] = (uint64_t)rows * cols; s[2] = (uint64_t)H * rows * cols;
+    box[0] = 64; box[1] = box_rows; box[2] = 1; box[3] = 1;
+    *rowdim = 1;
+  } else {
+    d[0] = cols; d[1] = H; d[2] = rows; d[3] = B;
+    s[0] = cols; s[1] = (uint64_t)H * cols; s[2] = (uint64_t)rows * H * cols;
+    box[0] = 64; box[1] = 1; box[2] = box_rows; box[3] = 1;
+    *rowdim = 2;
+  }
+  return make_map(m, ptr, d, s, box);
+}
+
+int sm_count() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+template <int STAGES>
+cudaError_t launch_bh(const CUtensorMap* m, const BhParams& p, cudaStream_t st) {
+  const uint32_t stage_bytes = kXBytes + (p.row_out ? kYBytes : 0) + (p.col_out ? kYBytes : 0);
+  const size_t smem = 1024 + STAGES * stage_bytes + 4 * 2 * 4096 + (2 * STAGES + 2) * 8 + 16;
+  cudaFuncSetAttribute(attn_bh_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  const int grid = p.units < sm_count() ? p.units : sm_count();
+  attn_bh_kernel<STAGES><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// J = K keys, a multiple of 128 up to 512 (every output row tile of a (b, h) in TMEM)
+bool attn_bh_supported(int J, int P) { return P == 64 && J % 128 == 0 && J >= 128 && J <= 512; }
+
+// which: ENC_AG_AV (1): C = A V,  ENC_AG_DV (3): dV = A^T dC,
+//        ENC_AG_DQ (4): dQ = dS K,  ENC_AG_DK (5): dK = dS^T Q.
+// launch_attn_dqdk_bh computes dQ and dK from one read of dS.
+static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const void* Yr,
+                             bool yr_tok, const void* Yc, bool yc_tok, void* Or, bool or_tok,
+                             void* Oc, bool oc_tok, cudaStream_t st) {
+  if (!attn_bh_supported(J, P)) return cudaErrorInvalidValue;
+  BhParams p{};
+  p.H = H;
+  p.nt = J / 128;
+  p.units = B * H;
+  p.row_out = Or != nullptr;
+  p.col_out = Oc != nullptr;
+  CUtensorMap m[5];
+  int rd;
+  bool ok = map_op(&m[0], X, false, B, H, J, J, 128, &rd);
+  m[1] = m[0];
+  m[2] = m[0];
+  m[3] = m[0];
+  m[4] = m[0];
+  if (p.row_out) {
+    ok &= map_op(&m[1], Yr, yr_tok, B, H, J, P, 128, &p.yr_rowdim);
+    ok &= map_op(&m[3], Or, or_tok, B, H, J, P, 32, &p.or_rowdim);
+  }
+  if (p.col_out) {
+    ok &= map_op(&m[2], Yc, yc_tok, B, H, J, P, 128, &p.yc_rowdim);
+    ok &= map_op(&m[4], Oc, oc_tok, B, H, J, P, 32, &p.oc_rowdim);
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  if (p.units == 0) return cudaSuccess;
+  if (p.row_out && p.col_out) return launch_bh<3>(m, p, st);
+  return launch_bh<4>(m, p, st);
+}
+
+cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V, void* C,
+                              cudaStream_t st) {
+  // C is token-major [B, J, H, P]
+  return bh_launch(B, H, J, P, A, V, false, nullptr, false, C, true, nullptr, false, st);
+}
+
+cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
+                              void* dV, cudaStream_t st) {
+  // dC is token-major [B, J, H, P]; dV head-major [B, H, K, P]
+  return bh_launch(B, H, J, P, A, nullptr, false, dC, true, nullptr, false, dV, false, st);
+}
+
+cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
+                                const void* Q, void* dQ, void* dK, cudaStream_t st) {
+  return bh_launch(B, H, J, P, dS, Kt, false, Q, false, dQ, false, dK, false, st);
+}
+
+}  // namespace enc

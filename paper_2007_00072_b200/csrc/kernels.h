@@ -113,8 +113,19 @@ CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32
                            CUtensorMapInterleave il, CUtensorMapSwizzle sw,
                            CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob);
 
+// Per-(b, h) tcgen05 contractions over the [J x K] probability / gradient matrices
+// (attn_bh.cu): one CTA streams a whole (b, h) matrix once, outputs resident in TMEM.
+// bf16, P == 64, J = K a multiple of 128 up to 512.
+bool attn_bh_supported(int J, int P);
+cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V, void* C,
+                              cudaStream_t st);
+cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
+                              void* dV, cudaStream_t st);
+cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
+                                const void* Q, void* dQ, void* dK, cudaStream_t st);
+
 // Fused tcgen05 score kernels (attn_fused.cu): QK^T + BSB (writes P, A) and dC V^T +
-// BSB-bwd (writes dS), bf16, P == 64, J in {256, 512}.
+// BSB-bwd (writes dS), bf16, P == 64, J == 512.
 bool attn_fused_supported(int J, int P);
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                const void* Kt, const float* mask_bias, const PhiloxKey& pk,

@@ -34,7 +34,7 @@ def host(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("B,H,J", [(1, 1, 256), (2, 3, 512), (8, 16, 512), (3, 2, 256)])
+@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512), (3, 2, 512)])
 @pytest.mark.parametrize("masked", [False, True])
 @pytest.mark.parametrize("p", [0.1, 0.0])
 def test_fused_forward(ops, ctx, B, H, J, masked, p):
@@ -63,7 +63,7 @@ def test_fused_forward(ops, ctx, B, H, J, masked, p):
     assert np.allclose(gP.sum(-1), 1.0, atol=2e-2)
 
 
-@pytest.mark.parametrize("B,H,J", [(1, 1, 256), (2, 3, 512), (8, 16, 512)])
+@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512)])
 @pytest.mark.parametrize("p", [0.1, 0.0])
 def test_fused_backward(ops, ctx, B, H, J, p):
     P = 64
@@ -79,3 +79,14 @@ def test_fused_backward(ops, ctx, B, H, J, p):
     g = host(dS)
     assert np.isfinite(g).all()
     assert_parity("dS", g, dSo, "bf16")
+
+
+@pytest.mark.parametrize("J,P", [(256, 64), (384, 64), (512, 32)])
+def test_fused_unsupported_shapes(ops, ctx, J, P):
+    """The fused kernels hold a whole 512-key score row in TMEM; other shapes are refused
+    (the layer then takes the unfused tcgen05 path)."""
+    from paper_2007_00072_b200._abi import EncError
+    x = torch.zeros((1, 1, J, P), dtype=torch.bfloat16, device="cuda")
+    o = torch.zeros((1, 1, J, J), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(EncError):
+        ops.enc_attn_fwd_fused(ctx, 1, 1, J, P, 0.125, x, x, None, 0.1, SEED, 0, 0, o, o)

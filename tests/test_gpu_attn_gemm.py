@@ -30,12 +30,20 @@ def host(t):
 
 
 SHAPES = [(1, 1, 128, 64), (2, 3, 256, 64), (8, 16, 512, 64), (3, 2, 384, 64)]
+# more (b, h) pairs than SMs (the per-(b, h) kernel loops), and J > 512 (tiled fallback)
+SHAPES_BH = [(10, 16, 256, 64), (1, 2, 640, 64)]
 
 
-@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("shape", SHAPES + SHAPES_BH)
 @pytest.mark.parametrize("which", range(6))
-def test_attn_gemm(ops, ctx, shape, which):
+@pytest.mark.parametrize("bh", [1, 0])
+def test_attn_gemm(ops, ctx, shape, which, bh):
+    """bh=1: AV / DV / DQ / DK on the per-(b, h) streaming kernel where it applies;
+    bh=0: every form on the tiled kernel."""
     B, H, J, P = shape
+    if shape in SHAPES_BH and not bh:
+        pytest.skip("tiled kernel covered by SHAPES")
+    ops.enc_set_option(ctx, ops.OPT_ATTN_BH, bh)
     K = J
     bhjp = (B, H, J, P)
     bhjk = (B, H, J, K)
@@ -67,6 +75,7 @@ def test_attn_gemm(ops, ctx, shape, which):
     Z = torch.full(zshape, float("nan"), dtype=torch.bfloat16, device="cuda")
     ops.enc_attn_gemm(ctx, which, B, H, J, P, dev(X), dev(Y), Z)
     torch.cuda.synchronize()
+    ops.enc_set_option(ctx, ops.OPT_ATTN_BH, 1)
     got = host(Z)
     assert np.isfinite(got).all(), "unwritten output elements"
     # fp32 accumulation of exact bf16 products, one bf16 rounding of the result

@@ -112,7 +112,7 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     dCbh = b["dC"].reshape(B, J, H, P).transpose(0, 2, 1, 3)
     dAo = dCbh @ s["V"].transpose(0, 1, 3, 2)
     pairs += [("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
-    if dtype == "bf16" and P == 64 and J in (256, 512):
+    if dtype == "bf16" and P == 64 and J == 512:
         # fused dC V^T + BSB-bwd kernel: dA never leaves TMEM; dS from the fp64 product
         pairs += [("dS", b["dS"], E.bsb_bwd(dAo, s["P"], sc, ocfg.p_attn, seed, sub(0), boff))]
     else:
@@ -164,6 +164,7 @@ def test_layer_L_fp32_full():
     (Dims(B=2, J=64, H=4, P=16, U=256), "gelu", True),      # cuBLAS attention path
     (Dims(B=3, J=40, H=2, P=24, U=96), "relu", True),       # cuBLAS attention path
     (Dims(B=2, J=256, H=4, P=64, U=1024), "gelu", True),    # tcgen05 attention path
+    (Dims(B=2, J=512, H=2, P=64, U=512), "gelu", True),     # fused score kernels
 ])
 def test_layer_small_bf16_stagewise(dims, act, kp):
     pairs, f32 = _stagewise(dims, "bf16", act, kp, weight_std=0.06)
