@@ -98,13 +98,24 @@ typedef struct {
   float *dbqkv, *dbo, *db1, *db2, *dg1, *dbe1, *dg2, *dbe2;
 } enc_grads;
 
-/* Views into the caller's `saved` buffer (forward -> backward contract).  No dropout
- * mask is stored.  Q, K, V, P, A in the attention layout [B,H,J,P] / [B,H,J,K];
- * C, X1, xhat1, xhat2 [B,J,I]; h, A1 [B,J,U] (enc_dtype); rstd1, rstd2 [B,J] fp32. */
+/* Views into the caller's `saved` buffer (forward -> backward contract).  Q, K, V, P, A in
+ * the attention layout [B,H,J,P] / [B,H,J,K]; C, X1, xhat1, xhat2 [B,J,I]; h, A1 [B,J,U]
+ * (enc_dtype); rstd1, rstd2 [B,J] fp32.  keep_attn: the attention-dropout keep flags as
+ * 1-bit words, [B,H,J,ceil(K/32)] uint32 (ENC_KEEP_BITS layout below), written by the fused
+ * forward score kernel and read by the fused backward so it need not regenerate the Philox
+ * stream (unused on the other attention paths).  The BDRLN / BAD dropout masks are not
+ * stored: their backward regenerates them. */
 typedef struct {
   void *Q, *K, *V, *P, *A, *C, *X1, *xhat1, *h, *A1, *xhat2;
   float *rstd1, *rstd2;
+  uint32_t* keep_attn;
 } enc_saved_view;
+
+/* ENC_KEEP_BITS layout: word w of row (b,h,j) holds the keep flags of columns
+ * 32w .. 32w+31; column 32w + 8c + u (c = 0..3, u = 0..7) is bit
+ * (u odd ? 31 : 15) - u/2 - 4c.  (u is the 16-bit Philox lane of chunk c: lanes 2i / 2i+1
+ * are the low / high halves of output word i, R5; the order falls out of a
+ * SIMD-within-a-register compare of the two lanes of a word.) */
 
 /* Views into `scratch` of the backward temporaries, valid after encoder_layer_backward
  * until the next forward/backward call on the same scratch (parity / inspection hook):
@@ -257,20 +268,24 @@ enum { ENC_AG_QK = 0, ENC_AG_AV, ENC_AG_DA, ENC_AG_DV, ENC_AG_DQ, ENC_AG_DK };
 int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const void* X,
                   const void* Y, void* Z, enc_stream_t stream);
 
-/* Fused score kernels (bf16, P == 64, J == K == 512, the paper's sequence length): one tcgen05 kernel computes the
- * contraction into TMEM and applies the fused normalisation in its epilogue, so the score
- * tensor never reaches HBM.
+/* Fused score kernels (bf16, P == 64, J == K == 512, the paper's sequence length): one
+ * tcgen05 kernel computes the contraction into TMEM and applies the fused normalisation in
+ * its epilogue, so the score tensor never reaches HBM.
  *   enc_attn_fwd_fused: S = Q K^T (:551) then BSB (:552) -> P, A [B,H,J,K]
  *   enc_attn_bwd_fused: dA = dC V^T (:588, dC in [B,J,H,P]) then BSB-bwd (:590) with the
  *                       saved P -> dS [B,H,J,K]
- * Same dropout / scale conventions as enc_bsb_fwd / enc_bsb_bwd. */
+ * Same dropout / scale conventions as enc_bsb_fwd / enc_bsb_bwd.  keep_bits (optional,
+ * 8-B aligned, [B,H,J,K/32] uint32, ENC_KEEP_BITS layout): the forward writes the keep
+ * flags it used there; the backward, given the forward's words, reads them instead of
+ * regenerating the Philox stream (null: regenerate; both give the same dS). */
 int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
                        const void* K, const float* mask_bias, float p, uint64_t seed,
                        uint64_t subseq, int64_t batch_offset, void* P_out, void* A,
-                       enc_stream_t stream);
+                       uint32_t* keep_bits, enc_stream_t stream);
 int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
                        const void* V, const void* P_in, float p, uint64_t seed, uint64_t subseq,
-                       int64_t batch_offset, void* dS, enc_stream_t stream);
+                       int64_t batch_offset, const uint32_t* keep_bits, void* dS,
+                       enc_stream_t stream);
 
 /* Options of a context.  ENC_OPT_ATTN_TC: 1 = the layer runs its attention contractions on
  * the hand-written tcgen05 kernels (default when supported), 0 = cuBLAS.

@@ -29,7 +29,8 @@ class enc_cfg(ctypes.Structure):
 
 PARAM_FIELDS = ("Wqkv", "Wo", "W1", "W2", "bqkv", "bo", "b1", "b2", "g1", "be1", "g2", "be2")
 GRAD_FIELDS = tuple("d" + n for n in PARAM_FIELDS)
-SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2")
+SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2",
+                "keep_attn")
 
 
 class enc_params(ctypes.Structure):
@@ -107,10 +108,10 @@ _SIGS = {
     "enc_set_option": (c_int, [c_void_p, c_int, c_int]),
     "enc_attn_fwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
-                                   c_void_p, c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p, c_void_p]),
     "enc_attn_bwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
-                                   c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 

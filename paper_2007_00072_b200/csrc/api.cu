@@ -257,7 +257,8 @@ static int check_cfg(const enc_cfg* c) {
 
 // ------------------------------------------------------------------ buffer layouts
 namespace {
-enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_N };
+enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_KB,
+               S_N };
 enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y1, F_Y2, F_N };
 enum BwdId { B_PTR, B_DY2, B_DA1, B_DH, B_DX1, B_DYO, B_DC, B_DA, B_DS, B_DQ, B_DK, B_DV, B_DQKV, B_N };
 
@@ -280,7 +281,7 @@ static Layout make_layout(const size_t* sizes, int n) {
 }
 
 struct Sizes {
-  size_t BJI, BJU, BHJK, BJ3I, BJ, ptr;
+  size_t BJI, BJU, BHJK, BJ3I, BJ, ptr, KB;
 };
 static Sizes sizes_of(const enc_dims* d, int dtype) {
   const size_t es = esize(dtype);
@@ -292,12 +293,13 @@ static Sizes sizes_of(const enc_dims* d, int dtype) {
   s.BJ3I = BJ * 3 * d->I * es;
   s.BJ = BJ * sizeof(float);
   s.ptr = (size_t)5 * d->B * d->H * sizeof(void*);
+  s.KB = (size_t)d->B * d->H * d->J * ((d->K + 31) / 32) * sizeof(uint32_t);  // keep-flag words
   return s;
 }
 static Layout saved_layout(const enc_dims* d, int dtype) {
   const Sizes s = sizes_of(d, dtype);
   const size_t sz[S_N] = {s.BJI, s.BJI, s.BJI, s.BHJK, s.BHJK, s.BJI, s.BJI,
-                          s.BJI, s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ};
+                          s.BJI, s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ, s.KB};
   return make_layout(sz, S_N);
 }
 static Layout fwd_layout(const enc_dims* d, int dtype) {
@@ -345,6 +347,7 @@ int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* v
   v->xhat2 = at(saved, L.off[S_XH2]);
   v->rstd1 = (float*)at(saved, L.off[S_R1]);
   v->rstd2 = (float*)at(saved, L.off[S_R2]);
+  v->keep_attn = (uint32_t*)at(saved, L.off[S_KB]);
   return ENC_OK;
 }
 
@@ -547,22 +550,24 @@ int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const voi
 int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
                        const void* Kt, const float* mask_bias, float p, uint64_t seed,
                        uint64_t subseq, int64_t batch_offset, void* Pout, void* A,
-                       enc_stream_t stream) {
+                       uint32_t* keep_bits, enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
   if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
   if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
   CHECK_PTRS(Q, Kt, Pout, A);
   if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if (keep_bits && ((uintptr_t)keep_bits & 7u)) return ENC_EALIGN;
   if (B == 0) return ENC_OK;
   OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
   CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias, make_philox_key(p, seed, subseq),
-                        batch_offset, Pout, A, (cudaStream_t)stream));
+                        batch_offset, Pout, A, keep_bits, (cudaStream_t)stream));
   return ENC_OK;
 }
 
 int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
                        const void* V, const void* Pin, float p, uint64_t seed, uint64_t subseq,
-                       int64_t batch_offset, void* dS, enc_stream_t stream) {
+                       int64_t batch_offset, const uint32_t* keep_bits, void* dS,
+                       enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
   if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
   if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
@@ -570,7 +575,7 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   if (B == 0) return ENC_OK;
   OpTimer _t(ctx, ENC_OP_BSB_BWD, (cudaStream_t)stream, 1);
   CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pin, make_philox_key(p, seed, subseq),
-                         batch_offset, dS, (cudaStream_t)stream));
+                         batch_offset, keep_bits, dS, (cudaStream_t)stream));
   return ENC_OK;
 }
 
@@ -666,7 +671,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
     CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias,
-                          make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+                          make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A,
+                          (uint32_t*)at(saved, SL.off[S_KB]), st));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {
@@ -861,7 +867,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
     if (fused_attn)  // Gamma dX1 (:588) + BSB-bwd (:590): dA stays in TMEM
       CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pm,
-                             make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
+                             make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff,
+                             (const uint32_t*)at(sv, SL.off[S_KB]), dS, st));
     else
       CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
                         make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));

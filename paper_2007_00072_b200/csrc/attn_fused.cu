@@ -49,6 +49,8 @@ struct FusedParams {
   float c;          // scale * log2(e)   (fwd)  |  scale  (bwd)
   int64_t g0;       // Philox chunk index of element (b=0,h=0,j=0,k=0) of this call
   const float* mask_bias;  // [B, K] or null (fwd)
+  uint32_t* keep_bits;     // [B, H, J, K/32] keep-flag words (fwd: written if non-null;
+                           // bwd: read instead of recomputing Philox when kBits)
 };
 
 __device__ __forceinline__ void qbar(int q) {   // the 8 warps of TMEM lane quarter q
@@ -68,9 +70,44 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
   return u;
 }
 
+// mask-bias load kept in program order (volatile): hoisting all 64 loads above the MMA
+// wait would spill
+__device__ __forceinline__ float4 ld_mask4(const float4* p) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+
 // 16-B chunk c (0..3) of row r in a 64-B-row tile with the 64-byte TMA swizzle
 __device__ __forceinline__ uint32_t sw64(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+}
+
+// Keep bits of the 8 elements of Philox chunk g (R5: element 2i <-> low 16-bit
+// lane of word i, 2i+1 <-> high lane; keep iff lane >= T), as a SWAR compare: with
+// C = per-lane (0x8000 - T) for T < 0x8000, x >= T  <=>  x >= 0x8000 or (x & 0x7FFF) + C has
+// bit 15 set (no carry leaves a lane), so bit 15 / 31 of ((w & 0x7FFF7FFF) + C) | w is
+// the keep bit of the low / high lane.  T >= 0x8000 (p >= 1/2): C = 0x10000 - T and AND.
+// The four words' flags are packed as: element u of the chunk -> bit (u odd ? 31 : 15)
+// - u/2, then shifted right by `sh`.
+__device__ __forceinline__ uint32_t keep_flags(uint64_t g, const PhiloxKey& pk, uint32_t C2,
+                                               bool hiT, int sh) {
+  const uint4 w = philox4x32_10(g, pk);
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  uint32_t f = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t t = (wv[i] & 0x7FFF7FFFu) + C2;
+    const uint32_t gi = (hiT ? (t & wv[i]) : (t | wv[i])) & 0x80008000u;
+    f |= gi >> (i + sh);
+  }
+  return f;
+}
+// bit of element u (0..7) of chunk j (0..3) in a 32-element flag word
+__device__ __forceinline__ constexpr int flag_bit(int j, int u) {
+  return ((u & 1) ? 31 : 15) - (u >> 1) - 4 * j;
 }
 
 // shared-memory layout (bytes from a 1024-aligned base)
@@ -78,15 +115,15 @@ __device__ __forceinline__ uint32_t sw64(int r, int c) {
 //   [16K, 80K)   K / V  tile [512 x 64] bf16 K-major SW128 (two 256-row boxes)
 //   [80K, 208K)  per-warp 4 KB regions: fwd staging ([32 x 32] P tile + A tile, SW64);
 //                bwd the warp's [32 x 64] P sub-tile (SW128), overwritten in place by dS
-//   then stats [8 slices][128 rows] float2, mask bias [512] float, barriers, tmem slot
+//   then row statistics [2 parities][8 slices][128 rows] float2, barriers, tmem slot
 constexpr uint32_t kOpA = 0, kOpB = 16384, kOpX = 81920;
 constexpr uint32_t kStats = kOpX + kWarps * 4096;
-constexpr uint32_t kMb = kStats + kSlices * kRows * 8;
-constexpr uint32_t kBars = kMb + kK * 4;
+constexpr uint32_t kBars = kStats + 2 * kSlices * kRows * 8;
 constexpr size_t kSmem = 1024 + kBars + (4 + kWarps) * 8 + 16;
 static_assert(kSmem <= 227 * 1024, "smem");
+static_assert(kW == 64, "two keep-flag words per thread");
 
-template <bool kBwd, bool kMask>
+template <bool kBwd, bool kMask, bool kBits>
 __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtensorMap& mapB,
                                            const CUtensorMap& mapP, const CUtensorMap& mapO1,
                                            const CUtensorMap& mapO2, const FusedParams& prm,
@@ -99,9 +136,10 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   const int cb = slice * kW;          // first column of this warp
   const int mtiles = prm.J / kRows;
   const bool leader = (warp == 0 && lane == 0);
+  const bool hiT = pk.T >= 0x8000u;
+  const uint32_t C2 = (hiT ? 0x10000u - pk.T : 0x8000u - pk.T) * 0x10001u;
 
-  float2* stats = reinterpret_cast<float2*>(base + kStats);   // [8][128]
-  float* mb = reinterpret_cast<float*>(base + kMb);            // [512]
+  float2* stats = reinterpret_cast<float2*>(base + kStats);   // [2][8][128]
   uint64_t* op_full = reinterpret_cast<uint64_t*>(base + kBars);
   uint64_t* op_empty = op_full + 1;
   uint64_t* tm_full = op_full + 2;
@@ -165,8 +203,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
     if (leader) {
-      // MMA of this tile once every warp released TMEM and the operands landed; then the
-      // operand loads of the next tile as soon as the MMA has read these
+      // MMA of this tile once every warp released TMEM and the operands landed
       mbar_wait(tm_empty, (it & 1) ^ 1);
       mbar_wait(op_full, it & 1);
       tc::fence_after_sync();
@@ -180,109 +217,165 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
                        tc::smem_desc(b0 + nh * 256 * 128 + k * 32, 16, 1024), idesc, k != 0);
       tc::mma_commit(tm_full);
       tc::mma_commit(op_empty);
-      if (t + (int)gridDim.x < prm.tiles) {
-        mbar_wait(op_empty, it & 1);
-        load_operands(t + gridDim.x);
-      }
     }
     __syncwarp();
-    if (kMask && !kBwd) {   // mask bias of this b (x log2 e); all warps done with the last one
-      __syncthreads();
-      for (int k = threadIdx.x; k < kK; k += kThreads) mb[k] = prm.mask_bias[(int64_t)b * kK + k] * kL2e;
-      __syncthreads();
+    // keep flags of this thread's 64 elements while the MMA runs (data independent):
+    // recomputed from Philox, or (bwd) read back from the forward's keep-bit words
+    const int64_t rowi = (int64_t)bh * prm.J + m0 + r;
+    uint32_t kf[kW / 32];
+    uint32_t* kbw = prm.keep_bits + rowi * (kK / 32) + cb / 32;
+    if (kBwd && kBits) {
+      const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(kbw));
+      kf[0] = w2.x;
+      kf[1] = w2.y;
+    } else {
+      const int64_t grow = prm.g0 + rowi * (kK / 8) + cb / 8;
+#pragma unroll
+      for (int c = 0; c < kW / 32; ++c) {
+        uint32_t f = 0;
+#pragma unroll 2   // two Philox calls in flight: more would spill at 64 registers
+        for (int j = 0; j < 4; ++j)
+          f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, hiT, 4 * j);
+        kf[c] = f;
+      }
+      if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     }
-    const int64_t grow = prm.g0 + ((int64_t)bh * prm.J + m0 + r) * (kK / 8) + cb / 8;
     mbar_wait(tm_full, it & 1);
     tc::fence_after_sync();
-    // fwd: .x is written in pass 1 and read before barrier 2, .y written in pass 2 and read
-    // before the next tile's barrier 1, so one slot set suffices
+    if (leader && t + (int)gridDim.x < prm.tiles) {   // operands free: prefetch the next tile
+      mbar_wait(op_empty, it & 1);
+      load_operands(t + gridDim.x);
+    }
+    float v[32];
     if (!kBwd) {
+      // pass 1: per sub-chunk of kSub columns, y = scale*log2e*S (+ mask), sub-chunk max
+      // m_c, e = 2^(y - m_c) back into TMEM, sub-chunk sum l_c.  The masked variant works
+      // on 16 columns at a time (the mask values would otherwise spill at 64 registers).
+      constexpr int kSub = kMask ? 16 : 32;
+      constexpr int kNs = kW / kSub;
       const float c = prm.c;
-      float v[32];
-      // pass 1: row max over this slice
-      float m = -INFINITY;
+      float mc[kNs], lc[kNs];
 #pragma unroll
-      for (int c0 = 0; c0 < kW; c0 += 32) {
-        tc::tmem_ld32(trow + c0, v);
+      for (int ch = 0; ch < kNs; ++ch) {
+        float m;
+        if (kMask) {
+          tc::tmem_ld16(trow + ch * kSub, v);
+          const float4* mb4 =
+              reinterpret_cast<const float4*>(prm.mask_bias + (int64_t)b * kK + cb + ch * kSub);
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          m = fmaxf(m, kMask ? fmaf(v[i], c, mb[cb + c0 + i]) : v[i] * c);
-      }
-      stats[slice * kRows + r].x = m;
-      qbar(q);
-      float M = stats[r].x;
+          for (int i = 0; i < 4; ++i) {
+            const float4 mm = ld_mask4(mb4 + i);
+            v[4 * i + 0] = fmaf(v[4 * i + 0], c, mm.x * kL2e);
+            v[4 * i + 1] = fmaf(v[4 * i + 1], c, mm.y * kL2e);
+            v[4 * i + 2] = fmaf(v[4 * i + 2], c, mm.z * kL2e);
+            v[4 * i + 3] = fmaf(v[4 * i + 3], c, mm.w * kL2e);
+          }
+          m = v[0];
 #pragma unroll
-      for (int s = 1; s < kSlices; ++s) M = fmaxf(M, stats[s * kRows + r].x);
-      // pass 2: e = 2^(y - M) into TMEM, row sum
-      float l = 0.f;
+          for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
+          const float mr = m == -INFINITY ? 0.f : m;
+          float l = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < kW; c0 += 32) {
-        tc::tmem_ld32(trow + c0, v);
+          for (int i = 0; i < kSub; ++i) {
+            v[i] = tc::ex2(v[i] - mr);
+            l += v[i];
+          }
+          lc[ch] = l;
+          tc::tmem_st16(trow + ch * kSub, v);
+        } else {
+          tc::tmem_ld32(trow + ch * kSub, v);
+          m = v[0];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] = tc::ex2(kMask ? fmaf(v[i], c, mb[cb + c0 + i] - M) : fmaf(v[i], c, -M));
-          l += v[i];
+          for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
+          m *= c;   // c > 0
+          float l = 0.f;
+#pragma unroll
+          for (int i = 0; i < kSub; ++i) {
+            v[i] = tc::ex2(fmaf(v[i], c, -m));
+            l += v[i];
+          }
+          lc[ch] = l;
+          tc::tmem_st32(trow + ch * kSub, v);
         }
-        tc::tmem_st32(trow + c0, v);
+        mc[ch] = m;
       }
+      float mt = mc[0];
+#pragma unroll
+      for (int ch = 1; ch < kNs; ++ch) mt = fmaxf(mt, mc[ch]);
+      const float mtr = mt == -INFINITY ? 0.f : mt;
+      float lt = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < kNs; ++ch) lt += lc[ch] * tc::ex2(mc[ch] - mtr);
+      float2* st = stats + (it & 1) * (kSlices * kRows);
+      st[slice * kRows + r] = make_float2(mt, lt);
       tc::tmem_wait_st();
-      stats[slice * kRows + r].y = l;
       qbar(q);
+      // row max M and sum L over the 8 slices
+      float M = st[r].x;
+#pragma unroll
+      for (int s2 = 1; s2 < kSlices; ++s2) M = fmaxf(M, st[s2 * kRows + r].x);
+      const float Mr = M == -INFINITY ? 0.f : M;
       float L = 0.f;
 #pragma unroll
-      for (int s = 0; s < kSlices; ++s) L += stats[s * kRows + r].y;
-      const float inv = __fdividef(1.f, L);
-      // pass 3: P and A = dropout(P), 32 columns per round through the 4 KB staging pair
+      for (int s2 = 0; s2 < kSlices; ++s2) {
+        const float2 x = st[s2 * kRows + r];
+        L += x.y * tc::ex2(x.x - Mr);
+      }
+      const float invL = __fdividef(1.f, L);
+      const float ds = pk.scale;
+      // pass 2: P = e * 2^(m_c - M) / L and A = keep ? P * scale : 0, through the staging
+      // pair, 32 columns per round
+      float fP[kNs];
 #pragma unroll
-      for (int c0 = 0; c0 < kW; c0 += 32) {
+      for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
+#pragma unroll
+      for (int ch = 0; ch < kW / 32; ++ch) {
         if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
         __syncwarp();
-        tc::tmem_ld32(trow + c0, v);
-        if (c0 + 32 >= kW) {   // last TMEM read of this tile by this warp
+        tc::tmem_ld32(trow + ch * 32, v);
+        if (ch + 1 == kW / 32) {   // last TMEM read of this tile by this warp
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) mbar_arrive(tm_empty);
         }
+        const uint32_t f = kf[ch];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float* x = v + 8 * j;
+          float x[8], a[8];
+          const float fp = fP[(ch * 32 + 8 * j) / kSub], fa = fp * ds;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) x[u] *= inv;
+          for (int u = 0; u < 8; ++u) {
+            x[u] = v[8 * j + u] * fp;
+            a[u] = ((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] * fa : 0.f;
+          }
           *reinterpret_cast<uint4*>(own + sw64(lane, j)) = pack8(x);
-          dropout8(x, (uint64_t)(grow + c0 / 8 + j), pk);
-          *reinterpret_cast<uint4*>(own + 2048 + sw64(lane, j)) = pack8(x);
+          *reinterpret_cast<uint4*>(own + 2048 + sw64(lane, j)) = pack8(a);
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tc::tma_store_4d(&mapO1, own, cb + c0, m0 + q * 32, h, b);
-          tc::tma_store_4d(&mapO2, own + 2048, cb + c0, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
           tc::bulk_commit();
         }
       }
     } else {
-      // pass 1: dot = sum_k dropout(dA)_k * P_k over this slice
+      // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
       mbar_wait(&p_full[warp], it & 1);
-      const float sc = pk.scale, scale = prm.c;
-      float v[32];
-      uint32_t kbits[kW / 32];
       float dot = 0.f;
 #pragma unroll
-      for (int c0 = 0; c0 < kW; c0 += 32) {
-        tc::tmem_ld32(trow + c0, v);
-        uint32_t word = 0;
+      for (int ch = 0; ch < kW / 32; ++ch) {
+        tc::tmem_ld32(trow + ch * 32, v);
+        const uint32_t f = kf[ch];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           float p[8];
-          const uint32_t kb = keep_bits8((uint64_t)(grow + (c0 + 8 * j) / 8), pk);
-          word |= kb << (8 * j);
           Chunk<__nv_bfloat16>::unpack(
-              *reinterpret_cast<const uint4*>(own + tc::sw128(lane, c0 / 8 + j)), p);
+              *reinterpret_cast<const uint4*>(own + tc::sw128(lane, ch * 4 + j)), p);
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            dot = fmaf(((kb >> u) & 1u) ? v[8 * j + u] * sc : 0.f, p[u], dot);
+            dot = fmaf(((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u], dot);
         }
-        kbits[c0 / 32] = word;
       }
       // row statistics alternate between the .x / .y slots by tile parity: a slot is
       // rewritten two tiles later, after every warp of the quarter passed the next barrier
@@ -291,28 +384,29 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       qbar(q);
       float D = 0.f;
 #pragma unroll
-      for (int s = 0; s < kSlices; ++s) D += st[2 * (s * kRows + r)];
-      // pass 2: dS = scale * P * (dP - D) over the P sub-tile in place
+      for (int s2 = 0; s2 < kSlices; ++s2) D += st[2 * (s2 * kRows + r)];
+      // dS = scale * P * (dP - D'),  dP = keep ? sc * dA : 0,  D' = sc * dot
+      const float ss = prm.c * pk.scale;        // scale * dropout scale
+      const float nDs = -D * ss;                // -scale * D'
+      // pass 2: dS over the P sub-tile in place
 #pragma unroll
-      for (int c0 = 0; c0 < kW; c0 += 32) {
-        tc::tmem_ld32(trow + c0, v);
-        if (c0 + 32 >= kW) {
+      for (int ch = 0; ch < kW / 32; ++ch) {
+        tc::tmem_ld32(trow + ch * 32, v);
+        if (ch + 1 == kW / 32) {
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) mbar_arrive(tm_empty);
         }
-        const uint32_t word = kbits[c0 / 32];
+        const uint32_t f = kf[ch];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          float p[8], o[8];
-          uint4* loc = reinterpret_cast<uint4*>(own + tc::sw128(lane, c0 / 8 + j));
+          float p[8];
+          uint4* loc = reinterpret_cast<uint4*>(own + tc::sw128(lane, ch * 4 + j));
           Chunk<__nv_bfloat16>::unpack(*loc, p);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const float dp = ((word >> (8 * j + u)) & 1u) ? v[8 * j + u] * sc : 0.f;
-            o[u] = scale * p[u] * (dp - D);
-          }
-          *loc = pack8(o);
+          for (int u = 0; u < 8; ++u)
+            p[u] *= ((f >> flag_bit(j, u)) & 1u) ? fmaf(v[8 * j + u], ss, nDs) : nDs;
+          *loc = pack8(p);
         }
       }
       fence_proxy_async_smem();
@@ -335,21 +429,24 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   if (warp == 0) tc::tmem_dealloc(tmem, kK);
 }
 
-template <bool kMask>
+template <bool kMask, bool kBits>
 __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_kernel(
     const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
     const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapA,
     FusedParams prm, PhiloxKey pk) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  fused_body<false, kMask>(mapQ, mapK, mapQ, mapP, mapA, prm, pk, tc::align1024(smem_raw));
+  fused_body<false, kMask, kBits>(mapQ, mapK, mapQ, mapP, mapA, prm, pk,
+                                  tc::align1024(smem_raw));
 }
 
+template <bool kBits>
 __global__ void __launch_bounds__(kThreads, 1) attn_da_bsbb_kernel(
     const __grid_constant__ CUtensorMap mapdC, const __grid_constant__ CUtensorMap mapV,
     const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapdS,
     FusedParams prm, PhiloxKey pk) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  fused_body<true, false>(mapdC, mapV, mapP, mapdS, mapdS, prm, pk, tc::align1024(smem_raw));
+  fused_body<true, false, kBits>(mapdC, mapV, mapP, mapdS, mapdS, prm, pk,
+                                 tc::align1024(smem_raw));
 }
 
 bool map4(CUtensorMap* m, const void* ptr, const uint64_t d[4], const uint64_t s[3],
@@ -405,7 +502,8 @@ bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
 
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                const void* Kt, const float* mask_bias, const PhiloxKey& pk,
-                               int64_t batch_offset, void* Pout, void* Aout, cudaStream_t st) {
+                               int64_t batch_offset, void* Pout, void* Aout, uint32_t* keep_bits,
+                               cudaStream_t st) {
   const int K = J;
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_bhrc(&mq, Q, B, H, J, P, 64, kRows) && map_bhrc(&mk, Kt, B, H, K, P, 64, 256) &&
@@ -413,22 +511,31 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
             map_bhrc(&ma, Aout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
-  FusedParams prm{H, J, tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8), mask_bias};
-  return mask_bias ? launch_persistent(attn_qk_bsb_kernel<true>, tiles, mq, mk, mp, ma, prm, pk, st)
-                   : launch_persistent(attn_qk_bsb_kernel<false>, tiles, mq, mk, mp, ma, prm, pk, st);
+  FusedParams prm{H, J, tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8), mask_bias,
+                  keep_bits};
+  if (mask_bias)
+    return keep_bits
+               ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st)
+               : launch_persistent(attn_qk_bsb_kernel<true, false>, tiles, mq, mk, mp, ma, prm, pk, st);
+  return keep_bits
+             ? launch_persistent(attn_qk_bsb_kernel<false, true>, tiles, mq, mk, mp, ma, prm, pk, st)
+             : launch_persistent(attn_qk_bsb_kernel<false, false>, tiles, mq, mk, mp, ma, prm, pk, st);
 }
 
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 const void* V, const void* Pin, const PhiloxKey& pk,
-                                int64_t batch_offset, void* dS, cudaStream_t st) {
+                                int64_t batch_offset, const uint32_t* keep_bits, void* dS,
+                                cudaStream_t st) {
   const int K = J;
   CUtensorMap mc, mv, mp, ms;
   bool ok = map_brhc(&mc, dC, B, H, J, P, kRows) && map_bhrc(&mv, V, B, H, K, P, 64, 256) &&
             map_bhrc(&mp, Pin, B, H, J, K, 64, 32) && map_bhrc(&ms, dS, B, H, J, K, 64, 32);
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
-  FusedParams prm{H, J, tiles, scale, batch_offset * (int64_t)H * J * (K / 8), nullptr};
-  return launch_persistent(attn_da_bsbb_kernel, tiles, mc, mv, mp, ms, prm, pk, st);
+  FusedParams prm{H, J, tiles, scale, batch_offset * (int64_t)H * J * (K / 8), nullptr,
+                  const_cast<uint32_t*>(keep_bits)};
+  return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st)
+                   : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st);
 }
 
 }  // namespace enc

@@ -127,12 +127,16 @@ cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, cons
 // Fused tcgen05 score kernels (attn_fused.cu): QK^T + BSB (writes P, A) and dC V^T +
 // BSB-bwd (writes dS), bf16, P == 64, J == 512.
 bool attn_fused_supported(int J, int P);
+// keep_bits: [B,H,J,K/32] keep-flag words (layout in include/encoder.h), written by the
+// forward when non-null and read by the backward instead of recomputing Philox when non-null.
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                const void* Kt, const float* mask_bias, const PhiloxKey& pk,
-                               int64_t batch_offset, void* Pout, void* Aout, cudaStream_t st);
+                               int64_t batch_offset, void* Pout, void* Aout, uint32_t* keep_bits,
+                               cudaStream_t st);
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 const void* V, const void* Pin, const PhiloxKey& pk,
-                                int64_t batch_offset, void* dS, cudaStream_t st);
+                                int64_t batch_offset, const uint32_t* keep_bits, void* dS,
+                                cudaStream_t st);
 
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.

@@ -166,12 +166,13 @@ class EncoderLayer:
         shapes = {"Q": (B, H, J, P), "K": (B, H, J, P), "V": (B, H, J, P), "P": (B, H, J, J),
                   "A": (B, H, J, J), "C": (B, J, I), "X1": (B, J, I), "xhat1": (B, J, I),
                   "h": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I), "rstd1": (B, J),
-                  "rstd2": (B, J)}
+                  "rstd2": (B, J), "keep_attn": (B, H, J, (J + 31) // 32)}
         base = self.saved.data_ptr()
         out = {}
         for n in _abi.SAVED_FIELDS:
             off = getattr(v, n) - base
-            dt = torch.float32 if n.startswith("rstd") else self.tdt
+            dt = (torch.float32 if n.startswith("rstd") else
+                  torch.int32 if n == "keep_attn" else self.tdt)
             numel = int(np.prod(shapes[n]))
             nbytes = numel * torch.empty((), dtype=dt).element_size()
             out[n] = self.saved[off:off + nbytes].view(dt).view(shapes[n])

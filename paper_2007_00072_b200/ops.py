@@ -131,14 +131,14 @@ OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH = 0, 1,
 
 
 def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
-                       Pout, A, stream=None):
+                       Pout, A, keep_bits=None, stream=None):
     check("enc_attn_fwd_fused", _abi.load().enc_attn_fwd_fused(
         ctx.ptr, B, H, J, P, scale, _p(Q), _p(K), _p(mask_bias), p, seed, subseq, batch_offset,
-        _p(Pout), _p(A), _stream(stream)))
+        _p(Pout), _p(A), _p(keep_bits), _stream(stream)))
 
 
 def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batch_offset, dS,
-                       stream=None):
+                       keep_bits=None, stream=None):
     check("enc_attn_bwd_fused", _abi.load().enc_attn_bwd_fused(
         ctx.ptr, B, H, J, P, scale, _p(dC), _p(V), _p(Pin), p, seed, subseq, batch_offset,
-        _p(dS), _stream(stream)))
+        _p(keep_bits), _p(dS), _stream(stream)))

@@ -8,6 +8,7 @@ import torch
 
 from oracle import encoder as E
 from oracle import philox
+from keepbits import decode
 from synth import make_positive_rows, make_tensor
 from tol import assert_parity
 
@@ -36,7 +37,7 @@ def host(t):
 
 @pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512), (3, 2, 512)])
 @pytest.mark.parametrize("masked", [False, True])
-@pytest.mark.parametrize("p", [0.1, 0.0])
+@pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
 def test_fused_forward(ops, ctx, B, H, J, masked, p):
     P = 64
     Q = make_tensor((B, H, J, P), 21, "bf16", std=0.8)
@@ -49,8 +50,10 @@ def test_fused_forward(ops, ctx, B, H, J, masked, p):
     boff, sub, scale = 5, 8, 0.125
     Pm = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
     A = torch.full_like(Pm, float("nan"))
+    bits = torch.full((B, H, J, J // 32), -1, dtype=torch.int32, device="cuda")
     Mt = None if M is None else torch.tensor(M, device="cuda")
-    ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, dev(Q), dev(K), Mt, p, SEED, sub, boff, Pm, A)
+    ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, dev(Q), dev(K), Mt, p, SEED, sub, boff, Pm, A,
+                           keep_bits=bits)
     torch.cuda.synchronize()
     S = Q.astype(np.float64) @ K.astype(np.float64).transpose(0, 1, 3, 2)
     Po, Ao = E.bsb_fwd(S, M, scale, p, SEED, sub, boff)
@@ -60,19 +63,32 @@ def test_fused_forward(ops, ctx, B, H, J, masked, p):
     assert_parity("A", gA, Ao, "bf16")
     keep = philox.keep_mask_tensor(S.shape, boff, p, SEED, sub)
     assert (gA[~keep] == 0).all()
+    # the stored keep-flag words are exactly the oracle's keep mask
+    assert np.array_equal(decode(bits.cpu().numpy(), J), keep)
     assert np.allclose(gP.sum(-1), 1.0, atol=2e-2)
 
 
 @pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512)])
-@pytest.mark.parametrize("p", [0.1, 0.0])
-def test_fused_backward(ops, ctx, B, H, J, p):
+@pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
+@pytest.mark.parametrize("stored", [False, True])
+def test_fused_backward(ops, ctx, B, H, J, p, stored):
+    """stored=True: the keep flags come from words the fused forward wrote (for the same
+    seed / subsequence / batch offset) instead of being regenerated."""
     P = 64
     dC = make_tensor((B, J, H, P), 31, "bf16")          # [B,J,H,P]
     V = make_tensor((B, H, J, P), 32, "bf16")
     Pm = make_positive_rows((B, H, J, J), 33, "bf16")
     boff, sub, scale = 2, 4, 0.125
     dS = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
-    ops.enc_attn_bwd_fused(ctx, B, H, J, P, scale, dev(dC), dev(V), dev(Pm), p, SEED, sub, boff, dS)
+    bits = None
+    if stored:
+        bits = torch.zeros((B, H, J, J // 32), dtype=torch.int32, device="cuda")
+        q = dev(make_tensor((B, H, J, P), 34, "bf16"))
+        junk = torch.empty((B, H, J, J), dtype=torch.bfloat16, device="cuda")
+        ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, q, q, None, p, SEED, sub, boff, junk,
+                               torch.empty_like(junk), keep_bits=bits)
+    ops.enc_attn_bwd_fused(ctx, B, H, J, P, scale, dev(dC), dev(V), dev(Pm), p, SEED, sub, boff, dS,
+                           keep_bits=bits)
     torch.cuda.synchronize()
     dA = dC.astype(np.float64).transpose(0, 2, 1, 3) @ V.astype(np.float64).transpose(0, 1, 3, 2)
     dSo = E.bsb_bwd(dA, Pm, scale, p, SEED, sub, boff)

@@ -12,7 +12,9 @@ import numpy as np
 import pytest
 import torch
 
+from keepbits import decode
 from oracle import encoder as E
+from oracle import philox
 from synth import CONFIGS, Dims, make_inputs, make_params
 from tol import assert_parity, errors
 
@@ -70,7 +72,7 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     W = {k: np.asarray(v, np.float64) for k, v in prm.items()}
     X = np.asarray(inp["X"], np.float64)
     dY = np.asarray(inp["dY"], np.float64)
-    s = {k: f64(v) for k, v in layer.saved_views().items()}
+    s = {k: f64(v) for k, v in layer.saved_views().items() if k != "keep_attn"}
     b = {k: f64(v) for k, v in layer.bwd_views().items()}
     g = {k: f64(v) for k, v in layer.grads.items()}
     pairs = []
@@ -113,6 +115,10 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     dAo = dCbh @ s["V"].transpose(0, 1, 3, 2)
     pairs += [("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
     if dtype == "bf16" and P == 64 and J == 512:
+        # fused kernels: the forward's stored keep-flag words are the oracle's mask exactly
+        kb = layer.saved_views()["keep_attn"].cpu().numpy()
+        assert np.array_equal(decode(kb, J), philox.keep_mask_tensor(
+            (B, H, J, J), boff, ocfg.p_attn, seed, sub(0))), "attention keep bits"
         # fused dC V^T + BSB-bwd kernel: dA never leaves TMEM; dS from the fp64 product
         pairs += [("dS", b["dS"], E.bsb_bwd(dAo, s["P"], sc, ocfg.p_attn, seed, sub(0), boff))]
     else:

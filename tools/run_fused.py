@@ -31,14 +31,17 @@ def main():
     Pm = torch.empty((B, H, J, J), device=dev, dtype=bf)
     A = torch.empty_like(Pm)
     dS = torch.empty_like(Pm)
+    bits = torch.zeros((B, H, J, J // 32), dtype=torch.int32, device=dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     st = torch.cuda.current_stream()
 
     def fwd():
-        ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, M, 0.1, 2007000072, 0, 0, Pm, A)
+        ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, M, 0.1, 2007000072, 0, 0, Pm, A,
+                               keep_bits=bits)
 
     def bwd():
-        ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, 0.1, 2007000072, 0, 0, dS)
+        ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, 0.1, 2007000072, 0, 0, dS,
+                               keep_bits=bits)
 
     for name, fn in (("attn_fwd_fused", fwd), ("attn_bwd_fused", bwd)):
         ts = []
