@@ -39,6 +39,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=2)
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--no-qkv-direct", action="store_true",
+                    help="separate AIB / AIB-bwd passes instead of the in-place QKV layout")
     ap.add_argument("--no-attn-bh", action="store_true",
                     help="AV / dV / dQ / dK on the tiled tcgen05 kernel instead of the "
                          "per-(b, h) streaming kernel")
@@ -197,6 +199,8 @@ def main():
     _abi.check("enc_set_option", _abi.load().enc_set_option(
         layer.ctx.ptr, 1, int(args.attn_backend == "fused")))
     _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 4, int(not args.no_attn_bh)))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 5,
+                                                            int(not args.no_qkv_direct)))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)

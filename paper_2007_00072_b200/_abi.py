@@ -42,14 +42,14 @@ class enc_grads(ctypes.Structure):
 
 
 class enc_saved_view(ctypes.Structure):
-    _fields_ = [(n, c_void_p) for n in SAVED_FIELDS]
+    _fields_ = [(n, c_void_p) for n in SAVED_FIELDS] + [("qkv_ld", c_int64)]
 
 
 BWD_FIELDS = ("dY2", "dA1", "dh", "dX1", "dYo", "dC", "dA", "dS", "dQ", "dK", "dV", "dQKV")
 
 
 class enc_bwd_view(ctypes.Structure):
-    _fields_ = [(n, c_void_p) for n in BWD_FIELDS]
+    _fields_ = [(n, c_void_p) for n in BWD_FIELDS] + [("dqkv_ld", c_int64)]
 
 
 # name -> (restype, argtypes); mirrors include/encoder.h exactly
@@ -60,8 +60,10 @@ _SIGS = {
     "enc_last_cuda_error": (c_int, []),
     "enc_version": (c_char_p, []),
     "enc_layer_sizes": (c_int, [POINTER(enc_dims), c_int, POINTER(c_size_t), POINTER(c_size_t)]),
-    "enc_saved_views": (c_int, [POINTER(enc_dims), c_int, c_void_p, POINTER(enc_saved_view)]),
-    "enc_bwd_views": (c_int, [POINTER(enc_dims), c_int, c_void_p, POINTER(enc_bwd_view)]),
+    "enc_saved_views": (c_int, [c_void_p, POINTER(enc_dims), c_int, c_void_p,
+                                POINTER(enc_saved_view)]),
+    "enc_bwd_views": (c_int, [c_void_p, POINTER(enc_dims), c_int, c_void_p,
+                              POINTER(enc_bwd_view)]),
     "encoder_layer_forward": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
                                       POINTER(enc_params), c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p]),

@@ -34,6 +34,7 @@ struct enc_ctx {
   int attn_tc = 1;           // ENC_OPT_ATTN_TC
   int attn_fused = 1;        // ENC_OPT_ATTN_FUSED
   int attn_bh = 1;           // ENC_OPT_ATTN_BH
+  int qkv_direct = 1;        // ENC_OPT_QKV_DIRECT
   LtCtx* lt = nullptr;       // cuBLASLt + measured algorithm cache (weight GEMMs)
   int use_lt = 1;            // ENC_OPT_GEMM_LT
 };
@@ -46,6 +47,18 @@ static cublasStatus_t wgemm(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt
     return lt_gemm_rm(ctx->lt, in_dt, out_dt, tA, tB, M, N, K, A, lda, B, ldb, beta, C, ldc,
                       LT_EPI_NONE, nullptr, st);
   return gemm_rm(ctx->blas, in_dt, out_dt, tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+}
+
+// Same with a cuBLASLt epilogue (LT_EPI_BIAS / LT_EPI_BGRAD_A into `bias`).  Returns false
+// (nothing launched) when the epilogue is unavailable -- cuBLAS path selected, or no
+// cuBLASLt algorithm for it -- and the caller then runs the plain contraction plus its own
+// bias kernel.
+static bool wgemm_epi(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA, bool tB,
+                      int M, int N, int K, const void* A, int lda, const void* B, int ldb,
+                      void* C, int ldc, int epi, float* bias) {
+  if (!ctx->lt || !ctx->use_lt) return false;
+  return lt_gemm_rm(ctx->lt, in_dt, out_dt, tA, tB, M, N, K, A, lda, B, ldb, 0.f, C, ldc, epi,
+                    bias, st) == CUBLAS_STATUS_SUCCESS;
 }
 
 namespace {
@@ -207,18 +220,27 @@ static ReduceWs ws_of(const enc_ctx* c) { return ReduceWs{c->red, c->red_floats,
 static bool use_bh(const enc_ctx* ctx, int J, int P) {
   return ctx->attn_bh && attn_bh_supported(J, P);
 }
+static bool tc_attn_of(const enc_ctx* ctx, int dtype, int J, int P) {
+  return ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
+}
 static cudaError_t attn_contract(const enc_ctx* ctx, int which, int B, int H, int J, int P,
-                                 const void* X, const void* Y, void* Z, cudaStream_t st) {
+                                 const void* X, int64_t ldx, const void* Y, int64_t ldy, void* Z,
+                                 int64_t ldz, cudaStream_t st) {
   if (use_bh(ctx, J, P)) {
     switch (which) {
-      case ENC_AG_AV: return launch_attn_av_bh(B, H, J, P, X, Y, Z, st);
-      case ENC_AG_DV: return launch_attn_dv_bh(B, H, J, P, X, Y, Z, st);
-      case ENC_AG_DQ: return launch_attn_dqdk_bh(B, H, J, P, X, Y, nullptr, Z, nullptr, st);
-      case ENC_AG_DK: return launch_attn_dqdk_bh(B, H, J, P, X, nullptr, Y, nullptr, Z, st);
+      case ENC_AG_AV: return launch_attn_av_bh(B, H, J, P, X, Y, ldy, Z, ldz, st);
+      case ENC_AG_DV:
+        return launch_attn_dv_bh(B, H, J, P, X, Y, ldy, Z, ldz, nullptr, 0, st);
+      case ENC_AG_DQ:
+        return launch_attn_dqdk_bh(B, H, J, P, X, Y, ldy, nullptr, 0, Z, ldz, nullptr, 0,
+                                   nullptr, nullptr, 0, st);
+      case ENC_AG_DK:
+        return launch_attn_dqdk_bh(B, H, J, P, X, nullptr, 0, Y, ldy, nullptr, 0, Z, ldz,
+                                   nullptr, nullptr, 0, st);
       default: break;
     }
   }
-  return launch_attn_gemm(which, B, H, J, P, X, Y, Z, st);
+  return launch_attn_gemm(which, B, H, J, P, X, ldx, Y, ldy, Z, ldz, st);
 }
 
 // ------------------------------------------------------------------ dims validation
@@ -329,14 +351,31 @@ int enc_layer_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* s
   return ENC_OK;
 }
 
-int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
+// The tcgen05 attention paths consume the QKV contraction output in place: Q, K, V are the
+// three column blocks of one [B, J, 3I] tensor spanning the Q, K, V regions (row stride 3I),
+// and dQ, dK, dV the blocks of dQKV.  Other paths: separate [B,H,J,P] tensors.
+static bool qkv_direct(const enc_ctx* ctx, const enc_dims* d, int dtype) {
+  return ctx->qkv_direct && tc_attn_of(ctx, dtype, d->J, d->P);
+}
+
+int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
+  if (!ctx) return ENC_ENULL;
   int r = check_dims(d, dtype);
   if (r) return r;
   if (!saved || !v) return ENC_ENULL;
   const Layout L = saved_layout(d, dtype);
-  v->Q = at(saved, L.off[S_Q]);
-  v->K = at(saved, L.off[S_K]);
-  v->V = at(saved, L.off[S_V]);
+  const size_t ies = (size_t)d->I * esize(dtype);
+  if (qkv_direct(ctx, d, dtype)) {
+    v->Q = at(saved, L.off[S_Q]);
+    v->K = at(saved, L.off[S_Q] + ies);
+    v->V = at(saved, L.off[S_Q] + 2 * ies);
+    v->qkv_ld = 3LL * d->I;
+  } else {
+    v->Q = at(saved, L.off[S_Q]);
+    v->K = at(saved, L.off[S_K]);
+    v->V = at(saved, L.off[S_V]);
+    v->qkv_ld = d->P;
+  }
   v->P = at(saved, L.off[S_P]);
   v->A = at(saved, L.off[S_A]);
   v->C = at(saved, L.off[S_C]);
@@ -351,7 +390,8 @@ int enc_saved_views(const enc_dims* d, int dtype, void* saved, enc_saved_view* v
   return ENC_OK;
 }
 
-int enc_bwd_views(const enc_dims* d, int dtype, void* scratch, enc_bwd_view* v) {
+int enc_bwd_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* scratch, enc_bwd_view* v) {
+  if (!ctx) return ENC_ENULL;
   int r = check_dims(d, dtype);
   if (r) return r;
   if (!scratch || !v) return ENC_ENULL;
@@ -364,10 +404,19 @@ int enc_bwd_views(const enc_dims* d, int dtype, void* scratch, enc_bwd_view* v) 
   v->dC = at(scratch, L.off[B_DC]);
   v->dA = at(scratch, L.off[B_DA]);
   v->dS = at(scratch, L.off[B_DS]);
-  v->dQ = at(scratch, L.off[B_DQ]);
-  v->dK = at(scratch, L.off[B_DK]);
-  v->dV = at(scratch, L.off[B_DV]);
   v->dQKV = at(scratch, L.off[B_DQKV]);
+  if (qkv_direct(ctx, d, dtype)) {
+    const size_t ies = (size_t)d->I * esize(dtype);
+    v->dQ = at(scratch, L.off[B_DQKV]);
+    v->dK = at(scratch, L.off[B_DQKV] + ies);
+    v->dV = at(scratch, L.off[B_DQKV] + 2 * ies);
+    v->dqkv_ld = 3LL * d->I;
+  } else {
+    v->dQ = at(scratch, L.off[B_DQ]);
+    v->dK = at(scratch, L.off[B_DK]);
+    v->dV = at(scratch, L.off[B_DV]);
+    v->dqkv_ld = d->P;
+  }
   return ENC_OK;
 }
 
@@ -542,7 +591,13 @@ int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const voi
   if (!attn_gemm_supported(J, P)) return ENC_EUNSUPPORTED;
   CHECK_PTRS(X, Y, Z);
   if (B == 0) return ENC_OK;
-  CK(attn_contract(ctx, which, B, H, J, P, X, Y, Z, (cudaStream_t)stream));
+  // documented layouts: Q, K, V, dQ, dK, dV head-major (ld = P), C / dC token-major
+  // [B,J,H,P] (ld = H*P)
+  const int64_t hp = (int64_t)H * P;
+  const int64_t ldx = which == ENC_AG_DA ? hp : P;
+  const int64_t ldy = which == ENC_AG_DV ? hp : P;
+  const int64_t ldz = which == ENC_AG_AV ? hp : P;
+  CK(attn_contract(ctx, which, B, H, J, P, X, ldx, Y, ldy, Z, ldz, (cudaStream_t)stream));
   ctx->launches += 1;
   return ENC_OK;
 }
@@ -559,8 +614,9 @@ int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   if (keep_bits && ((uintptr_t)keep_bits & 7u)) return ENC_EALIGN;
   if (B == 0) return ENC_OK;
   OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
-  CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias, make_philox_key(p, seed, subseq),
-                        batch_offset, Pout, A, keep_bits, (cudaStream_t)stream));
+  CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, P, Kt, P, mask_bias,
+                        make_philox_key(p, seed, subseq), batch_offset, Pout, A, keep_bits,
+                        (cudaStream_t)stream));
   return ENC_OK;
 }
 
@@ -574,8 +630,9 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   CHECK_PTRS(dC, V, Pin, dS);
   if (B == 0) return ENC_OK;
   OpTimer _t(ctx, ENC_OP_BSB_BWD, (cudaStream_t)stream, 1);
-  CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pin, make_philox_key(p, seed, subseq),
-                         batch_offset, keep_bits, dS, (cudaStream_t)stream));
+  CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, (int64_t)H * P, V, P, Pin,
+                         make_philox_key(p, seed, subseq), batch_offset, keep_bits, dS,
+                         (cudaStream_t)stream));
   return ENC_OK;
 }
 
@@ -599,6 +656,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_ATTN_BH) {
     ctx->attn_bh = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_QKV_DIRECT) {
+    ctx->qkv_direct = value ? 1 : 0;
     return ENC_OK;
   }
   return ENC_EINVAL;
@@ -653,24 +714,49 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   const uint64_t l4 = 4ull * cfg->layer_id;
   const float scale = 1.0f / sqrtf((float)P);  // DESIGN.md R3
   const int64_t boff = cfg->batch_offset;
-  const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
+  const bool tc_attn = tc_attn_of(ctx, dtype, J, P);
   const bool fused_attn = tc_attn && ctx->attn_fused && attn_fused_supported(J, P);
+  // tcgen05 paths: Q, K, V are read in place from the QKV contraction output (row stride
+  // 3I, spanning the saved Q, K, V regions); the AIB bias rides in the contraction epilogue
+  const bool direct = qkv_direct(ctx, d, dtype);
+  const int64_t ldqkv = direct ? 3LL * I : P;
+  void* QKVs = Q;
+  if (direct) {
+    Kt = (char*)QKVs + (size_t)I * es;
+    V = (char*)QKVs + 2 * (size_t)I * es;
+    if (SL.off[S_K] != SL.off[S_Q] + (size_t)BJ * I * es ||
+        SL.off[S_V] != SL.off[S_K] + (size_t)BJ * I * es)
+      return ENC_EUNSUPPORTED;   // Q, K, V regions not contiguous (cannot happen: J % 128 == 0)
+  }
 
-  // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T
+  // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T (+ bqkv, AIB :550, on the direct path)
+  // (cuBLASLt takes a bf16 output's bias in bf16: the bias is rounded to bf16 for the
+  // epilogue, R18; the conversion is one tiny kernel)
+  bool bias_done = false;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
-               QKV, 3 * I));
+    if (direct && ctx->lt && ctx->use_lt && ctx->red_floats >= (size_t)3 * I) {
+      CK(launch_f32_to_bf16(3 * I, prm->bqkv, ctx->red, st));
+      ctx->launches += 1;
+      bias_done = wgemm_epi(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I,
+                            QKVs, 3 * I, LT_EPI_BIAS, ctx->red);
+    }
+    if (!bias_done)
+      CB(wgemm(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
+               direct ? QKVs : QKV, 3 * I));
   }
-  // AIB (:550)
+  // AIB (:550): in place on the direct path unless the epilogue added the bias
   {
-    OpTimer _t(ctx, ENC_OP_AIB_FWD, st, 1);
-    CK(launch_aib_fwd(dtype, B, J, H, P, QKV, prm->bqkv, Q, Kt, V, st));
+    OpTimer _t(ctx, ENC_OP_AIB_FWD, st, direct && bias_done ? 0 : 1);
+    if (!direct)
+      CK(launch_aib_fwd(dtype, B, J, H, P, QKV, prm->bqkv, Q, Kt, V, st));
+    else if (!bias_done)
+      CK(launch_bias_rows(dtype, BJ, 3 * I, QKVs, prm->bqkv, st));
   }
   if (fused_attn) {
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
-    CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, Kt, mask_bias,
+    CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias,
                           make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A,
                           (uint32_t*)at(saved, SL.off[S_KB]), st));
   } else {
@@ -678,7 +764,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     {
       OpTimer _t(ctx, ENC_OP_GEMM_QK, st, tc_attn ? 1 : 0);
       if (tc_attn)
-        CK(launch_attn_gemm(ENC_AG_QK, B, H, J, P, Q, Kt, S, st));
+        CK(launch_attn_gemm(ENC_AG_QK, B, H, J, P, Q, ldqkv, Kt, ldqkv, S, 0, st));
       else
         CB(gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, Q, P, (long long)J * P,
                            Kt, P, (long long)K * P, 0.f, S, K, (long long)J * K, BH));
@@ -694,7 +780,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
     if (tc_attn) {
-      CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, V, C, st));
+      CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, 0, V, ldqkv, C, I, st));
     } else {
       CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
       CB(gemm_rm_batched(ctx->blas, dtype, false, false, J, P, K, 1.f, (const void* const*)ptr, K,
@@ -785,9 +871,20 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   const uint64_t l4 = 4ull * cfg->layer_id;
   const float scale = 1.0f / sqrtf((float)P);
   const int64_t boff = cfg->batch_offset;
-  const bool tc_attn = ctx->attn_tc && dtype == ENC_BF16 && attn_gemm_supported(J, P);
+  const bool tc_attn = tc_attn_of(ctx, dtype, J, P);
   const bool fused_attn = tc_attn && ctx->attn_fused && attn_fused_supported(J, P);
   const int F32 = ENC_FP32;
+  // direct QKV layout (see forward): Q, K, V read from the QKV tensor, dQ, dK, dV written
+  // straight into the column blocks of dQKV, row stride 3I
+  const bool direct = qkv_direct(ctx, d, dtype);
+  const int64_t ldqkv = direct ? 3LL * I : P;
+  if (direct) {
+    Kt = (char*)Q + (size_t)I * es;
+    V = (char*)Q + 2 * (size_t)I * es;
+    dQ = dQKV;
+    dK = (char*)dQKV + (size_t)I * es;
+    dV = (char*)dQKV + 2 * (size_t)I * es;
+  }
 
   if (parts & 1) {
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
@@ -845,7 +942,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     if (fused_attn) {
       // dA is produced inside the fused dA + BSB-bwd kernel below
     } else if (tc_attn) {
-      CK(launch_attn_gemm(ENC_AG_DA, B, H, J, P, dC, V, dA, st));
+      CK(launch_attn_gemm(ENC_AG_DA, B, H, J, P, dC, I, V, ldqkv, dA, 0, st));
     } else {
       CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, dC, dA, dV, ptr, st));
       CB(gemm_rm_batched(ctx->blas, dtype, false, true, J, K, P, 1.f,
@@ -853,10 +950,16 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                          0.f, (void* const*)(ptr + 3 * BH), K, BH));
     }
   }
+  // direct layout on the per-(b, h) kernels: AIB-bwd's bias gradient (:595) accumulates as
+  // column sums in the dV / dQ / dK epilogues (partials [B*4][3I] in the reduction space)
+  const bool bgrad_epi = direct && use_bh(ctx, J, P) && (size_t)B * 4 * 3 * I <= ws.cap_floats;
+  float* bg = ws.partials;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
-    if (tc_attn)
-      CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, dC, dV, st));
+    if (bgrad_epi)
+      CK(launch_attn_dv_bh(B, H, J, P, A, dC, I, dV, ldqkv, bg + 2 * I, 3 * I, st));
+    else if (tc_attn)
+      CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, 0, dC, I, dV, ldqkv, st));
     else
       CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
                          (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH),
@@ -866,7 +969,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   {
     OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
     if (fused_attn)  // Gamma dX1 (:588) + BSB-bwd (:590): dA stays in TMEM
-      CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, V, Pm,
+      CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, I, V, ldqkv, Pm,
                              make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff,
                              (const uint32_t*)at(sv, SL.off[S_KB]), dS, st));
     else
@@ -878,9 +981,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QK_DQ, st, tc_attn ? 1 : 0);
     if (dqdk_one_pass)   // dQ and dK from one read of dS
-      CK(launch_attn_dqdk_bh(B, H, J, P, dS, Kt, Q, dQ, dK, st));
+      CK(launch_attn_dqdk_bh(B, H, J, P, dS, Kt, ldqkv, Q, ldqkv, dQ, ldqkv, dK, ldqkv,
+                             bgrad_epi ? bg : nullptr, bgrad_epi ? bg + I : nullptr, 3 * I, st));
     else if (tc_attn)
-      CK(launch_attn_gemm(ENC_AG_DQ, B, H, J, P, dS, Kt, dQ, st));
+      CK(launch_attn_gemm(ENC_AG_DQ, B, H, J, P, dS, 0, Kt, ldqkv, dQ, ldqkv, st));
     else
       CB(gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, dS, K, (long long)J * K, Kt,
                          P, (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
@@ -890,13 +994,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     if (dqdk_one_pass) {
       // computed with dQ above
     } else if (tc_attn)
-      CK(launch_attn_gemm(ENC_AG_DK, B, H, J, P, dS, Q, dK, st));
+      CK(launch_attn_gemm(ENC_AG_DK, B, H, J, P, dS, 0, Q, ldqkv, dK, ldqkv, st));
     else
       CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,
                          (long long)J * P, 0.f, dK, P, (long long)K * P, BH));
   }
-  // AIB-bwd (:595)
-  {
+  // AIB-bwd (:595): the layout pass; on the direct path dQKV is already assembled and the
+  // bias gradient rides in the QKV dW contraction's epilogue (or a column sum below)
+  if (!direct) {
     OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
     CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, ws, st));
   }
@@ -908,8 +1013,18 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   }
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, st, 0);
-    CB(wgemm(ctx, st,dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
-               g->dWqkv, I));
+    CB(wgemm(ctx, st, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
+             g->dWqkv, I));
+  }
+  if (bgrad_epi) {
+    // finish the bias gradient: fixed-order sum of the B*4 epilogue partial rows
+    OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 1);
+    CK(launch_colsum_finalize(bg, B * 4, 3 * I, 3 * I, g->dbqkv, nullptr, nullptr, st));
+  } else if (direct) {
+    // bias gradient as a column sum of dQKV (cuBLASLt's BGRAD epilogue on the dW
+    // contraction measured slower than this separate pass)
+    OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
+    CK(launch_colsum(dtype, BJ, 3 * I, dQKV, g->dbqkv, ws, st));
   }
   return ENC_OK;
 }

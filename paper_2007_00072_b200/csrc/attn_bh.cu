@@ -36,6 +36,11 @@ struct BhParams {
   int units;           // B * H
   int row_out, col_out;  // which outputs this launch computes
   int yr_rowdim, yc_rowdim, or_rowdim, oc_rowdim;  // 4-D map dim holding the row index
+  // optional column sums of the (bf16-rounded) row / column outputs over their rows:
+  // ps_*[(b * 4 + quarter) * ps_ld + h * 64 + c], summed over b and quarter afterwards
+  float* ps_r;
+  float* ps_c;
+  int ps_ld;
 };
 
 __device__ __forceinline__ void coords(int rowdim, int inner, int row, int h, int b, int* c) {
@@ -61,8 +66,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
   unsigned char* stg_all = base + STAGES * stage_bytes;        // 4 warps x 2 x 4 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(stg_all + 4 * 2 * 4096);
   uint64_t* empty = full + STAGES;
-  uint64_t* tm_full = empty + STAGES;
-  uint64_t* tm_empty = tm_full + 1;
+  uint64_t* tm_full = empty + STAGES;   // [4]: outer tile o of the streamed output done
+  uint64_t* tm_empty = tm_full + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 1);
 
   const int warp = threadIdx.x >> 5;
@@ -70,6 +75,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
   const int nt = p.nt;
   const int nblk = nt * nt;
   const uint32_t col_off = p.row_out ? nt * 64 : 0;   // TMEM column of the column outputs
+  // Block order: the outer index is the row tile of the output that completes tile by tile
+  // (jt for C / dQ, kt when dV is the only output), so its epilogue overlaps the rest of the
+  // stream; with both dQ and dK, dK finishes with the last block.
+  const bool col_outer = p.col_out && !p.row_out;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&mapX);
@@ -79,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tm_full, 1);
+    for (int o = 0; o < 4; ++o) mbar_init(&tm_full[o], 1);
     mbar_init(tm_empty, 4);
     fence_mbar_init();
   }
@@ -96,7 +105,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         const int b = u / p.H, h = u - (u / p.H) * p.H;
         for (int blk = 0; blk < nblk; ++blk, ++g) {
-          const int jt = blk / nt, kt = blk - (blk / nt) * nt;
+          const int o = blk / nt, i = blk - (blk / nt) * nt;
+          const int jt = col_outer ? i : o, kt = col_outer ? o : i;
           const int s = g % STAGES;
           mbar_wait(&empty[s], ((g / STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], stage_bytes);
@@ -127,7 +137,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
       mbar_wait(tm_empty, (it & 1) ^ 1);   // epilogue released the accumulators
       tc::fence_after_sync();
       for (int blk = 0; blk < nblk; ++blk, ++g) {
-        const int jt = blk / nt, kt = blk - (blk / nt) * nt;
+        const int o = blk / nt, i = blk - (blk / nt) * nt;
+        const int jt = col_outer ? i : o, kt = col_outer ? o : i;
         const int s = g % STAGES;
         mbar_wait(&full[s], (g / STAGES) & 1);
         tc::fence_after_sync();
@@ -153,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
                            (jt | ks) != 0);
           }
           tc::mma_commit(&empty[s]);
-          if (blk == nblk - 1) tc::mma_commit(tm_full);
+          if (i == nt - 1) tc::mma_commit(&tm_full[o]);   // outer tile o complete
         }
         __syncwarp();
       }
@@ -165,13 +176,16 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
     int it = 0, n = 0;
     for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
       const int b = u / p.H, h = u - (u / p.H) * p.H;
-      mbar_wait(tm_full, it & 1);
-      tc::fence_after_sync();
       const int ngroups = (p.row_out ? nt : 0) + (p.col_out ? nt : 0);
+      float sr0 = 0.f, sr1 = 0.f, sc0 = 0.f, sc1 = 0.f;   // column sums (row / col output)
 #pragma unroll 1
       for (int gi = 0; gi < ngroups; ++gi, ++n) {
         const bool is_r = p.row_out && gi < nt;
         const int t = p.row_out && !is_r ? gi - nt : gi;   // row tile of this output group
+        // groups 0..nt-1 are the streamed output's tiles (outer order); the remaining
+        // (dK with dQ) need the last block
+        mbar_wait(&tm_full[gi < nt ? gi : nt - 1], it & 1);
+        tc::fence_after_sync();
         unsigned char* buf = stg + (n & 1) * 4096;
         if (lane == 0) tc::bulk_wait_read<1>();
         __syncwarp();
@@ -203,7 +217,31 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
           tc::tma_store_4d(is_r ? &mapOr : &mapOc, buf, c[0], c[1], c[2], c[3]);
           tc::bulk_commit();
         }
+        if (is_r ? p.ps_r != nullptr : p.ps_c != nullptr) {
+          // column sums of the values as stored (the bf16 staging tile), over this warp's 32
+          // rows: lane l reads the bf16 pair of columns (2l, 2l+1) of every row
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll 8
+          for (int rr = 0; rr < 32; ++rr) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(
+                buf + tc::sw128(rr, lane >> 2) + (lane & 3) * 4);
+            a0 += __uint_as_float(w << 16);
+            a1 += __uint_as_float(w & 0xFFFF0000u);
+          }
+          if (is_r) {
+            sr0 += a0;
+            sr1 += a1;
+          } else {
+            sc0 += a0;
+            sc1 += a1;
+          }
+        }
       }
+      const int64_t pso = (int64_t)(b * 4 + q) * p.ps_ld + h * 64 + 2 * lane;
+      if (p.ps_r != nullptr && p.row_out)
+        *reinterpret_cast<float2*>(p.ps_r + pso) = make_float2(sr0, sr1);
+      if (p.ps_c != nullptr && p.col_out)
+        *reinterpret_cast<float2*>(p.ps_c + pso) = make_float2(sc0, sc1);
     }
     if (lane == 0) tc::bulk_wait<0>();
     __syncwarp();
@@ -255,7 +293,7 @@ int sm_count() {
 template <int STAGES>
 cudaError_t launch_bh(const CUtensorMap* m, const BhParams& p, cudaStream_t st) {
   const uint32_t stage_bytes = kXBytes + (p.row_out ? kYBytes : 0) + (p.col_out ? kYBytes : 0);
-  const size_t smem = 1024 + STAGES * stage_bytes + 4 * 2 * 4096 + (2 * STAGES + 2) * 8 + 16;
+  const size_t smem = 1024 + STAGES * stage_bytes + 4 * 2 * 4096 + (2 * STAGES + 5) * 8 + 16;
   cudaFuncSetAttribute(attn_bh_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const int grid = p.units < sm_count() ? p.units : sm_count();
@@ -268,12 +306,12 @@ cudaError_t launch_bh(const CUtensorMap* m, const BhParams& p, cudaStream_t st) 
 // J = K keys, a multiple of 128 up to 512 (every output row tile of a (b, h) in TMEM)
 bool attn_bh_supported(int J, int P) { return P == 64 && J % 128 == 0 && J >= 128 && J <= 512; }
 
-// which: ENC_AG_AV (1): C = A V,  ENC_AG_DV (3): dV = A^T dC,
-//        ENC_AG_DQ (4): dQ = dS K,  ENC_AG_DK (5): dK = dS^T Q.
-// launch_attn_dqdk_bh computes dQ and dK from one read of dS.
+// C = A V (AV), dV = A^T dC (DV), dQ = dS K and dK = dS^T Q (DQ / DK, or both from one
+// read of dS).  P-wide operands take row strides (kernels.h, map_pop).
 static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const void* Yr,
-                             bool yr_tok, const void* Yc, bool yc_tok, void* Or, bool or_tok,
-                             void* Oc, bool oc_tok, cudaStream_t st) {
+                             int64_t ldyr, const void* Yc, int64_t ldyc, void* Or, int64_t ldor,
+                             void* Oc, int64_t ldoc, float* ps_r, float* ps_c, int ps_ld,
+                             cudaStream_t st) {
   if (!attn_bh_supported(J, P)) return cudaErrorInvalidValue;
   BhParams p{};
   p.H = H;
@@ -281,6 +319,10 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
   p.units = B * H;
   p.row_out = Or != nullptr;
   p.col_out = Oc != nullptr;
+  p.yr_rowdim = p.yc_rowdim = p.or_rowdim = p.oc_rowdim = 2;   // map_pop: (p, h, row, b)
+  p.ps_r = ps_r;
+  p.ps_c = ps_c;
+  p.ps_ld = ps_ld;
   CUtensorMap m[5];
   int rd;
   bool ok = map_op(&m[0], X, false, B, H, J, J, 128, &rd);
@@ -289,12 +331,12 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
   m[3] = m[0];
   m[4] = m[0];
   if (p.row_out) {
-    ok &= map_op(&m[1], Yr, yr_tok, B, H, J, P, 128, &p.yr_rowdim);
-    ok &= map_op(&m[3], Or, or_tok, B, H, J, P, 32, &p.or_rowdim);
+    ok &= map_pop(&m[1], Yr, B, H, J, P, ldyr, 128);
+    ok &= map_pop(&m[3], Or, B, H, J, P, ldor, 32);
   }
   if (p.col_out) {
-    ok &= map_op(&m[2], Yc, yc_tok, B, H, J, P, 128, &p.yc_rowdim);
-    ok &= map_op(&m[4], Oc, oc_tok, B, H, J, P, 32, &p.oc_rowdim);
+    ok &= map_pop(&m[2], Yc, B, H, J, P, ldyc, 128);
+    ok &= map_pop(&m[4], Oc, B, H, J, P, ldoc, 32);
   }
   if (!ok) return cudaErrorInvalidValue;
   if (p.units == 0) return cudaSuccess;
@@ -302,21 +344,24 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
   return launch_bh<4>(m, p, st);
 }
 
-cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V, void* C,
-                              cudaStream_t st) {
-  // C is token-major [B, J, H, P]
-  return bh_launch(B, H, J, P, A, V, false, nullptr, false, C, true, nullptr, false, st);
+cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
+                              int64_t ldv, void* C, int64_t ldc, cudaStream_t st) {
+  return bh_launch(B, H, J, P, A, V, ldv, nullptr, 0, C, ldc, nullptr, 0, nullptr, nullptr, 0,
+                   st);
 }
 
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
-                              void* dV, cudaStream_t st) {
-  // dC is token-major [B, J, H, P]; dV head-major [B, H, K, P]
-  return bh_launch(B, H, J, P, A, nullptr, false, dC, true, nullptr, false, dV, false, st);
+                              int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
+                              cudaStream_t st) {
+  return bh_launch(B, H, J, P, A, nullptr, 0, dC, lddc, nullptr, 0, dV, lddv, nullptr, ps_dv,
+                   ps_ld, st);
 }
 
 cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
-                                const void* Q, void* dQ, void* dK, cudaStream_t st) {
-  return bh_launch(B, H, J, P, dS, Kt, false, Q, false, dQ, false, dK, false, st);
+                                int64_t ldk, const void* Q, int64_t ldq, void* dQ, int64_t lddq,
+                                void* dK, int64_t lddk, float* ps_dq, float* ps_dk, int ps_ld,
+                                cudaStream_t st) {
+  return bh_launch(B, H, J, P, dS, Kt, ldk, Q, ldq, dQ, lddq, dK, lddk, ps_dq, ps_dk, ps_ld, st);
 }
 
 }  // namespace enc

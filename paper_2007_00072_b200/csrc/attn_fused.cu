@@ -158,12 +158,10 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
     mbar_arrive_expect_tx(op_full, (uint32_t)(kRows + kK) * 128);
-    if (!kBwd)
-      tc::tma_load_4d(base + kOpA, &mapA, op_full, 0, m0, h, b);        // Q  [B,H,J,P]
-    else
-      tc::tma_load_4d(base + kOpA, &mapA, op_full, 0, h, m0, b);        // dC [B,J,H,P]
-    tc::tma_load_4d(base + kOpB, &mapB, op_full, 0, 0, h, b);           // K or V rows 0..255
-    tc::tma_load_4d(base + kOpB + 256 * 128, &mapB, op_full, 0, 256, h, b);
+    // P-wide operand maps (map_pop): coordinates (p, h, row, b)
+    tc::tma_load_4d(base + kOpA, &mapA, op_full, 0, h, m0, b);          // Q / dC rows m0..
+    tc::tma_load_4d(base + kOpB, &mapB, op_full, 0, h, 0, b);           // K or V rows 0..255
+    tc::tma_load_4d(base + kOpB + 256 * 128, &mapB, op_full, 0, h, 256, b);
   };
   auto load_psub = [&](int t) {      // bwd: this warp's [32 x 64] P sub-tile of tile t
     int b, h, m0, bh;
@@ -470,14 +468,6 @@ bool map_bhrc(CUtensorMap* m, const void* p, int B, int H, int rows, int cols, i
   return map4(m, p, d, s, box, sw);
 }
 
-// [B][rows][H][cols] (cols = P) with box {64, 1, box_rows, 1}
-bool map_brhc(CUtensorMap* m, const void* p, int B, int H, int rows, int cols, int box_rows) {
-  const uint64_t d[4] = {(uint64_t)cols, (uint64_t)H, (uint64_t)rows, (uint64_t)B};
-  const uint64_t s[3] = {(uint64_t)cols, (uint64_t)H * cols, (uint64_t)rows * H * cols};
-  const uint32_t box[4] = {64, 1, (uint32_t)box_rows, 1};
-  return map4(m, p, d, s, box, CU_TENSOR_MAP_SWIZZLE_128B);
-}
-
 int persistent_grid(int tiles) {
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -501,12 +491,12 @@ cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const 
 bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
 
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
-                               const void* Kt, const float* mask_bias, const PhiloxKey& pk,
-                               int64_t batch_offset, void* Pout, void* Aout, uint32_t* keep_bits,
-                               cudaStream_t st) {
+                               int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
+                               const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
+                               uint32_t* keep_bits, cudaStream_t st) {
   const int K = J;
   CUtensorMap mq, mk, mp, ma;
-  bool ok = map_bhrc(&mq, Q, B, H, J, P, 64, kRows) && map_bhrc(&mk, Kt, B, H, K, P, 64, 256) &&
+  bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
             map_bhrc(&mp, Pout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B) &&
             map_bhrc(&ma, Aout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cudaErrorInvalidValue;
@@ -523,12 +513,12 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
 }
 
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
-                                const void* V, const void* Pin, const PhiloxKey& pk,
-                                int64_t batch_offset, const uint32_t* keep_bits, void* dS,
-                                cudaStream_t st) {
+                                int64_t lddc, const void* V, int64_t ldv, const void* Pin,
+                                const PhiloxKey& pk, int64_t batch_offset,
+                                const uint32_t* keep_bits, void* dS, cudaStream_t st) {
   const int K = J;
   CUtensorMap mc, mv, mp, ms;
-  bool ok = map_brhc(&mc, dC, B, H, J, P, kRows) && map_bhrc(&mv, V, B, H, K, P, 64, 256) &&
+  bool ok = map_pop(&mc, dC, B, H, J, P, lddc, kRows) && map_pop(&mv, V, B, H, K, P, ldv, 256) &&
             map_bhrc(&mp, Pin, B, H, J, K, 64, 32) && map_bhrc(&ms, dS, B, H, J, K, 64, 32);
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;

@@ -240,50 +240,56 @@ static cudaError_t launch_tile(dim3 grid, const CUtensorMap& ma, const CUtensorM
 }
 
 // which: 0 S=QK^T, 1 C=AV, 2 dA=dC V^T, 3 dV=A^T dC, 4 dQ=dS K, 5 dK=dS^T Q
-cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, const void* Y,
-                             void* Z, cudaStream_t st) {
+// P-wide operands through map_pop (coordinates (p, h, row, b): row dim 2) with their row
+// strides; [J x K] operands head-major [B,H,J,K] (row dim 1).
+cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, int64_t ldx,
+                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st) {
   const int K = J;
   AttnGemmParams p{};
   p.H = H;
   CUtensorMap ma, mb, mc;
   bool ok = true;
   int BN = 64;
+  auto pop = [&](CUtensorMap* m, const void* ptr, int rows, int64_t ld, int box, int* rowdim) {
+    *rowdim = 2;
+    return map_pop(m, ptr, B, H, rows, P, ld, box);
+  };
   switch (which) {
     case 0:  // S[J,K] = Q[J,P] K[K,P]^T : A K-major (Q rows), B K-major (K rows)
       p.M = J; p.N = K; p.Kred = P; BN = K % 256 == 0 ? 256 : 128;
-      ok &= operand_map(&ma, X, BHJX, B, H, J, P, kBM, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BHJX, B, H, K, P, BN, &p.b_rowdim);
+      ok &= pop(&ma, X, J, ldx, kBM, &p.a_rowdim);
+      ok &= pop(&mb, Y, K, ldy, BN, &p.b_rowdim);
       ok &= operand_map(&mc, Z, BHJX, B, H, J, K, 32, &p.c_rowdim);
       break;
-    case 1:  // C[J,P] = A[J,K] V[K,P] : A K-major, B MN-major (V rows = K), C in [B,J,H,P]
+    case 1:  // C[J,P] = A[J,K] V[K,P] : A K-major, B MN-major (V rows = K)
       p.M = J; p.N = P; p.Kred = K; BN = P; p.b_mn = 1;
       ok &= operand_map(&ma, X, BHJX, B, H, J, K, kBM, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BHJX, B, H, K, P, kBK, &p.b_rowdim);
-      ok &= operand_map(&mc, Z, BJHP, B, H, J, P, 32, &p.c_rowdim);
+      ok &= pop(&mb, Y, K, ldy, kBK, &p.b_rowdim);
+      ok &= pop(&mc, Z, J, ldz, 32, &p.c_rowdim);
       break;
-    case 2:  // dA[J,K] = dC[J,P] V[K,P]^T : dC in [B,J,H,P] K-major, V K-major
+    case 2:  // dA[J,K] = dC[J,P] V[K,P]^T : dC K-major, V K-major
       p.M = J; p.N = K; p.Kred = P; BN = K % 256 == 0 ? 256 : 128;
-      ok &= operand_map(&ma, X, BJHP, B, H, J, P, kBM, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BHJX, B, H, K, P, BN, &p.b_rowdim);
+      ok &= pop(&ma, X, J, ldx, kBM, &p.a_rowdim);
+      ok &= pop(&mb, Y, K, ldy, BN, &p.b_rowdim);
       ok &= operand_map(&mc, Z, BHJX, B, H, J, K, 32, &p.c_rowdim);
       break;
     case 3:  // dV[K,P] = A[J,K]^T dC[J,P] : A MN-major (rows = J = Kred), dC MN-major
       p.M = K; p.N = P; p.Kred = J; BN = P; p.a_mn = 1; p.b_mn = 1;
       ok &= operand_map(&ma, X, BHJX, B, H, J, K, kBK, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BJHP, B, H, J, P, kBK, &p.b_rowdim);
-      ok &= operand_map(&mc, Z, BHJX, B, H, K, P, 32, &p.c_rowdim);
+      ok &= pop(&mb, Y, J, ldy, kBK, &p.b_rowdim);
+      ok &= pop(&mc, Z, K, ldz, 32, &p.c_rowdim);
       break;
     case 4:  // dQ[J,P] = dS[J,K] K[K,P] : dS K-major, K MN-major
       p.M = J; p.N = P; p.Kred = K; BN = P; p.b_mn = 1;
       ok &= operand_map(&ma, X, BHJX, B, H, J, K, kBM, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BHJX, B, H, K, P, kBK, &p.b_rowdim);
-      ok &= operand_map(&mc, Z, BHJX, B, H, J, P, 32, &p.c_rowdim);
+      ok &= pop(&mb, Y, K, ldy, kBK, &p.b_rowdim);
+      ok &= pop(&mc, Z, J, ldz, 32, &p.c_rowdim);
       break;
     case 5:  // dK[K,P] = dS[J,K]^T Q[J,P] : dS MN-major (rows = J), Q MN-major
       p.M = K; p.N = P; p.Kred = J; BN = P; p.a_mn = 1; p.b_mn = 1;
       ok &= operand_map(&ma, X, BHJX, B, H, J, K, kBK, &p.a_rowdim);
-      ok &= operand_map(&mb, Y, BHJX, B, H, J, P, kBK, &p.b_rowdim);
-      ok &= operand_map(&mc, Z, BHJX, B, H, K, P, 32, &p.c_rowdim);
+      ok &= pop(&mb, Y, J, ldy, kBK, &p.b_rowdim);
+      ok &= pop(&mc, Z, K, ldz, 32, &p.c_rowdim);
       break;
     default:
       return cudaErrorInvalidValue;

@@ -20,7 +20,8 @@ enum { LT_EPI_NONE = 0, LT_EPI_BIAS = 1, LT_EPI_BGRAD_A = 2 };
 LtCtx* lt_create(void* workspace, size_t workspace_bytes);
 void lt_destroy(LtCtx* c);
 void lt_set_autotune(LtCtx* c, int on);
-// Row-major C[M,N] = op(A) op(B) + beta C; epi: LT_EPI_BIAS adds bias[N] (fp32) to every row;
+// Row-major C[M,N] = op(A) op(B) + beta C; epi: LT_EPI_BIAS adds bias[N] to every row (bias in
+// the output type: bf16 for a bf16 output, fp32 for fp32);
 // LT_EPI_BGRAD_A also writes bias[M] = sum over K of op(A) (fp32 column sums of the
 // reduction dimension).
 cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool tB, int M, int N,

@@ -95,7 +95,10 @@ cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool t
   cublasLtMatmulDescSetAttribute(d.op, CUBLASLT_MATMUL_DESC_EPILOGUE, &e, sizeof(e));
   if (epi != LT_EPI_NONE) {
     cublasLtMatmulDescSetAttribute(d.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
-    const cudaDataType_t bt = CUDA_R_32F;
+    // cuBLASLt accepts an fp32 bias only with an fp32 output: a bf16 output takes its bias
+    // in bf16 (the caller passes a bf16 vector then); bias gradients are fp32
+    const cudaDataType_t bt =
+        epi == LT_EPI_BIAS && out_dtype == 0 ? CUDA_R_16BF : CUDA_R_32F;
     cublasLtMatmulDescSetAttribute(d.op, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt));
   }
   // column-major views (see gemm.cu): Lt A = our B, Lt B = our A, D = C^T [N x M]

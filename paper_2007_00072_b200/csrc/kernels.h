@@ -56,6 +56,15 @@ cudaError_t launch_aib_bwd(int dtype, int B, int J, int H, int P, const void* dq
                            const void* dk, const void* dv, void* dqkv, float* dbqkv,
                            const ReduceWs& ws, cudaStream_t st);
 
+// X[r, :] += bias (in place, [rows, cols], cols % 8 == 0) and deterministic column sums
+// out[c] = sum_r X[r, c]: the AIB bias / bias gradient when the QKV contraction output is
+// consumed in place (ops_attn.cu).
+cudaError_t launch_bias_rows(int dtype, int64_t rows, int cols, void* X, const float* bias,
+                             cudaStream_t st);
+cudaError_t launch_colsum(int dtype, int rows, int cols, const void* X, float* out,
+                          const ReduceWs& ws, cudaStream_t st);
+cudaError_t launch_f32_to_bf16(int n, const float* src, void* dst, cudaStream_t st);
+
 cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
                            const float* mask_bias, const PhiloxKey& pk, int64_t batch_offset,
                            void* P, void* A, cudaStream_t st);
@@ -101,10 +110,11 @@ cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int 
 
 // Hand-written tcgen05 attention contractions (attn_gemm.cu), bf16 in / fp32 accumulate /
 // bf16 out.  which: 0 S=Q K^T, 1 C=A V (C in [B,J,H,P]), 2 dA=dC V^T (dC in [B,J,H,P]),
-// 3 dV=A^T dC, 4 dQ=dS K, 5 dK=dS^T Q; all other operands [B,H,rows,cols].
+// 3 dV=A^T dC, 4 dQ=dS K, 5 dK=dS^T Q; [J x K] operands [B,H,J,K]; P-wide operands with
+// row strides ldx / ldy / ldz (map_pop below; ignored for [J x K] operands).
 bool attn_gemm_supported(int J, int P);
-cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, const void* Y,
-                             void* Z, cudaStream_t st);
+cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, int64_t ldx,
+                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st);
 
 // cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
 CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,
@@ -113,30 +123,45 @@ CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32
                            CUtensorMapInterleave il, CUtensorMapSwizzle sw,
                            CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob);
 
+// P-wide attention operands (Q, K, V, C and their gradients) are described by a row
+// stride `ld` in elements: ld == P is the head-major [B][H][rows][P] layout; any other ld
+// is token-major, element (b, h, j, p) at b*rows*ld + j*ld + h*P + p (C / dC: ld = H*P;
+// Q/K/V inside the QKV GEMM output [B, J, 3, H, P]: ld = 3*H*P).
+// map_pop: bf16 TMA map with coordinates (p, h, row, b), box {64, 1, box_rows, 1}, SW128.
+bool map_pop(CUtensorMap* m, const void* ptr, int B, int H, int rows, int P, int64_t ld,
+             int box_rows);
+
 // Per-(b, h) tcgen05 contractions over the [J x K] probability / gradient matrices
 // (attn_bh.cu): one CTA streams a whole (b, h) matrix once, outputs resident in TMEM.
 // bf16, P == 64, J = K a multiple of 128 up to 512.
 bool attn_bh_supported(int J, int P);
-cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V, void* C,
-                              cudaStream_t st);
+// dQ / dK may be null (that output is skipped).  ps_* (optional): per-(b, TMEM quarter)
+// column sums of the bf16-rounded output, written at ps[(b*4 + q)*ps_ld + h*P + c] (AIB-bwd's
+// bias gradient, finished by launch_colsum_finalize over the B*4 partial rows).
+cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
+                              int64_t ldv, void* C, int64_t ldc, cudaStream_t st);
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
-                              void* dV, cudaStream_t st);
+                              int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
+                              cudaStream_t st);
 cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
-                                const void* Q, void* dQ, void* dK, cudaStream_t st);
+                                int64_t ldk, const void* Q, int64_t ldq, void* dQ, int64_t lddq,
+                                void* dK, int64_t lddk, float* ps_dq, float* ps_dk, int ps_ld,
+                                cudaStream_t st);
 
 // Fused tcgen05 score kernels (attn_fused.cu): QK^T + BSB (writes P, A) and dC V^T +
 // BSB-bwd (writes dS), bf16, P == 64, J == 512.
 bool attn_fused_supported(int J, int P);
 // keep_bits: [B,H,J,K/32] keep-flag words (layout in include/encoder.h), written by the
 // forward when non-null and read by the backward instead of recomputing Philox when non-null.
+// Q, K (fwd) and dC, V (bwd) are P-wide operands with row strides ldq, ldk, lddc, ldv.
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
-                               const void* Kt, const float* mask_bias, const PhiloxKey& pk,
-                               int64_t batch_offset, void* Pout, void* Aout, uint32_t* keep_bits,
-                               cudaStream_t st);
+                               int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
+                               const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
+                               uint32_t* keep_bits, cudaStream_t st);
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
-                                const void* V, const void* Pin, const PhiloxKey& pk,
-                                int64_t batch_offset, const uint32_t* keep_bits, void* dS,
-                                cudaStream_t st);
+                                int64_t lddc, const void* V, int64_t ldv, const void* Pin,
+                                const PhiloxKey& pk, int64_t batch_offset,
+                                const uint32_t* keep_bits, void* dS, cudaStream_t st);
 
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.

@@ -380,4 +380,112 @@ cudaError_t launch_make_attn_ptrs(int B, int H, int J, int P, size_t esize, cons
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ bias rows / column sums
+// Used when the QKV contraction writes [B*J, 3I] directly (no AIB pass) and cuBLASLt's
+// bias / bias-gradient epilogues are not in use: X[r, :] += bias (AIB's bias, :550) and
+// out = sum_r X[r, :] (AIB-bwd's bias gradient, :595), deterministic (partials + fixed-order
+// finalize).
+template <typename T>
+__global__ void __launch_bounds__(256) bias_rows_kernel(T* __restrict__ X,
+                                                        const float* __restrict__ bias,
+                                                        int64_t nchunks, int cols) {
+  const int nc = cols >> 3;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nchunks;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % nc) * 8;
+    float x[8];
+    Chunk<T>::unpack(Chunk<T>::ld(X + i * 8), x);
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(bias + c));
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(bias + c) + 1);
+    x[0] += b0.x; x[1] += b0.y; x[2] += b0.z; x[3] += b0.w;
+    x[4] += b1.x; x[5] += b1.y; x[6] += b1.z; x[7] += b1.w;
+    Chunk<T>::store(X + i * 8, x);
+  }
+}
+
+cudaError_t launch_bias_rows(int dtype, int64_t rows, int cols, void* X, const float* bias,
+                             cudaStream_t st) {
+  const int64_t nchunks = rows * (cols / 8);
+  if (nchunks == 0) return cudaSuccess;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (nchunks + 255) / 256;
+  if (grid > 8LL * (sms > 0 ? sms : 148)) grid = 8LL * (sms > 0 ? sms : 148);
+  if (dtype == 0)
+    bias_rows_kernel<__nv_bfloat16><<<(int)grid, 256, 0, st>>>((__nv_bfloat16*)X, bias, nchunks,
+                                                               cols);
+  else
+    bias_rows_kernel<float><<<(int)grid, 256, 0, st>>>((float*)X, bias, nchunks, cols);
+  return cudaGetLastError();
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
+                                   int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+cudaError_t launch_f32_to_bf16(int n, const float* src, void* dst, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
+  f32_to_bf16_kernel<<<grid, 256, 0, st>>>(src, (__nv_bfloat16*)dst, n);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) colsum_partials_kernel(const T* __restrict__ X,
+                                                              float* __restrict__ partials,
+                                                              int rows, int rpb, int cols) {
+  const int ch = blockIdx.x * blockDim.x + threadIdx.x;
+  if (ch >= (cols >> 3)) return;
+  const int col = ch << 3;
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  const int r0 = blockIdx.y * rpb;
+  const int r1 = min(rows, r0 + rpb);
+  constexpr int kU = 8;
+  for (int rb = r0; rb < r1; rb += kU) {
+    typename Chunk<T>::Raw raw[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (rb + u < r1) raw[u] = Chunk<T>::ld(X + (int64_t)(rb + u) * cols + col);
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (rb + u < r1) {
+        float x[8];
+        Chunk<T>::unpack(raw[u], x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] += x[i];
+      }
+  }
+  float* out = partials + (int64_t)blockIdx.y * cols + col;
+  reinterpret_cast<float4*>(out)[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  reinterpret_cast<float4*>(out)[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+cudaError_t launch_colsum(int dtype, int rows, int cols, const void* X, float* out,
+                          const ReduceWs& ws, cudaStream_t st) {
+  if (rows == 0) return cudaMemsetAsync(out, 0, sizeof(float) * cols, st);
+  const int gx = (cols / 8 + 127) / 128;
+  int R = (4 * ws.num_sms + gx - 1) / gx;
+  const size_t cap_rows = ws.cap_floats / (size_t)cols;
+  if ((size_t)R > cap_rows) R = (int)cap_rows;
+  if (R > rows) R = rows;
+  if (R < 1) R = 1;
+  const int rpb = (rows + R - 1) / R;
+  R = (rows + rpb - 1) / rpb;
+  dim3 grid(gx, R);
+  if (dtype == 0)
+    colsum_partials_kernel<__nv_bfloat16><<<grid, 128, 0, st>>>((const __nv_bfloat16*)X,
+                                                                ws.partials, rows, rpb, cols);
+  else
+    colsum_partials_kernel<float><<<grid, 128, 0, st>>>((const float*)X, ws.partials, rows, rpb,
+                                                        cols);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_colsum_finalize(ws.partials, R, cols, cols, out, nullptr, nullptr, st);
+}
+
 }  // namespace enc

@@ -158,18 +158,33 @@ class EncoderLayer:
             self.saved.data_ptr(), self.scratch.data_ptr(), self._stream(stream)))
 
     # ------------------------------------------------------------------ inspection
+    def _pop_view(self, buf: torch.Tensor, ptr: int, ld: int) -> torch.Tensor:
+        """[B,H,J,P] view of a P-wide attention operand with row stride `ld` (elements):
+        ld == P head-major contiguous, else token-major (include/encoder.h qkv_ld)."""
+        B, J, H, P = self.B, self.J, self.H, self.P
+        es = torch.empty((), dtype=self.tdt).element_size()
+        flat = buf.view(self.tdt)
+        off = (ptr - buf.data_ptr()) // es
+        if ld == P:
+            return flat[off:off + B * H * J * P].view(B, H, J, P)
+        return flat.as_strided((B, H, J, P), (J * ld, P, ld, 1), off)
+
     def saved_views(self) -> dict:
+        """Tensors in `saved` (valid after forward()); Q, K, V may be strided views."""
         v = _abi.enc_saved_view()
-        check("enc_saved_views", self.lib.enc_saved_views(ctypes.byref(self.dims), self.adt,
-                                                          self.saved.data_ptr(), ctypes.byref(v)))
+        check("enc_saved_views", self.lib.enc_saved_views(self.ctx.ptr, ctypes.byref(self.dims),
+                                                          self.adt, self.saved.data_ptr(),
+                                                          ctypes.byref(v)))
         B, J, H, P, I, U = self.B, self.J, self.H, self.P, self.I, self.U
-        shapes = {"Q": (B, H, J, P), "K": (B, H, J, P), "V": (B, H, J, P), "P": (B, H, J, J),
-                  "A": (B, H, J, J), "C": (B, J, I), "X1": (B, J, I), "xhat1": (B, J, I),
-                  "h": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I), "rstd1": (B, J),
-                  "rstd2": (B, J), "keep_attn": (B, H, J, (J + 31) // 32)}
+        shapes = {"P": (B, H, J, J), "A": (B, H, J, J), "C": (B, J, I), "X1": (B, J, I),
+                  "xhat1": (B, J, I), "h": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I),
+                  "rstd1": (B, J), "rstd2": (B, J), "keep_attn": (B, H, J, (J + 31) // 32)}
         base = self.saved.data_ptr()
         out = {}
         for n in _abi.SAVED_FIELDS:
+            if n in ("Q", "K", "V"):
+                out[n] = self._pop_view(self.saved, getattr(v, n), v.qkv_ld)
+                continue
             off = getattr(v, n) - base
             dt = (torch.float32 if n.startswith("rstd") else
                   torch.int32 if n == "keep_attn" else self.tdt)
@@ -179,19 +194,23 @@ class EncoderLayer:
         return out
 
     def bwd_views(self) -> dict:
-        """Backward temporaries in `scratch` (valid after backward())."""
+        """Backward temporaries in `scratch` (valid after backward()); dQ, dK, dV may be
+        strided views into dQKV."""
         v = _abi.enc_bwd_view()
-        check("enc_bwd_views", self.lib.enc_bwd_views(ctypes.byref(self.dims), self.adt,
-                                                      self.scratch.data_ptr(), ctypes.byref(v)))
+        check("enc_bwd_views", self.lib.enc_bwd_views(self.ctx.ptr, ctypes.byref(self.dims),
+                                                      self.adt, self.scratch.data_ptr(),
+                                                      ctypes.byref(v)))
         B, J, H, P, I, U = self.B, self.J, self.H, self.P, self.I, self.U
         shapes = {"dY2": (B, J, I), "dA1": (B, J, U), "dh": (B, J, U), "dX1": (B, J, I),
                   "dYo": (B, J, I), "dC": (B, J, I), "dA": (B, H, J, J), "dS": (B, H, J, J),
-                  "dQ": (B, H, J, P), "dK": (B, H, J, P), "dV": (B, H, J, P),
                   "dQKV": (B, J, 3 * I)}
         base = self.scratch.data_ptr()
         es = torch.empty((), dtype=self.tdt).element_size()
         out = {}
         for n in _abi.BWD_FIELDS:
+            if n in ("dQ", "dK", "dV"):
+                out[n] = self._pop_view(self.scratch, getattr(v, n), v.dqkv_ld)
+                continue
             off = getattr(v, n) - base
             numel = int(np.prod(shapes[n]))
             out[n] = self.scratch[off:off + numel * es].view(self.tdt).view(shapes[n])
