@@ -247,8 +247,10 @@ def main():
         for i, n in enumerate(names):
             per_op[n].append(ms_buf[i])
     per_op = {n: statistics.median(v) for n, v in per_op.items()}
+    tc_path = args.attn_backend in ("fused", "tc") and args.dtype == "bf16"
     fused = tally.fused_bytes(dims, es, fused_attn=(args.attn_backend == "fused"
-                                                    and args.dtype == "bf16"))
+                                                    and args.dtype == "bf16"),
+                              direct=tc_path and not args.no_qkv_direct)
     flops = tally.gemm_flops(dims)
     dominant = max(per_op, key=per_op.get)
     dom_id = names.index(dominant)

@@ -29,7 +29,7 @@ class enc_cfg(ctypes.Structure):
 
 PARAM_FIELDS = ("Wqkv", "Wo", "W1", "W2", "bqkv", "bo", "b1", "b2", "g1", "be1", "g2", "be2")
 GRAD_FIELDS = tuple("d" + n for n in PARAM_FIELDS)
-SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2",
+SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "Y1", "A1", "xhat2", "rstd1", "rstd2",
                 "keep_attn")
 
 

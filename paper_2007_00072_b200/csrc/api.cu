@@ -281,7 +281,7 @@ static int check_cfg(const enc_cfg* c) {
 namespace {
 enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_KB,
                S_N };
-enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y1, F_Y2, F_N };
+enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y2, F_N };
 enum BwdId { B_PTR, B_DY2, B_DA1, B_DH, B_DX1, B_DYO, B_DC, B_DA, B_DS, B_DQ, B_DK, B_DV, B_DQKV, B_N };
 
 struct Layout {
@@ -326,7 +326,7 @@ static Layout saved_layout(const enc_dims* d, int dtype) {
 }
 static Layout fwd_layout(const enc_dims* d, int dtype) {
   const Sizes s = sizes_of(d, dtype);
-  const size_t sz[F_N] = {s.ptr, s.BJ3I, s.BHJK, s.BJI, s.BJU, s.BJI};
+  const size_t sz[F_N] = {s.ptr, s.BJ3I, s.BHJK, s.BJI, s.BJI};
   return make_layout(sz, F_N);
 }
 static Layout bwd_layout(const enc_dims* d, int dtype) {
@@ -381,7 +381,7 @@ int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc
   v->C = at(saved, L.off[S_C]);
   v->X1 = at(saved, L.off[S_X1]);
   v->xhat1 = at(saved, L.off[S_XH1]);
-  v->h = at(saved, L.off[S_H]);
+  v->Y1 = at(saved, L.off[S_H]);
   v->A1 = at(saved, L.off[S_A1]);
   v->xhat2 = at(saved, L.off[S_XH2]);
   v->rstd1 = (float*)at(saved, L.off[S_R1]);
@@ -577,8 +577,8 @@ int enc_bad_bwd(enc_ctx* ctx, int dtype, int B, int J, int U, const void* dA1, c
   CHECK_PTRS(dA1, h, dh, db1);
   {
     OpTimer _t(ctx, ENC_OP_BAD_BWD, (cudaStream_t)stream, 2);
-    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, act, make_philox_key(p, seed, subseq), batch_offset,
-                      dh, db1, ws_of(ctx), (cudaStream_t)stream));
+    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, nullptr, act, make_philox_key(p, seed, subseq),
+                      batch_offset, dh, db1, ws_of(ctx), (cudaStream_t)stream));
   }
   return ENC_OK;
 }
@@ -709,7 +709,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   float *r1 = (float*)at(saved, SL.off[S_R1]), *r2 = (float*)at(saved, SL.off[S_R2]);
   void** ptr = (void**)at(scratch, FL.off[F_PTR]);
   void *QKV = at(scratch, FL.off[F_QKV]), *S = at(scratch, FL.off[F_S]);
-  void *Yo = at(scratch, FL.off[F_YO]), *Y1 = at(scratch, FL.off[F_Y1]);
+  void* Yo = at(scratch, FL.off[F_YO]);
   void* Y2 = at(scratch, FL.off[F_Y2]);
   const uint64_t l4 = 4ull * cfg->layer_id;
   const float scale = 1.0f / sqrtf((float)P);  // DESIGN.md R3
@@ -799,16 +799,17 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st));
   }
-  // Linear (:559)
+  // Linear (:559): Y1 = X1 W1^T, kept for the backward (saved.Y1): BAD-bwd recomputes the
+  // activation input h = Y1 + b1 instead of BAD storing h (one write of [B,J,U] saved)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, Y1, U));
+    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, h, U));
   }
   // BAD (:560-562)
   {
     OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 1);
-    CK(launch_bad_fwd(dtype, B, J, U, Y1, prm->b1, cfg->act,
-                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, h, A1, st));
+    CK(launch_bad_fwd(dtype, B, J, U, h, prm->b1, cfg->act,
+                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, nullptr, A1, st));
   }
   // Linear (:563)
   {
@@ -906,7 +907,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // BAD-bwd (:576-578)
   {
     OpTimer _t(ctx, ENC_OP_BAD_BWD, st, 2);
-    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, cfg->act,
+    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, prm->b1, cfg->act,
                       make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, ws, st));
   }
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)

@@ -96,7 +96,10 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* h,
                            void* A1, cudaStream_t st);
+// launch_bad_fwd: h may be null (not stored).  launch_bad_bwd: h is the activation input,
+// or with b1 non-null the pre-bias contraction output Y1 (h = Y1 + b1 recomputed).
 cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, const void* h,
+                           const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* dh,
                            float* db1, const ReduceWs& ws, cudaStream_t st);
 

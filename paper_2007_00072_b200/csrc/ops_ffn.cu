@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) bad_fwd_kernel(const T* __restrict__ Y1,
           y[j] += b[j];
           a[j] = act_f<ACT>(y[j]) * m[j];
         }
-        Chunk<T>::store(h_out + c * 8, y);
+        if (h_out != nullptr) Chunk<T>::store(h_out + c * 8, y);
         Chunk<T>::store(A1 + c * 8, a);
       }
     }
@@ -127,9 +127,11 @@ cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const
 }
 
 // ------------------------------------------------------------------ BAD backward
+// h: the activation input, or (b1 != null) the pre-bias contraction output Y1, h = Y1 + b1
 template <typename T, int ACT>
 __global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
                                                       const T* __restrict__ h,
+                                                      const float* __restrict__ b1,
                                                       T* __restrict__ dh,
                                                       float* __restrict__ partials, int rows,
                                                       int rpb, int U, int64_t g0, PhiloxKey pk) {
@@ -137,9 +139,14 @@ __global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
   const int ch = blockIdx.x * blockDim.x + threadIdx.x;
   if (ch >= ncU) return;
   const int col = ch << 3;
-  float acc[8];
+  float acc[8], bb[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  if (b1 != nullptr)
+    load_f32x8(b1 + col, bb);
+  else
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bb[j] = 0.f;
   const int r0 = blockIdx.y * rpb;
   const int r1 = min(rows, r0 + rpb);
   constexpr int kU = 4;  // rows in flight per thread
@@ -160,6 +167,8 @@ __global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
         float d[8], x[8];
         Chunk<T>::unpack(rd[u], d);
         Chunk<T>::unpack(rh[u], x);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] += bb[j];
         float m[8];
         keep_mul8((uint64_t)(g0 + (int64_t)r * ncU + ch), pk, m);
 #pragma unroll
@@ -177,8 +186,8 @@ __global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
 }
 
 cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, const void* h,
-                           int act, const PhiloxKey& pk, int64_t batch_offset, void* dh,
-                           float* db1, const ReduceWs& ws, cudaStream_t st) {
+                           const float* b1, int act, const PhiloxKey& pk, int64_t batch_offset,
+                           void* dh, float* db1, const ReduceWs& ws, cudaStream_t st) {
   const int rows = B * J;
   if (rows == 0) return cudaMemsetAsync(db1, 0, sizeof(float) * U, st);
   const int ncU = U / 8;
@@ -195,10 +204,10 @@ cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, cons
   ENC_ACT_DISPATCH(act, {
     if (dtype == 0)
       bad_bwd_kernel<__nv_bfloat16, ACT><<<grid, 128, 0, st>>>(
-          (const __nv_bfloat16*)dA1, (const __nv_bfloat16*)h, (__nv_bfloat16*)dh, ws.partials,
-          rows, rpb, U, g0, pk);
+          (const __nv_bfloat16*)dA1, (const __nv_bfloat16*)h, b1, (__nv_bfloat16*)dh,
+          ws.partials, rows, rpb, U, g0, pk);
     else
-      bad_bwd_kernel<float, ACT><<<grid, 128, 0, st>>>((const float*)dA1, (const float*)h,
+      bad_bwd_kernel<float, ACT><<<grid, 128, 0, st>>>((const float*)dA1, (const float*)h, b1,
                                                        (float*)dh, ws.partials, rows, rpb, U,
                                                        g0, pk);
   });

@@ -4,7 +4,8 @@
 // of the columns, at most 2 chunks of 8 per lane), so a warp's per-row work is a quarter of
 // the one-warp-per-row kernels in ops_ln.cu and four times as many rows are in flight per
 // SM.  Persistent CTAs of 4 groups (512 threads); each group streams its rows through a
-// 2-stage shared-memory ring filled by the bulk-copy (TMA) engine one row ahead.  The
+// 2- or 4-stage shared-memory ring filled by the bulk-copy (TMA) engine.  A lane always owns
+// the same columns, so bias / gamma / beta are loaded into registers once.  The
 // row statistics of the 4 quarters are combined through shared memory behind one named
 // barrier per row (forward: Chan's parallel mean / M2 combination, backward: the two
 // LayerNorm-gradient sums), always in quarter order, so results do not depend on timing.
@@ -22,24 +23,24 @@ namespace {
 constexpr int kGroups = 4;              // row groups per CTA
 constexpr int kGWarps = 4;              // warps per row group
 constexpr int kRgThreads = kGroups * kGWarps * 32;
-constexpr int kRgStages = 2;
+constexpr int kRgMaxStages = 4;
 
 __device__ __forceinline__ void gbar(int group) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(kGWarps * 32) : "memory");
 }
 
-// shared layout: mbar[group][stage] (64 B) | red2[group][stage][4] float4 (512 B) |
+// shared layout: mbar[group][stage] (128 B) | red2[group][stage][4] float4 (1 KB) |
 // ring[group][stage][ntens][I] T | (bwd, after the loop) colsum[group][3][I] float
-constexpr int kRgHdr = 64 + kGroups * kRgStages * kGWarps * 16;
+constexpr int kRgHdr = 128 + kGroups * kRgMaxStages * kGWarps * 16;
 
-template <typename T, int NT>
+template <typename T, int NT, int STG>
 __device__ __forceinline__ T* ring_row(unsigned char* smem, int I, int g, int s, int t) {
-  return reinterpret_cast<T*>(smem + kRgHdr) + (((size_t)g * kRgStages + s) * NT + t) * I;
+  return reinterpret_cast<T*>(smem + kRgHdr) + (((size_t)g * STG + s) * NT + t) * I;
 }
 
 // ------------------------------------------------------------------ forward
-template <typename T, int CPW>
-__global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
+template <typename T, int CPW, int STG>
+__global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_kernel(
     const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
@@ -50,30 +51,39 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
   const int g = warp / kGWarps, w = warp % kGWarps;
   const int nc = I >> 3, ncq = nc / kGWarps;          // chunks per row, per quarter
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * kRgStages;
-  float4* red = reinterpret_cast<float4*>(smem + 64) + (size_t)g * kRgStages * kGWarps;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
+  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * kGWarps;
   const int stride = gridDim.x * kGroups;
   const int first = blockIdx.x * kGroups + g;
   const bool leader = (w == 0 && lane == 0);
   if (leader) {
-    for (int s = 0; s < kRgStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < STG; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
-    for (int s = 0; s < kRgStages; ++s) {
+    for (int s = 0; s < STG; ++s) {
       const int r = first + s * stride;
       if (r < rows) {
         mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), Y + (int64_t)r * I, row_bytes, &bar[s]);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), R + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 0), Y + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 1), R + (int64_t)r * I, row_bytes, &bar[s]);
       }
     }
+  }
+  // this lane's columns are the same for every row: parameters into registers once
+  float pb[CPW][8], pg[CPW][8], pe[CPW][8];
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int ch = w * ncq + min(lane + 32 * i, ncq - 1);
+    load_f32x8(bias + ch * 8, pb[i]);
+    load_f32x8(gamma + ch * 8, pg[i]);
+    load_f32x8(beta + ch * 8, pe[i]);
   }
   gbar(g);
   int k = 0;
   for (int row = first; row < rows; row += stride, ++k) {
-    const int s = k & 1;
-    mbar_wait(&bar[s], (uint32_t)(k >> 1) & 1u);
-    const T* sy = ring_row<T, 2>(smem, I, g, s, 0);
-    const T* sr = ring_row<T, 2>(smem, I, g, s, 1);
+    const int s = k % STG;
+    mbar_wait(&bar[s], (uint32_t)(k / STG) & 1u);
+    const T* sy = ring_row<T, 2, STG>(smem, I, g, s, 0);
+    const T* sr = ring_row<T, 2, STG>(smem, I, g, s, 1);
     float z[CPW][8];
     float lsum = 0.f;
 #pragma unroll
@@ -81,14 +91,13 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
       const int cq = lane + 32 * i;
       if (cq < ncq) {
         const int ch = w * ncq + cq;
-        float y[8], b[8], m[8];
+        float y[8], m[8];
         C::unpack(C::ld_smem(sy + ch * 8), y);
         C::unpack(C::ld_smem(sr + ch * 8), z[i]);
-        load_f32x8(bias + ch * 8, b);
         keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          z[i][j] = fmaf(y[j] + b[j], m[j], z[i][j]);
+          z[i][j] = fmaf(y[j] + pb[i][j], m[j], z[i][j]);
           lsum += z[i][j];
         }
       }
@@ -111,12 +120,12 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
     if (lane == 0) red[s * kGWarps + w] = make_float4(qmean, m2, 0.f, 0.f);
     gbar(g);   // quarter stats visible; every warp of the group has read this ring stage
     if (leader) {
-      const int nr = row + kRgStages * stride;
+      const int nr = row + STG * stride;
       if (nr < rows) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), Y + (int64_t)nr * I, row_bytes, &bar[s]);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), R + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 0), Y + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 1), R + (int64_t)nr * I, row_bytes, &bar[s]);
       }
     }
     float mean = 0.f;
@@ -137,13 +146,11 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
       const int cq = lane + 32 * i;
       if (cq < ncq) {
         const int ch = w * ncq + cq;
-        float gm[8], be[8], xh[8], o[8];
-        load_f32x8(gamma + ch * 8, gm);
-        load_f32x8(beta + ch * 8, be);
+        float xh[8], o[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           xh[j] = (z[i][j] - mean) * rstd;
-          o[j] = fmaf(gm[j], xh[j], be[j]);
+          o[j] = fmaf(pg[i][j], xh[j], pe[i][j]);
         }
         C::store(out + base + ch * 8, o);
         C::store(xhat + base + ch * 8, xh);
@@ -154,8 +161,8 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_fwd_rg_kernel(
 }
 
 // ------------------------------------------------------------------ backward
-template <typename T, int CPW>
-__global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
+template <typename T, int CPW, int STG>
+__global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
     float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk) {
@@ -166,20 +173,20 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
   const int nc = I >> 3, ncq = nc / kGWarps;
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
   const float inv_n = 1.f / (float)I;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * kRgStages;
-  float4* red = reinterpret_cast<float4*>(smem + 64) + (size_t)g * kRgStages * kGWarps;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
+  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * kGWarps;
   const int stride = gridDim.x * kGroups;
   const int first = blockIdx.x * kGroups + g;
   const bool leader = (w == 0 && lane == 0);
   if (leader) {
-    for (int s = 0; s < kRgStages; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < STG; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
-    for (int s = 0; s < kRgStages; ++s) {
+    for (int s = 0; s < STG; ++s) {
       const int r = first + s * stride;
       if (r < rows) {
         mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), dOut + (int64_t)r * I, row_bytes, &bar[s]);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), xhat + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 0), dOut + (int64_t)r * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 1), xhat + (int64_t)r * I, row_bytes, &bar[s]);
       }
     }
   }
@@ -191,10 +198,11 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
     for (int j = 0; j < 8; ++j) acc_g[i][j] = acc_b[i][j] = acc_d[i][j] = 0.f;
   int k = 0;
   for (int row = first; row < rows; row += stride, ++k) {
-    const int s = k & 1;
-    mbar_wait(&bar[s], (uint32_t)(k >> 1) & 1u);
-    const T* sg = ring_row<T, 2>(smem, I, g, s, 0);
-    const T* sx = ring_row<T, 2>(smem, I, g, s, 1);
+    const int s = k % STG;
+    const float rs = __ldg(rstd + row);   // issued early: used after the row reduction
+    mbar_wait(&bar[s], (uint32_t)(k / STG) & 1u);
+    const T* sg = ring_row<T, 2, STG>(smem, I, g, s, 0);
+    const T* sx = ring_row<T, 2, STG>(smem, I, g, s, 1);
     float go[CPW][8], xh[CPW][8];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
       const int cq = lane + 32 * i;
       if (cq < ncq) {
         const int ch = w * ncq + cq;
-        float gm[8];
+        float gm[8];   // (gamma per row from L1: 24 accumulators already hold registers)
         C::unpack(C::ld_smem(sg + ch * 8), go[i]);
         C::unpack(C::ld_smem(sx + ch * 8), xh[i]);
         load_f32x8(gamma + ch * 8, gm);
@@ -221,12 +229,12 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
     if (lane == 0) red[s * kGWarps + w] = make_float4(s1, s2, 0.f, 0.f);
     gbar(g);
     if (leader) {
-      const int nr = row + kRgStages * stride;
+      const int nr = row + STG * stride;
       if (nr < rows) {
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&bar[s], 2 * row_bytes);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 0), dOut + (int64_t)nr * I, row_bytes, &bar[s]);
-        bulk_g2s(ring_row<T, 2>(smem, I, g, s, 1), xhat + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 0), dOut + (int64_t)nr * I, row_bytes, &bar[s]);
+        bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 1), xhat + (int64_t)nr * I, row_bytes, &bar[s]);
       }
     }
     float t1 = 0.f, t2 = 0.f;
@@ -237,7 +245,6 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
       t2 += st.y;
     }
     const float mg = t1 * inv_n, mgx = t2 * inv_n;
-    const float rs = __ldg(rstd + row);
     const int64_t base = (int64_t)row * I;
 #pragma unroll
     for (int i = 0; i < CPW; ++i) {
@@ -287,8 +294,13 @@ __global__ void __launch_bounds__(kRgThreads) bdrln_bwd_rg_kernel(
   }
 }
 
+// ring depth: 4 stages when the ring stays within ~96 KB (two CTAs per SM), else 2
+int rg_stages(int I, size_t es) {
+  return (size_t)kGroups * 4 * 2 * I * es <= 96 * 1024 ? 4 : 2;
+}
+
 size_t rg_smem(int I, size_t es, bool bwd) {
-  const size_t ring = (size_t)kGroups * kRgStages * 2 * I * es;
+  const size_t ring = (size_t)kGroups * rg_stages(I, es) * 2 * I * es;
   const size_t cols = bwd ? (size_t)kGroups * 3 * I * sizeof(float) : 0;
   return kRgHdr + (ring > cols ? ring : cols);
 }
@@ -318,6 +330,11 @@ bool bdrln_rg_supported(int I) { return I % 32 == 0 && I <= 2048; }
     if ((ncq) <= 32) { constexpr int CPW = 1; __VA_ARGS__; }   \
     else { constexpr int CPW = 2; __VA_ARGS__; }               \
   } while (0)
+#define ENC_STG_DISPATCH(stg, ...)                             \
+  do {                                                         \
+    if ((stg) == 4) { constexpr int STG = 4; __VA_ARGS__; }    \
+    else { constexpr int STG = 2; __VA_ARGS__; }               \
+  } while (0)
 
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
@@ -327,19 +344,20 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false);
-  ENC_CPW_DISPATCH(nc / 4, {
+  const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
+  ENC_CPW_DISPATCH(nc / 4, ENC_STG_DISPATCH(stg, {
     if (dtype == 0) {
-      auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW>;
+      auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG>;
       kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
           (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
           (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk);
     } else {
-      auto kern = bdrln_fwd_rg_kernel<float, CPW>;
+      auto kern = bdrln_fwd_rg_kernel<float, CPW, STG>;
       kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
           (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat, rstd,
           rows, I, eps, g0, pk);
     }
-  });
+  }));
   return cudaGetLastError();
 }
 
@@ -354,22 +372,23 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
   const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, true);
   const int cap = (int)(ws.cap_floats / (size_t)(3 * I));
   int G = 1;
-  ENC_CPW_DISPATCH(nc / 4, {
+  const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
+  ENC_CPW_DISPATCH(nc / 4, ENC_STG_DISPATCH(stg, {
     if (dtype == 0) {
-      auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW>;
+      auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW, STG>;
       G = rg_grid(kern, rows, smem);
       if (G > cap) G = cap;
       kern<<<G, kRgThreads, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
                                         rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
                                         ws.partials, rows, I, g0, pk);
     } else {
-      auto kern = bdrln_bwd_rg_kernel<float, CPW>;
+      auto kern = bdrln_bwd_rg_kernel<float, CPW, STG>;
       G = rg_grid(kern, rows, smem);
       if (G > cap) G = cap;
       kern<<<G, kRgThreads, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
                                         (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
     }
-  });
+  }));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_colsum_finalize(ws.partials, G, 3 * I, I, dgamma, dbeta, dbias, st);

@@ -2,7 +2,8 @@
 DESIGN.md; no compute).
 
 Algorithmic bytes = the bytes the fused operator must move given its inputs/outputs in
-HBM (masks regenerated, never stored): SURVEY.md 8(d) "Algorithmic bytes per token".
+HBM: SURVEY.md 8(d) "Algorithmic bytes per token".  BDRLN / BAD masks are regenerated;
+the fused attention kernels store / read the attention keep mask as 1-bit words.
 Flops of the contractions follow Table A.1, e.g. Q,K,V = 2*3*B*J*I*I.
 """
 from __future__ import annotations
@@ -13,30 +14,35 @@ def _d(d):
     return B, J, H, P, H * P, U
 
 
-def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = False) -> dict:
+def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = False,
+                direct: bool = False) -> dict:
     """Algorithmic HBM bytes per launch of each fused operator (es = activation bytes).
     fused_attn: BSB / BSB-bwd run fused with their contraction (QK^T + BSB reads Q, K and
-    writes P, A; dC V^T + BSB-bwd reads dC, V, P and writes dS)."""
+    writes P, A and the keep bits; dC V^T + BSB-bwd reads dC, V, P and the keep bits and
+    writes dS).  direct: AIB / AIB-bwd are fused into the QKV contraction epilogue and the
+    attention kernels (no separate pass: 0 bytes).  BAD-fwd reads Y1 and writes A1 (the
+    activation input is recomputed by BAD-bwd from Y1 + b1)."""
     B, J, H, P, I, U = _d(d)
     BJ, BJI, BJU, BHJK = B * J, B * J * I, B * J * U, B * H * J * J
     f = 4  # fp32
     if fused_attn:
-        bsb_f = 2 * BJI * es + 2 * BHJK * es + (B * J * f if mask_bias else 0)
-        bsb_b = 2 * BJI * es + 2 * BHJK * es
+        bits = BHJK // 8
+        bsb_f = 2 * BJI * es + 2 * BHJK * es + bits + (B * J * f if mask_bias else 0)
+        bsb_b = 2 * BJI * es + 2 * BHJK * es + bits
     else:
         bsb_f = 3 * BHJK * es + (B * J * f if mask_bias else 0)
         bsb_b = 3 * BHJK * es
     return {
-        "aib_fwd": 2 * BJ * 3 * I * es + 3 * I * f,
+        "aib_fwd": 0 if direct else 2 * BJ * 3 * I * es + 3 * I * f,
         "bsb_fwd": bsb_f,
         "bdrln_fwd1": 4 * BJI * es + BJ * f + 3 * I * f,
-        "bad_fwd": 3 * BJU * es + U * f,
+        "bad_fwd": 2 * BJU * es + U * f,
         "bdrln_fwd2": 4 * BJI * es + BJ * f + 3 * I * f,
         "bdrln_bwd2": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
         "bad_bwd": 3 * BJU * es + U * f,
         "bdrln_bwd1": 4 * BJI * es + BJ * f + I * f + 3 * I * f,
         "bsb_bwd": bsb_b,
-        "aib_bwd": 2 * BJ * 3 * I * es + 3 * I * f,
+        "aib_bwd": 0 if direct else 2 * BJ * 3 * I * es + 3 * I * f,
     }
 
 

@@ -57,9 +57,12 @@ def _end_to_end(dims, dtype, act, key_padding, **kw):
         gpu["d" + n] = f64(layer.grads[n])
         ref["d" + n] = go[n]
     s = layer.saved_views()
-    for n in ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2"):
+    for n in ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "A1", "xhat2", "rstd1", "rstd2"):
         gpu["saved." + n] = f64(s[n])
         ref["saved." + n] = sv[n]
+    # the layer keeps the pre-bias Y1 = X1 W1^T; the oracle's saved h = Y1 + b1
+    gpu["saved.h"] = f64(s["Y1"]) + np.asarray(prm["b1"], np.float64)
+    ref["saved.h"] = sv["h"]
     return gpu, ref
 
 
@@ -88,8 +91,9 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     X1o, xh1o, r1o = E.bdrln_fwd(s["C"] @ W["Wo"].T, W["bo"], X, W["g1"], W["be1"],
                                  ocfg.ln_eps, ocfg.p_hidden, seed, sub(1), boff)
     pairs += [("X1", s["X1"], X1o), ("xhat1", s["xhat1"], xh1o)]
-    ho, A1o = E.bad_fwd(s["X1"] @ W["W1"].T, W["b1"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
-    pairs += [("h", s["h"], ho), ("A1", s["A1"], A1o)]
+    pairs += [("Y1", s["Y1"], s["X1"] @ W["W1"].T)]
+    _, A1o = E.bad_fwd(s["Y1"], W["b1"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
+    pairs += [("A1", s["A1"], A1o)]
     Yo, xh2o, r2o = E.bdrln_fwd(s["A1"] @ W["W2"].T, W["b2"], s["X1"], W["g2"], W["be2"],
                                 ocfg.ln_eps, ocfg.p_hidden, seed, sub(3), boff)
     pairs += [("Y", Y, Yo), ("xhat2", s["xhat2"], xh2o)]
@@ -101,7 +105,7 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
               ("db2", g["b2"], db2o)]
     pairs += [("dA1", b["dA1"], b["dY2"] @ W["W2"]),
               ("dW2", g["W2"], np.einsum("bji,bju->iu", b["dY2"], s["A1"]))]
-    dho, db1o = E.bad_bwd(b["dA1"], s["h"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
+    dho, db1o = E.bad_bwd(b["dA1"], s["Y1"] + W["b1"], ocfg.act, ocfg.p_ffn, seed, sub(2), boff)
     pairs += [("dh", b["dh"], dho), ("db1", g["b1"], db1o)]
     pairs += [("dX1", b["dX1"], b["dh"] @ W["W1"] + dz2o),
               ("dW1", g["W1"], np.einsum("bju,bji->ui", b["dh"], s["X1"]))]

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--B", type=int, default=8)
     ap.add_argument("--mask", action="store_true")
+    ap.add_argument("--p", type=float, default=0.1)
     args = ap.parse_args()
     import torch
     from paper_2007_00072_b200 import ops
@@ -36,11 +37,11 @@ def main():
     st = torch.cuda.current_stream()
 
     def fwd():
-        ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, M, 0.1, 2007000072, 0, 0, Pm, A,
+        ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, M, args.p, 2007000072, 0, 0, Pm, A,
                                keep_bits=bits)
 
     def bwd():
-        ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, 0.1, 2007000072, 0, 0, dS,
+        ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, args.p, 2007000072, 0, 0, dS,
                                keep_bits=bits)
 
     for name, fn in (("attn_fwd_fused", fwd), ("attn_bwd_fused", bwd)):
