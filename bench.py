@@ -37,7 +37,7 @@ def parse():
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-samples", type=int, default=2)
+    ap.add_argument("--cpu-samples", type=int, default=6)  # ~13 s of oracle work
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
     ap.add_argument("--no-qkv-direct", action="store_true",
                     help="separate AIB / AIB-bwd passes instead of the in-place QKV layout")

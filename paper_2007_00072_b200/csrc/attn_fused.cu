@@ -28,7 +28,6 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "kernels.h"
 #include "tc_gemm.cuh"
@@ -52,7 +51,6 @@ struct FusedParams {
   const float* mask_bias;  // [B, K] or null (fwd)
   uint32_t* keep_bits;     // [B, H, J, K/32] keep-flag words (fwd: written if non-null;
                            // bwd: read instead of recomputing Philox when kBits)
-  int dbg;
 };
 
 __device__ __forceinline__ void qbar(int q) {   // the 8 warps of TMEM lane quarter q
@@ -357,8 +355,8 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (!(prm.dbg & 2)) tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
-          if (!(prm.dbg & 1)) tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
           tc::bulk_commit();
         }
       }
@@ -507,7 +505,7 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H, J, tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8), mask_bias,
-                  keep_bits, getenv("ENC_DBG") ? atoi(getenv("ENC_DBG")) : 0};
+                  keep_bits};
   if (mask_bias)
     return keep_bits
                ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st)
