@@ -92,16 +92,18 @@ __device__ __forceinline__ uint32_t sw64(int r, int c) {
 // the keep bit of the low / high lane.  T >= 0x8000 (p >= 1/2): C = 0x10000 - T and AND.
 // The four words' flags are packed as: element u of the chunk -> bit (u odd ? 31 : 15)
 // - u/2, then shifted right by `sh`.
+// X = all ones for T < 0x8000 (OR), 0 for T >= 0x8000 (AND): (t & w) | ((t | w) & X) is
+// one LOP3; the flag bits are then masked as they are merged.
 __device__ __forceinline__ uint32_t keep_flags(uint64_t g, const PhiloxKey& pk, uint32_t C2,
-                                               bool hiT, int sh) {
+                                               uint32_t X, int sh) {
   const uint4 w = philox4x32_10(g, pk);
   const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
   uint32_t f = 0;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t t = (wv[i] & 0x7FFF7FFFu) + C2;
-    const uint32_t gi = (hiT ? (t & wv[i]) : (t | wv[i])) & 0x80008000u;
-    f |= gi >> (i + sh);
+    const uint32_t gi = (t & wv[i]) | ((t | wv[i]) & X);
+    f |= (gi >> (i + sh)) & (0x80008000u >> (i + sh));
   }
   return f;
 }
@@ -138,6 +140,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   const bool leader = (warp == 0 && lane == 0);
   const bool hiT = pk.T >= 0x8000u;
   const uint32_t C2 = (hiT ? 0x10000u - pk.T : 0x8000u - pk.T) * 0x10001u;
+  const uint32_t X = hiT ? 0u : 0xFFFFFFFFu;
 
   float2* stats = reinterpret_cast<float2*>(base + kStats);   // [2][8][128]
   uint64_t* op_full = reinterpret_cast<uint64_t*>(base + kBars);
@@ -236,12 +239,12 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
         uint32_t f = 0;
 #pragma unroll 2   // two Philox calls in flight: more would spill at 64 registers
         for (int j = 0; j < 4; ++j)
-          f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, hiT, 4 * j);
+          f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, X, 4 * j);
         kf[c] = f;
       }
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     }
-    mbar_wait(tm_full, it & 1);
+    mbar_wait_sleep(tm_full, it & 1);
     tc::fence_after_sync();
     if (leader && t + (int)gridDim.x < prm.tiles) {   // operands free: prefetch the next tile
       mbar_wait(op_empty, it & 1);
@@ -362,7 +365,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       }
     } else {
       // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
-      mbar_wait(&p_full[warp], it & 1);
+      mbar_wait_sleep(&p_full[warp], it & 1);
       float dot = 0.f;
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {

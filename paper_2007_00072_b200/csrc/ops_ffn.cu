@@ -129,7 +129,7 @@ cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const
 // ------------------------------------------------------------------ BAD backward
 // h: the activation input, or (b1 != null) the pre-bias contraction output Y1, h = Y1 + b1
 template <typename T, int ACT>
-__global__ void __launch_bounds__(128) bad_bwd_kernel(const T* __restrict__ dA1,
+__global__ void __launch_bounds__(128, sizeof(T) == 2 ? 8 : 4) bad_bwd_kernel(const T* __restrict__ dA1,
                                                       const T* __restrict__ h,
                                                       const float* __restrict__ b1,
                                                       T* __restrict__ dh,

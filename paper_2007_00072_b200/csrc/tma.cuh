@@ -43,6 +43,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Same, but each try_wait may suspend the thread until the phase completes (up to
+// `hint_ns`): for many warps waiting on one barrier, fewer polling instructions are issued.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase,
+                                                uint32_t hint_ns = 1000000u) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(hint_ns)
+      : "memory");
+}
+
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-B aligned),
 // completing on `bar`; L2 evict-first hint (streamed once).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
