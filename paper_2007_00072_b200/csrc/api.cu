@@ -228,9 +228,9 @@ static cudaError_t attn_contract(const enc_ctx* ctx, int which, int B, int H, in
                                  int64_t ldz, cudaStream_t st) {
   if (use_bh(ctx, J, P)) {
     switch (which) {
-      case ENC_AG_AV: return launch_attn_av_bh(B, H, J, P, X, Y, ldy, Z, ldz, st);
+      case ENC_AG_AV: return launch_attn_av_bh(B, H, J, P, X, Y, ldy, Z, ldz, nullptr, 1.f, st);
       case ENC_AG_DV:
-        return launch_attn_dv_bh(B, H, J, P, X, Y, ldy, Z, ldz, nullptr, 0, st);
+        return launch_attn_dv_bh(B, H, J, P, X, Y, ldy, Z, ldz, nullptr, 0, nullptr, 1.f, st);
       case ENC_AG_DQ:
         return launch_attn_dqdk_bh(B, H, J, P, X, Y, ldy, nullptr, 0, Z, ldz, nullptr, 0,
                                    nullptr, nullptr, 0, st);
@@ -609,7 +609,7 @@ int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   if (!ctx) return ENC_ENULL;
   if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
   if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
-  CHECK_PTRS(Q, Kt, Pout, A);
+  CHECK_PTRS(Q, Kt, Pout);   // A optional
   if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
   if (keep_bits && ((uintptr_t)keep_bits & 7u)) return ENC_EALIGN;
   if (B == 0) return ENC_OK;
@@ -753,12 +753,16 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     else if (!bias_done)
       CK(launch_bias_rows(dtype, BJ, 3 * I, QKVs, prm->bqkv, st));
   }
+  // fused + per-(b, h) path: A = dropout(P) is never stored -- the A V (and backward
+  // A^T dC) contraction applies the stored keep bits to P while it is in shared memory
+  const bool drop_on_load = fused_attn && use_bh(ctx, J, P);
+  const PhiloxKey pk_attn = make_philox_key(cfg->p_attn, cfg->seed, l4 + 0);
+  uint32_t* kbits = (uint32_t*)at(saved, SL.off[S_KB]);
   if (fused_attn) {
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
-    CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias,
-                          make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A,
-                          (uint32_t*)at(saved, SL.off[S_KB]), st));
+    CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias, pk_attn, boff, Pm,
+                          drop_on_load ? nullptr : A, kbits, st));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {
@@ -779,7 +783,9 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
-    if (tc_attn) {
+    if (drop_on_load) {
+      CK(launch_attn_av_bh(B, H, J, P, Pm, V, ldqkv, C, I, kbits, pk_attn.scale, st));
+    } else if (tc_attn) {
       CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, 0, V, ldqkv, C, I, st));
     } else {
       CK(launch_make_attn_ptrs(B, H, J, P, es, A, V, C, nullptr, nullptr, ptr, st));
@@ -957,8 +963,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   float* bg = ws.partials;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
-    if (bgrad_epi)
-      CK(launch_attn_dv_bh(B, H, J, P, A, dC, I, dV, ldqkv, bg + 2 * I, 3 * I, st));
+    if (fused_attn && use_bh(ctx, J, P))   // A was never stored: dropout on load from P
+      CK(launch_attn_dv_bh(B, H, J, P, Pm, dC, I, dV, ldqkv, bgrad_epi ? bg + 2 * I : nullptr,
+                           3 * I, (const uint32_t*)at(sv, SL.off[S_KB]),
+                           make_philox_key(cfg->p_attn, cfg->seed, l4 + 0).scale, st));
+    else if (bgrad_epi)
+      CK(launch_attn_dv_bh(B, H, J, P, A, dC, I, dV, ldqkv, bg + 2 * I, 3 * I, nullptr, 1.f,
+                           st));
     else if (tc_attn)
       CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, 0, dC, I, dV, ldqkv, st));
     else

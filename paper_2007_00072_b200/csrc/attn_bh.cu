@@ -27,7 +27,8 @@
 namespace enc {
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kXfWarps = 8;   // dropout-on-load: zero the dropped elements of each X block
+constexpr int kThreads = 192 + kXfWarps * 32;
 constexpr uint32_t kXBytes = 128 * 128 * 2;  // one 128 x 128 block (two 64-column boxes)
 constexpr uint32_t kYBytes = 128 * 64 * 2;   // one 128-row x 64 operand block
 
@@ -41,7 +42,19 @@ struct BhParams {
   float* ps_r;
   float* ps_c;
   int ps_ld;
+  // dropout applied on load (A = keep ? P * s : 0 from the stored P and keep words): the
+  // transform warps zero the dropped elements of each X block in shared memory before the
+  // MMA, and the epilogue multiplies the fp32 accumulators by out_scale (= s)
+  const uint32_t* keep;   // [B*H*J, K/32] ENC_KEEP_BITS words, or null (X used as is)
+  float out_scale;
 };
+
+// 0xFFFF / 0x0000 per 16-bit half from the sign bits 15 and 31 (prmt sign replication)
+__device__ __forceinline__ uint32_t half_mask(uint32_t g) {
+  uint32_t m;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(g));
+  return m;
+}
 
 __device__ __forceinline__ void coords(int rowdim, int inner, int row, int h, int b, int* c) {
   c[0] = inner;
@@ -68,7 +81,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
   uint64_t* empty = full + STAGES;
   uint64_t* tm_full = empty + STAGES;   // [4]: outer tile o of the streamed output done
   uint64_t* tm_empty = tm_full + 4;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 1);
+  uint64_t* xf = tm_empty + 1;           // [STAGES]: X block masked (dropout on load)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xf + STAGES);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -90,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
     }
     for (int o = 0; o < 4; ++o) mbar_init(&tm_full[o], 1);
     mbar_init(tm_empty, 4);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&xf[s], kXfWarps);
     fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
@@ -140,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
         const int o = blk / nt, i = blk - (blk / nt) * nt;
         const int jt = col_outer ? i : o, kt = col_outer ? o : i;
         const int s = g % STAGES;
-        mbar_wait(&full[s], (g / STAGES) & 1);
+        mbar_wait(p.keep ? &xf[s] : &full[s], (g / STAGES) & 1);
         tc::fence_after_sync();
         if (lane == 0) {
           const uint32_t x0 = smem_u32(base + s * stage_bytes);
@@ -169,6 +184,53 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
         __syncwarp();
       }
     }
+  } else if (warp >= 6) {
+    // ------------------------------------------------------------ dropout on load
+    // thread t of the 256 masks row t / 2, 64-column box t % 2 (8 chunks of 8 elements)
+    if (p.keep != nullptr) {
+      const int tt = (warp - 6) * 32 + lane;
+      const int row = tt >> 1, bx = tt & 1;
+      // keep words of this thread's row and 64 columns for block (u, blk)
+      auto kw_ptr = [&](int u, int blk) {
+        const int o = blk / nt, i = blk - (blk / nt) * nt;
+        const int jt = col_outer ? i : o, kt = col_outer ? o : i;
+        return reinterpret_cast<const uint2*>(
+            p.keep + ((int64_t)u * (nt * 128) + jt * 128 + row) * (nt * 4) + kt * 4 + bx * 2);
+      };
+      int g = 0;
+      uint2 kw_next = blockIdx.x < p.units ? __ldg(kw_ptr(blockIdx.x, 0)) : make_uint2(0, 0);
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        for (int blk = 0; blk < nblk; ++blk, ++g) {
+          const int s = g % STAGES;
+          const uint32_t kw[2] = {kw_next.x, kw_next.y};
+          // words of the next block, one block ahead (their latency hides behind this one)
+          if (blk + 1 < nblk)
+            kw_next = __ldg(kw_ptr(u, blk + 1));
+          else if (u + (int)gridDim.x < p.units)
+            kw_next = __ldg(kw_ptr(u + gridDim.x, 0));
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          unsigned char* sx = base + s * stage_bytes + bx * 16384;
+          uint4 x[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const uint4*>(sx + tc::sw128(row, c));
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const uint32_t f = kw[c >> 2];
+            const int j = c & 3;
+            x[c].x &= half_mask(f << (4 * j + 0));
+            x[c].y &= half_mask(f << (4 * j + 1));
+            x[c].z &= half_mask(f << (4 * j + 2));
+            x[c].w &= half_mask(f << (4 * j + 3));
+            *reinterpret_cast<uint4*>(sx + tc::sw128(row, c)) = x[c];
+          }
+          fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xf[s]))
+                         : "memory");
+        }
+      }
+    }
   } else {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
@@ -193,6 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
         const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + gi * 64;
         tc::tmem_ld32(taddr, v);
         tc::tmem_ld32(taddr + 32, v + 32);
+        if (p.out_scale != 1.f) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) v[i] *= p.out_scale;
+        }
         if (gi == ngroups - 1) {   // accumulators free for the next (b, h)
           tc::fence_before_sync();
           __syncwarp();
@@ -293,7 +359,7 @@ int sm_count() {
 template <int STAGES>
 cudaError_t launch_bh(const CUtensorMap* m, const BhParams& p, cudaStream_t st) {
   const uint32_t stage_bytes = kXBytes + (p.row_out ? kYBytes : 0) + (p.col_out ? kYBytes : 0);
-  const size_t smem = 1024 + STAGES * stage_bytes + 4 * 2 * 4096 + (2 * STAGES + 5) * 8 + 16;
+  const size_t smem = 1024 + STAGES * stage_bytes + 4 * 2 * 4096 + (3 * STAGES + 5) * 8 + 16;
   cudaFuncSetAttribute(attn_bh_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const int grid = p.units < sm_count() ? p.units : sm_count();
@@ -311,7 +377,7 @@ bool attn_bh_supported(int J, int P) { return P == 64 && J % 128 == 0 && J >= 12
 static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const void* Yr,
                              int64_t ldyr, const void* Yc, int64_t ldyc, void* Or, int64_t ldor,
                              void* Oc, int64_t ldoc, float* ps_r, float* ps_c, int ps_ld,
-                             cudaStream_t st) {
+                             const uint32_t* keep, float out_scale, cudaStream_t st) {
   if (!attn_bh_supported(J, P)) return cudaErrorInvalidValue;
   BhParams p{};
   p.H = H;
@@ -323,6 +389,8 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
   p.ps_r = ps_r;
   p.ps_c = ps_c;
   p.ps_ld = ps_ld;
+  p.keep = keep;
+  p.out_scale = out_scale;
   CUtensorMap m[5];
   int rd;
   bool ok = map_op(&m[0], X, false, B, H, J, J, 128, &rd);
@@ -345,23 +413,25 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
 }
 
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
-                              int64_t ldv, void* C, int64_t ldc, cudaStream_t st) {
+                              int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
+                              float scale, cudaStream_t st) {
   return bh_launch(B, H, J, P, A, V, ldv, nullptr, 0, C, ldc, nullptr, 0, nullptr, nullptr, 0,
-                   st);
+                   keep, keep ? scale : 1.f, st);
 }
 
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
                               int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
-                              cudaStream_t st) {
+                              const uint32_t* keep, float scale, cudaStream_t st) {
   return bh_launch(B, H, J, P, A, nullptr, 0, dC, lddc, nullptr, 0, dV, lddv, nullptr, ps_dv,
-                   ps_ld, st);
+                   ps_ld, keep, keep ? scale : 1.f, st);
 }
 
 cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
                                 int64_t ldk, const void* Q, int64_t ldq, void* dQ, int64_t lddq,
                                 void* dK, int64_t lddk, float* ps_dq, float* ps_dk, int ps_ld,
                                 cudaStream_t st) {
-  return bh_launch(B, H, J, P, dS, Kt, ldk, Q, ldq, dQ, lddq, dK, lddk, ps_dq, ps_dk, ps_ld, st);
+  return bh_launch(B, H, J, P, dS, Kt, ldk, Q, ldq, dQ, lddq, dK, lddk, ps_dq, ps_dk, ps_ld,
+                   nullptr, 1.f, st);
 }
 
 }  // namespace enc

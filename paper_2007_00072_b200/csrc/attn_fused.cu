@@ -51,6 +51,7 @@ struct FusedParams {
   const float* mask_bias;  // [B, K] or null (fwd)
   uint32_t* keep_bits;     // [B, H, J, K/32] keep-flag words (fwd: written if non-null;
                            // bwd: read instead of recomputing Philox when kBits)
+  int write_a;             // fwd: A = dropout(P) stored (0: only P and the keep words)
 };
 
 __device__ __forceinline__ void qbar(int q) {   // the 8 warps of TMEM lane quarter q
@@ -348,18 +349,20 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           float x[8], a[8];
           const float fp = fP[(ch * 32 + 8 * j) / kSub], fa = fp * ds;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            x[u] = v[8 * j + u] * fp;
-            a[u] = ((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] * fa : 0.f;
-          }
+          for (int u = 0; u < 8; ++u) x[u] = v[8 * j + u] * fp;
           *reinterpret_cast<uint4*>(own + sw64(lane, j)) = pack8(x);
-          *reinterpret_cast<uint4*>(own + 2048 + sw64(lane, j)) = pack8(a);
+          if (prm.write_a) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              a[u] = ((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] * fa : 0.f;
+            *reinterpret_cast<uint4*>(own + 2048 + sw64(lane, j)) = pack8(a);
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
-          tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
+          if (prm.write_a) tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
           tc::bulk_commit();
         }
       }
@@ -504,11 +507,11 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
             map_bhrc(&mp, Pout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B) &&
-            map_bhrc(&ma, Aout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+            map_bhrc(&ma, Aout ? Aout : Pout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
-  FusedParams prm{H, J, tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8), mask_bias,
-                  keep_bits};
+  FusedParams prm{H,         J,         tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8),
+                  mask_bias, keep_bits, Aout != nullptr};
   if (mask_bias)
     return keep_bits
                ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st)
@@ -528,8 +531,8 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
             map_bhrc(&mp, Pin, B, H, J, K, 64, 32) && map_bhrc(&ms, dS, B, H, J, K, 64, 32);
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
-  FusedParams prm{H, J, tiles, scale, batch_offset * (int64_t)H * J * (K / 8), nullptr,
-                  const_cast<uint32_t*>(keep_bits)};
+  FusedParams prm{H,       J,       tiles, scale, batch_offset * (int64_t)H * J * (K / 8),
+                  nullptr, const_cast<uint32_t*>(keep_bits), 0};
   return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st)
                    : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st);
 }

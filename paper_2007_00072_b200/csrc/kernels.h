@@ -141,11 +141,14 @@ bool attn_bh_supported(int J, int P);
 // dQ / dK may be null (that output is skipped).  ps_* (optional): per-(b, TMEM quarter)
 // column sums of the bf16-rounded output, written at ps[(b*4 + q)*ps_ld + h*P + c] (AIB-bwd's
 // bias gradient, finished by launch_colsum_finalize over the B*4 partial rows).
+// keep (optional): dropout on load -- A is the stored P and the dropout is applied from the
+// ENC_KEEP_BITS words while the block is in shared memory; the result is scaled by `scale`.
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
-                              int64_t ldv, void* C, int64_t ldc, cudaStream_t st);
+                              int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
+                              float scale, cudaStream_t st);
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
                               int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
-                              cudaStream_t st);
+                              const uint32_t* keep, float scale, cudaStream_t st);
 cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, const void* Kt,
                                 int64_t ldk, const void* Q, int64_t ldq, void* dQ, int64_t lddq,
                                 void* dK, int64_t lddk, float* ps_dq, float* ps_dk, int ps_ld,

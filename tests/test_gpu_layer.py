@@ -58,12 +58,20 @@ def _end_to_end(dims, dtype, act, key_padding, **kw):
         ref["d" + n] = go[n]
     s = layer.saved_views()
     for n in ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "A1", "xhat2", "rstd1", "rstd2"):
+        if n == "A" and _drop_on_load(dims, dtype):
+            continue   # A = dropout(P) is never stored on this path
         gpu["saved." + n] = f64(s[n])
         ref["saved." + n] = sv[n]
     # the layer keeps the pre-bias Y1 = X1 W1^T; the oracle's saved h = Y1 + b1
     gpu["saved.h"] = f64(s["Y1"]) + np.asarray(prm["b1"], np.float64)
     ref["saved.h"] = sv["h"]
     return gpu, ref
+
+
+def _drop_on_load(dims, dtype):
+    """The fused score kernels + per-(b,h) contractions (bf16, J = K = 512, P = 64) never
+    store A: A.V and A^T.dC apply the stored keep bits to P on load."""
+    return dtype == "bf16" and dims.P == 64 and dims.J == 512
 
 
 def _stagewise(dims, dtype, act, key_padding, **kw):
@@ -85,7 +93,13 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     pairs += [("Q", s["Q"], Qo), ("K", s["K"], Ko), ("V", s["V"], Vo)]
     Po, Ao = E.bsb_fwd(s["Q"] @ s["K"].transpose(0, 1, 3, 2), inp["mask_bias"], sc,
                        ocfg.p_attn, seed, sub(0), boff)
-    pairs += [("P", s["P"], Po), ("A", s["A"], Ao)]
+    pairs += [("P", s["P"], Po)]
+    if _drop_on_load(dims, dtype):
+        # A is not stored: the contraction uses keep(P) * s from the stored P
+        keep = philox.keep_mask_tensor((B, H, J, J), boff, ocfg.p_attn, seed, sub(0))
+        s["A"] = np.where(keep, s["P"] * philox.dropout_scale(ocfg.p_attn), 0.0)
+    else:
+        pairs += [("A", s["A"], Ao)]
     Co = (s["A"] @ s["V"]).transpose(0, 2, 1, 3).reshape(B, J, I)
     pairs += [("C", s["C"], Co)]
     X1o, xh1o, r1o = E.bdrln_fwd(s["C"] @ W["Wo"].T, W["bo"], X, W["g1"], W["be1"],
