@@ -145,9 +145,9 @@ __device__ __forceinline__ uint32_t keep_bits8(uint64_t g, const PhiloxKey& pk) 
 // word i, lane 2i+1 the high half.  r_hi >= T  <=>  w >= T<<16 and r_lo >= T  <=>
 // (w << 16) >= T<<16, so each decision is one compare (+ one shift for low halves).
 __device__ __forceinline__ void keep_mul8(uint64_t g, const PhiloxKey& pk, float m[8]) {
-  if (pk.T == 0) {
+  if (pk.T == 0) {   // everything kept; pk.scale is 1 for such a key (callers may rescale it)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) m[j] = 1.f;
+    for (int j = 0; j < 8; ++j) m[j] = pk.scale;
     return;
   }
   const uint4 w = philox4x32_10(g, pk);

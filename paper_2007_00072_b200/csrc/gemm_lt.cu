@@ -19,7 +19,7 @@
 namespace enc {
 
 namespace {
-constexpr int kMaxAlgos = 12;
+constexpr int kMaxAlgos = 32;
 
 cudaDataType_t dt(int dtype) { return dtype == 0 ? CUDA_R_16BF : CUDA_R_32F; }
 

@@ -18,41 +18,50 @@ enum { kActGeluErf = 0, kActGeluTanh = 1, kActRelu = 2 };
 // t = 1/(1 + p x), |error| <= 1.5e-7 (below fp32 resolution of 1 + erf).  With
 // x = |h|/sqrt(2), e^{-x^2} = e^{-h^2/2} is also the Gaussian density's exponential, so
 // GELU and GELU' share one MUFU.EX2 and one MUFU.RCP.
+__device__ __forceinline__ float ex2_approx(float x) {   // MUFU.EX2, flush-to-zero
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// ea = erf(|h| / sqrt 2) and e = exp(-h^2 / 2) (one MUFU.RCP, one MUFU.EX2, 4 FFMA for the
+// polynomial).  Then GELU(h) = h Phi(h) = (h + |h| ea) / 2 and
+// GELU'(h) = Phi(h) + h phi(h) = (1 + sign(h) ea) / 2 + h e / sqrt(2 pi).
 struct GeluErfParts {
-  float cdf2;  // 1 + erf(h / sqrt 2)  (= 2 Phi(h))
-  float e;     // exp(-h^2 / 2)
+  float ea;
+  float e;
 };
 __device__ __forceinline__ GeluErfParts gelu_erf_parts(float h) {
   const float x = fabsf(h) * 0.70710678118654752f;
   const float t = __fdividef(1.f, fmaf(0.3275911f, x, 1.f));  // MUFU.RCP
-  float p = fmaf(1.061405429f, t, -1.453152027f);
-  p = fmaf(p, t, 1.421413741f);
-  p = fmaf(p, t, -0.284496736f);
-  p = fmaf(p, t, 0.254829592f);
-  p *= t;
-  const float e = exp2f(-0.72134752044448170f * h * h);  // e^{-h^2/2}
-  const float erf_abs = fmaf(-p, e, 1.f);
+  float q = fmaf(1.061405429f, t, -1.453152027f);
+  q = fmaf(q, t, 1.421413741f);
+  q = fmaf(q, t, -0.284496736f);
+  q = fmaf(q, t, 0.254829592f);
+  // e^{-h^2/2} = 2^{-h^2 log2(e) / 2} (argument <= 0: result in [0, 1])
+  const float e = ex2_approx((-0.72134752044448170f * h) * h);
   GeluErfParts r;
-  r.cdf2 = 1.f + copysignf(erf_abs, h);
+  r.ea = fmaf(-q, t * e, 1.f);   // 1 - t q(t) e^{-x^2}
   r.e = e;
   return r;
 }
 
+// GELU scaled by 2 for the erf form (the caller folds the 1/2 into its multiplier)
 template <int ACT>
-__device__ __forceinline__ float act_f(float h) {
-  if (ACT == kActGeluErf) return 0.5f * h * gelu_erf_parts(h).cdf2;
+__device__ __forceinline__ float act_f2(float h) {
+  if (ACT == kActGeluErf) return fmaf(fabsf(h), gelu_erf_parts(h).ea, h);
   if (ACT == kActGeluTanh) {
     const float u = 0.7978845608028654f * fmaf(0.044715f * h, h * h, h);
-    return 0.5f * h * (1.f + tanhf(u));
+    return h * (1.f + tanhf(u));
   }
-  return h > 0.f ? h : 0.f;
+  return h > 0.f ? 2.f * h : 0.f;
 }
 
 template <int ACT>
 __device__ __forceinline__ float act_df(float h) {
   if (ACT == kActGeluErf) {
     const GeluErfParts g = gelu_erf_parts(h);
-    return fmaf(h * 0.3989422804014327f, g.e, 0.5f * g.cdf2);  // Phi(h) + h phi(h)
+    // Phi(h) + h phi(h)
+    return fmaf(h * 0.3989422804014327f, g.e, fmaf(0.5f, copysignf(g.ea, h), 0.5f));
   }
   if (ACT == kActGeluTanh) {
     const float c = 0.7978845608028654f;
@@ -71,6 +80,8 @@ __global__ void __launch_bounds__(256) bad_fwd_kernel(const T* __restrict__ Y1,
                                                       int ncU, int64_t g0, PhiloxKey pk) {
   constexpr int kU = 2;  // chunks in flight per thread
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  PhiloxKey pkh = pk;
+  pkh.scale *= 0.5f;
   for (int64_t c0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c0 < nchunks;
        c0 += kU * stride) {
     typename Chunk<T>::Raw raw[kU];
@@ -85,12 +96,12 @@ __global__ void __launch_bounds__(256) bad_fwd_kernel(const T* __restrict__ Y1,
         float y[8], b[8], a[8];
         Chunk<T>::unpack(raw[u], y);
         load_f32x8(b1 + col, b);
-        float m[8];
-        keep_mul8((uint64_t)(g0 + c), pk, m);
+        float m[8];   // keep ? scale / 2 : 0 (act_f2 returns 2 GELU)
+        keep_mul8((uint64_t)(g0 + c), pkh, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           y[j] += b[j];
-          a[j] = act_f<ACT>(y[j]) * m[j];
+          a[j] = act_f2<ACT>(y[j]) * m[j];
         }
         if (h_out != nullptr) Chunk<T>::store(h_out + c * 8, y);
         Chunk<T>::store(A1 + c * 8, a);

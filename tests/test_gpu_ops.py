@@ -157,12 +157,13 @@ BAD_SHAPES = [(2, 16, 64), (3, 7, 1000), (2, 33, 4096), (1, 5, 3072), (2, 3, 8)]
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("shape", BAD_SHAPES)
 @pytest.mark.parametrize("act", [E.ACT_GELU_ERF, E.ACT_GELU_TANH, E.ACT_RELU])
-def test_bad_fwd_bwd(ops, ctx, dtype, shape, act):
+@pytest.mark.parametrize("p", [0.1, 0.0])
+def test_bad_fwd_bwd(ops, ctx, dtype, shape, act, p):
     B, J, U = shape
     Y1 = make_tensor((B, J, U), 41, dtype, std=2.0)
     b1 = make_tensor((U,), 42, "fp32", std=0.1)
     dA1 = make_tensor((B, J, U), 43, dtype)
-    p, sub, boff = 0.1, 2, 4
+    sub, boff = 2, 4
     tY = dev(Y1, dtype)
     h, A1 = torch.empty_like(tY), torch.empty_like(tY)
     ops.enc_bad_fwd(ctx, B, J, U, tY, dev32(b1), act, p, SEED, sub, boff, h, A1)
