@@ -25,7 +25,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BERT-large encoder layer fwd+bwd tokens/s"
 UNIT = "tokens/s"
-WORKLOAD = "L: BERT-large encoder layer B=8/GPU J=K=512 H=16 P=64 I=1024 U=4096 p=0.1 GELU"
+WORKLOADS = {
+    "L": "L: BERT-large encoder layer B=8/GPU J=K=512 H=16 P=64 I=1024 U=4096 p=0.1 GELU",
+    "Bb": "Bb: BERT-base encoder layer B=96/GPU J=K=128 H=12 P=64 I=768 U=3072 p=0.1 GELU",
+}
 
 
 def parse():
@@ -34,6 +37,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["L", "Bb"], default="L",
+                    help="L: the paper's BERT-large layer (headline); Bb: BERT-base layer "
+                         "(BASELINE.json configs[2])")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-flush", action="store_true", help="skip the L2 flush between steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -136,24 +142,35 @@ def run_reference(args, rank, world):
     from synth import CONFIGS
     if rank != 0:
         return
-    dims = CONFIGS["L"]
+    dims = CONFIGS[args.config]
     J = dims.J
     if args.warmup:
         time_oracle(dims, min(args.warmup, 1), args.dtype)
     ts = time_oracle(dims, args.steps, args.dtype)
     total = sum(ts)
     value = args.steps * J / total
-    sample = f"1 sequence (B=1 slice of config L) fwd+bwd per step, fp64 numpy oracle"
+    sample = f"1 sequence (B=1 slice of config {args.config}) fwd+bwd per step, fp64 numpy oracle"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
+        "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def attention_desc(args, dims) -> str:
+    backend = args.attn_backend
+    if backend == "fused" and not (dims.J == 512 and dims.P == 64 and args.dtype == "bf16"):
+        backend = "tc" if args.dtype == "bf16" else "cublas"   # what the library selects
+    return {"fused": "fused tcgen05 QK^T+BSB / dA+BSB-bwd (S, dA in TMEM), dropout on load in "
+                     "the per-(b,h) A.V / A^T.dC contractions",
+            "tc": "tcgen05 QK^T / dA contractions + separate BSB kernels, per-(b,h) A.V, "
+                  "A^T.dC, dS.K + dS^T.Q",
+            "cublas": "cuBLAS contractions + separate BSB kernels"}[backend]
 
 
 # ------------------------------------------------------------------ our arm
@@ -185,9 +202,9 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    dims_global = CONFIGS["L"].with_batch(CONFIGS["L"].B * world)
+    dims_global = CONFIGS[args.config].with_batch(CONFIGS[args.config].B * world)
     boff, B = dp.shard(dims_global.B, world, rank)
-    dims = CONFIGS["L"].with_batch(B)
+    dims = CONFIGS[args.config].with_batch(B)
     es = 2 if args.dtype == "bf16" else 4
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
 
@@ -350,7 +367,9 @@ def main():
                 "unit": "TFLOP/s", "frac": ach / tc_peak, "traffic": None,
                 "algorithmic_flops": flops[dominant], "peak_source": peak_src + " (sustained)"}
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic_path):
+    # the committed ncu traffic figures are per launch at config L, bf16, default path
+    if os.path.exists(traffic_path) and args.config == "L" and args.dtype == "bf16" \
+            and args.attn_backend == "fused":
         try:
             roof["traffic"] = json.load(open(traffic_path)).get(dominant)
         except (OSError, ValueError):
@@ -391,23 +410,24 @@ def main():
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            ts = time_oracle(CONFIGS["L"], args.cpu_samples, args.dtype)
-            cpu = {"value": CONFIGS["L"].J * len(ts) / sum(ts), "unit": UNIT,
+            cd = CONFIGS[args.config]
+            ts = time_oracle(cd, args.cpu_samples if args.config == "L" else 4 * args.cpu_samples,
+                             args.dtype)
+            cpu = {"value": cd.J * len(ts) / sum(ts), "unit": UNIT,
                    "cores": cpu_cores(), "kind": "oracle",
-                   "sample": f"{len(ts)} x one sequence (B=1 slice of config L) fwd+bwd, "
-                             f"fp64 numpy oracle, {sum(ts):.1f} s"}
+                   "sample": f"{len(ts)} x one sequence (B=1 slice of config {args.config}) "
+                             f"fwd+bwd, fp64 numpy oracle, {sum(ts):.1f} s"}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": WORKLOAD, "global_batch": dims_global.B, "seq_len": dims.J,
+            "config": {"workload": WORKLOADS[args.config], "global_batch": dims_global.B,
+                       "seq_len": dims.J,
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
                        else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)",
-                       "attention": {"fused": "fused tcgen05 QK^T+BSB / dA+BSB-bwd + tcgen05 GEMMs",
-                                     "tc": "tcgen05 GEMMs + separate BSB kernels",
-                                     "cublas": "cuBLAS GEMMs + separate BSB kernels"}[args.attn_backend]},
+                       "attention": attention_desc(args, dims)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},

@@ -15,7 +15,7 @@ import torch
 from keepbits import decode
 from oracle import encoder as E
 from oracle import philox
-from synth import CONFIGS, Dims, make_inputs, make_params
+from synth import CONFIGS, Dims, bf16_round, make_inputs, make_params
 from tol import assert_parity, errors
 
 pytestmark = pytest.mark.gpu
@@ -91,8 +91,12 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     QKV = X @ W["Wqkv"].T
     Qo, Ko, Vo = E.aib_fwd(QKV, W["bqkv"], H, P)
     pairs += [("Q", s["Q"], Qo), ("K", s["K"], Ko), ("V", s["V"], Vo)]
-    Po, Ao = E.bsb_fwd(s["Q"] @ s["K"].transpose(0, 1, 3, 2), inp["mask_bias"], sc,
-                       ocfg.p_attn, seed, sub(0), boff)
+    S = s["Q"] @ s["K"].transpose(0, 1, 3, 2)
+    if dtype == "bf16" and not _drop_on_load(dims, dtype):
+        # the unfused paths store S in bf16 between the contraction and BSB: the BSB
+        # stage's input is that stored S (the fused kernel keeps S in fp32 TMEM)
+        S = bf16_round(S.astype(np.float32)).astype(np.float64)
+    Po, Ao = E.bsb_fwd(S, inp["mask_bias"], sc, ocfg.p_attn, seed, sub(0), boff)
     pairs += [("P", s["P"], Po)]
     if _drop_on_load(dims, dtype):
         # A is not stored: the contraction uses keep(P) * s from the stored P
@@ -189,6 +193,7 @@ def test_layer_L_fp32_full():
     (Dims(B=3, J=40, H=2, P=24, U=96), "relu", True),       # cuBLAS attention path
     (Dims(B=2, J=256, H=4, P=64, U=1024), "gelu", True),    # tcgen05 attention path
     (Dims(B=2, J=512, H=2, P=64, U=512), "gelu", True),     # fused score kernels
+    (Dims(B=3, J=128, H=12, P=64, U=3072), "gelu", True),   # BERT-base shape (config Bb)
 ])
 def test_layer_small_bf16_stagewise(dims, act, kp):
     pairs, f32 = _stagewise(dims, "bf16", act, kp, weight_std=0.06)
