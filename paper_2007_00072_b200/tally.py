@@ -68,3 +68,44 @@ def step_fused_bytes(d, es: int = 2) -> int:
 
 def step_flops(d) -> int:
     return sum(gemm_flops(d).values())
+
+
+def step_kernel_bytes(d, es: int = 2) -> dict:
+    """Algorithmic HBM bytes of every kernel of one fwd+bwd step on the default bf16 path at
+    J = 512 (fused score kernels, per-(b,h) contractions with dropout on load, in-place QKV,
+    cuBLASLt weight contractions), for the data-movement tally against the paper's Table A.1
+    totals (DESIGN.md section 6).  Weights counted once per contraction that reads them;
+    fp32 gradient outputs 4 B; BDRLN / BAD masks regenerated, attention mask as 1-bit words."""
+    B, J, H, P, I, U = _d(d)
+    BJ = B * J
+    x, xu, s = BJ * I * es, BJ * U * es, B * H * J * J * es     # [BJ,I], [BJ,U], [B,H,J,K]
+    bits = B * H * J * J // 8
+    wq, wo, w1 = 3 * I * I * es, I * I * es, U * I * es
+    f = 4
+    return {
+        # forward
+        "gemm_qkv+bias": x + wq + 3 * x,
+        "qk_bsb (fused)": 2 * x + s + bits,
+        "av (dropout on load)": s + bits + x + x,
+        "gemm_out": x + wo + x,
+        "bdrln_fwd1": 4 * x + BJ * f,
+        "gemm_l1": x + w1 + xu,
+        "bad_fwd": 2 * xu,
+        "gemm_l2": xu + w1 + x,
+        "bdrln_fwd2": 4 * x + BJ * f,
+        # backward
+        "bdrln_bwd2": 4 * x + BJ * f,
+        "gemm_l2_dx": x + w1 + xu,
+        "gemm_l2_dw": x + xu + I * U * f,
+        "bad_bwd": 3 * xu,
+        "gemm_l1_dx (+dz2)": xu + w1 + 2 * x,
+        "gemm_l1_dw": xu + x + U * I * f,
+        "bdrln_bwd1": 4 * x + BJ * f,
+        "gemm_out_dx": x + wo + x,
+        "gemm_out_dw": 2 * x + I * I * f,
+        "dv (dropout on load)": s + bits + x + x,
+        "da_bsb_bwd (fused)": 2 * x + s + bits + s,
+        "dq+dk": s + 2 * x + 2 * x,
+        "gemm_qkv_dx (+dz1)": 3 * x + wq + 2 * x,
+        "gemm_qkv_dw": 3 * x + x + 3 * I * I * f,
+    }
