@@ -210,18 +210,22 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
             kw_next = __ldg(kw_ptr(u + gridDim.x, 0));
           mbar_wait(&full[s], (g / STAGES) & 1);
           unsigned char* sx = base + s * stage_bytes + bx * 16384;
-          uint4 x[8];
-#pragma unroll
-          for (int c = 0; c < 8; ++c) x[c] = *reinterpret_cast<const uint4*>(sx + tc::sw128(row, c));
+          // only 8-element chunks with a dropped element are rewritten (at p = 0.1, 43 % of
+          // the chunks keep all 8)
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
             const uint32_t f = kw[c >> 2];
             const int j = c & 3;
-            x[c].x &= half_mask(f << (4 * j + 0));
-            x[c].y &= half_mask(f << (4 * j + 1));
-            x[c].z &= half_mask(f << (4 * j + 2));
-            x[c].w &= half_mask(f << (4 * j + 3));
-            *reinterpret_cast<uint4*>(sx + tc::sw128(row, c)) = x[c];
+            const uint32_t all = 0xF000F000u >> (4 * j);
+            if ((f & all) != all) {
+              uint4* loc = reinterpret_cast<uint4*>(sx + tc::sw128(row, c));
+              uint4 x = *loc;
+              x.x &= half_mask(f << (4 * j + 0));
+              x.y &= half_mask(f << (4 * j + 1));
+              x.z &= half_mask(f << (4 * j + 2));
+              x.w &= half_mask(f << (4 * j + 3));
+              *loc = x;
+            }
           }
           fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
           __syncwarp();
