@@ -28,13 +28,31 @@ def f64(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-def _setup(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weight_std=0.02):
+# option ids of include/encoder.h (enc_set_option)
+OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_ATTN_BH, OPT_QKV_DIRECT = 0, 1, 4, 5
+
+
+def _paths(dims, dtype, opts=None):
+    """Which attention path the library takes for these dims / options (mirrors api.cu)."""
+    o = {OPT_ATTN_TC: 1, OPT_ATTN_FUSED: 1, OPT_ATTN_BH: 1, OPT_QKV_DIRECT: 1}
+    o.update(opts or {})
+    tc = bool(o[OPT_ATTN_TC]) and dtype == "bf16" and dims.P == 64 and dims.J % 128 == 0
+    fused = tc and bool(o[OPT_ATTN_FUSED]) and dims.J == 512
+    bh = bool(o[OPT_ATTN_BH]) and dims.P == 64 and dims.J % 128 == 0 and dims.J <= 512
+    return {"tc": tc, "fused": fused, "drop_on_load": fused and bh}
+
+
+def _setup(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weight_std=0.02,
+           opts=None):
+    from paper_2007_00072_b200 import ops
     from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
     prm = make_params(dims, dtype, "parity", weight_std=weight_std)
     inp = make_inputs(dims, dtype, key_padding=key_padding)
     cfg = LayerCfg(p_attn=p, p_hidden=p, p_ffn=p, act=act, layer_id=layer_id,
                    batch_offset=batch_offset)
     layer = EncoderLayer(dims, dtype, cfg)
+    for key, val in (opts or {}).items():
+        ops.enc_set_option(layer.ctx, key, val)
     layer.set_params(prm)
     X = torch.tensor(inp["X"], device="cuda").to(TDT[dtype])
     dY = torch.tensor(inp["dY"], device="cuda").to(TDT[dtype])
@@ -68,15 +86,15 @@ def _end_to_end(dims, dtype, act, key_padding, **kw):
     return gpu, ref
 
 
-def _drop_on_load(dims, dtype):
+def _drop_on_load(dims, dtype, opts=None):
     """The fused score kernels + per-(b,h) contractions (bf16, J = K = 512, P = 64) never
     store A: A.V and A^T.dC apply the stored keep bits to P on load."""
-    return dtype == "bf16" and dims.P == 64 and dims.J == 512
+    return _paths(dims, dtype, opts)["drop_on_load"]
 
 
-def _stagewise(dims, dtype, act, key_padding, **kw):
+def _stagewise(dims, dtype, act, key_padding, opts=None, **kw):
     """(gpu, ref) pairs of every stage, the oracle fed with the GPU's stored inputs."""
-    layer, prm, inp, ocfg, Y, dX = _setup(dims, dtype, act, key_padding, **kw)
+    layer, prm, inp, ocfg, Y, dX = _setup(dims, dtype, act, key_padding, opts=opts, **kw)
     B, J, H, P, I = dims.B, dims.J, dims.H, dims.P, dims.I
     sub = lambda site: 4 * ocfg.layer_id + site  # noqa: E731
     sc, boff, seed = 1.0 / np.sqrt(P), ocfg.batch_offset, ocfg.seed
@@ -92,13 +110,13 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     Qo, Ko, Vo = E.aib_fwd(QKV, W["bqkv"], H, P)
     pairs += [("Q", s["Q"], Qo), ("K", s["K"], Ko), ("V", s["V"], Vo)]
     S = s["Q"] @ s["K"].transpose(0, 1, 3, 2)
-    if dtype == "bf16" and not _drop_on_load(dims, dtype):
+    if dtype == "bf16" and not _paths(dims, dtype, opts)["fused"]:
         # the unfused paths store S in bf16 between the contraction and BSB: the BSB
         # stage's input is that stored S (the fused kernel keeps S in fp32 TMEM)
         S = bf16_round(S.astype(np.float32)).astype(np.float64)
     Po, Ao = E.bsb_fwd(S, inp["mask_bias"], sc, ocfg.p_attn, seed, sub(0), boff)
     pairs += [("P", s["P"], Po)]
-    if _drop_on_load(dims, dtype):
+    if _drop_on_load(dims, dtype, opts):
         # A is not stored: the contraction uses keep(P) * s from the stored P
         keep = philox.keep_mask_tensor((B, H, J, J), boff, ocfg.p_attn, seed, sub(0))
         s["A"] = np.where(keep, s["P"] * philox.dropout_scale(ocfg.p_attn), 0.0)
@@ -136,7 +154,7 @@ def _stagewise(dims, dtype, act, key_padding, **kw):
     dCbh = b["dC"].reshape(B, J, H, P).transpose(0, 2, 1, 3)
     dAo = dCbh @ s["V"].transpose(0, 1, 3, 2)
     pairs += [("dV", b["dV"], s["A"].transpose(0, 1, 3, 2) @ dCbh)]
-    if dtype == "bf16" and P == 64 and J == 512:
+    if _paths(dims, dtype, opts)["fused"]:
         # fused kernels: the forward's stored keep-flag words are the oracle's mask exactly
         kb = layer.saved_views()["keep_attn"].cpu().numpy()
         assert np.array_equal(decode(kb, J), philox.keep_mask_tensor(
@@ -200,6 +218,21 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     for n, g, o in pairs:
         assert_parity(n, g, o, "bf16")
     for n, g, o in f32:   # rstd of the bf16-rounded GEMM output: bf16-level agreement
+        assert_parity(n, g, o, "bf16")
+
+
+@pytest.mark.parametrize("opts", [
+    {OPT_ATTN_BH: 0},                      # fused score kernels + tiled A.V (A stored)
+    {OPT_QKV_DIRECT: 0},                   # fused + per-(b,h) with separate AIB passes
+    {OPT_ATTN_FUSED: 0},                   # tiled QK^T + BSB kernels + per-(b,h)
+    {OPT_ATTN_FUSED: 0, OPT_ATTN_BH: 0},   # all tiled tcgen05
+    {OPT_ATTN_TC: 0},                      # cuBLAS attention
+])
+def test_layer_bf16_stagewise_paths(opts):
+    """Every attention-path option combination at a fused-capable shape (J = 512)."""
+    pairs, f32 = _stagewise(Dims(B=2, J=512, H=2, P=64, U=512), "bf16", "gelu", True,
+                            opts=opts, weight_std=0.06)
+    for n, g, o in pairs + f32:
         assert_parity(n, g, o, "bf16")
 
 
