@@ -893,13 +893,22 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     dV = (char*)dQKV + 2 * (size_t)I * es;
   }
 
+  // The column sums of each half are finished by one batched finalize launch at the end of
+  // the half (deferred jobs, disjoint partial regions of the reduction workspace).
+  auto after = [&](const ColsumJob& j) {   // workspace past a recorded job's partials
+    const size_t used = ((size_t)j.R * j.ncols + 63) & ~(size_t)63;
+    return ReduceWs{ws.partials + used, ws.cap_floats - used, ws.num_sms};
+  };
   if (parts & 1) {
+  ColsumJob ffn_jobs[2];
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
   {
-    OpTimer _t(ctx, ENC_OP_BDRLN_BWD2, st, 2);
+    OpTimer _t(ctx, ENC_OP_BDRLN_BWD2, st, 1);
+    ReduceWs w = ws;
+    w.defer = &ffn_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dY, xh2, r2, prm->g2,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, dX1, dY2, g->dg2,
-                        g->dbe2, g->db2, ws, st));
+                        g->dbe2, g->db2, w, st));
   }
   // Linear2 dX (:573), dW (:574)
   {
@@ -910,11 +919,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, st, 0);
     CB(wgemm(ctx, st,dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U));
   }
-  // BAD-bwd (:576-578)
+  // BAD-bwd (:576-578), then the FFN half's column sums (dg2, dbe2, db2, db1) in one launch
   {
     OpTimer _t(ctx, ENC_OP_BAD_BWD, st, 2);
+    ReduceWs w = after(ffn_jobs[0]);
+    w.defer = &ffn_jobs[1];
     CK(launch_bad_bwd(dtype, B, J, U, dA1, h, prm->b1, cfg->act,
-                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, ws, st));
+                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, w, st));
+    CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
   }
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
   {
@@ -927,13 +939,18 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   }
   }  // FFN half
   if (!(parts & 2)) return ENC_OK;
-  // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo
+  // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo; its column
+  // sums are finished with the QKV bias gradient at the end of the half
+  ColsumJob att_jobs[2];
   {
-    OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, st, 2);
+    OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, st, 1);
+    ReduceWs w = ws;
+    w.defer = &att_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dX1, xh1, r1, prm->g1,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, dX, dYo, g->dg1,
-                        g->dbe1, g->dbo, ws, st));
+                        g->dbe1, g->dbo, w, st));
   }
+  const ReduceWs wa = after(att_jobs[0]);   // the rest of the half reduces past those partials
   // Out dX (:586), dW (:587)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DX, st, 0);
@@ -959,8 +976,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   }
   // direct layout on the per-(b, h) kernels: AIB-bwd's bias gradient (:595) accumulates as
   // column sums in the dV / dQ / dK epilogues (partials [B*4][3I] in the reduction space)
-  const bool bgrad_epi = direct && use_bh(ctx, J, P) && (size_t)B * 4 * 3 * I <= ws.cap_floats;
-  float* bg = ws.partials;
+  const bool bgrad_epi = direct && use_bh(ctx, J, P) && (size_t)B * 4 * 3 * I <= wa.cap_floats;
+  float* bg = wa.partials;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
     if (fused_attn && use_bh(ctx, J, P))   // A was never stored: dropout on load from P
@@ -1015,7 +1032,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // bias gradient rides in the QKV dW contraction's epilogue (or a column sum below)
   if (!direct) {
     OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
-    CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, ws, st));
+    CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, wa, st));
   }
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
   {
@@ -1028,15 +1045,23 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     CB(wgemm(ctx, st, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
              g->dWqkv, I));
   }
-  if (bgrad_epi) {
-    // finish the bias gradient: fixed-order sum of the B*4 epilogue partial rows
-    OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 1);
-    CK(launch_colsum_finalize(bg, B * 4, 3 * I, 3 * I, g->dbqkv, nullptr, nullptr, st));
-  } else if (direct) {
+  if (direct && !bgrad_epi) {
     // bias gradient as a column sum of dQKV (cuBLASLt's BGRAD epilogue on the dW
     // contraction measured slower than this separate pass)
     OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
-    CK(launch_colsum(dtype, BJ, 3 * I, dQKV, g->dbqkv, ws, st));
+    CK(launch_colsum(dtype, BJ, 3 * I, dQKV, g->dbqkv, wa, st));
+  }
+  {
+    // the attention half's column sums in one launch: BDRLN-bwd site 1 (dg1, dbe1, dbo)
+    // and, on the per-(b,h) path, the QKV bias gradient from the B*4 epilogue partial rows
+    OpTimer _t(ctx, bgrad_epi ? ENC_OP_AIB_BWD : ENC_OP_BDRLN_BWD1, st, 1);
+    if (bgrad_epi) {
+      att_jobs[1].partials = bg;
+      att_jobs[1].R = B * 4;
+      att_jobs[1].ncols = att_jobs[1].nper = 3 * I;
+      att_jobs[1].out0 = g->dbqkv;
+    }
+    CK(launch_colsum_finalize_jobs(att_jobs, bgrad_epi ? 2 : 1, st));
   }
   return ENC_OK;
 }

@@ -34,11 +34,26 @@
 namespace enc {
 
 // Deterministic column-reduction workspace (owned by enc_ctx).
+// A pending fixed-order column-sum finalize: out_q[j] = sum_{r < R} partials[r*ncols +
+// q*nper + j].
+struct ColsumJob {
+  const float* partials = nullptr;
+  int R = 0, ncols = 0, nper = 0;
+  float *out0 = nullptr, *out1 = nullptr, *out2 = nullptr;
+};
+
 struct ReduceWs {
   float* partials;       // device, capacity `cap_floats`
   size_t cap_floats;
   int num_sms;
+  ColsumJob* defer = nullptr;   // non-null: record the finalize here instead of launching it
 };
+// The tail of every column-reducing launcher: finalize now, or record it in ws.defer so the
+// caller can batch several finalizes into one launch (launch_colsum_finalize_jobs).
+cudaError_t colsum_finish(const ReduceWs& ws, int R, int ncols, int nper, float* out0,
+                          float* out1, float* out2, cudaStream_t st);
+// One launch finishing up to 4 recorded jobs (their partial regions must not overlap).
+cudaError_t launch_colsum_finalize_jobs(const ColsumJob* jobs, int n, cudaStream_t st);
 
 PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq);
 

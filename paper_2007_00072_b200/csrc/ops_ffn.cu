@@ -224,7 +224,7 @@ cudaError_t launch_bad_bwd(int dtype, int B, int J, int U, const void* dA1, cons
   });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_colsum_finalize(ws.partials, R, U, U, db1, nullptr, nullptr, st);
+  return colsum_finish(ws, R, U, U, db1, nullptr, nullptr, st);
 }
 
 // ------------------------------------------------------------------ BEI

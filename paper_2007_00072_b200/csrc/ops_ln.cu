@@ -323,7 +323,7 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
   });
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_colsum_finalize(ws.partials, G, 3 * I, I, dgamma, dbeta, dbias, st);
+  return colsum_finish(ws, G, 3 * I, I, dgamma, dbeta, dbias, st);
 }
 
 // ------------------------------------------------------------------ column-sum finalize
@@ -370,6 +370,77 @@ cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int 
   dim3 block(32, kFinY);
   colsum_finalize_kernel<<<(ncols + 31) / 32, block, 0, st>>>(partials, R, ncols, nper, out0,
                                                               out1, out2);
+  return cudaGetLastError();
+}
+
+cudaError_t colsum_finish(const ReduceWs& ws, int R, int ncols, int nper, float* out0,
+                          float* out1, float* out2, cudaStream_t st) {
+  if (ws.defer != nullptr) {
+    ColsumJob& j = *ws.defer;
+    j.partials = ws.partials;
+    j.R = R;
+    j.ncols = ncols;
+    j.nper = nper;
+    j.out0 = out0;
+    j.out1 = out1;
+    j.out2 = out2;
+    return cudaSuccess;
+  }
+  return launch_colsum_finalize(ws.partials, R, ncols, nper, out0, out1, out2, st);
+}
+
+struct ColsumJobs4 {
+  ColsumJob j[4];
+  int first_block[5];   // block ranges per job
+};
+
+__global__ void __launch_bounds__(32 * kFinY) colsum_finalize_jobs_kernel(ColsumJobs4 js) {
+  __shared__ float sm[kFinY][33];
+  int k = 0;
+  while (k < 3 && (int)blockIdx.x >= js.first_block[k + 1]) ++k;
+  const ColsumJob& jb = js.j[k];
+  const int c = ((int)blockIdx.x - js.first_block[k]) * 32 + threadIdx.x;
+  float s = 0.f;
+  if (c < jb.ncols) {
+    for (int r0 = threadIdx.y; r0 < jb.R; r0 += kFinY * kFinMaxPer) {
+      float v[kFinMaxPer];
+#pragma unroll
+      for (int u = 0; u < kFinMaxPer; ++u) {
+        const int r = min(r0 + u * kFinY, jb.R - 1);
+        v[u] = __ldg(jb.partials + (int64_t)r * jb.ncols + c);
+      }
+#pragma unroll
+      for (int u = 0; u < kFinMaxPer; ++u) s += (r0 + u * kFinY < jb.R) ? v[u] : 0.f;
+    }
+  }
+  sm[threadIdx.y][threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.y == 0 && c < jb.ncols) {
+    float t = sm[0][threadIdx.x];
+#pragma unroll
+    for (int y = 1; y < kFinY; ++y) t += sm[y][threadIdx.x];
+    const int q = c / jb.nper;
+    const int jj = c - q * jb.nper;
+    float* o = q == 0 ? jb.out0 : (q == 1 ? jb.out1 : jb.out2);
+    o[jj] = t;
+  }
+}
+
+cudaError_t launch_colsum_finalize_jobs(const ColsumJob* jobs, int n, cudaStream_t st) {
+  if (n < 1 || n > 4) return cudaErrorInvalidValue;
+  ColsumJobs4 js{};
+  int nb = 0;
+  for (int k = 0; k < 4; ++k) {
+    js.first_block[k] = nb;
+    if (k < n) {
+      js.j[k] = jobs[k];
+      nb += (jobs[k].ncols + 31) / 32;
+    }
+  }
+  js.first_block[4] = nb;
+  if (nb == 0) return cudaSuccess;
+  dim3 block(32, kFinY);
+  colsum_finalize_jobs_kernel<<<nb, block, 0, st>>>(js);
   return cudaGetLastError();
 }
 

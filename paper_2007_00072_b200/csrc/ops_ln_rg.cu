@@ -391,7 +391,7 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
   }));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  return launch_colsum_finalize(ws.partials, G, 3 * I, I, dgamma, dbeta, dbias, st);
+  return colsum_finish(ws, G, 3 * I, I, dgamma, dbeta, dbias, st);
 }
 
 }  // namespace enc
