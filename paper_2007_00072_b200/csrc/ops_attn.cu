@@ -193,7 +193,25 @@ cudaError_t launch_aib_bwd(int dtype, int B, int J, int H, int P, const void* dq
 // sum; A = keep ? P*s : 0.  exp2 of the log2e-prescaled value equals exp(x - max x).
 constexpr float kLog2e = 1.4426950408889634f;
 
-template <typename T, int CPL>
+// Row-wide max / sum over the WPR warps sharing a row (WPR = 1: the warp's own value).
+template <int WPR>
+__device__ __forceinline__ float row_reduce(float v, bool is_max, float* red) {
+  v = is_max ? warp_max(v) : warp_sum(v);
+  if constexpr (WPR > 1) {
+    const int warp = threadIdx.x >> 5, g0w = warp - warp % WPR;
+    __syncthreads();   // previous use of red finished
+    if ((threadIdx.x & 31) == 0) red[warp] = v;
+    __syncthreads();
+    v = red[g0w];
+#pragma unroll
+    for (int k = 1; k < WPR; ++k) v = is_max ? fmaxf(v, red[g0w + k]) : v + red[g0w + k];
+  }
+  return v;
+}
+
+// WPR warps per row (long rows: K > 2048 splits a row over 2 warps), chunks of a row split
+// into WPR contiguous ranges of 32*CPL chunks.
+template <typename T, int CPL, int WPR>
 __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
                                                       const float* __restrict__ M,
                                                       T* __restrict__ Pout,
@@ -201,21 +219,25 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
                                                       int K, int HJ, float c, int64_t g0,
                                                       PhiloxKey pk) {
   using Cv = Chunk<T>;
+  __shared__ float red[8];
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int nc = K >> 3;
+  const int warp = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * ((blockDim.x >> 5) / WPR) + warp / WPR;
+  if (WPR == 1 && row >= rows) return;
+  const bool valid = row < rows;
+  const int nc = valid ? K >> 3 : 0;
+  const int cb = (warp % WPR) * 32 * CPL;   // first chunk of this warp's range
   const T* s = S + row * K;
   const float* m = M ? M + (int64_t)((int)row / HJ) * K : nullptr;  // rows < 2^31
   typename Cv::Raw raw[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i)
-    if (lane + 32 * i < nc) raw[i] = Cv::ld(s + (lane + 32 * i) * 8);
+    if (cb + lane + 32 * i < nc) raw[i] = Cv::ld(s + (cb + lane + 32 * i) * 8);
   float v[CPL][8];
   float mx = -INFINITY;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const int ch = lane + 32 * i;
+    const int ch = cb + lane + 32 * i;
     if (ch < nc) {
       Cv::unpack(raw[i], v[i]);
       if (m) {
@@ -231,11 +253,11 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
       for (int j = 0; j < 8; ++j) mx = fmaxf(mx, v[i][j]);
     }
   }
-  mx = warp_max(mx);
+  mx = row_reduce<WPR>(mx, true, red);
   float sum = 0.f;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    if (lane + 32 * i < nc) {
+    if (cb + lane + 32 * i < nc) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         v[i][j] = exp2f(v[i][j] - mx);
@@ -243,12 +265,12 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
       }
     }
   }
-  sum = warp_sum(sum);
+  sum = row_reduce<WPR>(sum, false, red);
   const float inv = 1.f / sum;
   const int64_t gbase = g0 + row * nc;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const int ch = lane + 32 * i;
+    const int ch = cb + lane + 32 * i;
     if (ch < nc) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[i][j] *= inv;
@@ -260,20 +282,24 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
 }
 
 // ------------------------------------------------------------------ BSB backward
-template <typename T, int CPL>
+template <typename T, int CPL, int WPR>
 __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
                                                       const T* __restrict__ Pin,
                                                       T* __restrict__ dS, int64_t rows, int K,
                                                       float scale, int64_t g0, PhiloxKey pk) {
   using Cv = Chunk<T>;
+  __shared__ float red[8];
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const int nc = K >> 3;
+  const int warp = threadIdx.x >> 5;
+  const int64_t row = (int64_t)blockIdx.x * ((blockDim.x >> 5) / WPR) + warp / WPR;
+  if (WPR == 1 && row >= rows) return;
+  const bool valid = row < rows;
+  const int nc = valid ? K >> 3 : 0;
+  const int cb = (warp % WPR) * 32 * CPL;
   typename Cv::Raw ra[CPL], rp[CPL];
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const int ch = lane + 32 * i;
+    const int ch = cb + lane + 32 * i;
     if (ch < nc) {
       ra[i] = Cv::ld(dA + row * K + ch * 8);
       rp[i] = Cv::ld(Pin + row * K + ch * 8);
@@ -284,7 +310,7 @@ __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
   const int64_t gbase = g0 + row * nc;
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const int ch = lane + 32 * i;
+    const int ch = cb + lane + 32 * i;
     if (ch < nc) {
       float p[8];
       Cv::unpack(ra[i], dp[i]);
@@ -294,10 +320,10 @@ __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
       for (int j = 0; j < 8; ++j) dot = fmaf(dp[i][j], p[j], dot);
     }
   }
-  dot = warp_sum(dot);
+  dot = row_reduce<WPR>(dot, false, red);
 #pragma unroll
   for (int i = 0; i < CPL; ++i) {
-    const int ch = lane + 32 * i;
+    const int ch = cb + lane + 32 * i;
     if (ch < nc) {
       float p[8], o[8];
       Cv::unpack(rp[i], p);
@@ -317,16 +343,27 @@ cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, c
   if (rows == 0) return cudaSuccess;
   const int nc = K / 8;
   const int64_t g0 = batch_offset * (int64_t)H * J * nc;
-  const int grid = (int)((rows + 7) / 8);
   const float c = scale * kLog2e;
-  ENC_CPL_DISPATCH(nc, {
+  if (nc > 256) {   // K > 2048: two warps per row, 8 chunks per lane
+    const int grid = (int)((rows + 3) / 4);
     if (dtype == 0)
-      bsb_fwd_kernel<__nv_bfloat16, CPL><<<grid, 256, 0, st>>>(
+      bsb_fwd_kernel<__nv_bfloat16, 8, 2><<<grid, 256, 0, st>>>(
           (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
           H * J, c, g0, pk);
     else
-      bsb_fwd_kernel<float, CPL><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
-                                                       (float*)A, rows, K, H * J, c, g0, pk);
+      bsb_fwd_kernel<float, 8, 2><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
+                                                        (float*)A, rows, K, H * J, c, g0, pk);
+    return cudaGetLastError();
+  }
+  const int grid = (int)((rows + 7) / 8);
+  ENC_CPL_DISPATCH(nc, {
+    if (dtype == 0)
+      bsb_fwd_kernel<__nv_bfloat16, CPL, 1><<<grid, 256, 0, st>>>(
+          (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
+          H * J, c, g0, pk);
+    else
+      bsb_fwd_kernel<float, CPL, 1><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
+                                                          (float*)A, rows, K, H * J, c, g0, pk);
   });
   return cudaGetLastError();
 }
@@ -338,15 +375,26 @@ cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, c
   if (rows == 0) return cudaSuccess;
   const int nc = K / 8;
   const int64_t g0 = batch_offset * (int64_t)H * J * nc;
-  const int grid = (int)((rows + 7) / 8);
-  ENC_CPL_DISPATCH(nc, {
+  if (nc > 256) {   // K > 2048: two warps per row, 8 chunks per lane
+    const int grid = (int)((rows + 3) / 4);
     if (dtype == 0)
-      bsb_bwd_kernel<__nv_bfloat16, CPL><<<grid, 256, 0, st>>>(
+      bsb_bwd_kernel<__nv_bfloat16, 8, 2><<<grid, 256, 0, st>>>(
           (const __nv_bfloat16*)dA, (const __nv_bfloat16*)P, (__nv_bfloat16*)dS, rows, K,
           scale, g0, pk);
     else
-      bsb_bwd_kernel<float, CPL><<<grid, 256, 0, st>>>((const float*)dA, (const float*)P,
-                                                       (float*)dS, rows, K, scale, g0, pk);
+      bsb_bwd_kernel<float, 8, 2><<<grid, 256, 0, st>>>((const float*)dA, (const float*)P,
+                                                        (float*)dS, rows, K, scale, g0, pk);
+    return cudaGetLastError();
+  }
+  const int grid = (int)((rows + 7) / 8);
+  ENC_CPL_DISPATCH(nc, {
+    if (dtype == 0)
+      bsb_bwd_kernel<__nv_bfloat16, CPL, 1><<<grid, 256, 0, st>>>(
+          (const __nv_bfloat16*)dA, (const __nv_bfloat16*)P, (__nv_bfloat16*)dS, rows, K,
+          scale, g0, pk);
+    else
+      bsb_bwd_kernel<float, CPL, 1><<<grid, 256, 0, st>>>((const float*)dA, (const float*)P,
+                                                          (float*)dS, rows, K, scale, g0, pk);
   });
   return cudaGetLastError();
 }

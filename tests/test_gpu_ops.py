@@ -53,7 +53,9 @@ def test_dropout_mask_bit_exact(ops, n, index0, p, sub):
 
 # ------------------------------------------------------------------ BSB
 BSB_SHAPES = [(2, 2, 16, 16), (3, 5, 7, 200), (2, 3, 9, 512), (1, 2, 5, 1024), (1, 1, 3, 4096),
-              (1, 1, 2, 8)]
+              (1, 1, 2, 8),
+              (1, 2, 7, 2056),   # K > 2048: two warps per row, the second range ragged
+              (2, 1, 5, 3000)]
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
