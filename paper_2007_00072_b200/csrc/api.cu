@@ -37,6 +37,10 @@ struct enc_ctx {
   int qkv_direct = 1;        // ENC_OPT_QKV_DIRECT
   LtCtx* lt = nullptr;       // cuBLASLt + measured algorithm cache (weight GEMMs)
   int use_lt = 1;            // ENC_OPT_GEMM_LT
+  // encoder_layer_step_host: host<->device copies on their own streams, overlapped with
+  // the layer (dY in during the forward, Y out during the backward)
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;
+  cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_start = nullptr;
 };
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
@@ -168,6 +172,12 @@ int enc_create(enc_ctx** out, int device) {
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1[i]);
   }
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
+  cudaEvent_t* evs[4] = {&c->ev_in, &c->ev_fwd, &c->ev_out, &c->ev_start};
+  for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+    e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
   cudaSetDevice(prev);
   *out = c;
@@ -205,6 +215,10 @@ void enc_destroy(enc_ctx* c) {
     if (c->ev1[i]) cudaEventDestroy(c->ev1[i]);
   }
   if (c->lt) lt_destroy(c->lt);
+  for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start})
+    if (ev) cudaEventDestroy(ev);
+  if (c->copy_in) cudaStreamDestroy(c->copy_in);
+  if (c->copy_out) cudaStreamDestroy(c->copy_out);
   if (c->blas) cublasDestroy(c->blas);
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->red) cudaFree(c->red);
@@ -1094,14 +1108,25 @@ int encoder_layer_step_host(enc_ctx* ctx, const enc_dims* d, int dtype, const en
   CHECK_PTRS(X_dev, dY_dev, Y_dev, dX_dev);
   cudaStream_t st = (cudaStream_t)stream;
   const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
+  // X in on the layer stream; dY in on copy_in while the forward runs; Y out on copy_out
+  // while the backward runs; dX out on the layer stream.  The call's stream finishes only
+  // after every copy (it waits for copy_out at the end).
+  CK(cudaEventRecord(ctx->ev_start, st));
+  CK(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_start, 0));
   CK(cudaMemcpyAsync(X_dev, X_host, bytes, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dY_dev, dY_host, bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dY_dev, dY_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+  CK(cudaEventRecord(ctx->ev_in, ctx->copy_in));
   r = encoder_layer_forward(ctx, d, dtype, cfg, prm, X_dev, mask_bias, Y_dev, saved, scratch, stream);
   if (r) return r;
+  CK(cudaEventRecord(ctx->ev_fwd, st));
+  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_fwd, 0));
+  CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  CK(cudaEventRecord(ctx->ev_out, ctx->copy_out));
+  CK(cudaStreamWaitEvent(st, ctx->ev_in, 0));
   r = encoder_layer_backward(ctx, d, dtype, cfg, prm, X_dev, saved, dY_dev, dX_dev, g, scratch, stream);
   if (r) return r;
-  CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(dX_host, dX_dev, bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
   return ENC_OK;
 }
 
