@@ -24,6 +24,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "BERT-large encoder layer fwd+bwd tokens/s"
+METRIC_STACK = "BERT-large encoder stack fwd+bwd tokens/s"   # --layers N > 1
 UNIT = "tokens/s"
 WORKLOADS = {
     "L": "L: BERT-large encoder layer B=8/GPU J=K=512 H=16 P=64 I=1024 U=4096 p=0.1 GELU",
@@ -53,6 +54,9 @@ def parse():
     ap.add_argument("--attn-backend", choices=["fused", "tc", "cublas"], default="fused",
                     help="attention: fused tcgen05 score kernels (QK^T+BSB, dA+BSB-bwd), "
                          "separate tcgen05 contractions, or cuBLAS contractions")
+    ap.add_argument("--layers", type=int, default=1,
+                    help="encoder layers per step (24 = the BERT-large encoder stack, config 4 "
+                         "of BASELINE.json; per-layer gradient all-reduce for N > 1)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every step eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -190,7 +194,8 @@ def main():
     __graft_entry__.build()
     from paper_2007_00072_b200 import _abi, dp, tally
     from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
-    from synth import CONFIGS, make_inputs, make_params
+    from paper_2007_00072_b200.stack import EncoderStack
+    from synth import CONFIGS, SEED_WEIGHTS, make_inputs, make_params
 
     # one process per GPU; ENC_DIST_BACKEND=gloo (test hook) lets several ranks share one GPU
     backend = os.environ.get("ENC_DIST_BACKEND", "nccl")
@@ -209,8 +214,15 @@ def main():
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
 
     cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff)
-    layer = EncoderLayer(dims, args.dtype, cfg)
-    layer.set_params(make_params(dims, args.dtype, "bench"))
+    stack = None
+    if args.layers > 1:
+        stack = EncoderStack(args.layers, dims, args.dtype, cfg)
+        stack.set_params([make_params(dims, args.dtype, "bench", seed=SEED_WEIGHTS + i)
+                          for i in range(args.layers)])
+        layer = stack.layers[0]     # the layers share one context (options, timing, counts)
+    else:
+        layer = EncoderLayer(dims, args.dtype, cfg)
+        layer.set_params(make_params(dims, args.dtype, "bench"))
     _abi.check("enc_set_option", _abi.load().enc_set_option(
         layer.ctx.ptr, 0, int(args.attn_backend in ("tc", "fused"))))
     _abi.check("enc_set_option", _abi.load().enc_set_option(
@@ -229,19 +241,41 @@ def main():
     names = [lib.enc_op_name(i).decode() for i in range(nops)]
     ms_buf = (_abi.c_float * nops)()
 
-    def step():
-        # data parallel: the FFN-gradient all-reduce is issued as soon as the FFN half of the
-        # backward is done and overlaps the attention half
-        layer.forward(X, None, Y)
+    # The step as a list of (device work, gradient buckets all-reduced right after it).
+    # Data parallel: every all-reduce is issued as soon as its gradients are final and
+    # overlaps the rest of the backward: one layer -> the FFN bucket after
+    # the FFN half of the backward, the attention bucket after the rest; a stack -> each
+    # layer's gradients after that layer's backward.
+    if stack is None:
         if world > 1:
-            layer.backward(X, dY, dX, part=layer.BWD_FFN)
-            w1 = dp.allreduce_buckets([layer.ffn_bucket], async_op=True)
-            layer.backward(X, dY, dX, part=layer.BWD_ATTN)
-            w2 = dp.allreduce_buckets([layer.attn_bucket], async_op=True)
-            for w in w1 + w2:
-                w.wait()
+            parts = [(lambda: (layer.forward(X, None, Y),
+                               layer.backward(X, dY, dX, part=layer.BWD_FFN)),
+                      [layer.ffn_bucket]),
+                     (lambda: layer.backward(X, dY, dX, part=layer.BWD_ATTN),
+                      [layer.attn_bucket])]
         else:
-            layer.backward(X, dY, dX)
+            parts = [(lambda: (layer.forward(X, None, Y), layer.backward(X, dY, dX)), [])]
+    elif world > 1:
+        def bwd_layer(i):
+            src = dY if i == args.layers - 1 else stack.grads_io[(i + 1) % 2]
+            return lambda: stack.layers[i].backward(stack.acts[i], src, stack.grads_io[i % 2])
+        parts = [(lambda: stack.forward(X), [])]
+        parts += [(bwd_layer(i), [stack.layers[i].grad_flat])
+                  for i in reversed(range(args.layers))]
+    else:
+        parts = [(lambda: (stack.forward(X), stack.backward(dY)), [])]
+
+    def run_parts(fns):
+        works = []
+        for fn, (_f, buckets) in zip(fns, parts):
+            fn()
+            if world > 1 and buckets:
+                works += dp.allreduce_buckets(buckets, async_op=True)
+        for w in works:
+            w.wait()
+
+    def step():
+        run_parts([f for f, _b in parts])
 
     def barrier():
         if world > 1:
@@ -273,29 +307,22 @@ def main():
     dom_id = names.index(dominant)
     lib.enc_set_timing(layer.ctx.ptr, 1 << dom_id)
     l0 = lib.enc_launch_count(layer.ctx.ptr)
-    layer.forward(X, None, Y)
-    layer.backward(X, dY, dX)
+    for fn, _b in parts:
+        fn()
     per_step_launches = lib.enc_launch_count(layer.ctx.ptr) - l0
 
-    # ---------------- CUDA graph of the layer step (fwd + bwd); events of the timed op
-    # (enabled above) are captured as event-record nodes of the graph
-    # two graphs for N > 1 (forward + FFN half of the backward | attention half) so the
-    # eager NCCL all-reduce of the FFN bucket overlaps the second graph
-    if world > 1:
-        parts = [lambda: (layer.forward(X, None, Y),
-                          layer.backward(X, dY, dX, part=layer.BWD_FFN)),
-                 lambda: layer.backward(X, dY, dX, part=layer.BWD_ATTN)]
-    else:
-        parts = [lambda: (layer.forward(X, None, Y), layer.backward(X, dY, dX))]
+    # ---------------- CUDA graphs of the step, one per part (one graph for N = 1); events of
+    # the timed op (enabled above) are captured as event-record nodes of the graph; the
+    # eager NCCL all-reduce issued after a part overlaps the replay of the next ones
     if not args.eager:
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
-            for fn in parts:
+            for fn, _b in parts:
                 fn()
         torch.cuda.current_stream(dev).wait_stream(side)
         graphs = []
-        for fn in parts:
+        for fn, _b in parts:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
@@ -303,13 +330,7 @@ def main():
         torch.cuda.synchronize()
 
         def step():  # noqa: F811
-            graphs[0].replay()
-            if world > 1:
-                w1 = dp.allreduce_buckets([layer.ffn_bucket], async_op=True)
-                graphs[1].replay()
-                w2 = dp.allreduce_buckets([layer.attn_bucket], async_op=True)
-                for w in w1 + w2:
-                    w.wait()
+            run_parts([g.replay for g in graphs])
         for _ in range(2):
             step()
         torch.cuda.synchronize()
@@ -366,6 +387,9 @@ def main():
         roof = {"kernel": dominant, "bound": "tensor", "achieved": ach, "peak": tc_peak,
                 "unit": "TFLOP/s", "frac": ach / tc_peak, "traffic": None,
                 "algorithmic_flops": flops[dominant], "peak_source": peak_src + " (sustained)"}
+    if stack is not None:   # the layers share the context's events: the last instance
+        roof["instance"] = "last launch of the step (layer 0's backward / layer {}'s forward)" \
+            .format(args.layers - 1)
     traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
     # the committed ncu traffic figures are per launch at config L, bf16, default path
     if os.path.exists(traffic_path) and args.config == "L" and args.dtype == "bf16" \
@@ -381,8 +405,18 @@ def main():
     Yh = torch.empty_like(Xh).pin_memory()
     dXh = torch.empty_like(Xh).pin_memory()
     lib.enc_set_timing(layer.ctx.ptr, 0)
+    if stack is not None:
+        def host_step():
+            stack.step_host(Xh, dYh, Yh, dXh)
+        e2e_buckets = [lay.grad_flat for lay in stack.layers]
+        e2e_api = f"EncoderStack.step_host ({args.layers} layers; "
+    else:
+        def host_step():
+            layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+        e2e_buckets = [layer.ffn_bucket, layer.attn_bucket]
+        e2e_api = "encoder_layer_step_host ("
     for _ in range(2):
-        layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+        host_step()
     torch.cuda.synchronize()
     # the call captured once in a CUDA graph (its copies from / to pinned host memory and
     # the copy-stream fork / join included) and replayed per step, like the device timing
@@ -390,7 +424,7 @@ def main():
     if not args.eager:
         g_e2e = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g_e2e):
-            layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+            host_step()
         g_e2e.replay()
         torch.cuda.synchronize()
     barrier()
@@ -400,16 +434,16 @@ def main():
         if g_e2e is not None:
             g_e2e.replay()
         else:
-            layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
+            host_step()
         if world > 1:
-            dp.allreduce_buckets([layer.ffn_bucket, layer.attn_bucket])
+            dp.allreduce_buckets(e2e_buckets)
     e1.record()
     barrier()
     e2e_ms = dp.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
     e2e = {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": 2 * X.numel() * es, "d2h_bytes_per_step": 2 * X.numel() * es,
            "ms_per_step": e2e_ms,
-           "how": "encoder_layer_step_host (H2D X, dY from pinned host memory; D2H Y, dX) "
+           "how": e2e_api + "H2D X, dY from pinned host memory; D2H Y, dX) "
                   + ("replayed as a CUDA graph" if g_e2e is not None else "eager")}
 
     if args.breakdown and rank == 0:
@@ -433,15 +467,19 @@ def main():
                    "sample": f"{len(ts)} x one sequence (B=1 slice of config {args.config}) "
                              f"fwd+bwd, fp64 numpy oracle, {sum(ts):.1f} s"}
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC if stack is None else METRIC_STACK, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "global_batch": dims_global.B,
+            "config": {"workload": WORKLOADS[args.config] if stack is None
+                       else f"Lx{args.layers}: {args.layers}-layer encoder stack of "
+                            + WORKLOADS[args.config],
+                       "layers": args.layers, "global_batch": dims_global.B,
                        "seq_len": dims.J,
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
-                       else "not flushed", "graph": "eager launches" if args.eager else "CUDA graph replay (fwd+bwd)",
+                       else "not flushed", "graph": "eager launches" if args.eager
+                       else f"CUDA graph replay (fwd+bwd, {len(parts)} graph(s) per step)",
                        "attention": attention_desc(args, dims)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,

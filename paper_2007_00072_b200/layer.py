@@ -59,7 +59,9 @@ class EncoderLayer:
     """
 
     def __init__(self, dims, dtype: str = "bf16", cfg: LayerCfg | None = None,
-                 ctx: Context | None = None, device=None):
+                 ctx: Context | None = None, device=None, scratch: torch.Tensor | None = None):
+        """scratch: optional shared temporaries buffer (layers of a stack run one at a time and
+        may share it); allocated here when None or too small."""
         self.lib = _abi.load()
         self.B, self.J, self.H, self.P, self.U = dims.B, dims.J, dims.H, dims.P, dims.U
         self.I = self.H * self.P
@@ -74,7 +76,10 @@ class EncoderLayer:
         check("enc_layer_sizes", self.lib.enc_layer_sizes(ctypes.byref(self.dims), self.adt,
                                                           ctypes.byref(sb), ctypes.byref(cb)))
         self.saved = torch.empty(max(sb.value, 16), dtype=torch.uint8, device=self.device)
-        self.scratch = torch.empty(max(cb.value, 16), dtype=torch.uint8, device=self.device)
+        if scratch is not None and scratch.numel() >= cb.value:
+            self.scratch = scratch
+        else:
+            self.scratch = torch.empty(max(cb.value, 16), dtype=torch.uint8, device=self.device)
         shapes = param_shapes(self.I, self.U)
         self.params = {}
         for n, s in shapes.items():
