@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=6)  # ~13 s of oracle work
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--bwd-side", action="store_true",
+                    help="weight-gradient contractions on a side stream (ENC_OPT_BWD_SIDE)")
     ap.add_argument("--no-qkv-direct", action="store_true",
                     help="separate AIB / AIB-bwd passes instead of the in-place QKV layout")
     ap.add_argument("--no-attn-bh", action="store_true",
@@ -230,6 +232,8 @@ def main():
     _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 4, int(not args.no_attn_bh)))
     _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 5,
                                                             int(not args.no_qkv_direct)))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 6,
+                                                            int(args.bwd_side)))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
@@ -483,7 +487,9 @@ def main():
                        "attention": attention_desc(args, dims)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
-            "per_op_us": {n: round(per_op[n] * 1e3, 2) for n in names},
+            # ops fused away on this path (no launch of their own) are null
+            "per_op_us": {n: (round(per_op[n] * 1e3, 2) if per_op[n] >= 0 else None)
+                          for n in names},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

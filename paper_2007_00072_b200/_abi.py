@@ -10,7 +10,8 @@ import os
 from ctypes import (POINTER, c_char_p, c_float, c_int, c_int64, c_size_t, c_uint32, c_uint64,
                     c_void_p)
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libencoder.so")
+LIB_PATH = os.environ.get("ENC_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libencoder.so")
 
 ENC_BF16 = 0
 ENC_FP32 = 1

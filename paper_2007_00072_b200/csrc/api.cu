@@ -41,15 +41,22 @@ struct enc_ctx {
   // the layer (dY in during the forward, Y out during the backward)
   cudaStream_t copy_in = nullptr, copy_out = nullptr;
   cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_start = nullptr;
+  // backward: weight-gradient contractions on a side stream (own cuBLASLt workspace),
+  // forked after their inputs are ready and joined at the end of each backward part
+  int bwd_side = 0;          // ENC_OPT_BWD_SIDE (off: measured +1 % at L, -3 % at Bb)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void* side_ws = nullptr;
 };
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
 static cublasStatus_t wgemm(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA,
                             bool tB, int M, int N, int K, float alpha, const void* A, int lda,
-                            const void* B, int ldb, float beta, void* C, int ldc) {
+                            const void* B, int ldb, float beta, void* C, int ldc,
+                            void* ws = nullptr) {
   if (ctx->lt && ctx->use_lt && alpha == 1.f)
     return lt_gemm_rm(ctx->lt, in_dt, out_dt, tA, tB, M, N, K, A, lda, B, ldb, beta, C, ldc,
-                      LT_EPI_NONE, nullptr, st);
+                      LT_EPI_NONE, nullptr, st, ws);
   return gemm_rm(ctx->blas, in_dt, out_dt, tA, tB, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
 }
 
@@ -160,6 +167,7 @@ int enc_create(enc_ctx** out, int device) {
   c->red_floats = (64u << 20) / sizeof(float);
   e = cudaMalloc(&c->blas_ws, c->blas_ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->red, c->red_floats * sizeof(float));
+  if (e == cudaSuccess) e = cudaMalloc(&c->side_ws, c->blas_ws_bytes);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   if (cublasSetWorkspace(c->blas, c->blas_ws, c->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS ||
       cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
@@ -174,8 +182,9 @@ int enc_create(enc_ctx** out, int device) {
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
-  cudaEvent_t* evs[4] = {&c->ev_in, &c->ev_fwd, &c->ev_out, &c->ev_start};
-  for (int i = 0; i < 4 && e == cudaSuccess; ++i)
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaEvent_t* evs[6] = {&c->ev_in, &c->ev_fwd, &c->ev_out, &c->ev_start, &c->ev_fork, &c->ev_join};
+  for (int i = 0; i < 6 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -215,8 +224,10 @@ void enc_destroy(enc_ctx* c) {
     if (c->ev1[i]) cudaEventDestroy(c->ev1[i]);
   }
   if (c->lt) lt_destroy(c->lt);
-  for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start})
+  for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join})
     if (ev) cudaEventDestroy(ev);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->side_ws) cudaFree(c->side_ws);
   if (c->copy_in) cudaStreamDestroy(c->copy_in);
   if (c->copy_out) cudaStreamDestroy(c->copy_out);
   if (c->blas) cublasDestroy(c->blas);
@@ -676,6 +687,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->qkv_direct = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_BWD_SIDE) {
+    ctx->bwd_side = value ? 1 : 0;
+    return ENC_OK;
+  }
   return ENC_EINVAL;
 }
 
@@ -913,6 +928,25 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     const size_t used = ((size_t)j.R * j.ncols + 63) & ~(size_t)63;
     return ReduceWs{ws.partials + used, ws.cap_floats - used, ws.num_sms};
   };
+  // weight-gradient contractions go to the side stream: fork once the inputs exist, join
+  // before returning (the next forward reuses the scratch they read)
+  const bool use_side = ctx->bwd_side && ctx->lt && ctx->use_lt && ctx->side;
+  bool forked = false;
+  auto fork = [&]() -> cudaStream_t {
+    if (!use_side) return st;
+    cudaEventRecord(ctx->ev_fork, st);
+    cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
+    forked = true;
+    return ctx->side;
+  };
+  void* const sws = use_side ? ctx->side_ws : nullptr;
+  auto join = [&]() -> cudaError_t {
+    if (!forked) return cudaSuccess;
+    forked = false;
+    cudaError_t e = cudaEventRecord(ctx->ev_join, ctx->side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ctx->ev_join, 0);
+    return e;
+  };
   if (parts & 1) {
   ColsumJob ffn_jobs[2];
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
@@ -930,8 +964,9 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, U, I, 1.f, dY2, I, prm->W2, U, 0.f, dA1, U));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, st, 0);
-    CB(wgemm(ctx, st,dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U));
+    cudaStream_t ss = fork();
+    OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
+    CB(wgemm(ctx, ss, dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U, sws));
   }
   // BAD-bwd (:576-578), then the FFN half's column sums (dg2, dbe2, db2, db1) in one launch
   {
@@ -948,9 +983,11 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, U, 1.f, dh, U, prm->W1, I, 1.f, dX1, I));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, st, 0);
-    CB(wgemm(ctx, st,dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I));
+    cudaStream_t ss = fork();
+    OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, ss, 0);
+    CB(wgemm(ctx, ss, dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I, sws));
   }
+  if (!(parts & 2)) CK(join());   // the FFN bucket is complete when the FFN part returns
   }  // FFN half
   if (!(parts & 2)) return ENC_OK;
   // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo; its column
@@ -971,8 +1008,9 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, I, 1.f, dYo, I, prm->Wo, I, 0.f, dC, I));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, st, 0);
-    CB(wgemm(ctx, st,dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I));
+    cudaStream_t ss = fork();
+    OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, ss, 0);
+    CB(wgemm(ctx, ss, dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I, sws));
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
@@ -1055,9 +1093,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                1.f, dX, I));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, st, 0);
-    CB(wgemm(ctx, st, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
-             g->dWqkv, I));
+    cudaStream_t ss = fork();
+    OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, ss, 0);
+    CB(wgemm(ctx, ss, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
+             g->dWqkv, I, sws));
   }
   if (direct && !bgrad_epi) {
     // bias gradient as a column sum of dQKV (cuBLASLt's BGRAD epilogue on the dW
@@ -1077,6 +1116,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     }
     CK(launch_colsum_finalize_jobs(att_jobs, bgrad_epi ? 2 : 1, st));
   }
+  CK(join());
   return ENC_OK;
 }
 

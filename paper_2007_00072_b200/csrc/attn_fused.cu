@@ -113,6 +113,21 @@ __device__ __forceinline__ constexpr int flag_bit(int j, int u) {
   return ((u & 1) ? 31 : 15) - (u >> 1) - 4 * j;
 }
 
+#ifdef ENC_FUSED_TRACE
+// Debug-only phase timestamps (tools/trace_fused.py builds a separate library with this on).
+__device__ unsigned long long g_fused_trace[148 * 2 * 8 * 8];
+__device__ __forceinline__ void trace_ev(int warp, int lane, int it, int e) {
+  if (lane == 0 && (warp == 0 || warp == 31) && it < 8 && blockIdx.x < 148) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_fused_trace[((blockIdx.x * 2 + (warp == 31)) * 8 + it) * 8 + e] = t;
+  }
+}
+#define TRACE(e) trace_ev(warp, lane, it, (e))
+#else
+#define TRACE(e) ((void)0)
+#endif
+
 // shared-memory layout (bytes from a 1024-aligned base)
 //   [0, 16K)     Q / dC tile [128 x 64] bf16 K-major SW128
 //   [16K, 80K)   K / V  tile [512 x 64] bf16 K-major SW128 (two 256-row boxes)
@@ -200,10 +215,35 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   if (leader && blockIdx.x < prm.tiles) load_operands(blockIdx.x);
   if (kBwd && lane == 0 && blockIdx.x < prm.tiles) load_psub(blockIdx.x);
 
+  // Forward: the keep flags of the NEXT tile are generated inside pass 1 of this tile, so
+  // the fma-pipe Philox work (IMAD.WIDE) interleaves with pass 1's MUFU / TMEM work instead
+  // of running alone at the head of every tile; the first tile's flags are made up front.
+  auto grow_of = [&](int t) -> int64_t {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    return prm.g0 + ((int64_t)bh * prm.J + m0 + r) * (kK / 8) + cb / 8;
+  };
+  // flags of Philox chunks 4c + j0 and 4c + j0 + 1 (two calls in flight)
+  auto flags_pair = [&](int64_t grow, int pi) -> uint32_t {
+    const int c = pi >> 1, j0 = 2 * (pi & 1);
+    return keep_flags((uint64_t)(grow + 4 * c + j0), pk, C2, X, 4 * j0) |
+           keep_flags((uint64_t)(grow + 4 * c + j0 + 1), pk, C2, X, 4 * j0 + 4);
+  };
+  uint32_t kfn[kW / 32] = {0xFFFFFFFFu, 0xFFFFFFFFu};
+  if (!kBwd && pk.T != 0 && blockIdx.x < prm.tiles) {
+    const int64_t grow = grow_of(blockIdx.x);
+#pragma unroll 1
+    for (int pi = 0; pi < 4; ++pi) {
+      const uint32_t f = flags_pair(grow, pi);
+      kfn[pi >> 1] = (pi & 1) ? (kfn[pi >> 1] | f) : f;
+    }
+  }
+
   int it = 0;
   for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
+    TRACE(0);
     if (leader) {
       // MMA of this tile once every warp released TMEM and the operands landed
       mbar_wait(tm_empty, (it & 1) ^ 1);
@@ -230,8 +270,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(kbw));
       kf[0] = w2.x;
       kf[1] = w2.y;
-    } else if (pk.T == 0) {   // p = 0: everything kept, no Philox stream
-      kf[0] = kf[1] = 0xFFFFFFFFu;
+    } else if (!kBwd || pk.T == 0) {   // fwd: made during the previous tile (all ones at p = 0)
+      kf[0] = kfn[0];
+      kf[1] = kfn[1];
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     } else {
       const int64_t grow = prm.g0 + rowi * (kK / 8) + cb / 8;
@@ -245,8 +286,10 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       }
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     }
+    TRACE(1);
     mbar_wait_sleep(tm_full, it & 1);
     tc::fence_after_sync();
+    TRACE(2);
     if (leader && t + (int)gridDim.x < prm.tiles) {   // operands free: prefetch the next tile
       mbar_wait(op_empty, it & 1);
       load_operands(t + gridDim.x);
@@ -260,6 +303,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       constexpr int kNs = kW / kSub;
       const float c = prm.c;
       float mc[kNs], lc[kNs];
+      const int tn = t + (int)gridDim.x;
+      const bool gen_next = pk.T != 0 && tn < prm.tiles;
+      const int64_t grown = gen_next ? grow_of(tn) : 0;
 #pragma unroll
       for (int ch = 0; ch < kNs; ++ch) {
         float m;
@@ -303,6 +349,14 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           tc::tmem_st32(trow + ch * kSub, v);
         }
         mc[ch] = m;
+        if (gen_next) {   // next tile's keep flags: 4 / kNs Philox pairs per sub-chunk
+#pragma unroll
+          for (int pp = 0; pp < 4 / kNs; ++pp) {
+            const int pi = ch * (4 / kNs) + pp;
+            const uint32_t f = flags_pair(grown, pi);
+            kfn[pi >> 1] = (pi & 1) ? (kfn[pi >> 1] | f) : f;
+          }
+        }
       }
       float mt = mc[0];
 #pragma unroll
@@ -314,7 +368,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       float2* st = stats + (it & 1) * (kSlices * kRows);
       st[slice * kRows + r] = make_float2(mt, lt);
       tc::tmem_wait_st();
+      TRACE(3);
       qbar(q);
+      TRACE(4);
       // row max M and sum L over the 8 slices
       float M = st[r].x;
 #pragma unroll
@@ -335,8 +391,13 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
-        if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
-        __syncwarp();
+        // without A the staging pair holds both 32-column P chunks, so the first chunk's
+        // store is not waited for and both drain under the next tile's pass 1
+        unsigned char* stg = own + (prm.write_a ? 0 : ch * 2048);
+        if (prm.write_a || ch == 0) {
+          if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
+          __syncwarp();
+        }
         tc::tmem_ld32(trow + ch * 32, v);
         if (ch + 1 == kW / 32) {   // last TMEM read of this tile by this warp
           tc::fence_before_sync();
@@ -350,7 +411,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           const float fp = fP[(ch * 32 + 8 * j) / kSub], fa = fp * ds;
 #pragma unroll
           for (int u = 0; u < 8; ++u) x[u] = v[8 * j + u] * fp;
-          *reinterpret_cast<uint4*>(own + sw64(lane, j)) = pack8(x);
+          *reinterpret_cast<uint4*>(stg + sw64(lane, j)) = pack8(x);
           if (prm.write_a) {
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -361,14 +422,16 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO1, stg, cb + ch * 32, m0 + q * 32, h, b);
           if (prm.write_a) tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
           tc::bulk_commit();
         }
       }
+      TRACE(5);
     } else {
       // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
       mbar_wait_sleep(&p_full[warp], it & 1);
+      TRACE(3);
       float dot = 0.f;
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
@@ -388,7 +451,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       // rewritten two tiles later, after every warp of the quarter passed the next barrier
       float* st = reinterpret_cast<float*>(stats) + (it & 1);
       st[2 * (slice * kRows + r)] = dot;
+      TRACE(4);
       qbar(q);
+      TRACE(5);
       float D = 0.f;
 #pragma unroll
       for (int s2 = 0; s2 < kSlices; ++s2) D += st[2 * (s2 * kRows + r)];
@@ -416,6 +481,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           *loc = pack8(p);
         }
       }
+      TRACE(6);
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -428,6 +494,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
         }
       }
       __syncwarp();
+      TRACE(7);
     }
   }
   if (lane == 0) tc::bulk_wait<0>();
@@ -536,5 +603,15 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
   return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st)
                    : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st);
 }
+
+#ifdef ENC_FUSED_TRACE
+extern "C" int enc_debug_fused_trace(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, g_fused_trace, bytes);
+}
+extern "C" int enc_debug_fused_trace_clear() {
+  static unsigned long long zero[148 * 2 * 8 * 8];
+  return (int)cudaMemcpyToSymbol(g_fused_trace, zero, sizeof(zero));
+}
+#endif
 
 }  // namespace enc

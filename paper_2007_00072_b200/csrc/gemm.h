@@ -26,5 +26,6 @@ void lt_set_autotune(LtCtx* c, int on);
 // reduction dimension).
 cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool tB, int M, int N,
                           int K, const void* A, int lda, const void* B, int ldb, float beta,
-                          void* C, int ldc, int epi, void* bias, cudaStream_t st);
+                          void* C, int ldc, int epi, void* bias, cudaStream_t st,
+                          void* ws_override = nullptr);
 }  // namespace enc

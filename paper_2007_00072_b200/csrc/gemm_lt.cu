@@ -79,7 +79,8 @@ struct Desc {
 // Row-major C[M,N] = op(A) op(B) (+ beta C) (+ epilogue); see gemm.cu for the operand swap.
 cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool tB, int M, int N,
                           int K, const void* A, int lda, const void* B, int ldb, float beta,
-                          void* C, int ldc, int epi, void* bias, cudaStream_t st) {
+                          void* C, int ldc, int epi, void* bias, cudaStream_t st, void* ws_override) {
+  void* const ws = ws_override ? ws_override : L->ws;
   const cublasComputeType_t ct = in_dtype == 0 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
   Desc d;
   cublasStatus_t s = cublasLtMatmulDescCreate(&d.op, ct, CUDA_R_32F);
@@ -154,12 +155,12 @@ cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool t
           bool ok = true;
           for (int w = 0; w < 2 && ok; ++w)   // warm-up
             ok = cublasLtMatmul(L->h, d.op, &alpha, B, d.a, A, d.b, &beta, L->tmp, d.c, L->tmp,
-                                d.c, &res[i].algo, L->ws, L->ws_bytes, st) == CUBLAS_STATUS_SUCCESS;
+                                d.c, &res[i].algo, ws, L->ws_bytes, st) == CUBLAS_STATUS_SUCCESS;
           if (!ok) continue;
           cudaEventRecord(e0, st);
           for (int r = 0; r < 5; ++r)
             cublasLtMatmul(L->h, d.op, &alpha, B, d.a, A, d.b, &beta, L->tmp, d.c, L->tmp, d.c,
-                           &res[i].algo, L->ws, L->ws_bytes, st);
+                           &res[i].algo, ws, L->ws_bytes, st);
           cudaEventRecord(e1, st);
           cudaEventSynchronize(e1);
           float ms = 0.f;
@@ -182,7 +183,7 @@ cublasStatus_t lt_gemm_rm(LtCtx* L, int in_dtype, int out_dtype, bool tA, bool t
     L->plans[key] = plan;
   }
   return cublasLtMatmul(L->h, d.op, &alpha, B, d.a, A, d.b, &beta, C, d.c, C, d.c, &plan.algo,
-                        L->ws, L->ws_bytes, st);
+                        ws, L->ws_bytes, st);
 }
 
 }  // namespace enc

@@ -127,7 +127,8 @@ def enc_set_option(ctx, key, value):
     check("enc_set_option", _abi.load().enc_set_option(ctx.ptr, key, value))
 
 
-OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT = range(6)
+(OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT,
+ OPT_BWD_SIDE) = range(7)
 
 
 def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
