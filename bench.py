@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=6)  # ~13 s of oracle work
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="e2e through encoder_layer_step_host (no cross-step input prefetch)")
     ap.add_argument("--bwd-side", action="store_true",
                     help="weight-gradient contractions on a side stream (ENC_OPT_BWD_SIDE)")
     ap.add_argument("--no-qkv-direct", action="store_true",
@@ -419,36 +421,66 @@ def main():
             layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
         e2e_buckets = [layer.ffn_bucket, layer.attn_bucket]
         e2e_api = "encoder_layer_step_host ("
-    for _ in range(2):
-        host_step()
-    torch.cuda.synchronize()
-    # the call captured once in a CUDA graph (its copies from / to pinned host memory and
-    # the copy-stream fork / join included) and replayed per step, like the device timing
+    pipelined = stack is None and not args.no_prefetch
     g_e2e = None
-    if not args.eager:
-        g_e2e = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g_e2e):
-            host_step()
-        g_e2e.replay()
+    if pipelined:
+        # a training loop over host batches: encoder_layer_step_host_pipelined prefetches
+        # step s+1's X, dY during step s and copies Y, dX back during step s+1; device
+        # buffers double-buffered; every step's copies are inside the timed region
+        Xd, dYd = [X, torch.empty_like(X)], [dY, torch.empty_like(dY)]
+        Yd, dXd = [Y, torch.empty_like(Y)], [dX, torch.empty_like(dX)]
+
+        def host_loop(n):
+            layer.prefetch_inputs(Xh, dYh, Xd[0], dYd[0])
+            for i in range(n):
+                a, b = i & 1, (i + 1) & 1
+                nxt = i + 1 < n
+                layer.step_host_pipelined(Yh, dXh, Xd[a], dYd[a], Yd[a], dXd[a],
+                                          Xh if nxt else None, dYh if nxt else None,
+                                          Xd[b], dYd[b])
+                if world > 1:
+                    dp.allreduce_buckets(e2e_buckets)
+            layer.outputs_wait()
+        host_loop(3)
         torch.cuda.synchronize()
+    else:
+        for _ in range(2):
+            host_step()
+        torch.cuda.synchronize()
+        # the call captured once in a CUDA graph (its copies from / to pinned host memory and
+        # the copy-stream fork / join included) and replayed per step, like the device timing
+        if not args.eager:
+            g_e2e = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_e2e):
+                host_step()
+            g_e2e.replay()
+            torch.cuda.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        if g_e2e is not None:
-            g_e2e.replay()
-        else:
-            host_step()
-        if world > 1:
-            dp.allreduce_buckets(e2e_buckets)
+    if pipelined:
+        host_loop(args.steps)
+    else:
+        for _ in range(args.steps):
+            if g_e2e is not None:
+                g_e2e.replay()
+            else:
+                host_step()
+            if world > 1:
+                dp.allreduce_buckets(e2e_buckets)
     e1.record()
     barrier()
     e2e_ms = dp.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
+    if pipelined:
+        how = ("encoder_layer_step_host_pipelined, eager loop of the timed steps (H2D X, dY "
+               "of step s+1 from pinned host memory prefetched during step s; D2H Y, dX on "
+               "the copy-out stream; the loop's first prefetch and last copies included)")
+    else:
+        how = (e2e_api + "H2D X, dY from pinned host memory; D2H Y, dX) "
+               + ("replayed as a CUDA graph" if g_e2e is not None else "eager"))
     e2e = {"value": tokens / (e2e_ms * 1e-3), "unit": UNIT,
            "h2d_bytes_per_step": 2 * X.numel() * es, "d2h_bytes_per_step": 2 * X.numel() * es,
-           "ms_per_step": e2e_ms,
-           "how": e2e_api + "H2D X, dY from pinned host memory; D2H Y, dX) "
-                  + ("replayed as a CUDA graph" if g_e2e is not None else "eager")}
+           "ms_per_step": e2e_ms, "how": how}
 
     if args.breakdown and rank == 0:
         for n in names:

@@ -47,6 +47,17 @@ struct enc_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* side_ws = nullptr;
+  // pipelined host steps: input prefetch done (ev_pf, recorded on copy_in), prefetch
+  // start / backward done markers on the layer stream, and the last two steps' output
+  // copies (device buffers read, completion event on copy_out)
+  cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
+  struct OutRec {
+    const void* y = nullptr;
+    const void* dx = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool live = false;
+  } orec[2];
+  int orec_i = 0;
 };
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
@@ -183,8 +194,10 @@ int enc_create(enc_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  cudaEvent_t* evs[6] = {&c->ev_in, &c->ev_fwd, &c->ev_out, &c->ev_start, &c->ev_fork, &c->ev_join};
-  for (int i = 0; i < 6 && e == cudaSuccess; ++i)
+  cudaEvent_t* evs[11] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
+                          &c->ev_fork, &c->ev_join, &c->ev_pf, &c->ev_pfs,
+                          &c->ev_bwd,  &c->orec[0].ev, &c->orec[1].ev};
+  for (int i = 0; i < 11 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -224,7 +237,8 @@ void enc_destroy(enc_ctx* c) {
     if (c->ev1[i]) cudaEventDestroy(c->ev1[i]);
   }
   if (c->lt) lt_destroy(c->lt);
-  for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join})
+  for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join,
+                         c->ev_pf, c->ev_pfs, c->ev_bwd, c->orec[0].ev, c->orec[1].ev})
     if (ev) cudaEventDestroy(ev);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side_ws) cudaFree(c->side_ws);
@@ -1167,6 +1181,93 @@ int encoder_layer_step_host(enc_ctx* ctx, const enc_dims* d, int dtype, const en
   if (r) return r;
   CK(cudaMemcpyAsync(dX_host, dX_dev, bytes, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+  return ENC_OK;
+}
+
+// input prefetch on copy_in, behind the work already on `st`
+static int prefetch(enc_ctx* ctx, size_t bytes, const void* X_host, const void* dY_host,
+                    void* X_dev, void* dY_dev, cudaStream_t st) {
+  CK(cudaEventRecord(ctx->ev_pfs, st));
+  CK(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_pfs, 0));
+  CK(cudaMemcpyAsync(X_dev, X_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+  CK(cudaMemcpyAsync(dY_dev, dY_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+  CK(cudaEventRecord(ctx->ev_pf, ctx->copy_in));
+  return ENC_OK;
+}
+
+int enc_prefetch_inputs(enc_ctx* ctx, const enc_dims* d, int dtype, const void* X_host,
+                        const void* dY_host, void* X_dev, void* dY_dev, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (!X_host || !dY_host) return ENC_ENULL;
+  CHECK_PTRS(X_dev, dY_dev);
+  return prefetch(ctx, (size_t)d->B * d->J * d->I * esize(dtype), X_host, dY_host, X_dev, dY_dev,
+                  (cudaStream_t)stream);
+}
+
+int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype,
+                                      const enc_cfg* cfg, const enc_params* prm, void* Y_host,
+                                      void* dX_host, const void* X_dev, const void* dY_dev,
+                                      void* Y_dev, void* dX_dev, const void* X_next_host,
+                                      const void* dY_next_host, void* X_next_dev,
+                                      void* dY_next_dev, const float* mask_bias,
+                                      const enc_grads* g, void* saved, void* scratch,
+                                      enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_dims(d, dtype);
+  if (r) return r;
+  if (!Y_host || !dX_host) return ENC_ENULL;
+  CHECK_PTRS(X_dev, dY_dev, Y_dev, dX_dev);
+  const bool next = X_next_host != nullptr || dY_next_host != nullptr;
+  if (next) {
+    if (!X_next_host || !dY_next_host) return ENC_ENULL;
+    CHECK_PTRS(X_next_dev, dY_next_dev);
+    if (X_next_dev == X_dev || dY_next_dev == dY_dev || X_next_dev == dY_dev ||
+        dY_next_dev == X_dev)
+      return ENC_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
+  // this step's inputs (previous prefetch), and earlier output copies reading our outputs
+  CK(cudaStreamWaitEvent(st, ctx->ev_pf, 0));
+  for (auto& o : ctx->orec)
+    if (o.live && (o.y == Y_dev || o.dx == Y_dev || o.y == dX_dev || o.dx == dX_dev))
+      CK(cudaStreamWaitEvent(st, o.ev, 0));
+  // the next step's inputs overlap this step's compute (their buffers' last reader, the
+  // previous step, is complete at this point of `st`)
+  if (next) {
+    r = prefetch(ctx, bytes, X_next_host, dY_next_host, X_next_dev, dY_next_dev, st);
+    if (r) return r;
+  }
+  r = encoder_layer_forward(ctx, d, dtype, cfg, prm, X_dev, mask_bias, Y_dev, saved, scratch,
+                            stream);
+  if (r) return r;
+  CK(cudaEventRecord(ctx->ev_fwd, st));
+  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_fwd, 0));
+  CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  r = encoder_layer_backward(ctx, d, dtype, cfg, prm, X_dev, saved, dY_dev, dX_dev, g, scratch,
+                             stream);
+  if (r) return r;
+  CK(cudaEventRecord(ctx->ev_bwd, st));
+  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_bwd, 0));
+  CK(cudaMemcpyAsync(dX_host, dX_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  auto& cur = ctx->orec[ctx->orec_i];
+  auto& prev = ctx->orec[ctx->orec_i ^ 1];
+  CK(cudaEventRecord(cur.ev, ctx->copy_out));
+  cur.y = Y_dev;
+  cur.dx = dX_dev;
+  cur.live = true;
+  // the previous step's host outputs are complete once `stream` passes this point
+  if (prev.live) CK(cudaStreamWaitEvent(st, prev.ev, 0));
+  ctx->orec_i ^= 1;
+  return ENC_OK;
+}
+
+int enc_outputs_wait(enc_ctx* ctx, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  for (auto& o : ctx->orec)
+    if (o.live) CK(cudaStreamWaitEvent((cudaStream_t)stream, o.ev, 0));
   return ENC_OK;
 }
 
