@@ -430,19 +430,56 @@ def main():
         Xd, dYd = [X, torch.empty_like(X)], [dY, torch.empty_like(dY)]
         Yd, dXd = [Y, torch.empty_like(Y)], [dX, torch.empty_like(dX)]
 
-        def host_loop(n):
+        def pstep(a, nxt, first=False):
+            # step of buffer parity a: next inputs into parity a^1, previous dX (a^1) out
+            b = a ^ 1
+            layer.step_host_pipelined(Xd[a], dYd[a], Yd[a], dXd[a], Yh,
+                                      Xh if nxt else None, dYh if nxt else None, Xd[b], dYd[b],
+                                      None if first else dXd[b], None if first else dXh)
+            if world > 1:
+                dp.allreduce_buckets(e2e_buckets)
+
+        def last_dx(n):   # the loop's last dX copy
+            dXh.copy_(dXd[(n - 1) & 1], non_blocking=True)
+
+        def host_loop_eager(n):
             layer.prefetch_inputs(Xh, dYh, Xd[0], dYd[0])
             for i in range(n):
-                a, b = i & 1, (i + 1) & 1
-                nxt = i + 1 < n
-                layer.step_host_pipelined(Yh, dXh, Xd[a], dYd[a], Yd[a], dXd[a],
-                                          Xh if nxt else None, dYh if nxt else None,
-                                          Xd[b], dYd[b])
-                if world > 1:
-                    dp.allreduce_buckets(e2e_buckets)
-            layer.outputs_wait()
-        host_loop(3)
+                pstep(i & 1, i + 1 < n, first=(i == 0))
+            last_dx(n)
+        host_loop_eager(4)
         torch.cuda.synchronize()
+        g_pair = None
+        if not args.eager and world == 1:
+            # a pair of steps (parities 0, 1; each copying the next inputs in and the
+            # previous dX out) captured as one graph; every call joins its copies, so the
+            # replays chain in stream order
+            g_pair = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g_pair):
+                pstep(0, True)
+                pstep(1, True)
+            g_pair.replay()
+            torch.cuda.synchronize()
+
+        def host_loop(n):
+            if g_pair is None:
+                host_loop_eager(n)
+                return
+            # first steps eager (no previous dX; the pair graph starts at parity 0), pairs
+            # of steps that both copy next inputs from the graph, the last steps eager
+            layer.prefetch_inputs(Xh, dYh, Xd[0], dYd[0])
+            pstep(0, n > 1, first=True)
+            i = 1
+            if i < n - 1:
+                pstep(1, True)
+                i = 2
+            while i + 2 < n:
+                g_pair.replay()
+                i += 2
+            while i < n:
+                pstep(i & 1, i + 1 < n)
+                i += 1
+            last_dx(n)
     else:
         for _ in range(2):
             host_step()
@@ -472,9 +509,10 @@ def main():
     barrier()
     e2e_ms = dp.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps
     if pipelined:
-        how = ("encoder_layer_step_host_pipelined, eager loop of the timed steps (H2D X, dY "
-               "of step s+1 from pinned host memory prefetched during step s; D2H Y, dX on "
-               "the copy-out stream; the loop's first prefetch and last copies included)")
+        how = ("encoder_layer_step_host_pipelined (H2D X, dY of step s+1 from pinned host "
+               "memory during step s; D2H Y of step s and dX of step s-1 on the copy-out "
+               "stream; the loop's first input copy and last dX copy included), "
+               + ("pairs of steps replayed as a CUDA graph" if g_pair is not None else "eager"))
     else:
         how = (e2e_api + "H2D X, dY from pinned host memory; D2H Y, dX) "
                + ("replayed as a CUDA graph" if g_e2e is not None else "eager"))

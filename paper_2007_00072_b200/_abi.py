@@ -86,10 +86,9 @@ _SIGS = {
                                                   POINTER(enc_cfg), POINTER(enc_params),
                                                   c_void_p, c_void_p, c_void_p, c_void_p,
                                                   c_void_p, c_void_p, c_void_p, c_void_p,
-                                                  c_void_p, c_void_p, c_void_p,
+                                                  c_void_p, c_void_p, c_void_p, c_void_p,
                                                   POINTER(enc_grads), c_void_p, c_void_p,
                                                   c_void_p]),
-    "enc_outputs_wait": (c_int, [c_void_p, c_void_p]),
     "enc_dropout_mask": (c_int, [c_int64, c_int64, c_float, c_uint64, c_uint64, c_void_p,
                                  c_void_p]),
     "enc_aib_fwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p, c_void_p,

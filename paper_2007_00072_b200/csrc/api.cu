@@ -47,17 +47,9 @@ struct enc_ctx {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* side_ws = nullptr;
-  // pipelined host steps: input prefetch done (ev_pf, recorded on copy_in), prefetch
-  // start / backward done markers on the layer stream, and the last two steps' output
-  // copies (device buffers read, completion event on copy_out)
+  // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
+  // stream (ev_pfs)
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
-  struct OutRec {
-    const void* y = nullptr;
-    const void* dx = nullptr;
-    cudaEvent_t ev = nullptr;
-    bool live = false;
-  } orec[2];
-  int orec_i = 0;
 };
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
@@ -194,10 +186,9 @@ int enc_create(enc_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  cudaEvent_t* evs[11] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
-                          &c->ev_fork, &c->ev_join, &c->ev_pf, &c->ev_pfs,
-                          &c->ev_bwd,  &c->orec[0].ev, &c->orec[1].ev};
-  for (int i = 0; i < 11 && e == cudaSuccess; ++i)
+  cudaEvent_t* evs[9] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start, &c->ev_fork,
+                         &c->ev_join, &c->ev_pf,  &c->ev_pfs, &c->ev_bwd};
+  for (int i = 0; i < 9 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -238,7 +229,7 @@ void enc_destroy(enc_ctx* c) {
   }
   if (c->lt) lt_destroy(c->lt);
   for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join,
-                         c->ev_pf, c->ev_pfs, c->ev_bwd, c->orec[0].ev, c->orec[1].ev})
+                         c->ev_pf, c->ev_pfs, c->ev_bwd})
     if (ev) cudaEventDestroy(ev);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side_ws) cudaFree(c->side_ws);
@@ -1184,7 +1175,7 @@ int encoder_layer_step_host(enc_ctx* ctx, const enc_dims* d, int dtype, const en
   return ENC_OK;
 }
 
-// input prefetch on copy_in, behind the work already on `st`
+// input copies on copy_in, behind the work already on `st`, joined into `st`
 static int prefetch(enc_ctx* ctx, size_t bytes, const void* X_host, const void* dY_host,
                     void* X_dev, void* dY_dev, cudaStream_t st) {
   CK(cudaEventRecord(ctx->ev_pfs, st));
@@ -1192,6 +1183,7 @@ static int prefetch(enc_ctx* ctx, size_t bytes, const void* X_host, const void* 
   CK(cudaMemcpyAsync(X_dev, X_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
   CK(cudaMemcpyAsync(dY_dev, dY_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
   CK(cudaEventRecord(ctx->ev_pf, ctx->copy_in));
+  CK(cudaStreamWaitEvent(st, ctx->ev_pf, 0));
   return ENC_OK;
 }
 
@@ -1207,17 +1199,18 @@ int enc_prefetch_inputs(enc_ctx* ctx, const enc_dims* d, int dtype, const void* 
 }
 
 int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype,
-                                      const enc_cfg* cfg, const enc_params* prm, void* Y_host,
-                                      void* dX_host, const void* X_dev, const void* dY_dev,
-                                      void* Y_dev, void* dX_dev, const void* X_next_host,
+                                      const enc_cfg* cfg, const enc_params* prm,
+                                      const void* X_dev, const void* dY_dev, void* Y_dev,
+                                      void* dX_dev, void* Y_host, const void* X_next_host,
                                       const void* dY_next_host, void* X_next_dev,
-                                      void* dY_next_dev, const float* mask_bias,
+                                      void* dY_next_dev, const void* dX_prev_dev,
+                                      void* dX_prev_host, const float* mask_bias,
                                       const enc_grads* g, void* saved, void* scratch,
                                       enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
   int r = check_dims(d, dtype);
   if (r) return r;
-  if (!Y_host || !dX_host) return ENC_ENULL;
+  if (!Y_host) return ENC_ENULL;
   CHECK_PTRS(X_dev, dY_dev, Y_dev, dX_dev);
   const bool next = X_next_host != nullptr || dY_next_host != nullptr;
   if (next) {
@@ -1227,18 +1220,27 @@ int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype
         dY_next_dev == X_dev)
       return ENC_EINVAL;
   }
+  const bool prev = dX_prev_dev != nullptr || dX_prev_host != nullptr;
+  if (prev) {
+    if (!dX_prev_host) return ENC_ENULL;
+    CHECK_PTRS(dX_prev_dev);
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
-  // this step's inputs (previous prefetch), and earlier output copies reading our outputs
-  CK(cudaStreamWaitEvent(st, ctx->ev_pf, 0));
-  for (auto& o : ctx->orec)
-    if (o.live && (o.y == Y_dev || o.dx == Y_dev || o.y == dX_dev || o.dx == dX_dev))
-      CK(cudaStreamWaitEvent(st, o.ev, 0));
-  // the next step's inputs overlap this step's compute (their buffers' last reader, the
-  // previous step, is complete at this point of `st`)
+  // fork both copy streams here: the next step's inputs in (their buffers' last reader,
+  // the previous step, is complete at this point of `st`), the previous step's dX out
+  CK(cudaEventRecord(ctx->ev_pfs, st));
   if (next) {
-    r = prefetch(ctx, bytes, X_next_host, dY_next_host, X_next_dev, dY_next_dev, st);
-    if (r) return r;
+    CK(cudaStreamWaitEvent(ctx->copy_in, ctx->ev_pfs, 0));
+    CK(cudaMemcpyAsync(X_next_dev, X_next_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+    CK(cudaMemcpyAsync(dY_next_dev, dY_next_host, bytes, cudaMemcpyHostToDevice, ctx->copy_in));
+    CK(cudaEventRecord(ctx->ev_pf, ctx->copy_in));
+  }
+  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_pfs, 0));
+  const bool dx_alias = prev && dX_prev_dev == dX_dev;
+  if (prev) {
+    CK(cudaMemcpyAsync(dX_prev_host, dX_prev_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+    if (dx_alias) CK(cudaEventRecord(ctx->ev_out, ctx->copy_out));
   }
   r = encoder_layer_forward(ctx, d, dtype, cfg, prm, X_dev, mask_bias, Y_dev, saved, scratch,
                             stream);
@@ -1246,28 +1248,15 @@ int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype
   CK(cudaEventRecord(ctx->ev_fwd, st));
   CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_fwd, 0));
   CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  // the previous step's dX in the same buffer: its copy finishes before the backward writes
+  if (dx_alias) CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
   r = encoder_layer_backward(ctx, d, dtype, cfg, prm, X_dev, saved, dY_dev, dX_dev, g, scratch,
                              stream);
   if (r) return r;
-  CK(cudaEventRecord(ctx->ev_bwd, st));
-  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_bwd, 0));
-  CK(cudaMemcpyAsync(dX_host, dX_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
-  auto& cur = ctx->orec[ctx->orec_i];
-  auto& prev = ctx->orec[ctx->orec_i ^ 1];
-  CK(cudaEventRecord(cur.ev, ctx->copy_out));
-  cur.y = Y_dev;
-  cur.dx = dX_dev;
-  cur.live = true;
-  // the previous step's host outputs are complete once `stream` passes this point
-  if (prev.live) CK(cudaStreamWaitEvent(st, prev.ev, 0));
-  ctx->orec_i ^= 1;
-  return ENC_OK;
-}
-
-int enc_outputs_wait(enc_ctx* ctx, enc_stream_t stream) {
-  if (!ctx) return ENC_ENULL;
-  for (auto& o : ctx->orec)
-    if (o.live) CK(cudaStreamWaitEvent((cudaStream_t)stream, o.ev, 0));
+  // join: every copy this call issued is complete when `stream` passes its end
+  CK(cudaEventRecord(ctx->ev_out, ctx->copy_out));
+  CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+  if (next) CK(cudaStreamWaitEvent(st, ctx->ev_pf, 0));
   return ENC_OK;
 }
 

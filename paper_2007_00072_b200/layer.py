@@ -168,28 +168,23 @@ class EncoderLayer:
             self.ctx.ptr, ctypes.byref(self.dims), self.adt, X_host.data_ptr(),
             dY_host.data_ptr(), X_dev.data_ptr(), dY_dev.data_ptr(), self._stream(stream)))
 
-    def step_host_pipelined(self, Y_host, dX_host, X_dev, dY_dev, Y_dev, dX_dev,
-                            X_next_host=None, dY_next_host=None, X_next_dev=None,
-                            dY_next_dev=None, mask_bias=None, stream=None):
-        """encoder_layer_step_host_pipelined: one step on prefetched inputs; prefetches the
-        next step's inputs (None on the last step); outputs copied back on the copy-out
-        stream (complete after the next step, or after outputs_wait())."""
+    def step_host_pipelined(self, X_dev, dY_dev, Y_dev, dX_dev, Y_host, X_next_host=None,
+                            dY_next_host=None, X_next_dev=None, dY_next_dev=None,
+                            dX_prev_dev=None, dX_prev_host=None, mask_bias=None, stream=None):
+        """encoder_layer_step_host_pipelined: one step on device-resident inputs; copies the
+        next step's inputs in and the previous step's dX out while it runs (None to skip);
+        Y copied back to Y_host.  Self-contained: all copies joined at the end."""
         cfg = self.cfg.to_c()
-        nx = None if X_next_host is None else X_next_host.data_ptr()
-        ndy = None if dY_next_host is None else dY_next_host.data_ptr()
-        nxd = None if X_next_dev is None else X_next_dev.data_ptr()
-        ndyd = None if dY_next_dev is None else dY_next_dev.data_ptr()
+
+        def ptr(t):
+            return None if t is None else t.data_ptr()
         check("encoder_layer_step_host_pipelined", self.lib.encoder_layer_step_host_pipelined(
             self.ctx.ptr, ctypes.byref(self.dims), self.adt, ctypes.byref(cfg),
-            ctypes.byref(self.c_params), Y_host.data_ptr(), dX_host.data_ptr(),
-            X_dev.data_ptr(), dY_dev.data_ptr(), Y_dev.data_ptr(), dX_dev.data_ptr(), nx, ndy,
-            nxd, ndyd, None if mask_bias is None else mask_bias.data_ptr(),
-            ctypes.byref(self.c_grads), self.saved.data_ptr(), self.scratch.data_ptr(),
-            self._stream(stream)))
-
-    def outputs_wait(self, stream=None):
-        """enc_outputs_wait: `stream` waits for every output copy issued so far."""
-        check("enc_outputs_wait", self.lib.enc_outputs_wait(self.ctx.ptr, self._stream(stream)))
+            ctypes.byref(self.c_params), X_dev.data_ptr(), dY_dev.data_ptr(), Y_dev.data_ptr(),
+            dX_dev.data_ptr(), Y_host.data_ptr(), ptr(X_next_host), ptr(dY_next_host),
+            ptr(X_next_dev), ptr(dY_next_dev), ptr(dX_prev_dev), ptr(dX_prev_host),
+            ptr(mask_bias), ctypes.byref(self.c_grads), self.saved.data_ptr(),
+            self.scratch.data_ptr(), self._stream(stream)))
 
     # ------------------------------------------------------------------ inspection
     def _pop_view(self, buf: torch.Tensor, ptr: int, ld: int) -> torch.Tensor:

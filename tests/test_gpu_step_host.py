@@ -86,10 +86,11 @@ def test_step_host_pipelined_matches_device_path(dims, dtype):
     for s in range(steps):
         a, b = s & 1, (s + 1) & 1
         nxt = s + 1 < steps
-        layer.step_host_pipelined(Yh[s], dXh[s], Xd[a], dYd[a], Yd[a], dXd[a],
+        layer.step_host_pipelined(Xd[a], dYd[a], Yd[a], dXd[a], Yh[s],
                                   Xh[s + 1] if nxt else None, dYh[s + 1] if nxt else None,
-                                  Xd[b], dYd[b])
-    layer.outputs_wait()
+                                  Xd[b], dYd[b],
+                                  dXd[b] if s else None, dXh[s - 1] if s else None)
+    dXh[steps - 1].copy_(dXd[(steps - 1) & 1], non_blocking=True)
     torch.cuda.synchronize()
     for s in range(steps):
         assert torch.equal(Yh[s], refs[s][0]), s
@@ -106,4 +107,4 @@ def test_step_host_pipelined_rejects_aliased_prefetch():
     X = torch.zeros((dims.B, dims.J, dims.I), device="cuda")
     h = X.cpu().pin_memory()
     with pytest.raises(EncError):
-        layer.step_host_pipelined(h, h, X, X.clone(), X.clone(), X.clone(), h, h, X, X.clone())
+        layer.step_host_pipelined(X, X.clone(), X.clone(), X.clone(), h, h, h, X, X.clone())
