@@ -25,6 +25,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "BERT-large encoder layer fwd+bwd tokens/s"
 METRIC_STACK = "BERT-large encoder stack fwd+bwd tokens/s"   # --layers N > 1
+METRIC_TRAIN = "BERT-large encoder stack training step (fwd+bwd+AdamW) tokens/s"  # + --optimizer
 UNIT = "tokens/s"
 WORKLOADS = {
     "L": "L: BERT-large encoder layer B=8/GPU J=K=512 H=16 P=64 I=1024 U=4096 p=0.1 GELU",
@@ -46,6 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=6)  # ~13 s of oracle work
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--optimizer", action="store_true",
+                    help="with --layers: AdamW update of every layer inside the step (the "
+                         "full training step of BASELINE config 4)")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="e2e through encoder_layer_step_host (no cross-step input prefetch)")
     ap.add_argument("--bwd-side", action="store_true",
@@ -271,7 +275,13 @@ def main():
     else:
         parts = [(lambda: (stack.forward(X), stack.backward(dY)), [])]
 
-    def run_parts(fns):
+    # a training step of the stack: AdamW on every layer once its gradients are reduced
+    post = []
+    if stack is not None and args.optimizer:
+        stack.init_optimizer()
+        post = [stack.optimizer_step]
+
+    def run_parts(fns, post_fns):
         works = []
         for fn, (_f, buckets) in zip(fns, parts):
             fn()
@@ -279,9 +289,11 @@ def main():
                 works += dp.allreduce_buckets(buckets, async_op=True)
         for w in works:
             w.wait()
+        for fn in post_fns:
+            fn()
 
     def step():
-        run_parts([f for f, _b in parts])
+        run_parts([f for f, _b in parts], post)
 
     def barrier():
         if world > 1:
@@ -324,19 +336,19 @@ def main():
         side = torch.cuda.Stream(dev)
         side.wait_stream(torch.cuda.current_stream(dev))
         with torch.cuda.stream(side):
-            for fn, _b in parts:
+            for fn in [f for f, _b in parts] + post:
                 fn()
         torch.cuda.current_stream(dev).wait_stream(side)
-        graphs = []
-        for fn, _b in parts:
+        graphs, post_graphs = [], []
+        for fn, dst in [(f, graphs) for f, _b in parts] + [(f, post_graphs) for f in post]:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
-            graphs.append(g)
+            dst.append(g)
         torch.cuda.synchronize()
 
         def step():  # noqa: F811
-            run_parts([g.replay for g in graphs])
+            run_parts([g.replay for g in graphs], [g.replay for g in post_graphs])
         for _ in range(2):
             step()
         torch.cuda.synchronize()
@@ -541,7 +553,8 @@ def main():
                    "sample": f"{len(ts)} x one sequence (B=1 slice of config {args.config}) "
                              f"fwd+bwd, fp64 numpy oracle, {sum(ts):.1f} s"}
         line = {
-            "metric": METRIC if stack is None else METRIC_STACK, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC if stack is None else (METRIC_TRAIN if post else METRIC_STACK),
+            "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
@@ -549,6 +562,8 @@ def main():
                        else f"Lx{args.layers}: {args.layers}-layer encoder stack of "
                             + WORKLOADS[args.config],
                        "layers": args.layers, "global_batch": dims_global.B,
+                       "optimizer": "AdamW (fp32 master, moments; one launch per layer)"
+                       if post else None,
                        "seq_len": dims.J,
                        "parallelism": f"dp{world}",
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush

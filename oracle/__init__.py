@@ -12,6 +12,7 @@ Contents
   encoder.py  per-operator functions (AIB, BSB, BDRLN, BAD, their backwards, BEI) and the
               whole layer forward / backward, in the order of Table A.1
               (PAPER.md:549-596).
+  optim.py    AdamW update of the stack's training step (outside the paper's method).
 
 Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
   * Philox: Random123 known-answer vectors (tests/golden/philox_kat.txt).
@@ -26,5 +27,6 @@ Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
     injected at torch's own four dropout sites (pins the dropout placement).
   * whole layer backward: central finite differences on the tiny config.
   * aib_fwd/aib_bwd are mutual inverses of the layout permutation.
+  * AdamW: torch.optim.AdamW (fp64) over five steps; the first step's closed form.
 Every function here is pinned; there is no "parity unpinned" function in this round.
 """

@@ -7,7 +7,7 @@ from __future__ import annotations
 
 import ctypes
 import os
-from ctypes import (POINTER, c_char_p, c_float, c_int, c_int64, c_size_t, c_uint32, c_uint64,
+from ctypes import (POINTER, c_char_p, c_double, c_float, c_int, c_int64, c_size_t, c_uint32, c_uint64,
                     c_void_p)
 
 LIB_PATH = os.environ.get("ENC_LIB_PATH") or os.path.join(
@@ -46,6 +46,10 @@ class enc_saved_view(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in SAVED_FIELDS] + [("qkv_ld", c_int64)]
 
 
+class enc_opt_segment(ctypes.Structure):
+    _fields_ = [("begin", c_int64), ("n", c_int64), ("out", c_void_p), ("dtype", c_int)]
+
+
 BWD_FIELDS = ("dY2", "dA1", "dh", "dX1", "dYo", "dC", "dA", "dS", "dQ", "dK", "dV", "dQKV")
 
 
@@ -80,6 +84,9 @@ _SIGS = {
                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                         c_void_p, POINTER(enc_grads), c_void_p, c_void_p,
                                         c_void_p]),
+    "enc_adamw_step": (c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                               POINTER(enc_opt_segment), c_int, c_double, c_double, c_double,
+                               c_double, c_double, c_int, c_double, c_void_p]),
     "enc_prefetch_inputs": (c_int, [c_void_p, POINTER(enc_dims), c_int, c_void_p, c_void_p,
                                     c_void_p, c_void_p, c_void_p]),
     "encoder_layer_step_host_pipelined": (c_int, [c_void_p, POINTER(enc_dims), c_int,

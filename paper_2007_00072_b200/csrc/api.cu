@@ -1187,6 +1187,36 @@ static int prefetch(enc_ctx* ctx, size_t bytes, const void* X_host, const void* 
   return ENC_OK;
 }
 
+int enc_adamw_step(enc_ctx* ctx, int64_t n, float* master, float* m, float* v, const float* grad,
+                   const enc_opt_segment* segs, int nseg, double lr, double beta1,
+                   double beta2, double eps, double weight_decay, int step, double grad_scale,
+                   enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (n < 0 || step < 1 || nseg < 1 || nseg > ENC_OPT_MAX_SEGMENTS || !(beta1 >= 0.0) ||
+      !(beta1 < 1.0) || !(beta2 >= 0.0) || !(beta2 < 1.0))
+    return ENC_EINVAL;
+  if (n % 4) return ENC_EALIGN;
+  if (!segs) return ENC_ENULL;
+  CHECK_PTRS(master, m, v, grad);
+  OptSeg s[kOptMaxSegs];
+  int64_t at = 0;
+  for (int k = 0; k < nseg; ++k) {
+    const enc_opt_segment& e = segs[k];
+    if (e.begin != at || e.n < 0) return ENC_EINVAL;
+    if (e.begin % 4 || e.n % 4) return ENC_EALIGN;
+    if (e.dtype != ENC_BF16 && e.dtype != ENC_FP32) return ENC_EDTYPE;
+    if (e.n > 0) CHECK_PTRS(e.out);
+    if (e.n > 0 && ((uintptr_t)e.out % (e.dtype == ENC_BF16 ? 8 : 16))) return ENC_EALIGN;
+    s[k] = OptSeg{e.begin, e.n, e.out, e.dtype};
+    at += e.n;
+  }
+  if (at != n) return ENC_EINVAL;
+  ctx->launches += n > 0;
+  CK(launch_adamw(n, master, m, v, grad, s, nseg, lr, beta1, beta2, eps, weight_decay, step,
+                  grad_scale, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
 int enc_prefetch_inputs(enc_ctx* ctx, const enc_dims* d, int dtype, const void* X_host,
                         const void* dY_host, void* X_dev, void* dY_dev, enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;

@@ -6,6 +6,21 @@
 
 #include "common.cuh"
 
+namespace enc {
+// AdamW model-copy segment: flat elements [begin, begin + n) are also written to `out`
+// (dtype 0 = bf16, 1 = fp32); begin and n multiples of 4 (mirrors enc_opt_segment)
+struct OptSeg {
+  int64_t begin;
+  int64_t n;
+  void* out;
+  int dtype;
+};
+constexpr int kOptMaxSegs = 32;
+cudaError_t launch_adamw(int64_t n, float* master, float* m1, float* m2, const float* g,
+                         const OptSeg* segs, int nseg, double lr, double b1, double b2,
+                         double eps, double wd, int step, double gscale, cudaStream_t st);
+}  // namespace enc
+
 // Chunks-per-lane dispatch for the warp-per-row operators: a row of n elements has
 // nc = n/8 chunks, lane l owns chunks l, l+32, ...; CPL = ceil(nc/32) rounded up to a
 // compiled variant (rows up to 4096 elements).

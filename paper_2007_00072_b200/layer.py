@@ -186,6 +186,34 @@ class EncoderLayer:
             ptr(mask_bias), ctypes.byref(self.c_grads), self.saved.data_ptr(),
             self.scratch.data_ptr(), self._stream(stream)))
 
+    # ------------------------------------------------------------------ optimizer
+    def init_optimizer(self):
+        """AdamW state: fp32 master parameters in the gradient buffer's flat order (copied
+        from the current parameters), first and second moments zeroed."""
+        order = FFN_BUCKET + ATTN_BUCKET
+        self.master = torch.cat([self.params[n].float().reshape(-1) for n in order])
+        self.adam_m = torch.zeros_like(self.master)
+        self.adam_v = torch.zeros_like(self.master)
+        self.adam_t = 0
+        segs, off = [], 0
+        for n in order:
+            t = self.params[n]
+            dt = _abi.ENC_BF16 if t.dtype == torch.bfloat16 else _abi.ENC_FP32
+            segs.append(_abi.enc_opt_segment(off, t.numel(), t.data_ptr(), dt))
+            off += t.numel()
+        self.c_segs = (_abi.enc_opt_segment * len(segs))(*segs)
+
+    def optimizer_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-6, weight_decay=0.01,
+                       grad_scale=1.0, stream=None):
+        """enc_adamw_step on this layer's gradients (one launch): updates the master
+        parameters and moments and rewrites the parameters the layer reads."""
+        self.adam_t += 1
+        check("enc_adamw_step", self.lib.enc_adamw_step(
+            self.ctx.ptr, self.master.numel(), self.master.data_ptr(), self.adam_m.data_ptr(),
+            self.adam_v.data_ptr(), self.grad_flat.data_ptr(), self.c_segs, len(self.c_segs),
+            lr, betas[0], betas[1], eps, weight_decay, self.adam_t, grad_scale,
+            self._stream(stream)))
+
     # ------------------------------------------------------------------ inspection
     def _pop_view(self, buf: torch.Tensor, ptr: int, ld: int) -> torch.Tensor:
         """[B,H,J,P] view of a P-wide attention operand with row stride `ld` (elements):

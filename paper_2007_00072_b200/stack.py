@@ -59,6 +59,26 @@ class EncoderStack:
             g = out
         return g
 
+    def init_optimizer(self):
+        """AdamW state (fp32 master parameters, moments) for every layer."""
+        for layer in self.layers:
+            layer.init_optimizer()
+
+    def optimizer_step(self, lr=1e-4, betas=(0.9, 0.999), eps=1e-6, weight_decay=0.01,
+                       stream=None):
+        """enc_adamw_step for every layer (one launch each)."""
+        for layer in self.layers:
+            layer.optimizer_step(lr, betas, eps, weight_decay, stream=stream)
+
+    def train_step(self, X, dY, lr=1e-4, reduce=None, mask_bias=None):
+        """One training step: forward, backward, AdamW.  reduce(layer), if given, is called
+        once a layer's gradients are final (e.g. the data-parallel all-reduce); the
+        parameters are updated after every layer's backward (and reduction)."""
+        self.forward(X, mask_bias)
+        done = None if reduce is None else (lambda i, layer: reduce(layer))
+        self.backward(dY, on_layer_done=done)
+        self.optimizer_step(lr)
+
     def step_host(self, X_host, dY_host, Y_host, dX_host, mask_bias=None, stream=None):
         """One training step from host memory: H2D X and dY (pinned host tensors), forward
         and backward through every layer, D2H the output Y and the input gradient dX."""
