@@ -215,30 +215,6 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   if (leader && blockIdx.x < prm.tiles) load_operands(blockIdx.x);
   if (kBwd && lane == 0 && blockIdx.x < prm.tiles) load_psub(blockIdx.x);
 
-  // Forward: the keep flags of the NEXT tile are generated inside pass 1 of this tile, so
-  // the fma-pipe Philox work (IMAD.WIDE) interleaves with pass 1's MUFU / TMEM work instead
-  // of running alone at the head of every tile; the first tile's flags are made up front.
-  auto grow_of = [&](int t) -> int64_t {
-    int b, h, m0, bh;
-    tile_coords(t, b, h, m0, bh);
-    return prm.g0 + ((int64_t)bh * prm.J + m0 + r) * (kK / 8) + cb / 8;
-  };
-  // flags of Philox chunks 4c + j0 and 4c + j0 + 1 (two calls in flight)
-  auto flags_pair = [&](int64_t grow, int pi) -> uint32_t {
-    const int c = pi >> 1, j0 = 2 * (pi & 1);
-    return keep_flags((uint64_t)(grow + 4 * c + j0), pk, C2, X, 4 * j0) |
-           keep_flags((uint64_t)(grow + 4 * c + j0 + 1), pk, C2, X, 4 * j0 + 4);
-  };
-  uint32_t kfn[kW / 32] = {0xFFFFFFFFu, 0xFFFFFFFFu};
-  if (!kBwd && pk.T != 0 && blockIdx.x < prm.tiles) {
-    const int64_t grow = grow_of(blockIdx.x);
-#pragma unroll 1
-    for (int pi = 0; pi < 4; ++pi) {
-      const uint32_t f = flags_pair(grow, pi);
-      kfn[pi >> 1] = (pi & 1) ? (kfn[pi >> 1] | f) : f;
-    }
-  }
-
   int it = 0;
   for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
     int b, h, m0, bh;
@@ -270,9 +246,8 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(kbw));
       kf[0] = w2.x;
       kf[1] = w2.y;
-    } else if (!kBwd || pk.T == 0) {   // fwd: made during the previous tile (all ones at p = 0)
-      kf[0] = kfn[0];
-      kf[1] = kfn[1];
+    } else if (pk.T == 0) {   // p = 0: everything kept, no Philox stream
+      kf[0] = kf[1] = 0xFFFFFFFFu;
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     } else {
       const int64_t grow = prm.g0 + rowi * (kK / 8) + cb / 8;
@@ -303,9 +278,6 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       constexpr int kNs = kW / kSub;
       const float c = prm.c;
       float mc[kNs], lc[kNs];
-      const int tn = t + (int)gridDim.x;
-      const bool gen_next = pk.T != 0 && tn < prm.tiles;
-      const int64_t grown = gen_next ? grow_of(tn) : 0;
 #pragma unroll
       for (int ch = 0; ch < kNs; ++ch) {
         float m;
@@ -349,14 +321,6 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           tc::tmem_st32(trow + ch * kSub, v);
         }
         mc[ch] = m;
-        if (gen_next) {   // next tile's keep flags: 4 / kNs Philox pairs per sub-chunk
-#pragma unroll
-          for (int pp = 0; pp < 4 / kNs; ++pp) {
-            const int pi = ch * (4 / kNs) + pp;
-            const uint32_t f = flags_pair(grown, pi);
-            kfn[pi >> 1] = (pi & 1) ? (kfn[pi >> 1] | f) : f;
-          }
-        }
       }
       float mt = mc[0];
 #pragma unroll
@@ -391,13 +355,8 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
-        // without A the staging pair holds both 32-column P chunks, so the first chunk's
-        // store is not waited for and both drain under the next tile's pass 1
-        unsigned char* stg = own + (prm.write_a ? 0 : ch * 2048);
-        if (prm.write_a || ch == 0) {
-          if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
-          __syncwarp();
-        }
+        if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
+        __syncwarp();
         tc::tmem_ld32(trow + ch * 32, v);
         if (ch + 1 == kW / 32) {   // last TMEM read of this tile by this warp
           tc::fence_before_sync();
@@ -411,7 +370,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           const float fp = fP[(ch * 32 + 8 * j) / kSub], fa = fp * ds;
 #pragma unroll
           for (int u = 0; u < 8; ++u) x[u] = v[8 * j + u] * fp;
-          *reinterpret_cast<uint4*>(stg + sw64(lane, j)) = pack8(x);
+          *reinterpret_cast<uint4*>(own + sw64(lane, j)) = pack8(x);
           if (prm.write_a) {
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -422,7 +381,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tc::tma_store_4d(&mapO1, stg, cb + ch * 32, m0 + q * 32, h, b);
+          tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
           if (prm.write_a) tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
           tc::bulk_commit();
         }
