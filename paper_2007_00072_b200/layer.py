@@ -186,6 +186,20 @@ class EncoderLayer:
             ptr(mask_bias), ctypes.byref(self.c_grads), self.saved.data_ptr(),
             self.scratch.data_ptr(), self._stream(stream)))
 
+    # ------------------------------------------------------------------ configuration
+    OPTION_KEYS = {"tc": 0, "fused": 1, "bh": 4, "direct": 5}
+
+    def apply_config(self, fname):
+        """Set the context's options from a configuration file written by the SSSP
+        configuration selection (config_select.emit_configuration; "used to
+        automatically define tensor layouts at the start of training")."""
+        from .config_select import load_configuration
+        _path, _total, knobs = load_configuration(fname)
+        for k, v in knobs.items():
+            check("enc_set_option",
+                  self.lib.enc_set_option(self.ctx.ptr, self.OPTION_KEYS[k], int(v)))
+        return knobs
+
     # ------------------------------------------------------------------ optimizer
     def init_optimizer(self):
         """AdamW state: fp32 master parameters in the gradient buffer's flat order (copied
