@@ -930,9 +930,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // The column sums of each half are finished by one batched finalize launch at the end of
   // the half (deferred jobs, disjoint partial regions of the reduction workspace).
   auto after = [&](const ColsumJob& j) {   // workspace past a recorded job's partials
-    const size_t used = ((size_t)j.R * j.ncols + 63) & ~(size_t)63;
-    return ReduceWs{ws.partials + used, ws.cap_floats - used, ws.num_sms};
+    float* base = const_cast<float*>(j.partials) + (((size_t)j.R * j.ncols + 63) & ~(size_t)63);
+    return ReduceWs{base, ws.cap_floats - (size_t)(base - ws.partials), ws.num_sms};
   };
+  // whole backward in one call: the FFN half's column sums are finished in the attention
+  // half's finalize launch (one launch per step; the split call finishes them early so the
+  // FFN bucket can be all-reduced while the attention half runs)
+  const bool ffn_deferred = (parts & 3) == 3;
+  ColsumJob ffn_jobs[2];
   // weight-gradient contractions go to the side stream: fork once the inputs exist, join
   // before returning (the next forward reuses the scratch they read)
   const bool use_side = ctx->bwd_side && ctx->lt && ctx->use_lt && ctx->side;
@@ -953,7 +958,6 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     return e;
   };
   if (parts & 1) {
-  ColsumJob ffn_jobs[2];
   // BDRLN-bwd site 2 (:570-572, bias2 dW :575): dz2 -> dX1 (residual path), dY2
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_BWD2, st, 1);
@@ -975,12 +979,12 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   }
   // BAD-bwd (:576-578), then the FFN half's column sums (dg2, dbe2, db2, db1) in one launch
   {
-    OpTimer _t(ctx, ENC_OP_BAD_BWD, st, 2);
+    OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 1 : 2);
     ReduceWs w = after(ffn_jobs[0]);
     w.defer = &ffn_jobs[1];
     CK(launch_bad_bwd(dtype, B, J, U, dA1, h, prm->b1, cfg->act,
                       make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, w, st));
-    CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+    if (!ffn_deferred) CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
   }
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
   {
@@ -997,10 +1001,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   if (!(parts & 2)) return ENC_OK;
   // BDRLN-bwd site 1 (:582-585): dz1 -> dX (residual to the layer input), dYo; its column
   // sums are finished with the QKV bias gradient at the end of the half
-  ColsumJob att_jobs[2];
+  ColsumJob att_jobs[4];
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_BWD1, st, 1);
-    ReduceWs w = ws;
+    ReduceWs w = ffn_deferred ? after(ffn_jobs[1]) : ws;
     w.defer = &att_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dX1, xh1, r1, prm->g1,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, dX, dYo, g->dg1,
@@ -1113,13 +1117,19 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     // the attention half's column sums in one launch: BDRLN-bwd site 1 (dg1, dbe1, dbo)
     // and, on the per-(b,h) path, the QKV bias gradient from the B*4 epilogue partial rows
     OpTimer _t(ctx, bgrad_epi ? ENC_OP_AIB_BWD : ENC_OP_BDRLN_BWD1, st, 1);
+    int nj = 1;
     if (bgrad_epi) {
       att_jobs[1].partials = bg;
       att_jobs[1].R = B * 4;
       att_jobs[1].ncols = att_jobs[1].nper = 3 * I;
       att_jobs[1].out0 = g->dbqkv;
+      nj = 2;
     }
-    CK(launch_colsum_finalize_jobs(att_jobs, bgrad_epi ? 2 : 1, st));
+    if (ffn_deferred) {
+      att_jobs[nj++] = ffn_jobs[0];
+      att_jobs[nj++] = ffn_jobs[1];
+    }
+    CK(launch_colsum_finalize_jobs(att_jobs, nj, st));
   }
   CK(join());
   return ENC_OK;
