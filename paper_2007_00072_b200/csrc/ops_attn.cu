@@ -334,6 +334,109 @@ __global__ void __launch_bounds__(256) bsb_bwd_kernel(const T* __restrict__ dA,
   }
 }
 
+// ------------------------------------------------------------------ short rows
+// K <= 128 (NC = K/8 chunks in {2, 4, 8, 16}): a warp holds 32/NC rows, lane l owns chunk
+// l % NC of row l / NC, and the row statistics are butterfly reductions over aligned
+// NC-lane segments -- no idle lanes (the one-warp-per-row kernels above leave 32 - NC of
+// them idle: half the warp at BERT-base's J = 128).
+template <int NC>
+__device__ __forceinline__ float seg_reduce(float v, bool is_max) {
+#pragma unroll
+  for (int o = NC / 2; o >= 1; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, w) : v + w;
+  }
+  return v;
+}
+
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) bsb_fwd_short_kernel(const T* __restrict__ S,
+                                                            const float* __restrict__ M,
+                                                            T* __restrict__ Pout,
+                                                            T* __restrict__ Aout, int64_t rows,
+                                                            int K, int HJ, float c, int64_t g0,
+                                                            PhiloxKey pk) {
+  using Cv = Chunk<T>;
+  constexpr int RPW = 32 / NC;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RPW + lane / NC;
+  const int ch = lane % NC;
+  const bool valid = row < rows;   // invalid lanes still take part in the shuffles
+  float v[8];
+  if (valid) {
+    Cv::unpack(Cv::ld(S + row * K + ch * 8), v);
+    if (M) {
+      float mb[8];
+      load_f32x8(M + (int64_t)((int)row / HJ) * K + ch * 8, mb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = fmaf(v[j], c, mb[j] * kLog2e);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] *= c;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = 0.f;
+  }
+  float mx = v[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) mx = fmaxf(mx, v[j]);
+  mx = seg_reduce<NC>(mx, true);
+  float sum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    v[j] = exp2f(v[j] - mx);
+    sum += v[j];
+  }
+  sum = seg_reduce<NC>(sum, false);
+  if (!valid) return;
+  const float inv = 1.f / sum;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] *= inv;
+  Cv::store(Pout + row * K + ch * 8, v);
+  dropout8(v, (uint64_t)(g0 + row * NC + ch), pk);
+  Cv::store(Aout + row * K + ch * 8, v);
+}
+
+template <typename T, int NC>
+__global__ void __launch_bounds__(256) bsb_bwd_short_kernel(const T* __restrict__ dA,
+                                                            const T* __restrict__ Pin,
+                                                            T* __restrict__ dS, int64_t rows,
+                                                            int K, float scale, int64_t g0,
+                                                            PhiloxKey pk) {
+  using Cv = Chunk<T>;
+  constexpr int RPW = 32 / NC;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * RPW + lane / NC;
+  const int ch = lane % NC;
+  const bool valid = row < rows;
+  float dp[8], p[8];
+  float dot = 0.f;
+  if (valid) {
+    Cv::unpack(Cv::ld(dA + row * K + ch * 8), dp);
+    Cv::unpack(Cv::ld(Pin + row * K + ch * 8), p);
+    dropout8(dp, (uint64_t)(g0 + row * NC + ch), pk);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dot = fmaf(dp[j], p[j], dot);
+  }
+  dot = seg_reduce<NC>(dot, false);
+  if (!valid) return;
+  float o[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) o[j] = scale * p[j] * (dp[j] - dot);
+  Cv::store(dS + row * K + ch * 8, o);
+}
+
+#define ENC_SHORT_DISPATCH(nc, ...)                               \
+  do {                                                            \
+    if ((nc) == 2) { constexpr int NC = 2; __VA_ARGS__; }         \
+    else if ((nc) == 4) { constexpr int NC = 4; __VA_ARGS__; }    \
+    else if ((nc) == 8) { constexpr int NC = 8; __VA_ARGS__; }    \
+    else { constexpr int NC = 16; __VA_ARGS__; }                  \
+  } while (0)
+
+static bool short_rows(int nc) { return nc == 2 || nc == 4 || nc == 8 || nc == 16; }
+
 bool rowop_supported(int n) { return n > 0 && (n % 8) == 0 && n <= 32 * 8 * 16; }
 
 cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
@@ -344,6 +447,19 @@ cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, c
   const int nc = K / 8;
   const int64_t g0 = batch_offset * (int64_t)H * J * nc;
   const float c = scale * kLog2e;
+  if (short_rows(nc)) {
+    const int grid = (int)((rows + 8 * (32 / nc) - 1) / (8 * (32 / nc)));
+    ENC_SHORT_DISPATCH(nc, {
+      if (dtype == 0)
+        bsb_fwd_short_kernel<__nv_bfloat16, NC><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
+            H * J, c, g0, pk);
+      else
+        bsb_fwd_short_kernel<float, NC><<<grid, 256, 0, st>>>(
+            (const float*)S, mask_bias, (float*)P, (float*)A, rows, K, H * J, c, g0, pk);
+    });
+    return cudaGetLastError();
+  }
   if (nc > 256) {   // K > 2048: two warps per row, 8 chunks per lane
     const int grid = (int)((rows + 3) / 4);
     if (dtype == 0)
@@ -375,6 +491,19 @@ cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, c
   if (rows == 0) return cudaSuccess;
   const int nc = K / 8;
   const int64_t g0 = batch_offset * (int64_t)H * J * nc;
+  if (short_rows(nc)) {
+    const int grid = (int)((rows + 8 * (32 / nc) - 1) / (8 * (32 / nc)));
+    ENC_SHORT_DISPATCH(nc, {
+      if (dtype == 0)
+        bsb_bwd_short_kernel<__nv_bfloat16, NC><<<grid, 256, 0, st>>>(
+            (const __nv_bfloat16*)dA, (const __nv_bfloat16*)P, (__nv_bfloat16*)dS, rows, K,
+            scale, g0, pk);
+      else
+        bsb_bwd_short_kernel<float, NC><<<grid, 256, 0, st>>>(
+            (const float*)dA, (const float*)P, (float*)dS, rows, K, scale, g0, pk);
+    });
+    return cudaGetLastError();
+  }
   if (nc > 256) {   // K > 2048: two warps per row, 8 chunks per lane
     const int grid = (int)((rows + 3) / 4);
     if (dtype == 0)

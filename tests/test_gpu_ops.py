@@ -55,7 +55,9 @@ def test_dropout_mask_bit_exact(ops, n, index0, p, sub):
 BSB_SHAPES = [(2, 2, 16, 16), (3, 5, 7, 200), (2, 3, 9, 512), (1, 2, 5, 1024), (1, 1, 3, 4096),
               (1, 1, 2, 8),
               (1, 2, 7, 2056),   # K > 2048: two warps per row, the second range ragged
-              (2, 1, 5, 3000)]
+              (2, 1, 5, 3000),
+              # K <= 128: several rows per warp (segmented reductions), ragged row counts
+              (3, 2, 5, 128), (2, 3, 7, 64), (1, 3, 11, 32), (4, 12, 128, 128)]
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
