@@ -1,7 +1,8 @@
 // Row-group BDRLN kernels (forward and backward) for I % 32 == 0, I <= 2048.
 //
-// A row of I elements is shared by a group of 4 warps (each warp owns a contiguous quarter
-// of the columns, at most 2 chunks of 8 per lane), so a warp's per-row work is a quarter of
+// A row of I elements is shared by a group of GW warps (GW = 4, or 3 when a third of the
+// row is exactly one 8-element chunk per lane, I = 768; each warp owns a contiguous part of
+// the columns, at most 2 chunks of 8 per lane), so a warp's per-row work is a quarter of
 // the one-warp-per-row kernels in ops_ln.cu and four times as many rows are in flight per
 // SM.  Persistent CTAs of 4 groups (512 threads); each group streams its rows through a
 // 2- or 4-stage shared-memory ring filled by the bulk-copy (TMA) engine.  A lane always owns
@@ -21,12 +22,12 @@ namespace enc {
 namespace {
 
 constexpr int kGroups = 4;              // row groups per CTA
-constexpr int kGWarps = 4;              // warps per row group
-constexpr int kRgThreads = kGroups * kGWarps * 32;
+constexpr int kGWarps = 4;              // most warps per row group (header sizing)
 constexpr int kRgMaxStages = 4;
 
+template <int GW>
 __device__ __forceinline__ void gbar(int group) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(kGWarps * 32) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(GW * 32) : "memory");
 }
 
 // shared layout: mbar[group][stage] (128 B) | red2[group][stage][4] float4 (1 KB) |
@@ -39,8 +40,8 @@ __device__ __forceinline__ T* ring_row(unsigned char* smem, int I, int g, int s,
 }
 
 // ------------------------------------------------------------------ forward
-template <typename T, int CPW, int STG>
-__global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_kernel(
+template <typename T, int CPW, int STG, int GW>
+__global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd_rg_kernel(
     const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
@@ -48,11 +49,11 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_ker
   using C = Chunk<T>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = warp / kGWarps, w = warp % kGWarps;
-  const int nc = I >> 3, ncq = nc / kGWarps;          // chunks per row, per quarter
+  const int g = warp / GW, w = warp % GW;
+  const int nc = I >> 3, ncq = nc / GW;          // chunks per row, per quarter
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
-  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * kGWarps;
+  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * GW;
   const int stride = gridDim.x * kGroups;
   const int first = blockIdx.x * kGroups + g;
   const bool leader = (w == 0 && lane == 0);
@@ -77,7 +78,7 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_ker
     load_f32x8(gamma + ch * 8, pg[i]);
     load_f32x8(beta + ch * 8, pe[i]);
   }
-  gbar(g);
+  gbar<GW>(g);
   int k = 0;
   for (int row = first; row < rows; row += stride, ++k) {
     const int s = k % STG;
@@ -117,8 +118,8 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_ker
       }
     }
     m2 = warp_sum(m2);
-    if (lane == 0) red[s * kGWarps + w] = make_float4(qmean, m2, 0.f, 0.f);
-    gbar(g);   // quarter stats visible; every warp of the group has read this ring stage
+    if (lane == 0) red[s * GW + w] = make_float4(qmean, m2, 0.f, 0.f);
+    gbar<GW>(g);   // quarter stats visible; every warp of the group has read this ring stage
     if (leader) {
       const int nr = row + STG * stride;
       if (nr < rows) {
@@ -130,12 +131,12 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_ker
     }
     float mean = 0.f;
 #pragma unroll
-    for (int q = 0; q < kGWarps; ++q) mean += red[s * kGWarps + q].x;
-    mean *= 0.25f;
+    for (int q = 0; q < GW; ++q) mean += red[s * GW + q].x;
+    mean *= 1.f / GW;
     float M2 = 0.f;
 #pragma unroll
-    for (int q = 0; q < kGWarps; ++q) {
-      const float4 st = red[s * kGWarps + q];
+    for (int q = 0; q < GW; ++q) {
+      const float4 st = red[s * GW + q];
       const float d = st.x - mean;
       M2 += st.y + qn * d * d;
     }
@@ -161,20 +162,20 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_fwd_rg_ker
 }
 
 // ------------------------------------------------------------------ backward
-template <typename T, int CPW, int STG>
-__global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_kernel(
+template <typename T, int CPW, int STG, int GW>
+__global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd_rg_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
     float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk) {
   using C = Chunk<T>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = warp / kGWarps, w = warp % kGWarps;
-  const int nc = I >> 3, ncq = nc / kGWarps;
+  const int g = warp / GW, w = warp % GW;
+  const int nc = I >> 3, ncq = nc / GW;
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
   const float inv_n = 1.f / (float)I;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
-  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * kGWarps;
+  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * GW;
   const int stride = gridDim.x * kGroups;
   const int first = blockIdx.x * kGroups + g;
   const bool leader = (w == 0 && lane == 0);
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_ker
       }
     }
   }
-  gbar(g);
+  gbar<GW>(g);
   float acc_g[CPW][8], acc_b[CPW][8], acc_d[CPW][8];
 #pragma unroll
   for (int i = 0; i < CPW; ++i)
@@ -226,8 +227,8 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_ker
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
-    if (lane == 0) red[s * kGWarps + w] = make_float4(s1, s2, 0.f, 0.f);
-    gbar(g);
+    if (lane == 0) red[s * GW + w] = make_float4(s1, s2, 0.f, 0.f);
+    gbar<GW>(g);
     if (leader) {
       const int nr = row + STG * stride;
       if (nr < rows) {
@@ -239,8 +240,8 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_ker
     }
     float t1 = 0.f, t2 = 0.f;
 #pragma unroll
-    for (int q = 0; q < kGWarps; ++q) {
-      const float4 st = red[s * kGWarps + q];
+    for (int q = 0; q < GW; ++q) {
+      const float4 st = red[s * GW + q];
       t1 += st.x;
       t2 += st.y;
     }
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kRgThreads, CPW == 1 ? 2 : 1) bdrln_bwd_rg_ker
   }
   __syncthreads();
   float* outp = partials + (int64_t)blockIdx.x * 3 * I;
-  for (int c = threadIdx.x; c < 3 * I; c += kRgThreads) {
+  for (int c = threadIdx.x; c < 3 * I; c += (kGroups * GW * 32)) {
     float v = colsum[c];
 #pragma unroll
     for (int q = 1; q < kGroups; ++q) v += colsum[(size_t)q * 3 * I + c];
@@ -308,12 +309,12 @@ size_t rg_smem(int I, size_t es, bool bwd) {
 // persistent grid: as many CTAs as can be resident (occupancy query), at most one group
 // per row
 template <typename Kern>
-int rg_grid(Kern kern, int rows, size_t smem) {
+int rg_grid(Kern kern, int rows, size_t smem, int threads) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRgThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
   int G = (rows + kGroups - 1) / kGroups;
   if (G > per_sm * sms) G = per_sm * sms;
@@ -330,6 +331,14 @@ bool bdrln_rg_supported(int I) { return I % 32 == 0 && I <= 2048; }
     if ((ncq) <= 32) { constexpr int CPW = 1; __VA_ARGS__; }   \
     else { constexpr int CPW = 2; __VA_ARGS__; }               \
   } while (0)
+// warps per row: 3 when a third of the row is exactly one chunk per lane (I = 768: BERT-base),
+// else 4 -- no idle lanes where the row allows it
+static int rg_gw(int nc) { return (nc % 96 == 0 && nc / 3 <= 64) ? 3 : 4; }
+#define ENC_GW_DISPATCH(gw, ...)                               \
+  do {                                                         \
+    if ((gw) == 3) { constexpr int GW = 3; __VA_ARGS__; }      \
+    else { constexpr int GW = 4; __VA_ARGS__; }                \
+  } while (0)
 #define ENC_STG_DISPATCH(stg, ...)                             \
   do {                                                         \
     if ((stg) == 4) { constexpr int STG = 4; __VA_ARGS__; }    \
@@ -345,19 +354,21 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false);
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
-  ENC_CPW_DISPATCH(nc / 4, ENC_STG_DISPATCH(stg, {
+  const int gw = rg_gw(nc);
+  ENC_GW_DISPATCH(gw, ENC_CPW_DISPATCH(nc / gw, ENC_STG_DISPATCH(stg, {
+    constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
-      auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG>;
-      kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
+      auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
+      kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
           (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
           (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk);
     } else {
-      auto kern = bdrln_fwd_rg_kernel<float, CPW, STG>;
-      kern<<<rg_grid(kern, rows, smem), kRgThreads, smem, st>>>(
+      auto kern = bdrln_fwd_rg_kernel<float, CPW, STG, GW>;
+      kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
           (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat, rstd,
           rows, I, eps, g0, pk);
     }
-  }));
+  })));
   return cudaGetLastError();
 }
 
@@ -373,22 +384,24 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
   const int cap = (int)(ws.cap_floats / (size_t)(3 * I));
   int G = 1;
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
-  ENC_CPW_DISPATCH(nc / 4, ENC_STG_DISPATCH(stg, {
+  const int gw = rg_gw(nc);
+  ENC_GW_DISPATCH(gw, ENC_CPW_DISPATCH(nc / gw, ENC_STG_DISPATCH(stg, {
+    constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
-      auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW, STG>;
-      G = rg_grid(kern, rows, smem);
+      auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
+      G = rg_grid(kern, rows, smem, thr);
       if (G > cap) G = cap;
-      kern<<<G, kRgThreads, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
-                                        rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
-                                        ws.partials, rows, I, g0, pk);
+      kern<<<G, thr, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
+                                 rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
+                                 ws.partials, rows, I, g0, pk);
     } else {
-      auto kern = bdrln_bwd_rg_kernel<float, CPW, STG>;
-      G = rg_grid(kern, rows, smem);
+      auto kern = bdrln_bwd_rg_kernel<float, CPW, STG, GW>;
+      G = rg_grid(kern, rows, smem, thr);
       if (G > cap) G = cap;
-      kern<<<G, kRgThreads, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
-                                        (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
+      kern<<<G, thr, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
+                                 (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
     }
-  }));
+  })));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return colsum_finish(ws, G, 3 * I, I, dgamma, dbeta, dbias, st);

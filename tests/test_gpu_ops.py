@@ -99,7 +99,8 @@ def test_bsb_bwd(ops, ctx, dtype, shape):
 
 
 # ------------------------------------------------------------------ BDRLN
-LN_SHAPES = [(2, 16, 16), (3, 7, 1000), (2, 33, 1024), (1, 5, 768), (1, 3, 2048), (4, 5, 8)]
+LN_SHAPES = [(2, 16, 16), (3, 7, 1000), (2, 33, 1024), (1, 5, 768), (1, 3, 2048), (4, 5, 8),
+             (8, 130, 768), (2, 37, 1536)]   # three warps per row (one or two chunks per lane)
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
