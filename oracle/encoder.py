@@ -47,6 +47,7 @@ class Cfg:
     batch_offset: int = 0
     ln_eps: float = 1e-5
     act: int = ACT_GELU_ERF
+    causal: bool = False   # DESIGN.md R22: key k > query j masked out
 
 
 def _f(a):
@@ -117,15 +118,20 @@ def aib_bwd(dQ, dK, dV):
 # BSB: (bias +) scaled softmax + dropout on attention scores (paper `sm`, PAPER.md:514;
 # Table A.1 "Scaled softmax" :552).  Backward: paper `bs`.
 # ----------------------------------------------------------------------------------
-def bsb_fwd(S, mask_bias, scale, p, seed, subseq, batch_offset=0):
+def bsb_fwd(S, mask_bias, scale, p, seed, subseq, batch_offset=0, causal=False):
     """S [B,H,J,K] raw scores Q.K^T; mask_bias [B,K] additive (R1) or None.
     P = softmax_k(scale*S + M[b,k]) (row max subtracted, "multiplied
     together and scaled ... followed by a softmax"); A = P * keep * s.
+    causal: the masking step that keeps a query from "seeing the future":
+    scores of keys k > j are -inf, so P[..., j, k] = 0 there (R22).
     Returns (P, A)."""
     S = _f(S)
     x = scale * S
     if mask_bias is not None:
         x = x + _f(mask_bias)[:, None, None, :]
+    if causal:
+        J, K = S.shape[-2], S.shape[-1]
+        x = np.where(np.arange(K)[None, :] > np.arange(J)[:, None], -np.inf, x)
     x = x - x.max(axis=-1, keepdims=True)
     e = np.exp(x)
     Pm = e / e.sum(axis=-1, keepdims=True)
@@ -223,7 +229,8 @@ def encoder_layer_forward(X, prm, H, cfg: Cfg, mask_bias=None):
     QKV = _lin(X, prm["Wqkv"])                                  # Q,K,V (:549)
     Q, K, V = aib_fwd(QKV, prm["bqkv"], H, P)                   # input bias (:550)
     S = np.matmul(Q, K.transpose(0, 1, 3, 2))                   # QK^T (:551)
-    Pm, A = bsb_fwd(S, mask_bias, scale, cfg.p_attn, cfg.seed, sub(SITE_ATTN), cfg.batch_offset)
+    Pm, A = bsb_fwd(S, mask_bias, scale, cfg.p_attn, cfg.seed, sub(SITE_ATTN), cfg.batch_offset,
+                    causal=cfg.causal)
     Cbh = np.matmul(A, V)                                       # Gamma (:553), [B,H,J,P]
     C = Cbh.transpose(0, 2, 1, 3).reshape(B, J, I)              # concatenate heads
     Yo = _lin(C, prm["Wo"])                                     # Out (:554)

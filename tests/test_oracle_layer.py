@@ -96,11 +96,12 @@ def _inject_attention_dropout(layer, m_attn, p):
         sa.forward = orig_fwd
 
 
-def _run_both(dims, act, key_padding, p, seed=2007000072, batch_offset=0, eps=1e-5):
+def _run_both(dims, act, key_padding, p, seed=2007000072, batch_offset=0, eps=1e-5,
+              causal=False):
     prm = make_params(dims, "fp32", "parity", weight_std=0.2)
     inp = make_inputs(dims, "fp32", key_padding=key_padding)
     cfg = E.Cfg(p_attn=p, p_hidden=p, p_ffn=p, seed=seed, layer_id=3,
-                batch_offset=batch_offset, ln_eps=eps, act=act)
+                batch_offset=batch_offset, ln_eps=eps, act=act, causal=causal)
     Y, saved = E.encoder_layer_forward(inp["X"], prm, dims.H, cfg, inp["mask_bias"])
     dX, grads, _ = E.encoder_layer_backward(inp["dY"], inp["X"], prm, dims.H, cfg, saved)
 
@@ -117,8 +118,12 @@ def _run_both(dims, act, key_padding, p, seed=2007000072, batch_offset=0, eps=1e
         layer.dropout = _Inject(mk((B, J, U), E.SITE_FFN))
         layer.dropout2 = _Inject(mk((B, J, I), E.SITE_FFN_OUT))
         ctx = _inject_attention_dropout(layer, mk((B, H, J, J), E.SITE_ATTN).reshape(B * H, J, J), p)
+    src_mask = None
+    if causal:   # torch's own "square subsequent" mask: -inf above the diagonal
+        src_mask = torch.nn.Transformer.generate_square_subsequent_mask(
+            dims.J, dtype=torch.float64)
     with ctx:
-        Yt = layer(X, src_key_padding_mask=kpm)
+        Yt = layer(X, src_mask=src_mask, src_key_padding_mask=kpm)
     Yt.backward(torch.tensor(inp["dY"].astype(np.float64)))
     return (Y, dX, grads), (Yt.detach().numpy(), X.grad.numpy(),
                             {k: v.numpy() for k, v in _torch_grads(layer).items()})
@@ -148,6 +153,31 @@ def test_layer_dropout_placement_matches_torch_sites(act):
     _assert_close(dX, dXt)
     for k in g:
         _assert_close(g[k], gt[k])
+
+
+@pytest.mark.parametrize("key_padding", [False, True])
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_layer_causal_equals_torch(key_padding, p):
+    """Causal masking (R22) against torch's layer with its
+    square-subsequent mask, with and without key padding and dropout."""
+    dims = CONFIGS["T"]
+    (Y, dX, g), (Yt, dXt, gt) = _run_both(dims, E.ACT_GELU_ERF, key_padding, p, causal=True,
+                                          batch_offset=2)
+    _assert_close(Y, Yt)
+    _assert_close(dX, dXt)
+    for k in g:
+        _assert_close(g[k], gt[k])
+
+
+def test_causal_softmax_rows():
+    """Row j of a causal P has j+1 nonzeros summing to 1; row 0 is the one-hot e_0."""
+    rng = np.random.default_rng(5)
+    S = rng.standard_normal((2, 3, 9, 9))
+    Pm, _ = E.bsb_fwd(S, None, 0.5, 0.0, 1, 0, causal=True)
+    assert np.allclose(Pm.sum(-1), 1.0, atol=1e-12)
+    assert np.all(np.triu(Pm, 1) == 0.0)
+    assert np.allclose(Pm[..., 0, 0], 1.0)
+    assert np.all(Pm[..., np.tril(np.ones((9, 9), bool))] > 0)
 
 
 def test_degenerate_single_head():
