@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-samples", type=int, default=6)  # ~13 s of oracle work
     ap.add_argument("--breakdown", action="store_true", help="print the per-op table to stderr")
+    ap.add_argument("--causal", action="store_true",
+                    help="causal masking of the attention scores (PAPER.md:494; decoder-style "
+                         "workload on the same kernels)")
     ap.add_argument("--optimizer", action="store_true",
                     help="with --layers: AdamW update of every layer inside the step (the "
                          "full training step of BASELINE config 4)")
@@ -221,7 +224,8 @@ def main():
     es = 2 if args.dtype == "bf16" else 4
     tdt = torch.bfloat16 if args.dtype == "bf16" else torch.float32
 
-    cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff)
+    cfg = LayerCfg(p_attn=0.1, p_hidden=0.1, p_ffn=0.1, act="gelu", batch_offset=boff,
+                   causal=args.causal)
     stack = None
     if args.layers > 1:
         stack = EncoderStack(args.layers, dims, args.dtype, cfg)
@@ -562,6 +566,7 @@ def main():
                        else f"Lx{args.layers}: {args.layers}-layer encoder stack of "
                             + WORKLOADS[args.config],
                        "layers": args.layers, "global_batch": dims_global.B,
+                       "causal": bool(args.causal),
                        "optimizer": "AdamW (fp32 master, moments; one launch per layer)"
                        if post else None,
                        "seq_len": dims.J,

@@ -25,7 +25,7 @@ class enc_dims(ctypes.Structure):
 class enc_cfg(ctypes.Structure):
     _fields_ = [("p_attn", c_float), ("p_hidden", c_float), ("p_ffn", c_float),
                 ("seed", c_uint64), ("layer_id", c_uint32), ("batch_offset", c_int64),
-                ("ln_eps", c_float), ("act", c_int)]
+                ("ln_eps", c_float), ("act", c_int), ("causal", c_int)]
 
 
 PARAM_FIELDS = ("Wqkv", "Wo", "W1", "W2", "bqkv", "bo", "b1", "b2", "g1", "be1", "g2", "be2")
@@ -104,7 +104,7 @@ _SIGS = {
                             c_void_p, c_void_p, c_void_p, c_void_p]),
     "enc_bsb_fwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p,
                             c_void_p, c_float, c_uint64, c_uint64, c_int64, c_void_p, c_void_p,
-                            c_void_p]),
+                            c_int, c_void_p]),
     "enc_bsb_bwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_int, c_float, c_void_p,
                             c_void_p, c_float, c_uint64, c_uint64, c_int64, c_void_p, c_void_p]),
     "enc_bdrln_fwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
@@ -127,7 +127,7 @@ _SIGS = {
     "enc_set_option": (c_int, [c_void_p, c_int, c_int]),
     "enc_attn_fwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
-                                   c_void_p, c_void_p, c_void_p, c_void_p]),
+                                   c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "enc_attn_bwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),

@@ -295,6 +295,7 @@ static int check_cfg(const enc_cfg* c) {
   if (c->act < ENC_ACT_GELU_ERF || c->act > ENC_ACT_RELU) return ENC_EINVAL;
   if (!(c->ln_eps >= 0.f)) return ENC_EINVAL;
   if (c->batch_offset < 0) return ENC_EINVAL;
+  if (c->causal != 0 && c->causal != 1) return ENC_EINVAL;
   return ENC_OK;
 }
 
@@ -504,17 +505,17 @@ static int check_bhjk(int dtype, int B, int H, int J, int K, float p) {
 
 int enc_bsb_fwd(enc_ctx* ctx, int dtype, int B, int H, int J, int K, float scale, const void* S,
                 const float* mask_bias, float p, uint64_t seed, uint64_t subseq,
-                int64_t batch_offset, void* P, void* A, enc_stream_t stream) {
+                int64_t batch_offset, void* P, void* A, int causal, enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
   int r = check_bhjk(dtype, B, H, J, K, p);
   if (r) return r;
-  if (batch_offset < 0) return ENC_EINVAL;
+  if (batch_offset < 0 || (causal && J != K)) return ENC_EINVAL;
   CHECK_PTRS(S, P, A);
   if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
   {
     OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
     CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias, make_philox_key(p, seed, subseq),
-                      batch_offset, P, A, (cudaStream_t)stream));
+                      batch_offset, P, A, (cudaStream_t)stream, causal ? 1 : 0));
   }
   return ENC_OK;
 }
@@ -635,7 +636,7 @@ int enc_attn_gemm(enc_ctx* ctx, int which, int B, int H, int J, int P, const voi
 int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
                        const void* Kt, const float* mask_bias, float p, uint64_t seed,
                        uint64_t subseq, int64_t batch_offset, void* Pout, void* A,
-                       uint32_t* keep_bits, enc_stream_t stream) {
+                       uint32_t* keep_bits, int causal, enc_stream_t stream) {
   if (!ctx) return ENC_ENULL;
   if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
   if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
@@ -646,7 +647,7 @@ int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
   CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, P, Kt, P, mask_bias,
                         make_philox_key(p, seed, subseq), batch_offset, Pout, A, keep_bits,
-                        (cudaStream_t)stream));
+                        (cudaStream_t)stream, causal ? 1 : 0));
   return ENC_OK;
 }
 
@@ -796,7 +797,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
     CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias, pk_attn, boff, Pm,
-                          drop_on_load ? nullptr : A, kbits, st));
+                          drop_on_load ? nullptr : A, kbits, st, cfg->causal ? 1 : 0));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {
@@ -811,7 +812,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     {
       OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
       CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias,
-                        make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st));
+                        make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, Pm, A, st,
+                        cfg->causal ? 1 : 0));
     }
   }
   // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]

@@ -141,7 +141,7 @@ constexpr size_t kSmem = 1024 + kBars + (4 + kWarps) * 8 + 16;
 static_assert(kSmem <= 227 * 1024, "smem");
 static_assert(kW == 64, "two keep-flag words per thread");
 
-template <bool kBwd, bool kMask, bool kBits>
+template <bool kBwd, bool kMask, bool kBits, bool kCausal = false>
 __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtensorMap& mapB,
                                            const CUtensorMap& mapP, const CUtensorMap& mapO1,
                                            const CUtensorMap& mapO2, const FusedParams& prm,
@@ -293,6 +293,11 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
             v[4 * i + 2] = fmaf(v[4 * i + 2], c, mm.z * kL2e);
             v[4 * i + 3] = fmaf(v[4 * i + 3], c, mm.w * kL2e);
           }
+          if (kCausal) {   // keys after the query row are masked out
+#pragma unroll
+            for (int i = 0; i < kSub; ++i)
+              if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
+          }
           m = v[0];
 #pragma unroll
           for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
@@ -307,14 +312,21 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           tc::tmem_st16(trow + ch * kSub, v);
         } else {
           tc::tmem_ld32(trow + ch * kSub, v);
+          if (kCausal) {   // keys after the query row are masked out
+#pragma unroll
+            for (int i = 0; i < kSub; ++i)
+              if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
+          }
           m = v[0];
 #pragma unroll
           for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
           m *= c;   // c > 0
+          // a fully masked chunk (causal) has m = -inf: exponentiate against 0 instead
+          const float mz = (kCausal && m == -INFINITY) ? 0.f : m;
           float l = 0.f;
 #pragma unroll
           for (int i = 0; i < kSub; ++i) {
-            v[i] = tc::ex2(fmaf(v[i], c, -m));
+            v[i] = tc::ex2(fmaf(v[i], c, -mz));
             l += v[i];
           }
           lc[ch] = l;
@@ -462,13 +474,13 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   if (warp == 0) tc::tmem_dealloc(tmem, kK);
 }
 
-template <bool kMask, bool kBits>
+template <bool kMask, bool kBits, bool kCausal = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_kernel(
     const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
     const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapA,
     FusedParams prm, PhiloxKey pk) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  fused_body<false, kMask, kBits>(mapQ, mapK, mapQ, mapP, mapA, prm, pk,
+  fused_body<false, kMask, kBits, kCausal>(mapQ, mapK, mapQ, mapP, mapA, prm, pk,
                                   tc::align1024(smem_raw));
 }
 
@@ -528,7 +540,7 @@ bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
-                               uint32_t* keep_bits, cudaStream_t st) {
+                               uint32_t* keep_bits, cudaStream_t st, int causal) {
   const int K = J;
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
@@ -538,6 +550,17 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,         J,         tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8),
                   mask_bias, keep_bits, Aout != nullptr};
+  if (causal) {   // the masking step: keys k > j of each query row j removed
+    if (mask_bias)
+      return keep_bits ? launch_persistent(attn_qk_bsb_kernel<true, true, true>, tiles, mq, mk, mp,
+                                           ma, prm, pk, st)
+                       : launch_persistent(attn_qk_bsb_kernel<true, false, true>, tiles, mq, mk,
+                                           mp, ma, prm, pk, st);
+    return keep_bits ? launch_persistent(attn_qk_bsb_kernel<false, true, true>, tiles, mq, mk, mp,
+                                         ma, prm, pk, st)
+                     : launch_persistent(attn_qk_bsb_kernel<false, false, true>, tiles, mq, mk,
+                                         mp, ma, prm, pk, st);
+  }
   if (mask_bias)
     return keep_bits
                ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st)

@@ -95,9 +95,10 @@ cudaError_t launch_colsum(int dtype, int rows, int cols, const void* X, float* o
                           const ReduceWs& ws, cudaStream_t st);
 cudaError_t launch_f32_to_bf16(int n, const float* src, void* dst, cudaStream_t st);
 
+// causal: scores of keys k > query j are -inf (J == K)
 cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
                            const float* mask_bias, const PhiloxKey& pk, int64_t batch_offset,
-                           void* P, void* A, cudaStream_t st);
+                           void* P, void* A, cudaStream_t st, int causal = 0);
 cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, const void* dA,
                            const void* P, const PhiloxKey& pk, int64_t batch_offset, void* dS,
                            cudaStream_t st);
@@ -193,7 +194,7 @@ bool attn_fused_supported(int J, int P);
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
-                               uint32_t* keep_bits, cudaStream_t st);
+                               uint32_t* keep_bits, cudaStream_t st, int causal = 0);
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,

@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
                                                       T* __restrict__ Pout,
                                                       T* __restrict__ Aout, int64_t rows,
                                                       int K, int HJ, float c, int64_t g0,
-                                                      PhiloxKey pk) {
+                                                      PhiloxKey pk, int causalJ) {
   using Cv = Chunk<T>;
   __shared__ float red[8];
   const int lane = threadIdx.x & 31;
@@ -248,6 +248,12 @@ __global__ void __launch_bounds__(256) bsb_fwd_kernel(const T* __restrict__ S,
       } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) v[i][j] *= c;
+      }
+      if (causalJ) {   // keys after the query are masked out (J == K)
+        const int jq = (int)(row % causalJ);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (ch * 8 + j > jq) v[i][j] = -INFINITY;
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) mx = fmaxf(mx, v[i][j]);
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(256) bsb_fwd_short_kernel(const T* __restrict_
                                                             T* __restrict__ Pout,
                                                             T* __restrict__ Aout, int64_t rows,
                                                             int K, int HJ, float c, int64_t g0,
-                                                            PhiloxKey pk) {
+                                                            PhiloxKey pk, int causalJ) {
   using Cv = Chunk<T>;
   constexpr int RPW = 32 / NC;
   const int lane = threadIdx.x & 31;
@@ -373,6 +379,12 @@ __global__ void __launch_bounds__(256) bsb_fwd_short_kernel(const T* __restrict_
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) v[j] *= c;
+    }
+    if (causalJ) {   // keys after the query are masked out (J == K)
+      const int jq = (int)(row % causalJ);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (ch * 8 + j > jq) v[j] = -INFINITY;
     }
   } else {
 #pragma unroll
@@ -441,7 +453,8 @@ bool rowop_supported(int n) { return n > 0 && (n % 8) == 0 && n <= 32 * 8 * 16; 
 
 cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, const void* S,
                            const float* mask_bias, const PhiloxKey& pk, int64_t batch_offset,
-                           void* P, void* A, cudaStream_t st) {
+                           void* P, void* A, cudaStream_t st, int causal) {
+  const int cj = causal ? J : 0;
   const int64_t rows = (int64_t)B * H * J;
   if (rows == 0) return cudaSuccess;
   const int nc = K / 8;
@@ -453,10 +466,10 @@ cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, c
       if (dtype == 0)
         bsb_fwd_short_kernel<__nv_bfloat16, NC><<<grid, 256, 0, st>>>(
             (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
-            H * J, c, g0, pk);
+            H * J, c, g0, pk, cj);
       else
         bsb_fwd_short_kernel<float, NC><<<grid, 256, 0, st>>>(
-            (const float*)S, mask_bias, (float*)P, (float*)A, rows, K, H * J, c, g0, pk);
+            (const float*)S, mask_bias, (float*)P, (float*)A, rows, K, H * J, c, g0, pk, cj);
     });
     return cudaGetLastError();
   }
@@ -465,10 +478,10 @@ cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, c
     if (dtype == 0)
       bsb_fwd_kernel<__nv_bfloat16, 8, 2><<<grid, 256, 0, st>>>(
           (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
-          H * J, c, g0, pk);
+          H * J, c, g0, pk, cj);
     else
       bsb_fwd_kernel<float, 8, 2><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
-                                                        (float*)A, rows, K, H * J, c, g0, pk);
+                                                        (float*)A, rows, K, H * J, c, g0, pk, cj);
     return cudaGetLastError();
   }
   const int grid = (int)((rows + 7) / 8);
@@ -476,10 +489,10 @@ cudaError_t launch_bsb_fwd(int dtype, int B, int H, int J, int K, float scale, c
     if (dtype == 0)
       bsb_fwd_kernel<__nv_bfloat16, CPL, 1><<<grid, 256, 0, st>>>(
           (const __nv_bfloat16*)S, mask_bias, (__nv_bfloat16*)P, (__nv_bfloat16*)A, rows, K,
-          H * J, c, g0, pk);
+          H * J, c, g0, pk, cj);
     else
       bsb_fwd_kernel<float, CPL, 1><<<grid, 256, 0, st>>>((const float*)S, mask_bias, (float*)P,
-                                                          (float*)A, rows, K, H * J, c, g0, pk);
+                                                          (float*)A, rows, K, H * J, c, g0, pk, cj);
   });
   return cudaGetLastError();
 }

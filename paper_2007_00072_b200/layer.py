@@ -37,10 +37,11 @@ class LayerCfg:
     batch_offset: int = 0
     ln_eps: float = 1e-5
     act: str = "gelu"
+    causal: bool = False   # masking step: query j attends to keys k <= j
 
     def to_c(self) -> _abi.enc_cfg:
         return _abi.enc_cfg(self.p_attn, self.p_hidden, self.p_ffn, self.seed, self.layer_id,
-                            self.batch_offset, self.ln_eps, ACTS[self.act])
+                            self.batch_offset, self.ln_eps, ACTS[self.act], int(self.causal))
 
 
 def param_shapes(I: int, U: int) -> dict:

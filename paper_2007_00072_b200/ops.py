@@ -72,10 +72,10 @@ def enc_aib_bwd(ctx, B, J, H, P, dq, dk, dv, dqkv, dbqkv, stream=None):
 
 
 def enc_bsb_fwd(ctx, B, H, J, K, scale, S, mask_bias, p, seed, subseq, batch_offset, P, A,
-                stream=None):
+                stream=None, causal=False):
     check("enc_bsb_fwd", _abi.load().enc_bsb_fwd(ctx.ptr, _dt(S), B, H, J, K, scale, _p(S),
                                                  _p(mask_bias), p, seed, subseq, batch_offset,
-                                                 _p(P), _p(A), _stream(stream)))
+                                                 _p(P), _p(A), int(causal), _stream(stream)))
 
 
 def enc_bsb_bwd(ctx, B, H, J, K, scale, dA, P, p, seed, subseq, batch_offset, dS, stream=None):
@@ -132,10 +132,10 @@ def enc_set_option(ctx, key, value):
 
 
 def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
-                       Pout, A, keep_bits=None, stream=None):
+                       Pout, A, keep_bits=None, stream=None, causal=False):
     check("enc_attn_fwd_fused", _abi.load().enc_attn_fwd_fused(
         ctx.ptr, B, H, J, P, scale, _p(Q), _p(K), _p(mask_bias), p, seed, subseq, batch_offset,
-        _p(Pout), _p(A), _p(keep_bits), _stream(stream)))
+        _p(Pout), _p(A), _p(keep_bits), int(causal), _stream(stream)))
 
 
 def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batch_offset, dS,

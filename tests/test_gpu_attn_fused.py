@@ -114,3 +114,46 @@ def test_fused_unsupported_shapes(ops, ctx, J, P):
     o = torch.zeros((1, 1, J, J), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(EncError):
         ops.enc_attn_fwd_fused(ctx, 1, 1, J, P, 0.125, x, x, None, 0.1, SEED, 0, 0, o, o)
+
+
+@pytest.mark.parametrize("B,H", [(1, 2), (2, 3)])
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("p", [0.1, 0.0])
+def test_fused_forward_causal(ops, ctx, B, H, masked, p):
+    """Causal masking step (R22) inside the fused kernel: P is
+    exactly zero above the diagonal (whole 32-column chunks and 64-column warp slices are
+    fully masked for the early rows) and matches the oracle's causal BSB elsewhere; the
+    fused backward run on that P matches the oracle's BSB-bwd."""
+    J, P = 512, 64
+    Q = make_tensor((B, H, J, P), 31, "bf16", std=0.8)
+    K = make_tensor((B, H, J, P), 32, "bf16", std=0.8)
+    M = None
+    if masked:
+        M = np.zeros((B, J), np.float32)
+        M[:, J - 40:] = -10000.0
+    boff, sub, scale = 3, 4, 0.125
+    Pm = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
+    bits = torch.full((B, H, J, J // 32), -1, dtype=torch.int32, device="cuda")
+    Mt = None if M is None else torch.tensor(M, device="cuda")
+    ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, dev(Q), dev(K), Mt, p, SEED, sub, boff, Pm,
+                           None, keep_bits=bits, causal=True)
+    torch.cuda.synchronize()
+    S = Q.astype(np.float64) @ K.astype(np.float64).transpose(0, 1, 3, 2)
+    Po, _ = E.bsb_fwd(S, M, scale, p, SEED, sub, boff, causal=True)
+    gP = host(Pm)
+    assert np.isfinite(gP).all()
+    assert (gP[..., np.triu(np.ones((J, J), bool), 1)] == 0).all()
+    assert_parity("P", gP, Po, "bf16")
+    assert np.allclose(gP.sum(-1), 1.0, atol=2e-2)
+    # backward from the causal P: dS vanishes above the diagonal
+    dC = make_tensor((B, J, H, P), 33, "bf16", std=1.0)
+    V = make_tensor((B, H, J, P), 34, "bf16", std=1.0)
+    dS = torch.full_like(Pm, float("nan"))
+    ops.enc_attn_bwd_fused(ctx, B, H, J, P, scale, dev(dC), dev(V), Pm, p, SEED, sub, boff, dS,
+                           keep_bits=bits)
+    torch.cuda.synchronize()
+    dA = np.einsum("bjhp,bhkp->bhjk", dC.astype(np.float64), V.astype(np.float64))
+    dSo = E.bsb_bwd(dA, gP, scale, p, SEED, sub, boff)
+    gdS = host(dS)
+    assert (gdS[..., np.triu(np.ones((J, J), bool), 1)] == 0).all()
+    assert_parity("dS", gdS, dSo, "bf16")

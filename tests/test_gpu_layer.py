@@ -43,13 +43,13 @@ def _paths(dims, dtype, opts=None):
 
 
 def _setup(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, weight_std=0.02,
-           opts=None):
+           opts=None, causal=False):
     from paper_2007_00072_b200 import ops
     from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
     prm = make_params(dims, dtype, "parity", weight_std=weight_std)
     inp = make_inputs(dims, dtype, key_padding=key_padding)
     cfg = LayerCfg(p_attn=p, p_hidden=p, p_ffn=p, act=act, layer_id=layer_id,
-                   batch_offset=batch_offset)
+                   batch_offset=batch_offset, causal=causal)
     layer = EncoderLayer(dims, dtype, cfg)
     for key, val in (opts or {}).items():
         ops.enc_set_option(layer.ctx, key, val)
@@ -61,7 +61,7 @@ def _setup(dims, dtype, act, key_padding, p=0.1, batch_offset=0, layer_id=0, wei
     dX = layer.backward(X, dY)
     torch.cuda.synchronize()
     ocfg = E.Cfg(p_attn=p, p_hidden=p, p_ffn=p, act=ACT[act], layer_id=layer_id,
-                 batch_offset=batch_offset)
+                 batch_offset=batch_offset, causal=causal)
     return layer, prm, inp, ocfg, f64(Y), f64(dX)
 
 
@@ -114,7 +114,8 @@ def _stagewise(dims, dtype, act, key_padding, opts=None, **kw):
         # the unfused paths store S in bf16 between the contraction and BSB: the BSB
         # stage's input is that stored S (the fused kernel keeps S in fp32 TMEM)
         S = bf16_round(S.astype(np.float32)).astype(np.float64)
-    Po, Ao = E.bsb_fwd(S, inp["mask_bias"], sc, ocfg.p_attn, seed, sub(0), boff)
+    Po, Ao = E.bsb_fwd(S, inp["mask_bias"], sc, ocfg.p_attn, seed, sub(0), boff,
+                       causal=ocfg.causal)
     pairs += [("P", s["P"], Po)]
     if _drop_on_load(dims, dtype, opts):
         # A is not stored: the contraction uses keep(P) * s from the stored P
@@ -188,6 +189,15 @@ def test_layer_T_fp32_batch_offset_and_layer_id():
         assert_parity(n, gpu[n], ref[n], "fp32")
 
 
+@pytest.mark.parametrize("key_padding", [False, True])
+def test_layer_T_fp32_causal(key_padding):
+    """The masking step (R22) end to end on the fp32 path."""
+    gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=key_padding,
+                           weight_std=0.2, causal=True)
+    for n in gpu:
+        assert_parity(n, gpu[n], ref[n], "fp32")
+
+
 def test_layer_T_fp32_no_dropout():
     gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=True, p=0.0,
                            weight_std=0.2)
@@ -232,6 +242,19 @@ def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
     pairs, f32 = _stagewise(Dims(B=2, J=512, H=2, P=64, U=512), "bf16", "gelu", True,
                             opts=opts, weight_std=0.06)
+    for n, g, o in pairs + f32:
+        assert_parity(n, g, o, "bf16")
+
+
+@pytest.mark.parametrize("dims,opts", [
+    (Dims(B=2, J=512, H=2, P=64, U=512), None),               # fused score kernels
+    (Dims(B=2, J=512, H=2, P=64, U=512), {OPT_ATTN_FUSED: 0}),  # tiled QK^T + BSB kernel
+    (Dims(B=3, J=128, H=4, P=64, U=512), None),               # short-row BSB kernels
+    (Dims(B=2, J=64, H=4, P=16, U=256), None),                # cuBLAS attention path
+])
+def test_layer_bf16_stagewise_causal(dims, opts):
+    """Causal masking (R22) stage by stage on every attention path."""
+    pairs, f32 = _stagewise(dims, "bf16", "gelu", True, opts=opts, weight_std=0.06, causal=True)
     for n, g, o in pairs + f32:
         assert_parity(n, g, o, "bf16")
 

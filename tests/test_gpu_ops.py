@@ -85,6 +85,40 @@ def test_bsb_fwd(ops, ctx, dtype, shape, masked):
 
 
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", [(2, 2, 16, 16), (2, 3, 64, 64), (3, 2, 128, 128),
+                                   (1, 2, 512, 512), (1, 1, 2056, 2056)])
+@pytest.mark.parametrize("masked", [False, True])
+def test_bsb_fwd_causal(ops, ctx, dtype, shape, masked):
+    """Causal masking step (R22) on the unfused BSB kernels: short
+    rows (several per warp), one warp per row and two warps per row."""
+    B, H, J, K = shape
+    S = make_tensor((B, H, J, K), 12, dtype, std=3.0)
+    M = None
+    if masked:
+        M = np.zeros((B, K), np.float32)
+        M[:, K - K // 4:] = -10000.0
+    scale, p, sub, boff = 0.125, 0.1, 4, 3
+    tS = dev(S, dtype)
+    P = torch.empty_like(tS)
+    A = torch.empty_like(tS)
+    ops.enc_bsb_fwd(ctx, B, H, J, K, scale, tS, None if M is None else dev32(M), p, SEED, sub,
+                    boff, P, A, causal=True)
+    Po, Ao = E.bsb_fwd(S, M, scale, p, SEED, sub, boff, causal=True)
+    hp = host(P)
+    assert (hp[..., np.triu(np.ones((J, K), bool), 1)] == 0).all()
+    assert_parity("P", hp, Po, dtype)
+    assert_parity("A", host(A), Ao, dtype)
+
+
+def test_bsb_fwd_causal_rejects_rectangular(ops, ctx):
+    from paper_2007_00072_b200._abi import EncError
+    t = torch.zeros((1, 1, 8, 16), device="cuda")
+    with pytest.raises(EncError):
+        ops.enc_bsb_fwd(ctx, 1, 1, 8, 16, 0.125, t, None, 0.1, SEED, 0, 0, t.clone(), t.clone(),
+                        causal=True)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("shape", BSB_SHAPES)
 def test_bsb_bwd(ops, ctx, dtype, shape):
     B, H, J, K = shape
