@@ -1,7 +1,7 @@
 // Row-group BDRLN kernels (forward and backward) for I % 32 == 0, I <= 2048.
 //
-// A row of I elements is shared by a group of GW warps (GW = 4, or 3 when a third of the
-// row is exactly one 8-element chunk per lane, I = 768; each warp owns a contiguous part of
+// A row of I elements is shared by a group of GW warps (GW = 2 at I = 1024, 3 when a third
+// of the row is exactly one 8-element chunk per lane, I = 768, else 4; each warp owns a contiguous part of
 // the columns, at most 2 chunks of 8 per lane), so a warp's per-row work is a quarter of
 // the one-warp-per-row kernels in ops_ln.cu and four times as many rows are in flight per
 // SM.  Persistent CTAs of 4 groups (512 threads); each group streams its rows through a
@@ -331,12 +331,17 @@ bool bdrln_rg_supported(int I) { return I % 32 == 0 && I <= 2048; }
     if ((ncq) <= 32) { constexpr int CPW = 1; __VA_ARGS__; }   \
     else { constexpr int CPW = 2; __VA_ARGS__; }               \
   } while (0)
-// warps per row: 3 when a third of the row is exactly one chunk per lane (I = 768: BERT-base),
-// else 4 -- no idle lanes where the row allows it
-static int rg_gw(int nc) { return (nc % 96 == 0 && nc / 3 <= 64) ? 3 : 4; }
+// warps per row: 2 at I = 1024 (two chunks per lane; in-graph A/B against 4 warps: BDRLN-bwd
+// 17.0 -> 14.8 us, the step -4.6 us), 3 when a third of the row is exactly one chunk per lane
+// (I = 768: BERT-base), else 4 -- no idle lanes where the row allows it
+static int rg_gw(int nc) {
+  if (nc == 128) return 2;   // I = 1024: two warps x two chunks per lane (measured faster than 4 x 1)
+  return (nc % 96 == 0 && nc / 3 <= 64) ? 3 : 4;
+}
 #define ENC_GW_DISPATCH(gw, ...)                               \
   do {                                                         \
-    if ((gw) == 3) { constexpr int GW = 3; __VA_ARGS__; }      \
+    if ((gw) == 2) { constexpr int GW = 2; __VA_ARGS__; }      \
+    else if ((gw) == 3) { constexpr int GW = 3; __VA_ARGS__; } \
     else { constexpr int GW = 4; __VA_ARGS__; }                \
   } while (0)
 #define ENC_STG_DISPATCH(stg, ...)                             \
