@@ -55,6 +55,8 @@ def parse():
                          "full training step of BASELINE config 4)")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="e2e through encoder_layer_step_host (no cross-step input prefetch)")
+    ap.add_argument("--attn-overlap", action="store_true",
+                    help="dV contraction beside the fused dA + BSB-bwd kernel (ENC_OPT_ATTN_OVERLAP)")
     ap.add_argument("--bwd-side", action="store_true",
                     help="weight-gradient contractions on a side stream (ENC_OPT_BWD_SIDE)")
     ap.add_argument("--no-qkv-direct", action="store_true",
@@ -244,6 +246,8 @@ def main():
                                                             int(not args.no_qkv_direct)))
     _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 6,
                                                             int(args.bwd_side)))
+    _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 7,
+                                                            int(args.attn_overlap)))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
@@ -308,7 +312,13 @@ def main():
         step()
     barrier()
 
-    # per-operator breakdown pass (all ops timed; not the timed region)
+    # per-operator breakdown pass (all ops timed; not the timed region).  Run with the
+    # side-stream overlaps off so every op's events bracket only its own kernels (an op on
+    # the side stream would otherwise include its wait for the fused kernel beside it).
+    set_opt = lambda k, v: _abi.check("enc_set_option", lib.enc_set_option(  # noqa: E731
+        layer.ctx.ptr, k, v))
+    set_opt(6, 0)
+    set_opt(7, 0)
     lib.enc_set_timing(layer.ctx.ptr, (1 << nops) - 1)
     per_op = {n: [] for n in names}
     for _ in range(3):
@@ -320,6 +330,8 @@ def main():
         for i, n in enumerate(names):
             per_op[n].append(ms_buf[i])
     per_op = {n: statistics.median(v) for n, v in per_op.items()}
+    set_opt(6, int(args.bwd_side))
+    set_opt(7, int(args.attn_overlap))
     tc_path = args.attn_backend in ("fused", "tc") and args.dtype == "bf16"
     fused = tally.fused_bytes(dims, es, fused_attn=(args.attn_backend == "fused"
                                                     and args.dtype == "bf16"),

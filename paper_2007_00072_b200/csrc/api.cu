@@ -44,6 +44,9 @@ struct enc_ctx {
   // backward: weight-gradient contractions on a side stream (own cuBLASLt workspace),
   // forked after their inputs are ready and joined at the end of each backward part
   int bwd_side = 0;          // ENC_OPT_BWD_SIDE (off: measured +1 % at L, -3 % at Bb)
+  int attn_overlap = 0;      // ENC_OPT_ATTN_OVERLAP: dV beside the fused dA + BSB-bwd (off:
+                             // -7 us per step, but the fused kernel's own time then includes
+                             // the SMs it shares with dV)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* side_ws = nullptr;
@@ -697,6 +700,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->bwd_side = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_ATTN_OVERLAP) {
+    ctx->attn_overlap = value ? 1 : 0;
+    return ENC_OK;
+  }
   return ENC_EINVAL;
 }
 
@@ -1041,32 +1048,45 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // column sums in the dV / dQ / dK epilogues (partials [B*4][3I] in the reduction space)
   const bool bgrad_epi = direct && use_bh(ctx, J, P) && (size_t)B * 4 * 3 * I <= wa.cap_floats;
   float* bg = wa.partials;
-  {
-    OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, st, tc_attn ? 1 : 0);
+  // fused + per-(b, h) path: the fused dA + BSB-bwd kernel is launched first and the dV
+  // contraction (which needs only dC, P and the keep bits) on the side stream after it, so
+  // dV's CTAs fill the SMs the fused kernel's uneven last wave leaves idle; joined before
+  // the QKV contractions read dQKV
+  const bool overlap = ctx->attn_overlap && ctx->side && fused_attn && use_bh(ctx, J, P);
+  auto dv_step = [&](cudaStream_t sdv) -> int {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DV, sdv, tc_attn ? 1 : 0);
     if (fused_attn && use_bh(ctx, J, P))   // A was never stored: dropout on load from P
       CK(launch_attn_dv_bh(B, H, J, P, Pm, dC, I, dV, ldqkv, bgrad_epi ? bg + 2 * I : nullptr,
                            3 * I, (const uint32_t*)at(sv, SL.off[S_KB]),
-                           make_philox_key(cfg->p_attn, cfg->seed, l4 + 0).scale, st));
+                           make_philox_key(cfg->p_attn, cfg->seed, l4 + 0).scale, sdv));
     else if (bgrad_epi)
       CK(launch_attn_dv_bh(B, H, J, P, A, dC, I, dV, ldqkv, bg + 2 * I, 3 * I, nullptr, 1.f,
-                           st));
+                           sdv));
     else if (tc_attn)
-      CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, 0, dC, I, dV, ldqkv, st));
+      CK(attn_contract(ctx, ENC_AG_DV, B, H, J, P, A, 0, dC, I, dV, ldqkv, sdv));
     else
       CB(gemm_rm_batched(ctx->blas, dtype, true, false, K, P, J, 1.f, (const void* const*)ptr, K,
                          (const void* const*)(ptr + 2 * BH), I, 0.f, (void* const*)(ptr + 4 * BH),
                          P, BH));
-  }
+    return ENC_OK;
+  };
+  if (overlap) CK(cudaEventRecord(ctx->ev_fork, st));   // dC ready
+  else if (int rr = dv_step(st)) return rr;
   // BSB-bwd (:590)
   {
     OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
     if (fused_attn)  // Gamma dX1 (:588) + BSB-bwd (:590): dA stays in TMEM
       CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, I, V, ldqkv, Pm,
                              make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff,
-                             (const uint32_t*)at(sv, SL.off[S_KB]), dS, st));
+                             (const uint32_t*)at(sv, SL.off[S_KB]), dS, st, overlap));
     else
       CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
                         make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));
+  }
+  if (overlap) {
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+    forked = true;
+    if (int rr = dv_step(ctx->side)) return rr;
   }
   // QK^T dX1 (:591): dQ = dS K;  dX2 (:592): dK = dS^T Q
   const bool dqdk_one_pass = tc_attn && use_bh(ctx, J, P);
@@ -1091,6 +1111,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
       CB(gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, dS, K, (long long)J * K, Q, P,
                          (long long)J * P, 0.f, dK, P, (long long)K * P, BH));
   }
+  if (overlap) CK(join());   // dV (side stream) complete: dQKV and its bias partials whole
   // AIB-bwd (:595): the layout pass; on the direct path dQKV is already assembled and the
   // bias gradient rides in the QKV dW contraction's epilogue (or a column sum below)
   if (!direct) {

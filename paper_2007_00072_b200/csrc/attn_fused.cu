@@ -526,10 +526,28 @@ int persistent_grid(int tiles) {
 template <typename Kern>
 cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const CUtensorMap& b,
                               const CUtensorMap& c, const CUtensorMap& d, const FusedParams& prm,
-                              const PhiloxKey& pk, cudaStream_t st) {
+                              const PhiloxKey& pk, cudaStream_t st, bool high_prio = false) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-  kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk);
-  return cudaGetLastError();
+  if (!high_prio) {
+    kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk);
+    return cudaGetLastError();
+  }
+  // the persistent kernel assumes all of its CTAs are resident at once: when a kernel on
+  // another stream is ready at the same moment (the layer's dV beside the fused backward),
+  // the block scheduler must place this one's CTAs first
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(persistent_grid(tiles));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributePriority;
+  at[0].val.priority = greatest;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk);
 }
 
 }  // namespace
@@ -573,7 +591,8 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,
-                                const uint32_t* keep_bits, void* dS, cudaStream_t st) {
+                                const uint32_t* keep_bits, void* dS, cudaStream_t st,
+                                bool high_prio) {
   const int K = J;
   CUtensorMap mc, mv, mp, ms;
   bool ok = map_pop(&mc, dC, B, H, J, P, lddc, kRows) && map_pop(&mv, V, B, H, K, P, ldv, 256) &&
@@ -582,8 +601,11 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,       J,       tiles, scale, batch_offset * (int64_t)H * J * (K / 8),
                   nullptr, const_cast<uint32_t*>(keep_bits), 0};
-  return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st)
-                   : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st);
+  return keep_bits
+             ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st,
+                                 high_prio)
+             : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st,
+                                 high_prio);
 }
 
 #ifdef ENC_FUSED_TRACE

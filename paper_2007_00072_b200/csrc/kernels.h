@@ -198,7 +198,8 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,
-                                const uint32_t* keep_bits, void* dS, cudaStream_t st);
+                                const uint32_t* keep_bits, void* dS, cudaStream_t st,
+                                bool high_prio = false);
 
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.

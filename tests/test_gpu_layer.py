@@ -301,3 +301,38 @@ def test_backward_halves_equal_full_backward():
     torch.cuda.synchronize()
     assert torch.equal(dX, dX_full)
     assert torch.equal(layer.grad_flat, g_full)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_attn_overlap_option_bitwise(graph):
+    """ENC_OPT_ATTN_OVERLAP (dV on the side stream beside the fused dA + BSB-bwd kernel)
+    changes only the schedule: dX and every gradient are bitwise those of the sequential
+    backward, eager and graph-captured."""
+    from paper_2007_00072_b200 import ops
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    dims = Dims(B=2, J=512, H=4, P=64, U=1024)
+    prm = make_params(dims, "bf16", "parity", weight_std=0.05)
+    inp = make_inputs(dims, "bf16")
+    X = torch.tensor(inp["X"], device="cuda").to(torch.bfloat16)
+    dY = torch.tensor(inp["dY"], device="cuda").to(torch.bfloat16)
+    out = []
+    for ov in (0, 1):
+        layer = EncoderLayer(dims, "bf16", LayerCfg())
+        ops.enc_set_option(layer.ctx, ops.OPT_ATTN_OVERLAP, ov)
+        layer.set_params(prm)
+        layer.forward(X)
+        dX = layer.backward(X, dY).clone()
+        if graph:
+            dXg = torch.empty_like(X)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                layer.forward(X)
+                layer.backward(X, dY, dXg)
+            layer.grad_flat.zero_()
+            g.replay()
+            torch.cuda.synchronize()
+            dX = dXg.clone()
+        torch.cuda.synchronize()
+        out.append((dX.cpu(), layer.grad_flat.cpu()))
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
