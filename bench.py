@@ -442,8 +442,12 @@ def main():
     if stack is not None:
         def host_step():
             stack.step_host(Xh, dYh, Yh, dXh)
+            if post and world == 1:   # the training step's AdamW (N > 1: after the reduce)
+                for fn in post:
+                    fn()
         e2e_buckets = [lay.grad_flat for lay in stack.layers]
-        e2e_api = f"EncoderStack.step_host ({args.layers} layers; "
+        e2e_api = (f"EncoderStack.step_host ({args.layers} layers"
+                   + (" + AdamW" if post else "") + "; ")
     else:
         def host_step():
             layer.step_host(Xh, dYh, Yh, dXh, X, dY, Y, dX)
@@ -533,6 +537,8 @@ def main():
                 host_step()
             if world > 1:
                 dp.allreduce_buckets(e2e_buckets)
+                for fn in post:
+                    fn()
     e1.record()
     barrier()
     e2e_ms = dp.max_over_ranks(e0.elapsed_time(e1), dev) / args.steps

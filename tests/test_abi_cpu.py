@@ -66,3 +66,31 @@ def test_binding_fails_loudly_without_library(tmp_path):
     from paper_2007_00072_b200 import _abi
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _abi.load(str(tmp_path / "missing.so"))
+
+
+@pytest.mark.parametrize("script", ["bench.py", "bench_ops.py", "__graft_entry__.py",
+                                    "tools/select_config.py", "tools/one_step.py",
+                                    "tools/trace_fused.py"])
+def test_driver_scripts_compile(script):
+    """The driver runs bench.py and __graft_entry__.py on the GPU box only: catch syntax
+    errors here."""
+    import py_compile
+    py_compile.compile(os.path.join(ROOT, script), doraise=True)
+
+
+def test_bench_parses_its_flags():
+    """bench.py's argument parser accepts every documented flag combination (no GPU)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    import importlib
+    bench = importlib.import_module("bench")
+    old = sys.argv
+    try:
+        for argv in (["bench.py"], ["bench.py", "--config", "Bb", "--causal", "--attn-overlap"],
+                     ["bench.py", "--layers", "24", "--optimizer", "--no-prefetch"],
+                     ["bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1"]):
+            sys.argv = argv
+            a = bench.parse()
+            assert a.steps >= 1
+    finally:
+        sys.argv = old
