@@ -124,15 +124,28 @@ cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const
   if (n == 0) return cudaSuccess;
   const int ncU = U / 8;
   const int64_t g0 = batch_offset * (int64_t)J * ncU;
+  // grid-stride over the chunks with exactly the resident number of blocks (one wave: at
+  // 40 registers six 256-thread blocks fit per SM, so a fixed 8-per-SM grid left a 1/3 tail)
+  auto resident = [](auto kern) -> int64_t {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0);
+    return (int64_t)(per < 1 ? 1 : per) * sms;
+  };
   int64_t grid = (n + 511) / 512;
-  if (grid > 148 * 8) grid = 148 * 8;
   ENC_ACT_DISPATCH(act, {
-    if (dtype == 0)
-      bad_fwd_kernel<__nv_bfloat16, ACT><<<(int)grid, 256, 0, st>>>(
+    if (dtype == 0) {
+      auto kern = bad_fwd_kernel<__nv_bfloat16, ACT>;
+      const int64_t cap = resident(kern);
+      kern<<<(int)(grid < cap ? grid : cap), 256, 0, st>>>(
           (const __nv_bfloat16*)Y1, b1, (__nv_bfloat16*)h, (__nv_bfloat16*)A1, n, ncU, g0, pk);
-    else
-      bad_fwd_kernel<float, ACT><<<(int)grid, 256, 0, st>>>((const float*)Y1, b1, (float*)h,
-                                                            (float*)A1, n, ncU, g0, pk);
+    } else {
+      auto kern = bad_fwd_kernel<float, ACT>;
+      const int64_t cap = resident(kern);
+      kern<<<(int)(grid < cap ? grid : cap), 256, 0, st>>>((const float*)Y1, b1, (float*)h,
+                                                           (float*)A1, n, ncU, g0, pk);
+    }
   });
   return cudaGetLastError();
 }
