@@ -330,7 +330,7 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
 // Block = 32 columns x 32 row-slices.  Thread (x, y) sums partial rows y, y+32, ... of its
 // column (all loads issued first, ascending order), then the 32 slice sums are added in
 // ascending y order: a fixed summation order, independent of timing.
-constexpr int kFinY = 32;
+constexpr int kFinY = 16;   // one resident wave of 512-thread blocks (32: 1.4 waves, +2 us)
 constexpr int kFinMaxPer = 16;  // partial rows per slice handled with loads in flight
 
 __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
