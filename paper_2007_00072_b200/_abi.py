@@ -30,7 +30,7 @@ class enc_cfg(ctypes.Structure):
 
 PARAM_FIELDS = ("Wqkv", "Wo", "W1", "W2", "bqkv", "bo", "b1", "b2", "g1", "be1", "g2", "be2")
 GRAD_FIELDS = tuple("d" + n for n in PARAM_FIELDS)
-SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "Y1", "A1", "xhat2", "rstd1", "rstd2",
+SAVED_FIELDS = ("Q", "K", "V", "P", "A", "C", "X1", "xhat1", "h", "A1", "xhat2", "rstd1", "rstd2",
                 "keep_attn")
 
 
@@ -132,6 +132,14 @@ _SIGS = {
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "enc_wgemm": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_int64, c_int, c_void_p,
+                          c_int64, c_int, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p]),
+    "enc_linear1_bad_fwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p,
+                                    c_void_p, c_int, c_float, c_uint64, c_uint64, c_int64,
+                                    c_void_p, c_void_p, c_void_p]),
+    "enc_linear2_dx_bad_bwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p,
+                                       c_void_p, c_void_p, c_int, c_float, c_uint64, c_uint64,
+                                       c_int64, c_void_p, c_void_p, c_void_p]),
 }
 
 EXPORTED = tuple(_SIGS)

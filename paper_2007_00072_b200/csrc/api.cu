@@ -9,7 +9,9 @@
 
 #include <climits>
 
+#include <mutex>
 #include <new>
+#include <unordered_map>
 
 #include "../../include/encoder.h"
 #include "gemm.h"
@@ -53,7 +55,23 @@ struct enc_ctx {
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
+  // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
+  int gemm_tc = 1;
+  void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
+  size_t wg_ws_bytes = 0;
+  // forward -> backward contract: the path flags each `saved` buffer was written with
+  std::mutex mu;
+  std::unordered_map<const void*, uint32_t> saved_paths;
 };
+
+// Weight contraction: row-major C[M,N] = op(A) op(B) (+ beta C), nn.Linear operand layouts
+// (tA: A stored [K][M]; tB: B stored [N][K]).  bf16: the hand-written tcgen05 kernel
+// (wgemm.cu) with an optional fp32 bias over columns; fp32 (or ENC_OPT_GEMM_TC off):
+// cuBLASLt / cuBLAS.  Returns an ENC_* code.
+static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA, bool tB,
+                     int M, int N, int K, const void* A, int lda, const void* B, int ldb,
+                     float beta, void* C, int ldc, const float* bias = nullptr,
+                     void* lt_ws = nullptr);
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
 static cublasStatus_t wgemm(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA,
@@ -132,10 +150,50 @@ static int cuda_fail(cudaError_t e) {
     if (_s != CUBLAS_STATUS_SUCCESS) return ENC_ECUBLAS; \
   } while (0)
 
+static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA, bool tB,
+                     int M, int N, int K, const void* A, int lda, const void* B, int ldb,
+                     float beta, void* C, int ldc, const float* bias, void* lt_ws) {
+  if (ctx->gemm_tc && in_dt == ENC_BF16 && (beta == 0.f || beta == 1.f)) {
+    WgemmArgs g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = A; g.lda = lda; g.a_mn = tA ? 1 : 0;
+    g.B = B; g.ldb = ldb; g.b_mn = tB ? 0 : 1;
+    g.C = C; g.ldc = ldc; g.out_f32 = out_dt == ENC_FP32 ? 1 : 0;
+    g.beta = beta != 0.f ? 1 : 0;
+    g.bias = bias;
+    g.ws = ctx->wg_ws;
+    g.ws_bytes = ctx->wg_ws_bytes;
+    if (wgemm_supported(g)) {
+      const cudaError_t e = launch_wgemm(g, ctx->num_sms, st);
+      if (e != cudaSuccess) return cuda_fail(e);
+      ctx->launches += wgemm_launches(g, ctx->num_sms);
+      return ENC_OK;
+    }
+  }
+  if (bias) {
+    if (out_dt == ENC_FP32 || in_dt != ENC_BF16) {
+      // fp32 output: cuBLASLt takes the fp32 bias directly
+      if (ctx->lt && ctx->use_lt && beta == 0.f &&
+          lt_gemm_rm(ctx->lt, in_dt, out_dt, tA, tB, M, N, K, A, lda, B, ldb, 0.f, C, ldc,
+                     LT_EPI_BIAS, const_cast<float*>(bias), st) == CUBLAS_STATUS_SUCCESS)
+        return ENC_OK;
+    }
+    return ENC_EUNSUPPORTED;   // the caller adds the bias itself
+  }
+  return wgemm(ctx, st, in_dt, out_dt, tA, tB, M, N, K, 1.f, A, lda, B, ldb, beta, C, ldc, lt_ws)
+             == CUBLAS_STATUS_SUCCESS
+             ? ENC_OK
+             : ENC_ECUBLAS;
+}
+
 static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 static size_t esize(int dtype) { return dtype == ENC_BF16 ? 2 : 4; }
 static bool valid_dtype(int dtype) { return dtype == ENC_BF16 || dtype == ENC_FP32; }
-static bool valid_p(float p) { return p >= 0.f && p < 1.f && p == p; }
+// p in [0, 1) whose 16-bit threshold T = floor(65536 p + 1/2) (R5) is below 65536:
+// p >= 1 - 2^-17 would give T = 65536, i.e. no kept value and an infinite scale
+static bool valid_p(float p) {
+  return p >= 0.f && p < 1.f && p == p && floor((double)p * 65536.0 + 0.5) < 65536.0;
+}
 
 extern "C" {
 
@@ -174,6 +232,8 @@ int enc_create(enc_ctx** out, int device) {
   e = cudaMalloc(&c->blas_ws, c->blas_ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->red, c->red_floats * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&c->side_ws, c->blas_ws_bytes);
+  c->wg_ws_bytes = 32u << 20;
+  if (e == cudaSuccess) e = cudaMalloc(&c->wg_ws, c->wg_ws_bytes);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   if (cublasSetWorkspace(c->blas, c->blas_ws, c->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS ||
       cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
@@ -241,6 +301,7 @@ void enc_destroy(enc_ctx* c) {
   if (c->blas) cublasDestroy(c->blas);
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->red) cudaFree(c->red);
+  if (c->wg_ws) cudaFree(c->wg_ws);
   delete c;
 }
 
@@ -372,6 +433,43 @@ static Layout bwd_layout(const enc_dims* d, int dtype) {
 static inline char* at(void* base, size_t off) { return (char*)base + off; }
 }  // namespace
 
+// Linear1 + BAD (EPI_BAD_FWD) and Linear2-dX + BAD-bwd (EPI_BAD_BWD) on the tcgen05 kernel;
+// M = 0 (rejected by wgemm_supported) when that path is off for this call
+static WgemmArgs ffn_fwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
+                              const enc_cfg* cfg, const void* X1, const void* W1, const float* b1,
+                              const PhiloxKey& pk, void* h, void* A1) {
+  WgemmArgs g;
+  if (!ctx->gemm_tc || dtype != ENC_BF16) return g;
+  g.M = d->B * d->J; g.N = d->U; g.K = d->I;
+  g.A = X1; g.lda = d->I;
+  g.B = W1; g.ldb = d->I;
+  g.C = h; g.ldc = d->U;
+  g.C2 = A1; g.ldc2 = d->U;
+  g.epi = EPI_BAD_FWD;
+  g.bias = b1;
+  g.act = cfg->act;
+  g.pk = pk;
+  g.g0 = cfg->batch_offset * (int64_t)d->J * (d->U / 8);
+  return g;
+}
+static WgemmArgs ffn_bwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
+                              const enc_cfg* cfg, const void* dY2, const void* W2, const void* h,
+                              const PhiloxKey& pk, void* dh, float* partials) {
+  WgemmArgs g;
+  if (!ctx->gemm_tc || dtype != ENC_BF16) return g;
+  g.M = d->B * d->J; g.N = d->U; g.K = d->I;
+  g.A = dY2; g.lda = d->I;
+  g.B = W2; g.ldb = d->U; g.b_mn = 1;
+  g.C = dh; g.ldc = d->U;
+  g.aux = h; g.ldaux = d->U;
+  g.partials = partials;
+  g.epi = EPI_BAD_BWD;
+  g.act = cfg->act;
+  g.pk = pk;
+  g.g0 = cfg->batch_offset * (int64_t)d->J * (d->U / 8);
+  return g;
+}
+
 extern "C" {
 
 int enc_layer_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* scratch_bytes) {
@@ -390,6 +488,15 @@ int enc_layer_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* s
 // and dQ, dK, dV the blocks of dQKV.  Other paths: separate [B,H,J,P] tensors.
 static bool qkv_direct(const enc_ctx* ctx, const enc_dims* d, int dtype) {
   return ctx->qkv_direct && tc_attn_of(ctx, dtype, d->J, d->P);
+}
+
+// The attention-path flags a forward wrote `saved` with (Q/K/V in place or permuted, fused
+// score kernels, A stored or applied on load): the backward must read it the same way
+static uint32_t path_flags(const enc_ctx* ctx, const enc_dims* d, int dtype) {
+  const bool tc = tc_attn_of(ctx, dtype, d->J, d->P);
+  const bool fused = tc && ctx->attn_fused && attn_fused_supported(d->J, d->P);
+  return (qkv_direct(ctx, d, dtype) ? 1u : 0u) | (tc ? 2u : 0u) | (fused ? 4u : 0u) |
+         (fused && use_bh(ctx, d->J, d->P) ? 8u : 0u) | 0x100u;
 }
 
 int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
@@ -415,7 +522,7 @@ int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc
   v->C = at(saved, L.off[S_C]);
   v->X1 = at(saved, L.off[S_X1]);
   v->xhat1 = at(saved, L.off[S_XH1]);
-  v->Y1 = at(saved, L.off[S_H]);
+  v->h = at(saved, L.off[S_H]);
   v->A1 = at(saved, L.off[S_A1]);
   v->xhat2 = at(saved, L.off[S_XH2]);
   v->rstd1 = (float*)at(saved, L.off[S_R1]);
@@ -704,7 +811,94 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->attn_overlap = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_GEMM_TC) {
+    ctx->gemm_tc = value ? 1 : 0;
+    return ENC_OK;
+  }
   return ENC_EINVAL;
+}
+
+int enc_wgemm(enc_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int tA,
+              const void* B, int64_t ldb, int tB, void* C, int64_t ldc, int c_dtype, int beta,
+              const float* bias, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (!valid_dtype(c_dtype)) return ENC_EDTYPE;
+  if (M <= 0 || N <= 0 || K <= 0 || (beta != 0 && beta != 1) || (beta && c_dtype == ENC_FP32))
+    return ENC_EINVAL;
+  if (lda < (tA ? M : K) || ldb < (tB ? K : N) || ldc < N) return ENC_EINVAL;
+  if (N % 8 || K % 8 || lda % 8 || ldb % 8 || ldc % (c_dtype == ENC_FP32 ? 4 : 8))
+    return ENC_EALIGN;
+  if (lda > INT32_MAX || ldb > INT32_MAX || ldc > INT32_MAX) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(A, B, C);
+  if (bias && !aligned16(bias)) return ENC_EALIGN;
+  WgemmArgs g;
+  g.M = M; g.N = N; g.K = K;
+  g.A = A; g.lda = lda; g.a_mn = tA ? 1 : 0;
+  g.B = B; g.ldb = ldb; g.b_mn = tB ? 0 : 1;
+  g.C = C; g.ldc = ldc; g.out_f32 = c_dtype == ENC_FP32;
+  g.beta = beta;
+  g.bias = bias;
+  g.ws = ctx->wg_ws;
+  g.ws_bytes = ctx->wg_ws_bytes;
+  if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
+  CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
+  ctx->launches += wgemm_launches(g, ctx->num_sms);
+  return ENC_OK;
+}
+
+static int check_ffn_call(int B, int J, int I, int U, float p, int act, int64_t boff) {
+  if (B <= 0 || J <= 0 || I <= 0 || U <= 0 || !valid_p(p) || act < 0 || act > 2 || boff < 0)
+    return ENC_EINVAL;
+  if (I % 8 || U % 8) return ENC_EALIGN;
+  if ((int64_t)B * J * U / 8 >= INT32_MAX) return ENC_EUNSUPPORTED;
+  return ENC_OK;
+}
+
+int enc_linear1_bad_fwd(enc_ctx* ctx, int B, int J, int I, int U, const void* X1,
+                        const void* W1, const float* b1, int act, float p, uint64_t seed,
+                        uint64_t subseq, int64_t batch_offset, void* h, void* A1,
+                        enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_ffn_call(B, J, I, U, p, act, batch_offset);
+  if (r) return r;
+  CHECK_PTRS(X1, W1, b1, h, A1);
+  enc_dims d{B, J, J, 1, I, I, I, U};
+  enc_cfg cfg{};
+  cfg.act = act;
+  cfg.batch_offset = batch_offset;
+  enc_ctx tmp_gate;   // the fused path regardless of ENC_OPT_GEMM_TC
+  tmp_gate.gemm_tc = 1;
+  WgemmArgs g = ffn_fwd_args(&tmp_gate, &d, ENC_BF16, &cfg, X1, W1, b1,
+                             make_philox_key(p, seed, subseq), h, A1);
+  if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
+  OpTimer _t(ctx, ENC_OP_GEMM_L1, (cudaStream_t)stream, 1);
+  CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
+  return ENC_OK;
+}
+
+int enc_linear2_dx_bad_bwd(enc_ctx* ctx, int B, int J, int I, int U, const void* dY2,
+                           const void* W2, const void* h, int act, float p, uint64_t seed,
+                           uint64_t subseq, int64_t batch_offset, void* dh, float* db1,
+                           enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_ffn_call(B, J, I, U, p, act, batch_offset);
+  if (r) return r;
+  CHECK_PTRS(dY2, W2, h, dh, db1);
+  const int R = ((B * J + 127) / 128) * 4;
+  if ((size_t)R * U > ctx->red_floats) return ENC_EUNSUPPORTED;
+  enc_dims d{B, J, J, 1, I, I, I, U};
+  enc_cfg cfg{};
+  cfg.act = act;
+  cfg.batch_offset = batch_offset;
+  enc_ctx tmp_gate;
+  tmp_gate.gemm_tc = 1;
+  WgemmArgs g = ffn_bwd_args(&tmp_gate, &d, ENC_BF16, &cfg, dY2, W2, h,
+                             make_philox_key(p, seed, subseq), dh, ctx->red);
+  if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
+  OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, (cudaStream_t)stream, 2);
+  CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
+  CK(launch_colsum_finalize(ctx->red, R, U, U, db1, nullptr, nullptr, (cudaStream_t)stream));
+  return ENC_OK;
 }
 
 int enc_bei(enc_ctx* ctx, int dtype, int64_t n, const void* a, const void* b, void* out,
@@ -777,15 +971,23 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   bool bias_done = false;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
-    if (direct && ctx->lt && ctx->use_lt && ctx->red_floats >= (size_t)3 * I) {
+    if (direct) {   // tcgen05 contraction: the fp32 bias is added in its epilogue
+      r = wcontract(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I, 0.f,
+                    QKVs, 3 * I, prm->bqkv);
+      if (r == ENC_OK) bias_done = true;
+      else if (r != ENC_EUNSUPPORTED) return r;
+    }
+    if (!bias_done && direct && ctx->lt && ctx->use_lt && ctx->red_floats >= (size_t)3 * I) {
+      // cuBLASLt takes a bf16 output's bias in bf16 (R18): one cast kernel
       CK(launch_f32_to_bf16(3 * I, prm->bqkv, ctx->red, st));
       ctx->launches += 1;
       bias_done = wgemm_epi(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I,
                             QKVs, 3 * I, LT_EPI_BIAS, ctx->red);
     }
     if (!bias_done)
-      CB(wgemm(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, 1.f, X, I, prm->Wqkv, I, 0.f,
-               direct ? QKVs : QKV, 3 * I));
+      if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I,
+                         0.f, direct ? QKVs : QKV, 3 * I)))
+        return r;
   }
   // AIB (:550): in place on the direct path unless the epilogue added the bias
   {
@@ -840,7 +1042,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Out (:554)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, I, I, 1.f, C, I, prm->Wo, I, 0.f, Yo, I));
+    if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, I, I, C, I, prm->Wo, I, 0.f, Yo, I)))
+      return r;
   }
   // BDRLN site 1 (:555-558)
   {
@@ -848,28 +1051,42 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st));
   }
-  // Linear (:559): Y1 = X1 W1^T, kept for the backward (saved.Y1): BAD-bwd recomputes the
-  // activation input h = Y1 + b1 instead of BAD storing h (one write of [B,J,U] saved)
-  {
-    OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, U, I, 1.f, X1, I, prm->W1, I, 0.f, h, U));
-  }
-  // BAD (:560-562)
-  {
-    OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 1);
-    CK(launch_bad_fwd(dtype, B, J, U, h, prm->b1, cfg->act,
-                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, nullptr, A1, st));
+  // Linear (:559) + BAD (:560-562).  The activation input h = X1 W1^T + b1 is kept for the
+  // backward (saved.h); on the tcgen05 path BAD runs in the contraction's epilogue
+  const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
+  WgemmArgs l1 = ffn_fwd_args(ctx, d, dtype, cfg, X1, prm->W1, prm->b1, pk_ffn, h, A1);
+  if (wgemm_supported(l1)) {
+    {
+      OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 1);
+      CK(launch_wgemm(l1, ctx->num_sms, st));
+    }
+    OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 0);   // fused away
+  } else {
+    {
+      OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
+      if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, U, I, X1, I, prm->W1, I, 0.f, h,
+                         U)))
+        return r;
+    }
+    OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 1);   // h = Y1 + b1 in place, A1
+    CK(launch_bad_fwd(dtype, B, J, U, h, prm->b1, cfg->act, pk_ffn, boff, h, A1, st));
   }
   // Linear (:563)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L2, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, true, BJ, I, U, 1.f, A1, U, prm->W2, U, 0.f, Y2, I));
+    if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, I, U, A1, U, prm->W2, U, 0.f, Y2, I)))
+      return r;
   }
   // BDRLN site 2 (:564-567)
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD2, st, 1);
     CK(launch_bdrln_fwd(dtype, B, J, I, Y2, prm->b2, X1, prm->g2, prm->be2, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st));
+  }
+  {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    if (ctx->saved_paths.size() > 4096) ctx->saved_paths.clear();
+    ctx->saved_paths[saved] = path_flags(ctx, d, dtype);
   }
   return ENC_OK;
 }
@@ -889,6 +1106,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   if (!g) return ENC_ENULL;
   CHECK_PTRS(X, saved, dY, dX, scratch, g->dWqkv, g->dWo, g->dW1, g->dW2, g->dbqkv, g->dbo, g->db1,
              g->db2, g->dg1, g->dbe1, g->dg2, g->dbe2);
+  {
+    // the saved set must be read with the attention path it was written with
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    auto it = ctx->saved_paths.find(saved);
+    if (it != ctx->saved_paths.end() && it->second != path_flags(ctx, d, dtype))
+      return ENC_EINVAL;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const int B = d->B, J = d->J, K = d->K, H = d->H, P = d->P, I = d->I, U = d->U;
   const int BJ = B * J, BH = B * H;
@@ -976,34 +1200,64 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, dX1, dY2, g->dg2,
                         g->dbe2, g->db2, w, st));
   }
-  // Linear2 dX (:573), dW (:574)
+  // Linear2 dX (:573) + BAD-bwd (:576-578) in one tcgen05 kernel on the bf16 path (dA1 never
+  // reaches HBM; db1 from its epilogue's column partials), else the contraction into dA1 and
+  // the BAD-bwd kernel; Linear2 dW (:574); then the FFN half's column sums (dg2, dbe2, db2,
+  // db1) in one launch
+  const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, U, I, 1.f, dY2, I, prm->W2, U, 0.f, dA1, U));
-  }
-  {
-    cudaStream_t ss = fork();
-    OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
-    CB(wgemm(ctx, ss, dtype, F32, true, false, I, U, BJ, 1.f, dY2, I, A1, U, 0.f, g->dW2, U, sws));
-  }
-  // BAD-bwd (:576-578), then the FFN half's column sums (dg2, dbe2, db2, db1) in one launch
-  {
-    OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 1 : 2);
     ReduceWs w = after(ffn_jobs[0]);
     w.defer = &ffn_jobs[1];
-    CK(launch_bad_bwd(dtype, B, J, U, dA1, h, prm->b1, cfg->act,
-                      make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2), boff, dh, g->db1, w, st));
-    if (!ffn_deferred) CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+    WgemmArgs l2 = ffn_bwd_args(ctx, d, dtype, cfg, dY2, prm->W2, h, pk_ffn, dh, w.partials);
+    const int R = ((BJ + 127) / 128) * 4;
+    if (wgemm_supported(l2) && (size_t)R * U <= w.cap_floats) {
+      {
+        OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 1);
+        CK(launch_wgemm(l2, ctx->num_sms, st));
+      }
+      {
+        cudaStream_t ss = fork();
+        OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
+        if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
+                           g->dW2, U, nullptr, sws)))
+          return r;
+      }
+      OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 0 : 1);   // fused away
+      CK(colsum_finish(w, R, U, U, g->db1, nullptr, nullptr, st));
+      if (!ffn_deferred) CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+    } else {
+      {
+        OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
+        if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, U, I, dY2, I, prm->W2, U, 0.f,
+                           dA1, U)))
+          return r;
+      }
+      {
+        cudaStream_t ss = fork();
+        OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
+        if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
+                           g->dW2, U, nullptr, sws)))
+          return r;
+      }
+      OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 1 : 2);
+      CK(launch_bad_bwd(dtype, B, J, U, dA1, h, nullptr, cfg->act, pk_ffn, boff, dh, g->db1, w,
+                        st));
+      if (!ffn_deferred) CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+    }
   }
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DX, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, U, 1.f, dh, U, prm->W1, I, 1.f, dX1, I));
+    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, U, dh, U, prm->W1, I, 1.f, dX1,
+                       I)))
+      return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, ss, 0);
-    CB(wgemm(ctx, ss, dtype, F32, true, false, U, I, BJ, 1.f, dh, U, X1, I, 0.f, g->dW1, I, sws));
+    if ((r = wcontract(ctx, ss, dtype, F32, true, false, U, I, BJ, dh, U, X1, I, 0.f, g->dW1, I,
+                       nullptr, sws)))
+      return r;
   }
   if (!(parts & 2)) CK(join());   // the FFN bucket is complete when the FFN part returns
   }  // FFN half
@@ -1023,12 +1277,16 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // Out dX (:586), dW (:587)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DX, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, I, 1.f, dYo, I, prm->Wo, I, 0.f, dC, I));
+    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, I, dYo, I, prm->Wo, I, 0.f, dC,
+                       I)))
+      return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, ss, 0);
-    CB(wgemm(ctx, ss, dtype, F32, true, false, I, I, BJ, 1.f, dYo, I, C, I, 0.f, g->dWo, I, sws));
+    if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, I, BJ, dYo, I, C, I, 0.f, g->dWo, I,
+                       nullptr, sws)))
+      return r;
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
@@ -1121,14 +1379,16 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
-    CB(wgemm(ctx, st,dtype, dtype, false, false, BJ, I, 3 * I, 1.f, dQKV, 3 * I, prm->Wqkv, I,
-               1.f, dX, I));
+    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, 3 * I, dQKV, 3 * I, prm->Wqkv,
+                       I, 1.f, dX, I)))
+      return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, ss, 0);
-    CB(wgemm(ctx, ss, dtype, F32, true, false, 3 * I, I, BJ, 1.f, dQKV, 3 * I, X, I, 0.f,
-             g->dWqkv, I, sws));
+    if ((r = wcontract(ctx, ss, dtype, F32, true, false, 3 * I, I, BJ, dQKV, 3 * I, X, I, 0.f,
+                       g->dWqkv, I, nullptr, sws)))
+      return r;
   }
   if (direct && !bgrad_epi) {
     // bias gradient as a column sum of dQKV (cuBLASLt's BGRAD epilogue on the dW

@@ -40,7 +40,7 @@ struct LtCtx {
   size_t tmp_bytes = 0;
   std::map<Key, Plan> plans;
   std::mutex mu;
-  int autotune = 1;
+  int autotune = 0;   // measuring is opt-in (ENC_OPT_GEMM_AUTOTUNE): it allocates and syncs
 };
 
 LtCtx* lt_create(void* ws, size_t ws_bytes) {

@@ -150,6 +150,30 @@ bool attn_gemm_supported(int J, int P);
 cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, int64_t ldx,
                              const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st);
 
+// Hand-written tcgen05 weight contractions with fused epilogues (wgemm.cu).  Row-major
+// C[M,N] = A B: A K-major [M][K] (a_mn = 0) or MN-major [K][M] (a_mn = 1); B K-major [N][K]
+// (b_mn = 0) or MN-major [K][N] (b_mn = 1); bf16 operands, fp32 accumulation.
+enum { EPI_STORE = 0, EPI_BAD_FWD = 1, EPI_BAD_BWD = 2 };
+struct WgemmArgs {
+  int M = 0, N = 0, K = 0;
+  const void* A = nullptr; int64_t lda = 0; int a_mn = 0;
+  const void* B = nullptr; int64_t ldb = 0; int b_mn = 0;
+  void* C = nullptr; int64_t ldc = 0; int out_f32 = 0;   // EPI_BAD_FWD: C = h
+  int epi = EPI_STORE;
+  int beta = 0;                  // EPI_STORE, bf16: C = acc (+ bias) + C
+  const float* bias = nullptr;   // [N] fp32 (EPI_STORE optional; EPI_BAD_FWD: b1)
+  void* C2 = nullptr; int64_t ldc2 = 0;          // EPI_BAD_FWD: A1
+  const void* aux = nullptr; int64_t ldaux = 0;  // EPI_BAD_BWD: h [M][N]
+  float* partials = nullptr;     // EPI_BAD_BWD: [ceil(M/128)*4][N] column partials of dh
+  int act = 0;
+  PhiloxKey pk{};
+  int64_t g0 = 0;                // Philox chunk index of element (0, 0)
+  void* ws = nullptr; size_t ws_bytes = 0;   // split-K slabs (fp32 EPI_STORE outputs)
+};
+bool wgemm_supported(const WgemmArgs& g);
+cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st);
+int wgemm_launches(const WgemmArgs& g, int num_sms);   // kernels launch_wgemm launches
+
 // cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
 CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,
                            void* addr, const cuuint64_t* dims, const cuuint64_t* strides,

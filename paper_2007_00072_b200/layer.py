@@ -249,7 +249,7 @@ class EncoderLayer:
                                                           ctypes.byref(v)))
         B, J, H, P, I, U = self.B, self.J, self.H, self.P, self.I, self.U
         shapes = {"P": (B, H, J, J), "A": (B, H, J, J), "C": (B, J, I), "X1": (B, J, I),
-                  "xhat1": (B, J, I), "Y1": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I),
+                  "xhat1": (B, J, I), "h": (B, J, U), "A1": (B, J, U), "xhat2": (B, J, I),
                   "rstd1": (B, J), "rstd2": (B, J), "keep_attn": (B, H, J, (J + 31) // 32)}
         base = self.saved.data_ptr()
         out = {}

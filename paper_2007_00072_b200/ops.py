@@ -128,7 +128,7 @@ def enc_set_option(ctx, key, value):
 
 
 (OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT,
- OPT_BWD_SIDE, OPT_ATTN_OVERLAP) = range(8)
+ OPT_BWD_SIDE, OPT_ATTN_OVERLAP, OPT_GEMM_TC) = range(9)
 
 
 def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
@@ -143,3 +143,31 @@ def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batc
     check("enc_attn_bwd_fused", _abi.load().enc_attn_bwd_fused(
         ctx.ptr, B, H, J, P, scale, _p(dC), _p(V), _p(Pin), p, seed, subseq, batch_offset,
         _p(keep_bits), _p(dS), _stream(stream)))
+
+
+def enc_wgemm(ctx, A, B, C, tA=False, tB=False, beta=0, bias=None, M=None, N=None, K=None,
+              stream=None):
+    """C[M,N] = op(A) op(B) (+ bias) (+ C) on the tcgen05 weight-contraction kernel; A, B
+    bf16 row-major ([M,K] or, tA, [K,M]; [K,N] or, tB, [N,K]); C bf16 or fp32 [M,N]."""
+    if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise TypeError("enc_wgemm takes bf16 operands")
+    M = C.shape[0] if M is None else M
+    N = C.shape[1] if N is None else N
+    K = (A.shape[0] if tA else A.shape[1]) if K is None else K
+    check("enc_wgemm", _abi.load().enc_wgemm(
+        ctx.ptr, M, N, K, _p(A), A.stride(0), int(tA), _p(B), B.stride(0), int(tB), _p(C),
+        C.stride(0), _dt(C), int(beta), _p(bias), _stream(stream)))
+
+
+def enc_linear1_bad_fwd(ctx, B, J, I, U, X1, W1, b1, act, p, seed, subseq, batch_offset, h, A1,
+                        stream=None):
+    check("enc_linear1_bad_fwd", _abi.load().enc_linear1_bad_fwd(
+        ctx.ptr, B, J, I, U, _p(X1), _p(W1), _p(b1), act, p, seed, subseq, batch_offset, _p(h),
+        _p(A1), _stream(stream)))
+
+
+def enc_linear2_dx_bad_bwd(ctx, B, J, I, U, dY2, W2, h, act, p, seed, subseq, batch_offset, dh,
+                           db1, stream=None):
+    check("enc_linear2_dx_bad_bwd", _abi.load().enc_linear2_dx_bad_bwd(
+        ctx.ptr, B, J, I, U, _p(dY2), _p(W2), _p(h), act, p, seed, subseq, batch_offset, _p(dh),
+        _p(db1), _stream(stream)))
