@@ -229,8 +229,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = mb * kBM + q * 32;
       const int row = row0 + lane;
       const int out_row0 = row0 + sp * p.M;   // split-K partial slab (EPI_STORE, fp32)
-      float colsum_acc = 0.f;
-      (void)colsum_acc;
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c, ++cidx) {
         const int col = nb * kBN + chalf * (kBN / 2) + c * CW;
@@ -247,17 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[as]);
         }
-        if (!aux) {
-          // the store issued from this buffer two chunks ago must have read it
-          if (EPI == EPI_BAD_FWD) {
-            if (lane == 0) tc::bulk_wait_read<0>();
-          } else {
-            if (lane == 0) tc::bulk_wait_read<1>();
-          }
-          __syncwarp();
-        } else {
-          mbar_wait(&xb[buf], (cidx >> 1) & 1);
-        }
+        // results are formed in registers first, so the stores issued from the staging
+        // buffers by the previous chunk drain while this chunk computes
+        uint4 o0[4], o1[4];
+        if (aux) mbar_wait(&xb[buf], (cidx >> 1) & 1);
         if (EPI == EPI_STORE) {
           if (p.bias != nullptr) {
 #pragma unroll
@@ -268,41 +259,55 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 8; ++i) v[j + i] += b[i];
             }
           }
-          if (OUTF32) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-              *reinterpret_cast<float4*>(sb + sw64(lane, j)) =
-                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
+          for (int j = 0; j < 4; ++j) {
+            if (OUTF32) {
+              o0[j] = make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                                 __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+            } else {
               if (p.beta) {
                 float r[8];
                 unpack_bf16x8(*reinterpret_cast<const uint4*>(sb + sw64(lane, j)), r);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) v[8 * j + i] += r[i];
               }
-              *reinterpret_cast<uint4*>(sb + sw64(lane, j)) = pack_bf16x8(v + 8 * j);
+              o0[j] = pack_bf16x8(v + 8 * j);
             }
           }
         } else if (EPI == EPI_BAD_FWD) {
           // h = acc + b1 (stored, bf16); A1 = keep ? act(h) * s : 0 from the stored h
           PhiloxKey pkh = p.pk;
           pkh.scale *= 0.5f;   // act_f2 returns 2 act(h)
-          unsigned char* sb2 = stg + (buf ^ 1) * kStg;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, hb[8], m[8], a[8];
             if (col + 8 * j < p.N) load_f32x8(p.bias + col + 8 * j, b);
 #pragma unroll
             for (int i = 0; i < 8; ++i) hb[i] = v[8 * j + i] + b[i];
-            const uint4 hu = pack_bf16x8(hb);
-            *reinterpret_cast<uint4*>(sb + sw64(lane, j)) = hu;
-            unpack_bf16x8(hu, hb);
+            o0[j] = pack_bf16x8(hb);
+            unpack_bf16x8(o0[j], hb);
             keep_mul8((uint64_t)(p.g0 + (int64_t)row * (p.N >> 3) + ((col >> 3) + j)), pkh, m);
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = act_f2<ACT>(hb[i]) * m[i];
-            *reinterpret_cast<uint4*>(sb2 + sw64(lane, j)) = pack_bf16x8(a);
+            o1[j] = pack_bf16x8(a);
+          }
+        }
+        if (EPI != EPI_BAD_BWD) {
+          if (!aux) {
+            // the stores issued from these buffers earlier must have read them
+            if (lane == 0) {
+              if (EPI == EPI_BAD_FWD)
+                tc::bulk_wait_read<0>();
+              else
+                tc::bulk_wait_read<1>();
+            }
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            *reinterpret_cast<uint4*>(sb + sw64(lane, j)) = o0[j];
+            if (EPI == EPI_BAD_FWD)
+              *reinterpret_cast<uint4*>(stg + (buf ^ 1) * kStg + sw64(lane, j)) = o1[j];
           }
         } else {   // EPI_BAD_BWD
           // dh = keep ? acc * s * act'(h) : 0, written over h in the staging buffer
