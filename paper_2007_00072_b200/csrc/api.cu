@@ -57,6 +57,7 @@ struct enc_ctx {
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   int gemm_tc = 1;
+  int gemm_cg = 0;           // ENC_OPT_GEMM_PAIR 1 (default) -> 0 (auto), 0 -> 1 (single CTAs)
   void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
   size_t wg_ws_bytes = 0;
   // forward -> backward contract: the path flags each `saved` buffer was written with
@@ -163,6 +164,7 @@ static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool 
     g.bias = bias;
     g.ws = ctx->wg_ws;
     g.ws_bytes = ctx->wg_ws_bytes;
+    g.cg = ctx->gemm_cg;
     if (wgemm_supported(g)) {
       const cudaError_t e = launch_wgemm(g, ctx->num_sms, st);
       if (e != cudaSuccess) return cuda_fail(e);
@@ -446,6 +448,7 @@ static WgemmArgs ffn_fwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
   g.C = h; g.ldc = d->U;
   g.C2 = A1; g.ldc2 = d->U;
   g.epi = EPI_BAD_FWD;
+  g.cg = ctx->gemm_cg;
   g.bias = b1;
   g.act = cfg->act;
   g.pk = pk;
@@ -464,6 +467,7 @@ static WgemmArgs ffn_bwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
   g.aux = h; g.ldaux = d->U;
   g.partials = partials;
   g.epi = EPI_BAD_BWD;
+  g.cg = ctx->gemm_cg;
   g.act = cfg->act;
   g.pk = pk;
   g.g0 = cfg->batch_offset * (int64_t)d->J * (d->U / 8);
@@ -815,6 +819,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->gemm_tc = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_GEMM_PAIR) {
+    ctx->gemm_cg = value ? 0 : 1;
+    return ENC_OK;
+  }
   return ENC_EINVAL;
 }
 
@@ -840,6 +848,7 @@ int enc_wgemm(enc_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int
   g.bias = bias;
   g.ws = ctx->wg_ws;
   g.ws_bytes = ctx->wg_ws_bytes;
+  g.cg = ctx->gemm_cg;
   if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
   CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
   ctx->launches += wgemm_launches(g, ctx->num_sms);
@@ -868,6 +877,7 @@ int enc_linear1_bad_fwd(enc_ctx* ctx, int B, int J, int I, int U, const void* X1
   cfg.batch_offset = batch_offset;
   enc_ctx tmp_gate;   // the fused path regardless of ENC_OPT_GEMM_TC
   tmp_gate.gemm_tc = 1;
+  tmp_gate.gemm_cg = ctx->gemm_cg;
   WgemmArgs g = ffn_fwd_args(&tmp_gate, &d, ENC_BF16, &cfg, X1, W1, b1,
                              make_philox_key(p, seed, subseq), h, A1);
   if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
@@ -884,16 +894,17 @@ int enc_linear2_dx_bad_bwd(enc_ctx* ctx, int B, int J, int I, int U, const void*
   int r = check_ffn_call(B, J, I, U, p, act, batch_offset);
   if (r) return r;
   CHECK_PTRS(dY2, W2, h, dh, db1);
-  const int R = ((B * J + 127) / 128) * 4;
-  if ((size_t)R * U > ctx->red_floats) return ENC_EUNSUPPORTED;
   enc_dims d{B, J, J, 1, I, I, I, U};
   enc_cfg cfg{};
   cfg.act = act;
   cfg.batch_offset = batch_offset;
   enc_ctx tmp_gate;
   tmp_gate.gemm_tc = 1;
+  tmp_gate.gemm_cg = ctx->gemm_cg;
   WgemmArgs g = ffn_bwd_args(&tmp_gate, &d, ENC_BF16, &cfg, dY2, W2, h,
                              make_philox_key(p, seed, subseq), dh, ctx->red);
+  const int R = wgemm_partial_rows(g);
+  if ((size_t)R * U > ctx->red_floats) return ENC_EUNSUPPORTED;
   if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
   OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, (cudaStream_t)stream, 2);
   CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
@@ -1209,7 +1220,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     ReduceWs w = after(ffn_jobs[0]);
     w.defer = &ffn_jobs[1];
     WgemmArgs l2 = ffn_bwd_args(ctx, d, dtype, cfg, dY2, prm->W2, h, pk_ffn, dh, w.partials);
-    const int R = ((BJ + 127) / 128) * 4;
+    const int R = wgemm_partial_rows(l2);
     if (wgemm_supported(l2) && (size_t)R * U <= w.cap_floats) {
       {
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 1);

@@ -169,10 +169,12 @@ struct WgemmArgs {
   PhiloxKey pk{};
   int64_t g0 = 0;                // Philox chunk index of element (0, 0)
   void* ws = nullptr; size_t ws_bytes = 0;   // split-K slabs (fp32 EPI_STORE outputs)
+  int cg = 0;                    // 0 = CTA pairs (cta_group::2) where M > 128, 1 = single CTAs
 };
 bool wgemm_supported(const WgemmArgs& g);
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st);
 int wgemm_launches(const WgemmArgs& g, int num_sms);   // kernels launch_wgemm launches
+int wgemm_partial_rows(const WgemmArgs& g);            // EPI_BAD_BWD partial rows written
 
 // cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
 CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,

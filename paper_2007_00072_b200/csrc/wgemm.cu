@@ -35,24 +35,36 @@
 namespace enc {
 namespace wg {
 
-constexpr int kBM = 128, kBN = 256, kBK = 64, kStages = 4;
+constexpr int kBM = 128, kBN = 256, kBK = 64;   // per-CTA accumulator tile 128 x 256
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB
-constexpr uint32_t kBBytes = kBN * kBK * 2;   // 32 KB
+constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB per stage
 constexpr uint32_t kStg = 32 * 64;            // one [32 rows x 64 B] staging buffer
-constexpr size_t kSmem =
-    1024 + (size_t)kStages * (kABytes + kBBytes) + (size_t)kEpiWarps * 2 * kStg + 256;
+
+// CG = 1: one CTA computes a 128 x 256 tile (tcgen05.mma.cta_group::1, M = 128, N = 256).
+// CG = 2: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256, N = 256) issued by the even CTA: each CTA stages
+// half of A (its 128 rows) and half of B (128 of the 256 columns) and holds its 128 rows x
+// 256 columns of the accumulator, so per-SM shared-memory and L2 operand traffic per MMA
+// drop by a third against CG = 1.
+template <int CG, int EPI>
+struct Cfg {
+  static constexpr uint32_t kBBytes = (kBN / CG) * kBK * 2;
+  static constexpr int kStages = CG == 2 ? (EPI == EPI_BAD_FWD ? 4 : 6) : 4;
+  static constexpr int kNBuf = (CG == 2 && EPI == EPI_BAD_FWD) ? 4 : 2;   // staging / warp
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) +
+                                  (size_t)kEpiWarps * kNBuf * kStg + 256;
+};
 
 struct Params {
   int M, N, K;
-  int tiles_m, tiles_n, splits, units;
+  int tiles_m, tiles_n, splits, units;   // tiles of (128 CG) x 256; units = tiles x splits
   int kb_per_split, nk;
   int beta;               // EPI_STORE: out = acc (+ bias) + out (bf16 output)
   const float* bias;      // [N] fp32 or null (EPI_STORE, EPI_BAD_FWD: b1)
   PhiloxKey pk;           // BAD epilogues (site 2)
   int64_t g0;             // Philox chunk index of element (0, 0): batch_offset * J * N / 8
-  float* partials;        // EPI_BAD_BWD: [tiles_m * 4][N] column partial sums of dh
+  float* partials;        // EPI_BAD_BWD: [ceil(M/128) * 4][N] column partial sums of dh
 };
 
 // byte offset of 16-B chunk c (0..3) of row r in a [32 x 64 B] SWIZZLE_64B tile
@@ -77,6 +89,66 @@ __device__ __forceinline__ uint4 pack_bf16x8(const float* v) {
   return u;
 }
 
+// ---- cluster (CTA pair) helpers
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;"
+               ::: "memory");
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t caddr) {
+  // default (.release.cta) semantics: what must be ordered before the arrive is this warp's
+  // tcgen05.ld of the accumulator, which tcgen05.fence::before_thread_sync covers
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(caddr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// TMA 2-D load into this CTA's shared memory completing on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map,
+                                                 uint32_t bar_caddr, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(bar_caddr)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the mbarrier at this offset in both CTAs of the pair when the pair's MMAs finish
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
 // unit -> (m block, n block, split); m fastest so concurrent CTAs share B tiles in L2
 __device__ __forceinline__ void decode(const Params& p, int u, int& mb, int& nb, int& sp) {
   const int t = u % (p.tiles_m * p.tiles_n);
@@ -85,17 +157,22 @@ __device__ __forceinline__ void decode(const Params& p, int u, int& mb, int& nb,
   nb = t / p.tiles_m;
 }
 
-template <int AMN, int BMN, int OUTF32, int EPI, int ACT>
+template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
 __global__ void __launch_bounds__(kThreads, 1)
     wgemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                  const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapC2,
                  const __grid_constant__ CUtensorMap mapX, const Params p) {
+  using C = Cfg<CG, EPI>;
+  constexpr int kStages = C::kStages;
+  constexpr uint32_t kBBytes = C::kBBytes;
+  constexpr int kNBuf = C::kNBuf;
+  constexpr int kBNc = kBN / CG;                 // B columns staged by this CTA
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = tc::align1024(smem_raw);
   unsigned char* sA = base;
   unsigned char* sB = base + kStages * kABytes;
   unsigned char* sStg = sB + kStages * kBBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + kEpiWarps * 2 * kStg);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStg + kEpiWarps * kNBuf * kStg);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -105,6 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   constexpr bool kAux = EPI == EPI_BAD_BWD;    // (+ p.beta at run time)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;   // 0 = the pair's MMA issuer
+  const int cid = blockIdx.x / CG;             // persistent scheduler: one unit per pair
+  const int ncl = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&mapA);
@@ -116,14 +196,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], kEpiWarps);
+      mbar_init(&tempty[s], kEpiWarps * CG);
     }
     for (int s = 0; s < 2 * kEpiWarps; ++s) mbar_init(&xbar[s], 1);
     fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  if (warp == 1) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                       smem_u32(tmem_slot))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tc::tmem_alloc(tmem_slot, 512);
+    }
+  }
   tc::fence_before_sync();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();
+  else
+    __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
@@ -131,68 +223,109 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t pc = 0;
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (int u = cid; u < p.units; u += ncl) {
         int mb, nb, sp;
         decode(p, u, mb, nb, sp);
-        const int m0 = mb * kBM, n0 = nb * kBN;
+        const int m0 = mb * kBM * CG + rank * kBM;       // this CTA's A rows
+        const int n0 = nb * kBN + rank * kBNc;           // this CTA's B columns
         const int kb0 = sp * p.kb_per_split;
         const int kb1 = min(p.nk, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++pc) {
           const uint32_t s = pc % kStages;
           mbar_wait(&empty[s], ((pc / kStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
           const int k0 = kb * kBK;
-          if (!AMN) {
-            tc::tma_load_2d(sA + s * kABytes, &mapA, &full[s], k0, m0);
-          } else {
+          if (CG == 1) {
+            mbar_arrive_expect_tx(&full[s], kABytes + kBBytes);
+            if (!AMN) {
+              tc::tma_load_2d(sA + s * kABytes, &mapA, &full[s], k0, m0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j)
-              tc::tma_load_2d(sA + s * kABytes + j * 8192, &mapA, &full[s], m0 + 64 * j, k0);
-          }
-          if (!BMN) {
-            tc::tma_load_2d(sB + s * kBBytes, &mapB, &full[s], k0, n0);
-          } else {
+              for (int j = 0; j < kBM / 64; ++j)
+                tc::tma_load_2d(sA + s * kABytes + j * 8192, &mapA, &full[s], m0 + 64 * j, k0);
+            }
+            if (!BMN) {
+              tc::tma_load_2d(sB + s * kBBytes, &mapB, &full[s], k0, n0);
+            } else {
 #pragma unroll
-            for (int j = 0; j < kBN / 64; ++j)
-              tc::tma_load_2d(sB + s * kBBytes + j * 8192, &mapB, &full[s], n0 + 64 * j, k0);
+              for (int j = 0; j < kBNc / 64; ++j)
+                tc::tma_load_2d(sB + s * kBBytes + j * 8192, &mapB, &full[s], n0 + 64 * j, k0);
+            }
+          } else {
+            // both CTAs' loads complete on the leader's full barrier, which expects them all
+            const uint32_t fb = mapa(&full[s], 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * (kABytes + kBBytes));
+            if (!AMN) {
+              tma_load_2d_pair(sA + s * kABytes, &mapA, fb, k0, m0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_2d_pair(sA + s * kABytes + j * 8192, &mapA, fb, m0 + 64 * j, k0);
+            }
+            if (!BMN) {
+              tma_load_2d_pair(sB + s * kBBytes, &mapB, fb, k0, n0);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBNc / 64; ++j)
+                tma_load_2d_pair(sB + s * kBBytes + j * 8192, &mapB, fb, n0 + 64 * j, k0);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kBM, kBN, AMN, BMN);
-    uint32_t pc = 0;
-    int it = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
-      int mb, nb, sp;
-      decode(p, u, mb, nb, sp);
-      const int kb0 = sp * p.kb_per_split;
-      const int kb1 = min(p.nk, kb0 + p.kb_per_split);
-      const int as = it & 1;
-      mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
-      tc::fence_after_sync();
-      const uint32_t dacc = tmem + as * kBN;
-      for (int kb = kb0; kb < kb1; ++kb, ++pc) {
-        const uint32_t s = pc % kStages;
-        mbar_wait(&full[s], (pc / kStages) & 1);
+    // ------------------------------------------------------------ MMA issuer (pair leader)
+    if (rank == 0) {
+      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kBM * CG, kBN, AMN, BMN);
+      uint32_t pc = 0;
+      int it = 0;
+      for (int u = cid; u < p.units; u += ncl, ++it) {
+        int mb, nb, sp;
+        decode(p, u, mb, nb, sp);
+        const int kb0 = sp * p.kb_per_split;
+        const int kb1 = min(p.nk, kb0 + p.kb_per_split);
+        const int as = it & 1;
+        if (CG == 2)
+          mbar_wait_cluster(&tempty[as], ((it >> 1) & 1) ^ 1);
+        else
+          mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
         tc::fence_after_sync();
-        if (lane == 0) {
-          const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+        const uint32_t dacc = tmem + as * kBN;
+        for (int kb = kb0; kb < kb1; ++kb, ++pc) {
+          const uint32_t s = pc % kStages;
+          if (CG == 2)
+            mbar_wait_cluster(&full[s], (pc / kStages) & 1);
+          else
+            mbar_wait(&full[s], (pc / kStages) & 1);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = AMN ? tc::smem_desc(a0 + k * 2048, 8192, 1024)
-                                    : tc::smem_desc(a0 + k * 32, 16, 1024);
-            const uint64_t bd = BMN ? tc::smem_desc(b0 + k * 2048, 8192, 1024)
-                                    : tc::smem_desc(b0 + k * 32, 16, 1024);
-            tc::mma_bf16(dacc, ad, bd, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t ad = AMN ? tc::smem_desc(a0 + k * 2048, 8192, 1024)
+                                      : tc::smem_desc(a0 + k * 32, 16, 1024);
+              const uint64_t bd = BMN ? tc::smem_desc(b0 + k * 2048, 8192, 1024)
+                                      : tc::smem_desc(b0 + k * 32, 16, 1024);
+              const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
+              if (CG == 2)
+                mma_bf16_pair(dacc, ad, bd, idesc, acc);
+              else
+                tc::mma_bf16(dacc, ad, bd, idesc, acc);
+            }
+            if (CG == 2)
+              mma_commit_pair(&empty[s]);
+            else
+              tc::mma_commit(&empty[s]);
           }
-          tc::mma_commit(&empty[s]);
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if (CG == 2)
+            mma_commit_pair(&tfull[as]);
+          else
+            tc::mma_commit(&tfull[as]);
         }
         __syncwarp();
       }
-      if (lane == 0) tc::mma_commit(&tfull[as]);
-      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -201,14 +334,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int chalf = ew >> 2;         // column half of the 256-wide tile
     constexpr int CW = OUTF32 ? 16 : 32;   // columns per 64-byte chunk
     constexpr int NCH = (kBN / 2) / CW;
-    unsigned char* stg = sStg + ew * 2 * kStg;
+    unsigned char* stg = sStg + ew * kNBuf * kStg;
     uint64_t* xb = xbar + 2 * ew;
     const bool aux = kAux || p.beta;
+    const uint32_t tempty_c = CG == 2 ? mapa(&tempty[0], 0) : 0;   // leader's barriers
     // chunk c of unit u: output coordinates
     auto chunk_coords = [&](int u, int c, int& row0, int& col) {
       int mb, nb, sp;
       decode(p, u, mb, nb, sp);
-      row0 = mb * kBM + q * 32;
+      row0 = mb * kBM * CG + rank * kBM + q * 32;
       col = nb * kBN + chalf * (kBN / 2) + c * CW;
     };
     auto issue_aux = [&](int u, int c, int buf) {
@@ -218,24 +352,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tma_load_2d(stg + buf * kStg, &mapX, &xb[buf], col, row0);
     };
     uint32_t cidx = 0;   // chunks processed by this warp (buffer parity, aux barrier phase)
-    if (aux && lane == 0 && (int)blockIdx.x < p.units) issue_aux(blockIdx.x, 0, 0);
+    if (aux && lane == 0 && cid < p.units) issue_aux(cid, 0, 0);
     int it = 0;
-    for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++it) {
+    for (int u = cid; u < p.units; u += ncl, ++it) {
       int mb, nb, sp;
       decode(p, u, mb, nb, sp);
       const int as = it & 1;
       mbar_wait_sleep(&tfull[as], (it >> 1) & 1, 20000u);
       tc::fence_after_sync();
-      const int row0 = mb * kBM + q * 32;
+      const int row0 = mb * kBM * CG + rank * kBM + q * 32;
       const int row = row0 + lane;
       const int out_row0 = row0 + sp * p.M;   // split-K partial slab (EPI_STORE, fp32)
+      const int prow = (mb * CG + (int)rank) * 4 + q;   // column-partial row (EPI_BAD_BWD)
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c, ++cidx) {
         const int col = nb * kBN + chalf * (kBN / 2) + c * CW;
-        const int buf = cidx & 1;
+        // staging buffers of this chunk: [buf] (and [buf + 1] for EPI_BAD_FWD's A1)
+        const int buf = kNBuf == 4 ? 2 * (cidx & 1) : (cidx & 1);
         unsigned char* sb = stg + buf * kStg;
+        unsigned char* sb2 = stg + (kNBuf == 4 ? buf + 1 : buf ^ 1) * kStg;
         float v[CW];
-        const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * (kBN / 2) + c * CW;
+        const uint32_t taddr =
+            tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * (kBN / 2) + c * CW;
         if (CW == 32)
           tc::tmem_ld32(taddr, v);
         else
@@ -243,12 +381,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c == NCH - 1) {   // accumulator drained: the MMA warp may reuse it
           tc::fence_before_sync();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[as]);
+          if (lane == 0) {
+            if (CG == 2)
+              mbar_arrive_cluster(tempty_c + as * 8);
+            else
+              mbar_arrive(&tempty[as]);
+          }
         }
         // results are formed in registers first, so the stores issued from the staging
-        // buffers by the previous chunk drain while this chunk computes
+        // buffers by earlier chunks drain while this chunk computes
         uint4 o0[4], o1[4];
-        if (aux) mbar_wait(&xb[buf], (cidx >> 1) & 1);
+        if (aux) mbar_wait(&xb[cidx & 1], (cidx >> 1) & 1);
         if (EPI == EPI_STORE) {
           if (p.bias != nullptr) {
 #pragma unroll
@@ -294,9 +437,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         if (EPI != EPI_BAD_BWD) {
           if (!aux) {
-            // the stores issued from these buffers earlier must have read them
+            // the stores issued from these buffers two chunks ago must have read them
             if (lane == 0) {
-              if (EPI == EPI_BAD_FWD)
+              if (EPI == EPI_BAD_FWD && kNBuf == 2)
                 tc::bulk_wait_read<0>();
               else
                 tc::bulk_wait_read<1>();
@@ -306,8 +449,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             *reinterpret_cast<uint4*>(sb + sw64(lane, j)) = o0[j];
-            if (EPI == EPI_BAD_FWD)
-              *reinterpret_cast<uint4*>(stg + (buf ^ 1) * kStg + sw64(lane, j)) = o1[j];
+            if (EPI == EPI_BAD_FWD) *reinterpret_cast<uint4*>(sb2 + sw64(lane, j)) = o1[j];
           }
         } else {   // EPI_BAD_BWD
           // dh = keep ? acc * s * act'(h) : 0, written over h in the staging buffer
@@ -331,14 +473,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[i] = keep + __shfl_xor_sync(0xFFFFFFFFu, send, s);
             }
           }
-          if (col + lane < p.N)
-            p.partials[(int64_t)(mb * 4 + q) * p.N + col + lane] = v[0];
+          if (col + lane < p.N) p.partials[(int64_t)prow * p.N + col + lane] = v[0];
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           tc::tma_store_2d(&mapC, sb, col, out_row0);
-          if (EPI == EPI_BAD_FWD) tc::tma_store_2d(&mapC2, stg + (buf ^ 1) * kStg, col, row0);
+          if (EPI == EPI_BAD_FWD) tc::tma_store_2d(&mapC2, sb2, col, row0);
           tc::bulk_commit();
           if (aux) {
             // prefetch the next chunk's auxiliary tile into the other buffer once the store
@@ -346,11 +487,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             int nu = u, nc = c + 1;
             if (nc == NCH) {
               nc = 0;
-              nu = u + gridDim.x;
+              nu = u + ncl;
             }
             if (nu < p.units) {
               tc::bulk_wait_read<1>();
-              issue_aux(nu, nc, buf ^ 1);
+              issue_aux(nu, nc, (cidx + 1) & 1);
             }
           }
         }
@@ -362,8 +503,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
   tc::fence_before_sync();
-  __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+  if (CG == 2) {
+    cluster_sync();   // both CTAs done with the pair's TMEM and barriers
+    if (warp == 1)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                   : "memory");
+  } else {
+    __syncthreads();
+    if (warp == 1) tc::tmem_dealloc(tmem, 512);
+  }
 }
 
 // split-K partial slabs [splits][M][N] fp32 -> C, summed in split order (deterministic)
@@ -401,20 +549,35 @@ bool map2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_t o
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int AMN, int BMN, int OUTF32, int EPI, int ACT>
+template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
 cudaError_t launch_t(int grid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                      const CUtensorMap& c2, const CUtensorMap& x, const wg::Params& p,
                      cudaStream_t st) {
-  auto kern = wg::wgemm_kernel<AMN, BMN, OUTF32, EPI, ACT>;
+  auto kern = wg::wgemm_kernel<CG, AMN, BMN, OUTF32, EPI, ACT>;
+  constexpr size_t smem = wg::Cfg<CG, EPI>::kSmem;
   static bool attr = false;   // per instantiation
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wg::kSmem);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<grid, wg::kThreads, wg::kSmem, st>>>(a, b, c, c2, x, p);
-  return cudaGetLastError();
+  if (CG == 1) {
+    kern<<<grid, wg::kThreads, smem, st>>>(a, b, c, c2, x, p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(wg::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a, b, c, c2, x, p);
 }
 }  // namespace
 
@@ -433,14 +596,18 @@ bool wgemm_supported(const WgemmArgs& g) {
   }
 }
 
+// CTA pairs (256-row tiles) unless the caller asked for single CTAs or the problem is a
+// single 128-row block
+static int pick_cg(const WgemmArgs& g) { return g.cg == 1 || g.M <= wg::kBM ? 1 : 2; }
+
 // split count for an fp32 output: minimise (waves x k-blocks per split) + the reduce pass
-static int choose_splits(int tiles, int nk, int num_sms, int64_t MN) {
+static int choose_splits(int tiles, int nk, int slots, int64_t MN) {
   int best = 1;
   double best_cost = 1e300;
   for (int s = 1; s <= 8; ++s) {
     const int kbs = (nk + s - 1) / s;
     if (s > 1 && (kbs < 4 || (int64_t)(s - 1) * kbs >= nk)) break;
-    const double waves = (double)((tiles * s + num_sms - 1) / num_sms);
+    const double waves = (double)((tiles * s + slots - 1) / slots);
     // one k-block of one tile ~ 0.3 us of MMA; the reduce reads s+1 slabs of M*N fp32 at
     // ~4 TB/s (mostly L2-resident)
     const double cost = waves * kbs * 0.3 + (s > 1 ? (double)(s + 1) * MN * 4 / 4.0e6 : 0.0);
@@ -452,28 +619,43 @@ static int choose_splits(int tiles, int nk, int num_sms, int64_t MN) {
   return best;
 }
 
-size_t wgemm_ws_bytes(int M, int N, int K, int num_sms) {
-  const int tiles = ((M + wg::kBM - 1) / wg::kBM) * ((N + wg::kBN - 1) / wg::kBN);
-  const int nk = (K + wg::kBK - 1) / wg::kBK;
-  const int s = choose_splits(tiles, nk, num_sms, (int64_t)M * N);
-  return s > 1 ? (size_t)s * M * N * sizeof(float) : 0;
+namespace {
+struct Plan {
+  int cg, tiles_m, tiles_n, nk, splits;
+};
+Plan plan_of(const WgemmArgs& g, int num_sms) {
+  Plan P;
+  P.cg = pick_cg(g);
+  P.tiles_m = (g.M + wg::kBM * P.cg - 1) / (wg::kBM * P.cg);
+  P.tiles_n = (g.N + wg::kBN - 1) / wg::kBN;
+  P.nk = (g.K + wg::kBK - 1) / wg::kBK;
+  P.splits = 1;
+  if (g.epi == EPI_STORE && g.out_f32 && g.ws)
+    P.splits = choose_splits(P.tiles_m * P.tiles_n, P.nk, num_sms / P.cg, (int64_t)g.M * g.N);
+  // the partial slabs are stacked along M: only whole M tiles keep them apart
+  if (P.splits > 1 && (g.M % (wg::kBM * P.cg) ||
+                       g.ws_bytes < (size_t)P.splits * g.M * g.N * sizeof(float)))
+    P.splits = 1;
+  return P;
+}
+}  // namespace
+
+int wgemm_partial_rows(const WgemmArgs& g) {
+  const int cg = pick_cg(g);
+  return ((g.M + wg::kBM * cg - 1) / (wg::kBM * cg)) * cg * 4;
 }
 
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (!wgemm_supported(g)) return cudaErrorInvalidValue;
+  const Plan P = plan_of(g, num_sms);
   wg::Params p{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
-  p.tiles_m = (g.M + wg::kBM - 1) / wg::kBM;
-  p.tiles_n = (g.N + wg::kBN - 1) / wg::kBN;
-  p.nk = (g.K + wg::kBK - 1) / wg::kBK;
-  p.splits = 1;
-  if (g.epi == EPI_STORE && g.out_f32 && g.ws)
-    p.splits = choose_splits(p.tiles_m * p.tiles_n, p.nk, num_sms, (int64_t)g.M * g.N);
-  // the partial slabs are stacked along M: only whole M tiles keep them apart
-  if (p.splits > 1 && (g.M % wg::kBM || g.ws_bytes < (size_t)p.splits * g.M * g.N * sizeof(float)))
-    p.splits = 1;
+  p.tiles_m = P.tiles_m;
+  p.tiles_n = P.tiles_n;
+  p.nk = P.nk;
+  p.splits = P.splits;
   p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
   p.units = p.tiles_m * p.tiles_n * p.splits;
   p.beta = g.beta;
@@ -485,11 +667,13 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   CUtensorMap ma, mb, mc, mc2, mx;
   bool ok = true;
   const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B, SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
-  // A: K-major [M][K] (box 64 x 128) or MN-major [K][M] (box 64 x 64, two per stage)
+  // A: K-major [M][K] (box 64 x 128) or MN-major [K][M] (box 64 x 64, two per stage);
+  // B: this CTA's 256/CG columns the same way
+  const uint32_t bcols = wg::kBN / P.cg;
   ok &= g.a_mn ? map2d(&ma, g.A, false, g.M, g.K, g.lda, 64, 64, SW128)
                : map2d(&ma, g.A, false, g.K, g.M, g.lda, 64, wg::kBM, SW128);
   ok &= g.b_mn ? map2d(&mb, g.B, false, g.N, g.K, g.ldb, 64, 64, SW128)
-               : map2d(&mb, g.B, false, g.K, g.N, g.ldb, 64, wg::kBN, SW128);
+               : map2d(&mb, g.B, false, g.K, g.N, g.ldb, 64, bcols, SW128);
   const bool f32 = g.out_f32 != 0;
   const uint32_t cw = f32 ? 16 : 32;
   if (p.splits > 1)
@@ -503,10 +687,16 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (g.beta) ok &= map2d(&mx, g.C, false, g.N, g.M, g.ldc, 32, 32, SW64);
   if (!ok) return cudaErrorInvalidValue;
 
-  const int grid = p.units < num_sms ? p.units : num_sms;
+  const int slots = num_sms / P.cg;
+  const int grid = (p.units < slots ? p.units : slots) * P.cg;
   cudaError_t e = cudaErrorInvalidValue;
-#define WG_LAUNCH(AM, BM, OF, EP, AC) \
-  e = launch_t<AM, BM, OF, EP, AC>(grid, ma, mb, mc, mc2, mx, p, st)
+#define WG_LAUNCH1(CG, AM, BM, OF, EP, AC) \
+  e = launch_t<CG, AM, BM, OF, EP, AC>(grid, ma, mb, mc, mc2, mx, p, st)
+#define WG_LAUNCH(AM, BM, OF, EP, AC)            \
+  do {                                           \
+    if (P.cg == 2) WG_LAUNCH1(2, AM, BM, OF, EP, AC); \
+    else WG_LAUNCH1(1, AM, BM, OF, EP, AC);       \
+  } while (0)
   if (g.epi == EPI_STORE) {
     if (!g.a_mn && !g.b_mn && !f32) WG_LAUNCH(0, 0, 0, EPI_STORE, 0);
     else if (!g.a_mn && g.b_mn && !f32) WG_LAUNCH(0, 1, 0, EPI_STORE, 0);
@@ -521,6 +711,7 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
     ENC_ACT_DISPATCH(g.act, WG_LAUNCH(0, 1, 0, EPI_BAD_BWD, ACT));
   }
 #undef WG_LAUNCH
+#undef WG_LAUNCH1
   if (e != cudaSuccess || p.splits == 1) return e;
   const int64_t n4 = (int64_t)g.M * g.N / 4;
   int64_t blocks = (n4 + 255) / 256;
@@ -531,12 +722,7 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
 }
 
 int wgemm_launches(const WgemmArgs& g, int num_sms) {
-  if (g.epi != EPI_STORE || !g.out_f32 || !g.ws) return 1;
-  const int tiles = ((g.M + wg::kBM - 1) / wg::kBM) * ((g.N + wg::kBN - 1) / wg::kBN);
-  const int nk = (g.K + wg::kBK - 1) / wg::kBK;
-  const int s = choose_splits(tiles, nk, num_sms, (int64_t)g.M * g.N);
-  return s > 1 && g.M % wg::kBM == 0 && g.ws_bytes >= (size_t)s * g.M * g.N * sizeof(float) ? 2
-                                                                                              : 1;
+  return plan_of(g, num_sms).splits > 1 ? 2 : 1;
 }
 
 }  // namespace enc

@@ -24,9 +24,13 @@ def ops():
     return _ops
 
 
-@pytest.fixture(scope="module")
-def ctx(ops):
-    return ops.Context(0)
+@pytest.fixture(scope="module", params=[1, 0], ids=["pair", "single"])
+def ctx(ops, request):
+    """Both tile schedules: 256 x 256 tiles on CTA pairs (tcgen05.mma.cta_group::2, the
+    default) and 128 x 256 tiles on single CTAs (ENC_OPT_GEMM_PAIR = 0)."""
+    c = ops.Context(0)
+    ops.enc_set_option(c, ops.OPT_GEMM_PAIR, request.param)
+    return c
 
 
 def bf(a):
@@ -48,7 +52,7 @@ def _fp32_close(name, g, o):
 
 
 SHAPES = [(128, 256, 64), (256, 512, 128), (300, 264, 200), (120, 72, 40), (512, 768, 1024),
-          (1000, 1032, 520)]
+          (1000, 1032, 520), (384, 256, 64)]
 
 
 @pytest.mark.parametrize("M,N,K", SHAPES)
@@ -79,7 +83,8 @@ def test_dx_form(ops, ctx, M, N, K, beta):
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 304), (264, 136, 520),
-                                   (1024, 1024, 4096), (768, 768, 2048), (384, 1024, 4096)])
+                                   (1024, 1024, 4096), (768, 768, 2048), (384, 1024, 4096),
+                                   (512, 256, 8192)])
 def test_dw_form(ops, ctx, M, N, K):
     """dW = dY^T X: A = dY [K,M] MN-major, B = X [K,N] MN-major, fp32 output (split over K
     into the context workspace and summed in a fixed order when that fills more SMs)."""
@@ -141,7 +146,8 @@ def test_config_L_shapes_sampled(ops, ctx):
 
 
 # ------------------------------------------------------------------ fused FFN kernels
-FFN_SHAPES = [(2, 64, 64, 256), (3, 40, 48, 264), (1, 128, 1024, 4096), (2, 100, 96, 520)]
+FFN_SHAPES = [(2, 64, 64, 256), (3, 40, 48, 264), (1, 128, 1024, 4096), (2, 100, 96, 520),
+              (2, 384, 256, 512)]
 
 
 @pytest.mark.parametrize("B,J,I,U", FFN_SHAPES)
