@@ -36,7 +36,8 @@ namespace enc {
 namespace wg {
 
 constexpr int kBM = 128, kBN = 256, kBK = 64;   // per-CTA accumulator tile 128 x 256
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter
+constexpr int kSliceCols = kBN / (kEpiWarps / 4);  // accumulator columns per epilogue warp
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kABytes = kBM * kBK * 2;   // 16 KB per stage
 constexpr uint32_t kStg = 32 * 64;            // one [32 rows x 64 B] staging buffer
@@ -50,8 +51,8 @@ constexpr uint32_t kStg = 32 * 64;            // one [32 rows x 64 B] staging bu
 template <int CG, int EPI>
 struct Cfg {
   static constexpr uint32_t kBBytes = (kBN / CG) * kBK * 2;
-  static constexpr int kStages = CG == 2 ? (EPI == EPI_BAD_FWD ? 4 : 6) : 4;
-  static constexpr int kNBuf = (CG == 2 && EPI == EPI_BAD_FWD) ? 4 : 2;   // staging / warp
+  static constexpr int kStages = CG == 2 ? 5 : 3;
+  static constexpr int kNBuf = 2;   // staging buffers per epilogue warp
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) +
                                   (size_t)kEpiWarps * kNBuf * kStg + 256;
 };
@@ -331,9 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
     const int q = warp & 3;            // TMEM lane quarter this warp may access
-    const int chalf = ew >> 2;         // column half of the 256-wide tile
+    const int chalf = ew >> 2;         // column slice of the 256-wide tile
     constexpr int CW = OUTF32 ? 16 : 32;   // columns per 64-byte chunk
-    constexpr int NCH = (kBN / 2) / CW;
+    constexpr int NCH = kSliceCols / CW;
     unsigned char* stg = sStg + ew * kNBuf * kStg;
     uint64_t* xb = xbar + 2 * ew;
     const bool aux = kAux || p.beta;
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int mb, nb, sp;
       decode(p, u, mb, nb, sp);
       row0 = mb * kBM * CG + rank * kBM + q * 32;
-      col = nb * kBN + chalf * (kBN / 2) + c * CW;
+      col = nb * kBN + chalf * kSliceCols + c * CW;
     };
     auto issue_aux = [&](int u, int c, int buf) {
       int row0, col;
@@ -366,14 +367,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int prow = (mb * CG + (int)rank) * 4 + q;   // column-partial row (EPI_BAD_BWD)
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c, ++cidx) {
-        const int col = nb * kBN + chalf * (kBN / 2) + c * CW;
-        // staging buffers of this chunk: [buf] (and [buf + 1] for EPI_BAD_FWD's A1)
-        const int buf = kNBuf == 4 ? 2 * (cidx & 1) : (cidx & 1);
+        const int col = nb * kBN + chalf * kSliceCols + c * CW;
+        // staging buffer of this chunk (EPI_BAD_FWD: both, h and A1)
+        const int buf = cidx & 1;
         unsigned char* sb = stg + buf * kStg;
-        unsigned char* sb2 = stg + (kNBuf == 4 ? buf + 1 : buf ^ 1) * kStg;
+        unsigned char* sb2 = stg + (buf ^ 1) * kStg;
         float v[CW];
         const uint32_t taddr =
-            tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * (kBN / 2) + c * CW;
+            tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * kSliceCols + c * CW;
         if (CW == 32)
           tc::tmem_ld32(taddr, v);
         else
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!aux) {
             // the stores issued from these buffers two chunks ago must have read them
             if (lane == 0) {
-              if (EPI == EPI_BAD_FWD && kNBuf == 2)
+              if (EPI == EPI_BAD_FWD)
                 tc::bulk_wait_read<0>();
               else
                 tc::bulk_wait_read<1>();
