@@ -27,7 +27,6 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdlib.h>
 
 #include "act.cuh"
 #include "kernels.h"
@@ -67,12 +66,6 @@ struct Params {
   PhiloxKey pk;           // BAD epilogues (site 2)
   int64_t g0;             // Philox chunk index of element (0, 0): batch_offset * J * N / 8
   float* partials;        // EPI_BAD_BWD: [ceil(M/128) * 4][N] column partial sums of dh
-  // outputs, written by the epilogue warps with 16-B stores (lsu_store) or by TMA
-  char* C;                // output (split-K: slab 0 of the workspace)
-  int64_t ldc_b, slab_b;  // row stride, split-K slab stride (bytes)
-  char* C2;               // EPI_BAD_FWD: A1
-  int64_t ldc2_b;
-  int lsu_store;
 };
 
 // byte offset of 16-B chunk c (0..3) of row r in a [32 x 64 B] SWIZZLE_64B tile
@@ -155,20 +148,6 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       " [%0], %1;" ::"r"(smem_u32(bar)),
       "h"((uint16_t)3)
       : "memory");
-}
-
-// Store a [32 rows x 64 B] SWIZZLE_64B staging tile to global memory with 16-B stores, eight
-// rows per warp instruction (each row's 64 B contiguous): no TMA request per row, so the
-// tensor-map unit stays free for the operand loads
-__device__ __forceinline__ void store_tile_lsu(const unsigned char* sb, char* base, int64_t ld_b,
-                                               int row0, int colb, int M, int Nb, int lane) {
-#pragma unroll
-  for (int pass = 0; pass < 4; ++pass) {
-    const int r = pass * 8 + (lane >> 2), pc = lane & 3;
-    const uint4 val = *reinterpret_cast<const uint4*>(sb + sw64(r, pc));
-    if (row0 + r < M && colb + pc * 16 < Nb)
-      *reinterpret_cast<uint4*>(base + (int64_t)(row0 + r) * ld_b + colb + pc * 16) = val;
-  }
 }
 
 // unit -> (m block, n block, split); m fastest so concurrent CTAs share B tiles in L2
@@ -458,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (EPI != EPI_BAD_BWD) {
-          if (!aux && !p.lsu_store) {
+          if (!aux) {
             // the stores issued from these buffers two chunks ago must have read them
             if (lane == 0) {
               if (EPI == EPI_BAD_FWD)
@@ -496,26 +475,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           if (col + lane < p.N) p.partials[(int64_t)prow * p.N + col + lane] = v[0];
-        }
-        if (p.lsu_store) {
-          __syncwarp();
-          constexpr int es = OUTF32 ? 4 : 2;
-          store_tile_lsu(sb, p.C + sp * p.slab_b, p.ldc_b, row0, col * es, p.M, p.N * es, lane);
-          if (EPI == EPI_BAD_FWD) store_tile_lsu(sb2, p.C2, p.ldc2_b, row0, col * 2, p.M, p.N * 2, lane);
-          __syncwarp();   // staging read back before the next chunk (or aux load) reuses it
-          if (aux && lane == 0) {
-            int nu = u, nc = c + 1;
-            if (nc == NCH) {
-              nc = 0;
-              nu = u + ncl;
-            }
-            if (nu < p.units) {
-              fence_proxy_async_smem();
-              issue_aux(nu, nc, (cidx + 1) & 1);
-            }
-          }
-          __syncwarp();
-          continue;
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -705,25 +664,6 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   p.pk = g.pk;
   p.g0 = g.g0;
   p.partials = g.partials;
-  {
-    static const int tma_store = [] {
-      const char* e = getenv("ENC_WGEMM_TMA_STORE");
-      return e && e[0] == '1' ? 1 : 0;
-    }();
-    p.lsu_store = !tma_store;
-  }
-  const int esz = g.out_f32 ? 4 : 2;
-  if (P.splits > 1) {
-    p.C = (char*)g.ws;
-    p.ldc_b = (int64_t)g.N * 4;
-    p.slab_b = (int64_t)g.M * g.N * 4;
-  } else {
-    p.C = (char*)g.C;
-    p.ldc_b = g.ldc * esz;
-    p.slab_b = 0;
-  }
-  p.C2 = (char*)g.C2;
-  p.ldc2_b = g.ldc2 * 2;
 
   CUtensorMap ma, mb, mc, mc2, mx;
   bool ok = true;
