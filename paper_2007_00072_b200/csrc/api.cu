@@ -58,7 +58,8 @@ struct enc_ctx {
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   int gemm_tc = 1;
   int gemm_cg = 0;           // ENC_OPT_GEMM_PAIR 1 (default) -> 0 (auto), 0 -> 1 (single CTAs)
-  void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
+  void* wg_ws = nullptr;     // stream-K workspace of the tcgen05 weight contractions
+  void* wg_ws_side = nullptr;   // the same for contractions on the side stream
   size_t wg_ws_bytes = 0;
   // forward -> backward contract: the path flags each `saved` buffer was written with
   std::mutex mu;
@@ -162,7 +163,7 @@ static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool 
     g.C = C; g.ldc = ldc; g.out_f32 = out_dt == ENC_FP32 ? 1 : 0;
     g.beta = beta != 0.f ? 1 : 0;
     g.bias = bias;
-    g.ws = ctx->wg_ws;
+    g.ws = lt_ws ? ctx->wg_ws_side : ctx->wg_ws;   // lt_ws set: the side stream's call
     g.ws_bytes = ctx->wg_ws_bytes;
     g.cg = ctx->gemm_cg;
     if (wgemm_supported(g)) {
@@ -234,8 +235,11 @@ int enc_create(enc_ctx** out, int device) {
   e = cudaMalloc(&c->blas_ws, c->blas_ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->red, c->red_floats * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&c->side_ws, c->blas_ws_bytes);
-  c->wg_ws_bytes = 32u << 20;
+  c->wg_ws_bytes = wgemm_ws_bytes(c->num_sms);
   if (e == cudaSuccess) e = cudaMalloc(&c->wg_ws, c->wg_ws_bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&c->wg_ws_side, c->wg_ws_bytes);
+  if (e == cudaSuccess) e = cudaMemset(c->wg_ws, 0, kWgemmFlagBytes);
+  if (e == cudaSuccess) e = cudaMemset(c->wg_ws_side, 0, kWgemmFlagBytes);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   if (cublasSetWorkspace(c->blas, c->blas_ws, c->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS ||
       cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
@@ -304,6 +308,7 @@ void enc_destroy(enc_ctx* c) {
   if (c->blas_ws) cudaFree(c->blas_ws);
   if (c->red) cudaFree(c->red);
   if (c->wg_ws) cudaFree(c->wg_ws);
+  if (c->wg_ws_side) cudaFree(c->wg_ws_side);
   delete c;
 }
 
@@ -439,9 +444,11 @@ static inline char* at(void* base, size_t off) { return (char*)base + off; }
 // M = 0 (rejected by wgemm_supported) when that path is off for this call
 static WgemmArgs ffn_fwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
                               const enc_cfg* cfg, const void* X1, const void* W1, const float* b1,
-                              const PhiloxKey& pk, void* h, void* A1) {
+                              const PhiloxKey& pk, void* h, void* A1, bool force = false) {
   WgemmArgs g;
-  if (!ctx->gemm_tc || dtype != ENC_BF16) return g;
+  if ((!ctx->gemm_tc && !force) || dtype != ENC_BF16) return g;
+  g.ws = ctx->wg_ws;
+  g.ws_bytes = ctx->wg_ws_bytes;
   g.M = d->B * d->J; g.N = d->U; g.K = d->I;
   g.A = X1; g.lda = d->I;
   g.B = W1; g.ldb = d->I;
@@ -457,9 +464,11 @@ static WgemmArgs ffn_fwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
 }
 static WgemmArgs ffn_bwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
                               const enc_cfg* cfg, const void* dY2, const void* W2, const void* h,
-                              const PhiloxKey& pk, void* dh, float* partials) {
+                              const PhiloxKey& pk, void* dh, float* partials, bool force = false) {
   WgemmArgs g;
-  if (!ctx->gemm_tc || dtype != ENC_BF16) return g;
+  if ((!ctx->gemm_tc && !force) || dtype != ENC_BF16) return g;
+  g.ws = ctx->wg_ws;
+  g.ws_bytes = ctx->wg_ws_bytes;
   g.M = d->B * d->J; g.N = d->U; g.K = d->I;
   g.A = dY2; g.lda = d->I;
   g.B = W2; g.ldb = d->U; g.b_mn = 1;
@@ -875,11 +884,9 @@ int enc_linear1_bad_fwd(enc_ctx* ctx, int B, int J, int I, int U, const void* X1
   enc_cfg cfg{};
   cfg.act = act;
   cfg.batch_offset = batch_offset;
-  enc_ctx tmp_gate;   // the fused path regardless of ENC_OPT_GEMM_TC
-  tmp_gate.gemm_tc = 1;
-  tmp_gate.gemm_cg = ctx->gemm_cg;
-  WgemmArgs g = ffn_fwd_args(&tmp_gate, &d, ENC_BF16, &cfg, X1, W1, b1,
-                             make_philox_key(p, seed, subseq), h, A1);
+  // the fused kernel regardless of ENC_OPT_GEMM_TC
+  WgemmArgs g = ffn_fwd_args(ctx, &d, ENC_BF16, &cfg, X1, W1, b1,
+                             make_philox_key(p, seed, subseq), h, A1, true);
   if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
   OpTimer _t(ctx, ENC_OP_GEMM_L1, (cudaStream_t)stream, 1);
   CK(launch_wgemm(g, ctx->num_sms, (cudaStream_t)stream));
@@ -898,11 +905,8 @@ int enc_linear2_dx_bad_bwd(enc_ctx* ctx, int B, int J, int I, int U, const void*
   enc_cfg cfg{};
   cfg.act = act;
   cfg.batch_offset = batch_offset;
-  enc_ctx tmp_gate;
-  tmp_gate.gemm_tc = 1;
-  tmp_gate.gemm_cg = ctx->gemm_cg;
-  WgemmArgs g = ffn_bwd_args(&tmp_gate, &d, ENC_BF16, &cfg, dY2, W2, h,
-                             make_philox_key(p, seed, subseq), dh, ctx->red);
+  WgemmArgs g = ffn_bwd_args(ctx, &d, ENC_BF16, &cfg, dY2, W2, h,
+                             make_philox_key(p, seed, subseq), dh, ctx->red, true);
   const int R = wgemm_partial_rows(g);
   if ((size_t)R * U > ctx->red_floats) return ENC_EUNSUPPORTED;
   if (!wgemm_supported(g)) return ENC_EUNSUPPORTED;
