@@ -835,6 +835,11 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   return ENC_EINVAL;
 }
 
+int enc_debug_wgemm_trace(unsigned long long* host) {
+  enc::wgemm_trace_read(host);
+  return 0;
+}
+
 int enc_wgemm(enc_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int tA,
               const void* B, int64_t ldb, int tB, void* C, int64_t ldc, int c_dtype, int beta,
               const float* bias, enc_stream_t stream) {

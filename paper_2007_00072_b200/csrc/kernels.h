@@ -178,7 +178,8 @@ size_t wgemm_ws_bytes(int num_sms);
 bool wgemm_supported(const WgemmArgs& g);
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st);
 int wgemm_launches(const WgemmArgs& g, int num_sms);   // kernels launch_wgemm launches
-int wgemm_partial_rows(const WgemmArgs& g);            // EPI_BAD_BWD partial rows written
+int wgemm_partial_rows(const WgemmArgs& g);
+void wgemm_trace_read(unsigned long long* host);            // EPI_BAD_BWD partial rows written
 
 // cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
 CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,

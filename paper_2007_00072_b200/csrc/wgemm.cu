@@ -27,6 +27,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "act.cuh"
 #include "kernels.h"
@@ -34,6 +36,14 @@
 
 namespace enc {
 namespace wg {
+__device__ unsigned long long g_trace[256 * 16];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define WG_TRACE(slot) \
+  do { if (ew == 0 && lane == 0 && it < 6) g_trace[blockIdx.x * 16 + (slot)] = gtime(); } while (0)
 
 constexpr int kBM = 128, kBN = 256, kBK = 64;   // per-CTA accumulator tile 128 x 256
 constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter
@@ -214,6 +224,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;   // 0 = the pair's MMA issuer
   const int cid = blockIdx.x / CG;             // stream-K worker: a CTA or a CTA pair
+  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 15] = gtime();
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&mapA);
@@ -379,7 +390,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::tma_load_2d(stg + buf * kStg, &mapX, &xb[buf], col, row0);
     };
     constexpr int kArrivals = kEpiWarps * CG;   // epilogue warps of a worker
-    const int64_t part_row = (int64_t)(rank * kBM + q * 32 + lane) * kBN;   // this thread's row
     uint32_t cidx = 0;   // epilogue chunks of this warp (buffer parity, aux barrier phase)
     SegIter si = seg_begin(p, cid);
     if (aux && lane == 0) {   // the first segment with an epilogue: k0 == 0
@@ -396,18 +406,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int as = it & 1;
       mbar_wait_sleep(&tfull[as], (it >> 1) & 1, 20000u);
       tc::fence_after_sync();
+      WG_TRACE(2 * it);
       const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * kSliceCols;
       if (k0 != 0) {
-        // tail of a tile: publish the fp32 partial sum for the worker owning its head
-        float* dst = p.sk_part + (int64_t)cid * (kBM * CG * kBN) + part_row + chalf * kSliceCols;
+        // tail of a tile: publish the fp32 partial sum for the worker owning its head, in a
+        // thread-major layout (float4 i of lane l of warp ew at [(rank, ew, i)][l]) that the
+        // head's epilogue thread with the same role reads back: 512 contiguous bytes per
+        // warp instruction
+        float4* dst = reinterpret_cast<float4*>(p.sk_part) +
+                      (int64_t)cid * (kBM * CG * kBN / 4) +
+                      (int64_t)((rank * kEpiWarps + ew) * (kSliceCols / 4)) * 32 + lane;
 #pragma unroll 1
         for (int c = 0; c < kSliceCols / 16; ++c) {
           float v[16];
           tc::tmem_ld16(tbase + c * 16, v);
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            __stcg(reinterpret_cast<float4*>(dst + c * 16) + j,
-                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+            dst[(c * 4 + j) * 32] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
         }
         tc::fence_before_sync();
         __threadfence();
@@ -419,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&tempty[as]);
           atomicAdd(p.sk_flag + cid, 1);
         }
+        WG_TRACE(2 * it + 1);
         continue;
       }
       // head of the tile: the workers after this one that hold its other k-blocks
@@ -438,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         __syncwarp();
+        if (ew == 0 && lane == 0) g_trace[blockIdx.x * 16 + 14] = gtime();
       }
       const int row0 = mb * kBM * CG + rank * kBM + q * 32;
       const int row = row0 + lane;
@@ -466,11 +483,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // the other workers' partial sums of this tile, in worker order
         for (int j = cid + 1; j < jend; ++j) {
-          const float4* src = reinterpret_cast<const float4*>(
-              p.sk_part + (int64_t)j * (kBM * CG * kBN) + part_row + chalf * kSliceCols + c * CW);
+          const float4* src = reinterpret_cast<const float4*>(p.sk_part) +
+                              (int64_t)j * (kBM * CG * kBN / 4) +
+                              (int64_t)((rank * kEpiWarps + ew) * (kSliceCols / 4) + c * (CW / 4)) *
+                                  32 + lane;
 #pragma unroll
           for (int i = 0; i < CW / 4; ++i) {
-            const float4 w4 = __ldcg(src + i);
+            const float4 w4 = src[i * 32];
             v[4 * i] += w4.x;
             v[4 * i + 1] += w4.y;
             v[4 * i + 2] += w4.z;
@@ -591,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
       }
       (void)row;
+      WG_TRACE(2 * it + 1);
       // release the partials this tile consumed: the last of the worker's warps resets the
       // flags for the next launch
       if (lane == 0)
@@ -633,18 +653,50 @@ bool map2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_t o
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Workers (CTAs, or CTA pairs for CG = 2) of this instantiation that can be resident at
+// once: the stream-K schedule needs every worker resident (a head waits for the partials of
+// the workers after it), and not every SM pair can host a cluster of two
+template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
+int resident_workers(int num_sms) {
+  auto kern = wg::wgemm_kernel<CG, AMN, BMN, OUTF32, EPI, ACT>;
+  constexpr size_t smem = wg::Cfg<CG, EPI>::kSmem;
+  static int cached = -1;   // per instantiation (one device per process)
+  if (cached >= 0) return cached;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return 0;
+  if (CG == 1) {
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, wg::kThreads, smem) !=
+        cudaSuccess)
+      return 0;
+    cached = per * num_sms;
+    return cached;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms, 1, 1);
+  cfg.blockDim = dim3(wg::kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return 0;
+  if (getenv("ENC_WGEMM_DEBUG")) fprintf(stderr, "wgemm: %d resident CTA pairs\n", n);
+  cached = n;
+  return cached;
+}
+
 template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
 cudaError_t launch_t(int grid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                      const CUtensorMap& c2, const CUtensorMap& x, const wg::Params& p,
                      cudaStream_t st) {
   auto kern = wg::wgemm_kernel<CG, AMN, BMN, OUTF32, EPI, ACT>;
   constexpr size_t smem = wg::Cfg<CG, EPI>::kSmem;
-  static bool attr = false;   // per instantiation
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   if (CG == 1) {
     kern<<<grid, wg::kThreads, smem, st>>>(a, b, c, c2, x, p);
     return cudaGetLastError();
@@ -718,6 +770,10 @@ int wgemm_partial_rows(const WgemmArgs& g) {
   return ((g.M + wg::kBM * cg - 1) / (wg::kBM * cg)) * cg * 4;
 }
 
+void wgemm_trace_read(unsigned long long* host) {
+  cudaMemcpyFromSymbol(host, wg::g_trace, sizeof(wg::g_trace));
+}
+
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (!wgemm_supported(g)) return cudaErrorInvalidValue;
   const Plan P = plan_of(g, num_sms);
@@ -761,10 +817,14 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (g.beta) ok &= map2d(&mx, g.C, false, g.N, g.M, g.ldc, 32, 32, SW64);
   if (!ok) return cudaErrorInvalidValue;
 
-  const int grid = P.P * P.cg;
   cudaError_t e = cudaErrorInvalidValue;
-#define WG_LAUNCH1(CG, AM, BM, OF, EP, AC) \
-  e = launch_t<CG, AM, BM, OF, EP, AC>(grid, ma, mb, mc, mc2, mx, p, st)
+#define WG_LAUNCH1(CG, AM, BM, OF, EP, AC)                                      \
+  do {                                                                         \
+    const int rw = resident_workers<CG, AM, BM, OF, EP, AC>(num_sms);          \
+    if (rw < 1) return cudaErrorInvalidConfiguration;                          \
+    if (p.P > rw) p.P = rw;                                                    \
+    e = launch_t<CG, AM, BM, OF, EP, AC>(p.P * CG, ma, mb, mc, mc2, mx, p, st); \
+  } while (0)
 #define WG_LAUNCH(AM, BM, OF, EP, AC)            \
   do {                                           \
     if (P.cg == 2) WG_LAUNCH1(2, AM, BM, OF, EP, AC); \
