@@ -58,7 +58,7 @@ struct enc_ctx {
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   int gemm_tc = 1;
   int gemm_cg = 0;           // ENC_OPT_GEMM_PAIR 1 (default) -> 0 (auto), 0 -> 1 (single CTAs)
-  void* wg_ws = nullptr;     // stream-K workspace of the tcgen05 weight contractions
+  void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
   void* wg_ws_side = nullptr;   // the same for contractions on the side stream
   size_t wg_ws_bytes = 0;
   // forward -> backward contract: the path flags each `saved` buffer was written with
@@ -235,11 +235,9 @@ int enc_create(enc_ctx** out, int device) {
   e = cudaMalloc(&c->blas_ws, c->blas_ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->red, c->red_floats * sizeof(float));
   if (e == cudaSuccess) e = cudaMalloc(&c->side_ws, c->blas_ws_bytes);
-  c->wg_ws_bytes = wgemm_ws_bytes(c->num_sms);
+  c->wg_ws_bytes = 32u << 20;
   if (e == cudaSuccess) e = cudaMalloc(&c->wg_ws, c->wg_ws_bytes);
   if (e == cudaSuccess) e = cudaMalloc(&c->wg_ws_side, c->wg_ws_bytes);
-  if (e == cudaSuccess) e = cudaMemset(c->wg_ws, 0, kWgemmFlagBytes);
-  if (e == cudaSuccess) e = cudaMemset(c->wg_ws_side, 0, kWgemmFlagBytes);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   if (cublasSetWorkspace(c->blas, c->blas_ws, c->blas_ws_bytes) != CUBLAS_STATUS_SUCCESS ||
       cublasSetMathMode(c->blas, CUBLAS_DEFAULT_MATH) != CUBLAS_STATUS_SUCCESS) {
@@ -833,11 +831,6 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   return ENC_EINVAL;
-}
-
-int enc_debug_wgemm_trace(unsigned long long* host) {
-  enc::wgemm_trace_read(host);
-  return 0;
 }
 
 int enc_wgemm(enc_ctx* ctx, int M, int N, int K, const void* A, int64_t lda, int tA,

@@ -168,18 +168,13 @@ struct WgemmArgs {
   int act = 0;
   PhiloxKey pk{};
   int64_t g0 = 0;                // Philox chunk index of element (0, 0)
-  // stream-K workspace (wgemm_ws_bytes; its first kWgemmFlagBytes zeroed once, reset by
-  // every launch); one per stream that runs these kernels concurrently
-  void* ws = nullptr; size_t ws_bytes = 0;
+  void* ws = nullptr; size_t ws_bytes = 0;   // split-K slabs (fp32 EPI_STORE outputs)
   int cg = 0;                    // 0 = CTA pairs (cta_group::2) where M > 128, 1 = single CTAs
 };
-constexpr size_t kWgemmFlagBytes = 4096;
-size_t wgemm_ws_bytes(int num_sms);
 bool wgemm_supported(const WgemmArgs& g);
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st);
 int wgemm_launches(const WgemmArgs& g, int num_sms);   // kernels launch_wgemm launches
-int wgemm_partial_rows(const WgemmArgs& g);
-void wgemm_trace_read(unsigned long long* host);            // EPI_BAD_BWD partial rows written
+int wgemm_partial_rows(const WgemmArgs& g);            // EPI_BAD_BWD partial rows written
 
 // cuTensorMapEncodeTiled resolved at run time (tmap.cu): the library does not link libcuda.
 CUresult tmap_encode_tiled(CUtensorMap* map, CUtensorMapDataType dtype, cuuint32_t rank,

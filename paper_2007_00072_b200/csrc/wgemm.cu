@@ -27,8 +27,6 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <stdio.h>
-#include <stdlib.h>
 
 #include "act.cuh"
 #include "kernels.h"
@@ -36,14 +34,6 @@
 
 namespace enc {
 namespace wg {
-__device__ unsigned long long g_trace[256 * 16];
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-#define WG_TRACE(slot) \
-  do { if (ew == 0 && lane == 0 && it < 6) g_trace[blockIdx.x * 16 + (slot)] = gtime(); } while (0)
 
 constexpr int kBM = 128, kBN = 256, kBK = 64;   // per-CTA accumulator tile 128 x 256
 constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter
@@ -69,14 +59,8 @@ struct Cfg {
 
 struct Params {
   int M, N, K;
-  int tiles_m, tiles_n, tiles, nk;      // tiles of (128 CG) x 256 outputs, k-blocks of 64
-  // stream-K schedule: worker w (a CTA or CTA pair) owns the k-block range
-  // [w T / P, (w+1) T / P) of the T = tiles * nk (tile, k-block) units in tile-major order
-  int P;
-  int64_t T;
-  float* sk_part;         // [P][128 CG][256] fp32: the partial sum of worker w's first segment
-  int* sk_flag;           // [P] arrivals of worker w's epilogue warps on its published partial
-  int* sk_done;           // [P] arrivals of the finishing worker's warps that consumed it
+  int tiles_m, tiles_n, splits, units;   // tiles of (128 CG) x 256; units = tiles x splits
+  int kb_per_split, nk;
   int beta;               // EPI_STORE: out = acc (+ bias) + out (bf16 output)
   const float* bias;      // [N] fp32 or null (EPI_STORE, EPI_BAD_FWD: b1)
   PhiloxKey pk;           // BAD epilogues (site 2)
@@ -166,35 +150,12 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
       : "memory");
 }
 
-// tile -> (m block, n block); m fastest so concurrent CTAs share B tiles in L2
-__device__ __forceinline__ void decode(const Params& p, int t, int& mb, int& nb) {
+// unit -> (m block, n block, split); m fastest so concurrent CTAs share B tiles in L2
+__device__ __forceinline__ void decode(const Params& p, int u, int& mb, int& nb, int& sp) {
+  const int t = u % (p.tiles_m * p.tiles_n);
+  sp = u / (p.tiles_m * p.tiles_n);
   mb = t % p.tiles_m;
   nb = t / p.tiles_m;
-}
-
-// Stream-K segments.  Worker w walks its range in order; a segment is the part of one tile
-// inside it.  k0 > 0: a tail of a tile whose head another (lower) worker owns -- always the
-// worker's first segment, published as an fp32 partial for that worker.  k0 == 0, k1 < nk: the
-// head of a tile continued by the following workers -- always the worker's last segment; it
-// adds their partials in worker order (a fixed summation order: deterministic) and runs the
-// epilogue.  A worker's first segment never waits, so the waits cannot form a cycle.
-__device__ __forceinline__ int64_t sk_lo(const Params& p, int w) {
-  return (int64_t)w * p.T / p.P;
-}
-struct SegIter {
-  int64_t pos, hi;
-};
-__device__ __forceinline__ SegIter seg_begin(const Params& p, int w) {
-  return SegIter{sk_lo(p, w), sk_lo(p, w + 1)};
-}
-__device__ __forceinline__ bool seg_next(const Params& p, SegIter& it, int& t, int& k0, int& k1) {
-  if (it.pos >= it.hi) return false;
-  t = (int)(it.pos / p.nk);
-  k0 = (int)(it.pos - (int64_t)t * p.nk);
-  const int64_t end = (int64_t)(t + 1) * p.nk;
-  k1 = (int)((it.hi < end ? it.hi : end) - (int64_t)t * p.nk);
-  it.pos = (int64_t)t * p.nk + k1;
-  return true;
 }
 
 template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
@@ -223,8 +184,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;   // 0 = the pair's MMA issuer
-  const int cid = blockIdx.x / CG;             // stream-K worker: a CTA or a CTA pair
-  if (threadIdx.x == 0) g_trace[blockIdx.x * 16 + 15] = gtime();
+  const int cid = blockIdx.x / CG;             // persistent scheduler: one unit per pair
+  const int ncl = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&mapA);
@@ -263,13 +224,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t pc = 0;
-      SegIter si = seg_begin(p, cid);
-      int t, kb0, kb1;
-      while (seg_next(p, si, t, kb0, kb1)) {
-        int mb, nb;
-        decode(p, t, mb, nb);
+      for (int u = cid; u < p.units; u += ncl) {
+        int mb, nb, sp;
+        decode(p, u, mb, nb, sp);
         const int m0 = mb * kBM * CG + rank * kBM;       // this CTA's A rows
         const int n0 = nb * kBN + rank * kBNc;           // this CTA's B columns
+        const int kb0 = sp * p.kb_per_split;
+        const int kb1 = min(p.nk, kb0 + p.kb_per_split);
         for (int kb = kb0; kb < kb1; ++kb, ++pc) {
           const uint32_t s = pc % kStages;
           mbar_wait(&empty[s], ((pc / kStages) & 1) ^ 1);
@@ -318,9 +279,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kBM * CG, kBN, AMN, BMN);
       uint32_t pc = 0;
       int it = 0;
-      SegIter si = seg_begin(p, cid);
-      int t, kb0, kb1;
-      for (; seg_next(p, si, t, kb0, kb1); ++it) {
+      for (int u = cid; u < p.units; u += ncl, ++it) {
+        int mb, nb, sp;
+        decode(p, u, mb, nb, sp);
+        const int kb0 = sp * p.kb_per_split;
+        const int kb1 = min(p.nk, kb0 + p.kb_per_split);
         const int as = it & 1;
         if (CG == 2)
           mbar_wait_cluster(&tempty[as], ((it >> 1) & 1) ^ 1);
@@ -376,88 +339,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* xb = xbar + 2 * ew;
     const bool aux = kAux || p.beta;
     const uint32_t tempty_c = CG == 2 ? mapa(&tempty[0], 0) : 0;   // leader's barriers
-    // chunk c of tile t: output coordinates
-    auto chunk_coords = [&](int t, int c, int& row0, int& col) {
-      int mb, nb;
-      decode(p, t, mb, nb);
+    // chunk c of unit u: output coordinates
+    auto chunk_coords = [&](int u, int c, int& row0, int& col) {
+      int mb, nb, sp;
+      decode(p, u, mb, nb, sp);
       row0 = mb * kBM * CG + rank * kBM + q * 32;
       col = nb * kBN + chalf * kSliceCols + c * CW;
     };
-    auto issue_aux = [&](int t, int c, int buf) {
+    auto issue_aux = [&](int u, int c, int buf) {
       int row0, col;
-      chunk_coords(t, c, row0, col);
+      chunk_coords(u, c, row0, col);
       mbar_arrive_expect_tx(&xb[buf], kStg);
       tc::tma_load_2d(stg + buf * kStg, &mapX, &xb[buf], col, row0);
     };
-    constexpr int kArrivals = kEpiWarps * CG;   // epilogue warps of a worker
-    uint32_t cidx = 0;   // epilogue chunks of this warp (buffer parity, aux barrier phase)
-    SegIter si = seg_begin(p, cid);
-    if (aux && lane == 0) {   // the first segment with an epilogue: k0 == 0
-      SegIter s2 = si;
-      int t, k0, k1;
-      bool have = seg_next(p, s2, t, k0, k1);
-      if (have && k0 != 0) have = seg_next(p, s2, t, k0, k1);
-      if (have) issue_aux(t, 0, 0);
-    }
-    int it = 0, t = 0, k0 = 0, k1 = 0;
-    for (; seg_next(p, si, t, k0, k1); ++it) {
-      int mb, nb;
-      decode(p, t, mb, nb);
+    uint32_t cidx = 0;   // chunks processed by this warp (buffer parity, aux barrier phase)
+    if (aux && lane == 0 && cid < p.units) issue_aux(cid, 0, 0);
+    int it = 0;
+    for (int u = cid; u < p.units; u += ncl, ++it) {
+      int mb, nb, sp;
+      decode(p, u, mb, nb, sp);
       const int as = it & 1;
       mbar_wait_sleep(&tfull[as], (it >> 1) & 1, 20000u);
       tc::fence_after_sync();
-      WG_TRACE(2 * it);
-      const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * kSliceCols;
-      if (k0 != 0) {
-        // tail of a tile: publish the fp32 partial sum for the worker owning its head, in a
-        // thread-major layout (float4 i of lane l of warp ew at [(rank, ew, i)][l]) that the
-        // head's epilogue thread with the same role reads back: 512 contiguous bytes per
-        // warp instruction
-        float4* dst = reinterpret_cast<float4*>(p.sk_part) +
-                      (int64_t)cid * (kBM * CG * kBN / 4) +
-                      (int64_t)((rank * kEpiWarps + ew) * (kSliceCols / 4)) * 32 + lane;
-#pragma unroll 1
-        for (int c = 0; c < kSliceCols / 16; ++c) {
-          float v[16];
-          tc::tmem_ld16(tbase + c * 16, v);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[(c * 4 + j) * 32] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-        }
-        tc::fence_before_sync();
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-          if (CG == 2)
-            mbar_arrive_cluster(tempty_c + as * 8);
-          else
-            mbar_arrive(&tempty[as]);
-          atomicAdd(p.sk_flag + cid, 1);
-        }
-        WG_TRACE(2 * it + 1);
-        continue;
-      }
-      // head of the tile: the workers after this one that hold its other k-blocks
-      int jend = cid + 1;
-      if (k1 < p.nk) {
-        const int64_t tile_end = (int64_t)(t + 1) * p.nk;
-        while (jend < p.P && sk_lo(p, jend) < tile_end) ++jend;
-        if (lane == 0) {
-          for (int j = cid + 1; j < jend; ++j) {
-            int f;
-            while (true) {
-              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(p.sk_flag + j)
-                           : "memory");
-              if (f >= kArrivals) break;
-              __nanosleep(128);
-            }
-          }
-        }
-        __syncwarp();
-        if (ew == 0 && lane == 0) g_trace[blockIdx.x * 16 + 14] = gtime();
-      }
       const int row0 = mb * kBM * CG + rank * kBM + q * 32;
       const int row = row0 + lane;
+      const int out_row0 = row0 + sp * p.M;   // split-K partial slab (EPI_STORE, fp32)
       const int prow = (mb * CG + (int)rank) * 4 + q;   // column-partial row (EPI_BAD_BWD)
 #pragma unroll 1
       for (int c = 0; c < NCH; ++c, ++cidx) {
@@ -467,10 +373,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         unsigned char* sb = stg + buf * kStg;
         unsigned char* sb2 = stg + (buf ^ 1) * kStg;
         float v[CW];
+        const uint32_t taddr =
+            tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * kSliceCols + c * CW;
         if (CW == 32)
-          tc::tmem_ld32(tbase + c * CW, v);
+          tc::tmem_ld32(taddr, v);
         else
-          tc::tmem_ld16(tbase + c * CW, v);
+          tc::tmem_ld16(taddr, v);
         if (c == NCH - 1) {   // accumulator drained: the MMA warp may reuse it
           tc::fence_before_sync();
           __syncwarp();
@@ -479,21 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_arrive_cluster(tempty_c + as * 8);
             else
               mbar_arrive(&tempty[as]);
-          }
-        }
-        // the other workers' partial sums of this tile, in worker order
-        for (int j = cid + 1; j < jend; ++j) {
-          const float4* src = reinterpret_cast<const float4*>(p.sk_part) +
-                              (int64_t)j * (kBM * CG * kBN / 4) +
-                              (int64_t)((rank * kEpiWarps + ew) * (kSliceCols / 4) + c * (CW / 4)) *
-                                  32 + lane;
-#pragma unroll
-          for (int i = 0; i < CW / 4; ++i) {
-            const float4 w4 = src[i * 32];
-            v[4 * i] += w4.x;
-            v[4 * i + 1] += w4.y;
-            v[4 * i + 2] += w4.z;
-            v[4 * i + 3] += w4.w;
           }
         }
         // results are formed in registers first, so the stores issued from the staging
@@ -586,39 +479,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tc::tma_store_2d(&mapC, sb, col, row0);
+          tc::tma_store_2d(&mapC, sb, col, out_row0);
           if (EPI == EPI_BAD_FWD) tc::tma_store_2d(&mapC2, sb2, col, row0);
           tc::bulk_commit();
           if (aux) {
             // prefetch the next chunk's auxiliary tile into the other buffer once the store
-            // issued from it (previous chunk) has read it; after this worker's first segment
-            // every segment runs an epilogue, so the next chunk is chunk 0 of the next one
-            int nt = t, nc = c + 1;
-            bool have = true;
+            // issued from it (previous chunk) has read it
+            int nu = u, nc = c + 1;
             if (nc == NCH) {
-              SegIter s2 = si;
-              int a0, a1;
               nc = 0;
-              have = seg_next(p, s2, nt, a0, a1);
+              nu = u + ncl;
             }
-            if (have) {
+            if (nu < p.units) {
               tc::bulk_wait_read<1>();
-              issue_aux(nt, nc, (cidx + 1) & 1);
+              issue_aux(nu, nc, (cidx + 1) & 1);
             }
           }
         }
         __syncwarp();
       }
       (void)row;
-      WG_TRACE(2 * it + 1);
-      // release the partials this tile consumed: the last of the worker's warps resets the
-      // flags for the next launch
-      if (lane == 0)
-        for (int j = cid + 1; j < jend; ++j)
-          if (atomicAdd(p.sk_done + j, 1) == kArrivals - 1) {
-            p.sk_flag[j] = 0;
-            p.sk_done[j] = 0;
-          }
     }
     if (lane == 0) tc::bulk_wait<0>();
     __syncwarp();
@@ -632,6 +512,23 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     __syncthreads();
     if (warp == 1) tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// split-K partial slabs [splits][M][N] fp32 -> C, summed in split order (deterministic)
+__global__ void splitk_reduce_kernel(const float4* __restrict__ ws, float4* __restrict__ C,
+                                     int64_t n4, int splits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 a = ws[i];
+    for (int s = 1; s < splits; ++s) {
+      const float4 b = ws[(int64_t)s * n4 + i];
+      a.x += b.x;
+      a.y += b.y;
+      a.z += b.z;
+      a.w += b.w;
+    }
+    C[i] = a;
   }
 }
 
@@ -653,50 +550,18 @@ bool map2d(CUtensorMap* m, const void* ptr, bool f32, uint64_t inner, uint64_t o
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Workers (CTAs, or CTA pairs for CG = 2) of this instantiation that can be resident at
-// once: the stream-K schedule needs every worker resident (a head waits for the partials of
-// the workers after it), and not every SM pair can host a cluster of two
-template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
-int resident_workers(int num_sms) {
-  auto kern = wg::wgemm_kernel<CG, AMN, BMN, OUTF32, EPI, ACT>;
-  constexpr size_t smem = wg::Cfg<CG, EPI>::kSmem;
-  static int cached = -1;   // per instantiation (one device per process)
-  if (cached >= 0) return cached;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return 0;
-  if (CG == 1) {
-    int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, wg::kThreads, smem) !=
-        cudaSuccess)
-      return 0;
-    cached = per * num_sms;
-    return cached;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(num_sms, 1, 1);
-  cfg.blockDim = dim3(wg::kThreads, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  int n = 0;
-  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) return 0;
-  if (getenv("ENC_WGEMM_DEBUG")) fprintf(stderr, "wgemm: %d resident CTA pairs\n", n);
-  cached = n;
-  return cached;
-}
-
 template <int CG, int AMN, int BMN, int OUTF32, int EPI, int ACT>
 cudaError_t launch_t(int grid, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                      const CUtensorMap& c2, const CUtensorMap& x, const wg::Params& p,
                      cudaStream_t st) {
   auto kern = wg::wgemm_kernel<CG, AMN, BMN, OUTF32, EPI, ACT>;
   constexpr size_t smem = wg::Cfg<CG, EPI>::kSmem;
+  static bool attr = false;   // per instantiation
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   if (CG == 1) {
     kern<<<grid, wg::kThreads, smem, st>>>(a, b, c, c2, x, p);
     return cudaGetLastError();
@@ -718,7 +583,7 @@ cudaError_t launch_t(int grid, const CUtensorMap& a, const CUtensorMap& b, const
 }  // namespace
 
 bool wgemm_supported(const WgemmArgs& g) {
-  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.N % 8 || g.K % 8 || !g.A || !g.B || !g.C || !g.ws)
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.N % 8 || g.K % 8 || !g.A || !g.B || !g.C)
     return false;
   switch (g.epi) {
     case EPI_STORE:
@@ -736,61 +601,64 @@ bool wgemm_supported(const WgemmArgs& g) {
 // single 128-row block
 static int pick_cg(const WgemmArgs& g) { return g.cg == 1 || g.M <= wg::kBM ? 1 : 2; }
 
+// split count for an fp32 output: minimise (waves x k-blocks per split) + the reduce pass
+static int choose_splits(int tiles, int nk, int slots, int64_t MN) {
+  int best = 1;
+  double best_cost = 1e300;
+  for (int s = 1; s <= 8; ++s) {
+    const int kbs = (nk + s - 1) / s;
+    if (s > 1 && (kbs < 4 || (int64_t)(s - 1) * kbs >= nk)) break;
+    const double waves = (double)((tiles * s + slots - 1) / slots);
+    // one k-block of one tile ~ 0.3 us of MMA; the reduce reads s+1 slabs of M*N fp32 at
+    // ~4 TB/s (mostly L2-resident)
+    const double cost = waves * kbs * 0.3 + (s > 1 ? (double)(s + 1) * MN * 4 / 4.0e6 : 0.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
+}
+
 namespace {
 struct Plan {
-  int cg, tiles_m, tiles_n, nk, P;
-  int64_t T;
+  int cg, tiles_m, tiles_n, nk, splits;
 };
-// Stream-K plan: P workers (one per SM or SM pair) share the T (tile, k-block) units
-// equally, each at least min(nk, 4) k-blocks
 Plan plan_of(const WgemmArgs& g, int num_sms) {
   Plan P;
   P.cg = pick_cg(g);
   P.tiles_m = (g.M + wg::kBM * P.cg - 1) / (wg::kBM * P.cg);
   P.tiles_n = (g.N + wg::kBN - 1) / wg::kBN;
   P.nk = (g.K + wg::kBK - 1) / wg::kBK;
-  P.T = (int64_t)P.tiles_m * P.tiles_n * P.nk;
-  const int slots = num_sms / P.cg;
-  const int64_t minseg = P.nk < 4 ? P.nk : 4;
-  int64_t w = P.T / minseg;
-  if (w > slots) w = slots;
-  if (w < 1) w = 1;
-  P.P = (int)w;
+  P.splits = 1;
+  if (g.epi == EPI_STORE && g.out_f32 && g.ws)
+    P.splits = choose_splits(P.tiles_m * P.tiles_n, P.nk, num_sms / P.cg, (int64_t)g.M * g.N);
+  // the partial slabs are stacked along M: only whole M tiles keep them apart
+  if (P.splits > 1 && (g.M % (wg::kBM * P.cg) ||
+                       g.ws_bytes < (size_t)P.splits * g.M * g.N * sizeof(float)))
+    P.splits = 1;
   return P;
 }
 }  // namespace
-
-size_t wgemm_ws_bytes(int num_sms) {
-  // flags + done counters, then one 256 x 256 fp32 partial per worker
-  return kWgemmFlagBytes + (size_t)num_sms * wg::kBM * wg::kBN * sizeof(float);
-}
 
 int wgemm_partial_rows(const WgemmArgs& g) {
   const int cg = pick_cg(g);
   return ((g.M + wg::kBM * cg - 1) / (wg::kBM * cg)) * cg * 4;
 }
 
-void wgemm_trace_read(unsigned long long* host) {
-  cudaMemcpyFromSymbol(host, wg::g_trace, sizeof(wg::g_trace));
-}
-
 cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (!wgemm_supported(g)) return cudaErrorInvalidValue;
   const Plan P = plan_of(g, num_sms);
-  if (g.ws_bytes < wgemm_ws_bytes(num_sms)) return cudaErrorInvalidValue;
   wg::Params p{};
   p.M = g.M;
   p.N = g.N;
   p.K = g.K;
   p.tiles_m = P.tiles_m;
   p.tiles_n = P.tiles_n;
-  p.tiles = P.tiles_m * P.tiles_n;
   p.nk = P.nk;
-  p.P = P.P;
-  p.T = P.T;
-  p.sk_flag = reinterpret_cast<int*>(g.ws);
-  p.sk_done = p.sk_flag + kWgemmFlagBytes / 8;
-  p.sk_part = reinterpret_cast<float*>(reinterpret_cast<char*>(g.ws) + kWgemmFlagBytes);
+  p.splits = P.splits;
+  p.kb_per_split = (p.nk + p.splits - 1) / p.splits;
+  p.units = p.tiles_m * p.tiles_n * p.splits;
   p.beta = g.beta;
   p.bias = g.bias;
   p.pk = g.pk;
@@ -809,7 +677,10 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
                : map2d(&mb, g.B, false, g.K, g.N, g.ldb, 64, bcols, SW128);
   const bool f32 = g.out_f32 != 0;
   const uint32_t cw = f32 ? 16 : 32;
-  ok &= map2d(&mc, g.C, f32, g.N, g.M, g.ldc, cw, 32, SW64);
+  if (p.splits > 1)
+    ok &= map2d(&mc, g.ws, true, g.N, (uint64_t)g.M * p.splits, g.N, cw, 32, SW64);
+  else
+    ok &= map2d(&mc, g.C, f32, g.N, g.M, g.ldc, cw, 32, SW64);
   mc2 = mc;
   mx = mc;
   if (g.epi == EPI_BAD_FWD) ok &= map2d(&mc2, g.C2, false, g.N, g.M, g.ldc2, 32, 32, SW64);
@@ -817,14 +688,11 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   if (g.beta) ok &= map2d(&mx, g.C, false, g.N, g.M, g.ldc, 32, 32, SW64);
   if (!ok) return cudaErrorInvalidValue;
 
+  const int slots = num_sms / P.cg;
+  const int grid = (p.units < slots ? p.units : slots) * P.cg;
   cudaError_t e = cudaErrorInvalidValue;
-#define WG_LAUNCH1(CG, AM, BM, OF, EP, AC)                                      \
-  do {                                                                         \
-    const int rw = resident_workers<CG, AM, BM, OF, EP, AC>(num_sms);          \
-    if (rw < 1) return cudaErrorInvalidConfiguration;                          \
-    if (p.P > rw) p.P = rw;                                                    \
-    e = launch_t<CG, AM, BM, OF, EP, AC>(p.P * CG, ma, mb, mc, mc2, mx, p, st); \
-  } while (0)
+#define WG_LAUNCH1(CG, AM, BM, OF, EP, AC) \
+  e = launch_t<CG, AM, BM, OF, EP, AC>(grid, ma, mb, mc, mc2, mx, p, st)
 #define WG_LAUNCH(AM, BM, OF, EP, AC)            \
   do {                                           \
     if (P.cg == 2) WG_LAUNCH1(2, AM, BM, OF, EP, AC); \
@@ -845,9 +713,17 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   }
 #undef WG_LAUNCH
 #undef WG_LAUNCH1
-  return e;
+  if (e != cudaSuccess || p.splits == 1) return e;
+  const int64_t n4 = (int64_t)g.M * g.N / 4;
+  int64_t blocks = (n4 + 255) / 256;
+  if (blocks > 8 * num_sms) blocks = 8 * num_sms;
+  wg::splitk_reduce_kernel<<<(int)blocks, 256, 0, st>>>((const float4*)g.ws, (float4*)g.C, n4,
+                                                        p.splits);
+  return cudaGetLastError();
 }
 
-int wgemm_launches(const WgemmArgs&, int) { return 1; }
+int wgemm_launches(const WgemmArgs& g, int num_sms) {
+  return plan_of(g, num_sms).splits > 1 ? 2 : 1;
+}
 
 }  // namespace enc
