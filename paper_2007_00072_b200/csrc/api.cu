@@ -56,7 +56,8 @@ struct enc_ctx {
   // stream (ev_pfs)
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
-  int gemm_tc = 1;
+  // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction
+  uint32_t gemm_tc = 0xFFFFFFFFu;
   int gemm_cg = 0;           // ENC_OPT_GEMM_PAIR 1 (default) -> 0 (auto), 0 -> 1 (single CTAs)
   void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
   void* wg_ws_side = nullptr;   // the same for contractions on the side stream
@@ -70,9 +71,9 @@ struct enc_ctx {
 // (tA: A stored [K][M]; tB: B stored [N][K]).  bf16: the hand-written tcgen05 kernel
 // (wgemm.cu) with an optional fp32 bias over columns; fp32 (or ENC_OPT_GEMM_TC off):
 // cuBLASLt / cuBLAS.  Returns an ENC_* code.
-static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA, bool tB,
-                     int M, int N, int K, const void* A, int lda, const void* B, int ldb,
-                     float beta, void* C, int ldc, const float* bias = nullptr,
+static int wcontract(enc_ctx* ctx, int op, cudaStream_t st, int in_dt, int out_dt, bool tA,
+                     bool tB, int M, int N, int K, const void* A, int lda, const void* B,
+                     int ldb, float beta, void* C, int ldc, const float* bias = nullptr,
                      void* lt_ws = nullptr);
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
@@ -152,10 +153,10 @@ static int cuda_fail(cudaError_t e) {
     if (_s != CUBLAS_STATUS_SUCCESS) return ENC_ECUBLAS; \
   } while (0)
 
-static int wcontract(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA, bool tB,
-                     int M, int N, int K, const void* A, int lda, const void* B, int ldb,
-                     float beta, void* C, int ldc, const float* bias, void* lt_ws) {
-  if (ctx->gemm_tc && in_dt == ENC_BF16 && (beta == 0.f || beta == 1.f)) {
+static int wcontract(enc_ctx* ctx, int op, cudaStream_t st, int in_dt, int out_dt, bool tA,
+                     bool tB, int M, int N, int K, const void* A, int lda, const void* B,
+                     int ldb, float beta, void* C, int ldc, const float* bias, void* lt_ws) {
+  if (((ctx->gemm_tc >> op) & 1u) && in_dt == ENC_BF16 && (beta == 0.f || beta == 1.f)) {
     WgemmArgs g;
     g.M = M; g.N = N; g.K = K;
     g.A = A; g.lda = lda; g.a_mn = tA ? 1 : 0;
@@ -444,7 +445,7 @@ static WgemmArgs ffn_fwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
                               const enc_cfg* cfg, const void* X1, const void* W1, const float* b1,
                               const PhiloxKey& pk, void* h, void* A1, bool force = false) {
   WgemmArgs g;
-  if ((!ctx->gemm_tc && !force) || dtype != ENC_BF16) return g;
+  if ((!((ctx->gemm_tc >> ENC_OP_GEMM_L1) & 1u) && !force) || dtype != ENC_BF16) return g;
   g.ws = ctx->wg_ws;
   g.ws_bytes = ctx->wg_ws_bytes;
   g.M = d->B * d->J; g.N = d->U; g.K = d->I;
@@ -464,7 +465,7 @@ static WgemmArgs ffn_bwd_args(const enc_ctx* ctx, const enc_dims* d, int dtype,
                               const enc_cfg* cfg, const void* dY2, const void* W2, const void* h,
                               const PhiloxKey& pk, void* dh, float* partials, bool force = false) {
   WgemmArgs g;
-  if ((!ctx->gemm_tc && !force) || dtype != ENC_BF16) return g;
+  if ((!((ctx->gemm_tc >> ENC_OP_GEMM_L2_DX) & 1u) && !force) || dtype != ENC_BF16) return g;
   g.ws = ctx->wg_ws;
   g.ws_bytes = ctx->wg_ws_bytes;
   g.M = d->B * d->J; g.N = d->U; g.K = d->I;
@@ -823,7 +824,11 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_TC) {
-    ctx->gemm_tc = value ? 1 : 0;
+    ctx->gemm_tc = value ? 0xFFFFFFFFu : 0u;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_GEMM_TC_MASK) {
+    ctx->gemm_tc = (uint32_t)value;
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_PAIR) {
@@ -985,8 +990,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
     if (direct) {   // tcgen05 contraction: the fp32 bias is added in its epilogue
-      r = wcontract(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I, 0.f,
-                    QKVs, 3 * I, prm->bqkv);
+      r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I,
+                    prm->Wqkv, I, 0.f, QKVs, 3 * I, prm->bqkv);
       if (r == ENC_OK) bias_done = true;
       else if (r != ENC_EUNSUPPORTED) return r;
     }
@@ -998,8 +1003,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
                             QKVs, 3 * I, LT_EPI_BIAS, ctx->red);
     }
     if (!bias_done)
-      if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I,
-                         0.f, direct ? QKVs : QKV, 3 * I)))
+      if ((r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, 3 * I, I, X,
+                         I, prm->Wqkv, I, 0.f, direct ? QKVs : QKV, 3 * I)))
         return r;
   }
   // AIB (:550): in place on the direct path unless the epilogue added the bias
@@ -1055,7 +1060,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Out (:554)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT, st, 0);
-    if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, I, I, C, I, prm->Wo, I, 0.f, Yo, I)))
+    if ((r = wcontract(ctx, ENC_OP_GEMM_OUT, st, dtype, dtype, false, true, BJ, I, I, C, I, prm->Wo, I, 0.f, Yo, I)))
       return r;
   }
   // BDRLN site 1 (:555-558)
@@ -1077,7 +1082,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   } else {
     {
       OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
-      if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, U, I, X1, I, prm->W1, I, 0.f, h,
+      if ((r = wcontract(ctx, ENC_OP_GEMM_L1, st, dtype, dtype, false, true, BJ, U, I, X1, I, prm->W1, I, 0.f, h,
                          U)))
         return r;
     }
@@ -1087,7 +1092,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // Linear (:563)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L2, st, 0);
-    if ((r = wcontract(ctx, st, dtype, dtype, false, true, BJ, I, U, A1, U, prm->W2, U, 0.f, Y2, I)))
+    if ((r = wcontract(ctx, ENC_OP_GEMM_L2, st, dtype, dtype, false, true, BJ, I, U, A1, U, prm->W2, U, 0.f, Y2, I)))
       return r;
   }
   // BDRLN site 2 (:564-567)
@@ -1231,7 +1236,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
       {
         cudaStream_t ss = fork();
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
-        if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
+        if ((r = wcontract(ctx, ENC_OP_GEMM_L2_DW, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
                            g->dW2, U, nullptr, sws)))
           return r;
       }
@@ -1241,14 +1246,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     } else {
       {
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
-        if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, U, I, dY2, I, prm->W2, U, 0.f,
+        if ((r = wcontract(ctx, ENC_OP_GEMM_L2_DX, st, dtype, dtype, false, false, BJ, U, I, dY2, I, prm->W2, U, 0.f,
                            dA1, U)))
           return r;
       }
       {
         cudaStream_t ss = fork();
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
-        if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
+        if ((r = wcontract(ctx, ENC_OP_GEMM_L2_DW, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
                            g->dW2, U, nullptr, sws)))
           return r;
       }
@@ -1261,14 +1266,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // Linear1 dX (:579) accumulated onto dz2 (residual, paper `ebsb` :581), dW (:580)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DX, st, 0);
-    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, U, dh, U, prm->W1, I, 1.f, dX1,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_L1_DX, st, dtype, dtype, false, false, BJ, I, U, dh, U, prm->W1, I, 1.f, dX1,
                        I)))
       return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, ss, 0);
-    if ((r = wcontract(ctx, ss, dtype, F32, true, false, U, I, BJ, dh, U, X1, I, 0.f, g->dW1, I,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_L1_DW, ss, dtype, F32, true, false, U, I, BJ, dh, U, X1, I, 0.f, g->dW1, I,
                        nullptr, sws)))
       return r;
   }
@@ -1290,14 +1295,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // Out dX (:586), dW (:587)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DX, st, 0);
-    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, I, dYo, I, prm->Wo, I, 0.f, dC,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_OUT_DX, st, dtype, dtype, false, false, BJ, I, I, dYo, I, prm->Wo, I, 0.f, dC,
                        I)))
       return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, ss, 0);
-    if ((r = wcontract(ctx, ss, dtype, F32, true, false, I, I, BJ, dYo, I, C, I, 0.f, g->dWo, I,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_OUT_DW, ss, dtype, F32, true, false, I, I, BJ, dYo, I, C, I, 0.f, g->dWo, I,
                        nullptr, sws)))
       return r;
   }
@@ -1392,14 +1397,14 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
-    if ((r = wcontract(ctx, st, dtype, dtype, false, false, BJ, I, 3 * I, dQKV, 3 * I, prm->Wqkv,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DX, st, dtype, dtype, false, false, BJ, I, 3 * I, dQKV, 3 * I, prm->Wqkv,
                        I, 1.f, dX, I)))
       return r;
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, ss, 0);
-    if ((r = wcontract(ctx, ss, dtype, F32, true, false, 3 * I, I, BJ, dQKV, 3 * I, X, I, 0.f,
+    if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, ss, dtype, F32, true, false, 3 * I, I, BJ, dQKV, 3 * I, X, I, 0.f,
                        g->dWqkv, I, nullptr, sws)))
       return r;
   }

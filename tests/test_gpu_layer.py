@@ -30,12 +30,16 @@ def f64(t):
 
 # option ids of include/encoder.h (enc_set_option)
 OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_ATTN_BH, OPT_QKV_DIRECT, OPT_GEMM_TC = 0, 1, 4, 5, 8
+OPT_GEMM_PAIR, OPT_GEMM_TC_MASK = 9, 10
 
 
 def _ffn_fused(dtype, opts=None):
     """bf16 with ENC_OPT_GEMM_TC on (default): Linear1 + BAD and Linear2-dX + BAD-bwd run as
     one tcgen05 kernel each (dA1 is never written)."""
-    return dtype == "bf16" and bool((opts or {}).get(OPT_GEMM_TC, 1))
+    o = opts or {}
+    if OPT_GEMM_TC_MASK in o:
+        return dtype == "bf16" and bool(o[OPT_GEMM_TC_MASK] >> 12 & 1)   # ENC_OP_GEMM_L2_DX
+    return dtype == "bf16" and bool(o.get(OPT_GEMM_TC, 1))
 
 
 def _paths(dims, dtype, opts=None):
@@ -249,6 +253,9 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {OPT_ATTN_FUSED: 0},                   # tiled QK^T + BSB kernels + per-(b,h)
     {OPT_ATTN_FUSED: 0, OPT_ATTN_BH: 0},   # all tiled tcgen05
     {OPT_ATTN_TC: 0},                      # cuBLAS attention
+    {OPT_GEMM_TC: 0},                      # weight contractions on cuBLASLt, BAD separate
+    {OPT_GEMM_TC_MASK: (1 << 7) | (1 << 12)},   # only the fused FFN kernels on tcgen05
+    {OPT_GEMM_PAIR: 0},                    # single-CTA weight-contraction tiles
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""

@@ -44,6 +44,8 @@ def main():
     a = ap.parse_args()
     from paper_2007_00072_b200 import ops
     ctx = ops.Context(0)
+    ctx1 = ops.Context(0)   # single-CTA tiles, for comparison
+    ops.enc_set_option(ctx1, ops.OPT_GEMM_PAIR, 0)
     BJ, I, U = (4096, 1024, 4096) if a.config == "L" else (12288, 768, 3072)
     bf = torch.bfloat16
     dev = "cuda"
@@ -77,12 +79,17 @@ def main():
             ref = lambda: torch.matmul(A.t(), B, out=Cb)  # noqa: E731
         t_m = graph_time(mine)
         t_r = graph_time(ref)
+        cs = ctx
+        ctx = ctx1
+        t_1 = graph_time(mine)
+        ctx = cs
         fl = 2.0 * M * N * K
         rows.append({"op": name, "M": M, "N": N, "K": K, "tc_us": round(t_m, 2),
                      "cublas_us": round(t_r, 2), "tc_tflops": round(fl / t_m / 1e6, 1),
                      "cublas_tflops": round(fl / t_r / 1e6, 1)})
         print(f"{name:8s} {M:6d}x{N:5d}x{K:6d}  tc {t_m:7.2f} us {fl / t_m / 1e6:7.1f} TF/s   "
-              f"cublas {t_r:7.2f} us {fl / t_r / 1e6:7.1f} TF/s   ratio {t_r / t_m:.3f}",
+              f"cublas {t_r:7.2f} us {fl / t_r / 1e6:7.1f} TF/s   ratio {t_r / t_m:.3f}   "
+              f"single-CTA {t_1:7.2f} us",
               flush=True)
     # fused FFN kernels against their unfused cuBLAS + element-wise baseline is timed by
     # the layer bench; here: the fused kernels alone
