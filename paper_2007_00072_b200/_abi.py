@@ -47,7 +47,8 @@ class enc_saved_view(ctypes.Structure):
 
 
 class enc_opt_segment(ctypes.Structure):
-    _fields_ = [("begin", c_int64), ("n", c_int64), ("out", c_void_p), ("dtype", c_int)]
+    _fields_ = [("begin", c_int64), ("n", c_int64), ("out", c_void_p), ("dtype", c_int),
+                ("no_decay", c_int)]
 
 
 BWD_FIELDS = ("dY2", "dA1", "dh", "dX1", "dYo", "dC", "dA", "dS", "dQ", "dK", "dV", "dQKV")

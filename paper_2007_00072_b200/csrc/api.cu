@@ -1518,7 +1518,8 @@ int enc_adamw_step(enc_ctx* ctx, int64_t n, float* master, float* m, float* v, c
     if (e.dtype != ENC_BF16 && e.dtype != ENC_FP32) return ENC_EDTYPE;
     if (e.n > 0) CHECK_PTRS(e.out);
     if (e.n > 0 && ((uintptr_t)e.out % (e.dtype == ENC_BF16 ? 8 : 16))) return ENC_EALIGN;
-    s[k] = OptSeg{e.begin, e.n, e.out, e.dtype};
+    if (e.no_decay != 0 && e.no_decay != 1) return ENC_EINVAL;
+    s[k] = OptSeg{e.begin, e.n, e.out, e.dtype, e.no_decay};
     at += e.n;
   }
   if (at != n) return ENC_EINVAL;
@@ -1553,21 +1554,37 @@ int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype
   if (r) return r;
   if (!Y_host) return ENC_ENULL;
   CHECK_PTRS(X_dev, dY_dev, Y_dev, dX_dev);
+  const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
+  // buffers the copies touch while the layer runs must not overlap what the layer reads or
+  // writes (byte ranges; the previous dX may BE this step's dX buffer, then the backward
+  // waits for its copy)
+  size_t sv_bytes = 0, sc_bytes = 0;
+  if ((r = enc_layer_sizes(d, dtype, &sv_bytes, &sc_bytes))) return r;
+  auto overlap = [](const void* a, size_t na, const void* b, size_t nb) {
+    const char *pa = (const char*)a, *pb = (const char*)b;
+    return a && b && pa < pb + nb && pb < pa + na;
+  };
+  const void* layer_bufs[6] = {X_dev, dY_dev, Y_dev, dX_dev, saved, scratch};
+  const size_t layer_sz[6] = {bytes, bytes, bytes, bytes, sv_bytes, sc_bytes};
   const bool next = X_next_host != nullptr || dY_next_host != nullptr;
   if (next) {
     if (!X_next_host || !dY_next_host) return ENC_ENULL;
     CHECK_PTRS(X_next_dev, dY_next_dev);
-    if (X_next_dev == X_dev || dY_next_dev == dY_dev || X_next_dev == dY_dev ||
-        dY_next_dev == X_dev)
-      return ENC_EINVAL;
+    if (overlap(X_next_dev, bytes, dY_next_dev, bytes)) return ENC_EINVAL;
+    for (int i = 0; i < 6; ++i)
+      if (overlap(X_next_dev, bytes, layer_bufs[i], layer_sz[i]) ||
+          overlap(dY_next_dev, bytes, layer_bufs[i], layer_sz[i]))
+        return ENC_EINVAL;
   }
   const bool prev = dX_prev_dev != nullptr || dX_prev_host != nullptr;
   if (prev) {
     if (!dX_prev_host) return ENC_ENULL;
     CHECK_PTRS(dX_prev_dev);
+    for (int i = 0; i < 6; ++i)
+      if (i != 3 && overlap(dX_prev_dev, bytes, layer_bufs[i], layer_sz[i])) return ENC_EINVAL;
+    if (overlap(dX_prev_dev, bytes, dX_dev, bytes) && dX_prev_dev != dX_dev) return ENC_EINVAL;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t bytes = (size_t)d->B * d->J * d->I * esize(dtype);
   // fork both copy streams here: the next step's inputs in (their buffers' last reader,
   // the previous step, is complete at this point of `st`), the previous step's dX out
   CK(cudaEventRecord(ctx->ev_pfs, st));
@@ -1583,17 +1600,27 @@ int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype
     CK(cudaMemcpyAsync(dX_prev_host, dX_prev_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
     if (dx_alias) CK(cudaEventRecord(ctx->ev_out, ctx->copy_out));
   }
+  // on an error after the fork, both copy streams are joined back into `st` before
+  // returning (an active capture must not be left with unjoined work)
+  auto join_copies = [&](int rc) {
+    cudaEventRecord(ctx->ev_out, ctx->copy_out);
+    cudaStreamWaitEvent(st, ctx->ev_out, 0);
+    if (next) cudaStreamWaitEvent(st, ctx->ev_pf, 0);
+    return rc;
+  };
   r = encoder_layer_forward(ctx, d, dtype, cfg, prm, X_dev, mask_bias, Y_dev, saved, scratch,
                             stream);
-  if (r) return r;
-  CK(cudaEventRecord(ctx->ev_fwd, st));
-  CK(cudaStreamWaitEvent(ctx->copy_out, ctx->ev_fwd, 0));
-  CK(cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out));
+  if (r) return join_copies(r);
+  cudaError_t ce = cudaEventRecord(ctx->ev_fwd, st);
+  if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ctx->copy_out, ctx->ev_fwd, 0);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(Y_host, Y_dev, bytes, cudaMemcpyDeviceToHost, ctx->copy_out);
   // the previous step's dX in the same buffer: its copy finishes before the backward writes
-  if (dx_alias) CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+  if (ce == cudaSuccess && dx_alias) ce = cudaStreamWaitEvent(st, ctx->ev_out, 0);
+  if (ce != cudaSuccess) return join_copies(cuda_fail(ce));
   r = encoder_layer_backward(ctx, d, dtype, cfg, prm, X_dev, saved, dY_dev, dX_dev, g, scratch,
                              stream);
-  if (r) return r;
+  if (r) return join_copies(r);
   // join: every copy this call issued is complete when `stream` passes its end
   CK(cudaEventRecord(ctx->ev_out, ctx->copy_out));
   CK(cudaStreamWaitEvent(st, ctx->ev_out, 0));

@@ -14,6 +14,7 @@ struct OptSeg {
   int64_t n;
   void* out;
   int dtype;
+  int no_decay;
 };
 constexpr int kOptMaxSegs = 32;
 cudaError_t launch_adamw(int64_t n, float* master, float* m1, float* m2, const float* g,

@@ -35,22 +35,24 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ master,
     float pv[4] = {p.x, p.y, p.z, p.w}, av[4] = {a.x, a.y, a.z, a.w};
     float bv[4] = {b.x, b.y, b.z, b.w};
     const float gv[4] = {gg.x, gg.y, gg.z, gg.w};
+    // the segment holding elements 4i .. 4i+3 (segments are 4-aligned): its model copy and
+    // whether it takes weight decay
+    const int64_t e = i * 4;
+    int k = 0;
+    while (k + 1 < segs.count && e >= segs.s[k + 1].begin) ++k;
+    const OptSeg& sg = segs.s[k];
+    const float dec = sg.no_decay ? 1.f : decay;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float gj = gv[j] * gscale;
       av[j] = fmaf(b1, av[j], omb1 * gj);
       bv[j] = fmaf(b2, bv[j], omb2 * gj * gj);
       const float denom = sqrtf(bv[j]) * rsbc2 + eps;   // sqrt(v / (1 - b2^t)) + eps
-      pv[j] = pv[j] * decay - lr_bc1 * av[j] / denom;   // lr_bc1 = lr / (1 - b1^t)
+      pv[j] = pv[j] * dec - lr_bc1 * av[j] / denom;   // lr_bc1 = lr / (1 - b1^t)
     }
     reinterpret_cast<float4*>(master)[i] = make_float4(pv[0], pv[1], pv[2], pv[3]);
     reinterpret_cast<float4*>(m1)[i] = make_float4(av[0], av[1], av[2], av[3]);
     reinterpret_cast<float4*>(m2)[i] = make_float4(bv[0], bv[1], bv[2], bv[3]);
-    // model copy: the segment holding elements 4i .. 4i+3 (segments are 4-aligned)
-    const int64_t e = i * 4;
-    int k = 0;
-    while (k + 1 < segs.count && e >= segs.s[k + 1].begin) ++k;
-    const OptSeg& sg = segs.s[k];
     const int64_t off = e - sg.begin;
     if (sg.dtype == 0) {
       uint2 u;

@@ -23,6 +23,7 @@ TORCH_DT = {"bf16": torch.bfloat16, "fp32": torch.float32}
 ABI_DT = {"bf16": _abi.ENC_BF16, "fp32": _abi.ENC_FP32}
 
 FFN_BUCKET = ("W1", "W2", "b1", "b2", "g2", "be2")
+WEIGHTS = ("Wqkv", "Wo", "W1", "W2")
 ATTN_BUCKET = ("Wqkv", "Wo", "bqkv", "bo", "g1", "be1")
 
 
@@ -214,7 +215,9 @@ class EncoderLayer:
         for n in order:
             t = self.params[n]
             dt = _abi.ENC_BF16 if t.dtype == torch.bfloat16 else _abi.ENC_FP32
-            segs.append(_abi.enc_opt_segment(off, t.numel(), t.data_ptr(), dt))
+            # biases and LayerNorm gamma/beta take no weight decay (the BERT recipe)
+            segs.append(_abi.enc_opt_segment(off, t.numel(), t.data_ptr(), dt,
+                                             0 if n in WEIGHTS else 1))
             off += t.numel()
         self.c_segs = (_abi.enc_opt_segment * len(segs))(*segs)
 

@@ -72,11 +72,18 @@ class EncoderStack:
 
     def train_step(self, X, dY, lr=1e-4, reduce=None, mask_bias=None):
         """One training step: forward, backward, AdamW.  reduce(layer), if given, is called
-        once a layer's gradients are final (e.g. the data-parallel all-reduce); the
-        parameters are updated after every layer's backward (and reduction)."""
+        once a layer's gradients are final (e.g. the data-parallel all-reduce); work handles it
+        returns (async collectives) are waited on before the parameters are updated."""
         self.forward(X, mask_bias)
-        done = None if reduce is None else (lambda i, layer: reduce(layer))
-        self.backward(dY, on_layer_done=done)
+        works = []
+
+        def done(i, layer):
+            w = reduce(layer)
+            if w is not None:   # asynchronous collectives: waited on before the update
+                works.extend(w if isinstance(w, (list, tuple)) else [w])
+        self.backward(dY, on_layer_done=None if reduce is None else done)
+        for w in works:
+            w.wait()
         self.optimizer_step(lr)
 
     def step_host(self, X_host, dY_host, Y_host, dX_host, mask_bias=None, stream=None):

@@ -112,7 +112,10 @@ def _stagewise(dims, dtype, act, key_padding, opts=None, **kw):
     dY = np.asarray(inp["dY"], np.float64)
     s = {k: f64(v) for k, v in layer.saved_views().items()
          if k != "keep_attn" and not (k == "A" and _drop_on_load(dims, dtype, opts))}
-    b = {k: f64(v) for k, v in layer.bwd_views().items()}
+    # temporaries a fused kernel keeps on chip are never written: not read back
+    unwritten = ({"dA"} if _paths(dims, dtype, opts)["fused"] else set()) | \
+        ({"dA1"} if _ffn_fused(dtype, opts) else set())
+    b = {k: f64(v) for k, v in layer.bwd_views().items() if k not in unwritten}
     g = {k: f64(v) for k, v in layer.grads.items()}
     pairs = []
     # ---- forward

@@ -30,8 +30,11 @@ def test_adamw_kernel_vs_oracle():
     outs = [torch.zeros(sz, device="cuda", dtype=torch.bfloat16 if dt == 0 else torch.float32)
             for sz, dt in zip(sizes, dts)]
     segs, off = [], 0
-    for sz, dt, o in zip(sizes, dts, outs):
-        segs.append(_abi.enc_opt_segment(off, sz, o.data_ptr(), dt))
+    nodec = [0, 1, 0, 1]   # segments exempt from weight decay
+    wdv = np.zeros(n)
+    for sz, dt, o, nd in zip(sizes, dts, outs, nodec):
+        segs.append(_abi.enc_opt_segment(off, sz, o.data_ptr(), dt, nd))
+        wdv[off:off + sz] = 0.0 if nd else 1.0
         off += sz
     c_segs = (_abi.enc_opt_segment * len(segs))(*segs)
     lr, b1, b2, eps, wd, gs = 1e-2, 0.9, 0.999, 1e-6, 0.01, 0.5
@@ -42,7 +45,7 @@ def test_adamw_kernel_vs_oracle():
         _abi.check("enc_adamw_step", lib.enc_adamw_step(
             ctx.ptr, n, master.data_ptr(), m.data_ptr(), v.data_ptr(), gd.data_ptr(), c_segs,
             len(segs), lr, b1, b2, eps, wd, t, gs, torch.cuda.current_stream().cuda_stream))
-        P, M, V = adamw_step(P, M, V, g, lr, b1, b2, eps, wd, t, grad_scale=gs)
+        P, M, V = adamw_step(P, M, V, g, lr, b1, b2, eps, wd * wdv, t, grad_scale=gs)
     torch.cuda.synchronize()
     mp = master.cpu().numpy().astype(np.float64)
     assert _rel(mp, P) <= 1e-5
@@ -80,7 +83,7 @@ def test_stack_train_step_updates_parameters():
     """Two training steps of a 2-layer bf16 stack: every layer's parameters equal the
     oracle's AdamW applied to that layer's gradients of each step (master in fp32, model
     copy rounded to bf16 / kept fp32)."""
-    from paper_2007_00072_b200.layer import FFN_BUCKET, ATTN_BUCKET, LayerCfg
+    from paper_2007_00072_b200.layer import FFN_BUCKET, ATTN_BUCKET, WEIGHTS, LayerCfg
     from paper_2007_00072_b200.stack import EncoderStack
     from synth import Dims, SEED_WEIGHTS, make_inputs, make_params
     dims = Dims(B=2, J=128, H=2, P=64, U=512)
@@ -93,6 +96,9 @@ def test_stack_train_step_updates_parameters():
     order = FFN_BUCKET + ATTN_BUCKET
     ref = [lay.master.double().cpu().numpy() for lay in st.layers]
     mom = [(np.zeros_like(r), np.zeros_like(r)) for r in ref]
+    # weight decay on the weight matrices only (biases, LayerNorm gamma/beta exempt)
+    wdv = np.concatenate([np.full(st.layers[0].params[n].numel(), 1.0 if n in WEIGHTS else 0.0)
+                          for n in order])
     for t in (1, 2):
         st.forward(X)
         st.backward(dY)
@@ -101,7 +107,7 @@ def test_stack_train_step_updates_parameters():
         torch.cuda.synchronize()
         for i, lay in enumerate(st.layers):
             ref[i], m, v = adamw_step(ref[i], mom[i][0], mom[i][1], grads[i], 1e-3, 0.9, 0.999,
-                                      1e-6, 0.01, t)
+                                      1e-6, 0.01 * wdv, t)
             mom[i] = (m, v)
             got = lay.master.double().cpu().numpy()
             assert _rel(got, ref[i]) <= 1e-5

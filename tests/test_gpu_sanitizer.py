@@ -1,0 +1,26 @@
+"""compute-sanitizer over one layer step on both the fp32 path and the bf16 product path
+(tools/sanitize_step.py): no memory errors (memcheck), no shared-memory races (racecheck),
+no illegal barrier use (synccheck).  SURVEY.md section 5 (race and failure detection)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    if not os.path.exists(SAN):
+        pytest.skip("compute-sanitizer not found")
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "17", "--target-processes", "all",
+           sys.executable, os.path.join(ROOT, "tools", "sanitize_step.py")]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1500)
+    text = out.stdout + out.stderr
+    assert "sanitize_step done" in text, text[-3000:]
+    assert out.returncode == 0, text[-3000:]
+    assert "ERROR SUMMARY: 0 errors" in text, text[-3000:]
