@@ -19,6 +19,9 @@ def main():
         inp = make_inputs(dims, dtype, key_padding=True)
         tdt = torch.float32 if dtype == "fp32" else torch.bfloat16
         layer = EncoderLayer(dims, dtype, LayerCfg())
+        if os.environ.get("ENC_SANITIZE_SINGLE_CTA") == "1":
+            from paper_2007_00072_b200 import ops
+            ops.enc_set_option(layer.ctx, ops.OPT_GEMM_PAIR, 0)
         layer.set_params(prm)
         X = torch.tensor(inp["X"], device="cuda").to(tdt)
         dY = torch.tensor(inp["dY"], device="cuda").to(tdt)
