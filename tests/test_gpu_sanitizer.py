@@ -28,4 +28,5 @@ def test_sanitizer_clean(tool):
     text = out.stdout + out.stderr
     assert "sanitize_step done" in text, text[-3000:]
     assert out.returncode == 0, text[-3000:]
-    assert "ERROR SUMMARY: 0 errors" in text, text[-3000:]
+    summary = "RACECHECK SUMMARY: 0 hazards" if tool == "racecheck" else "ERROR SUMMARY: 0 errors"
+    assert summary in text, text[-3000:]
