@@ -133,6 +133,11 @@ _SIGS = {
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "enc_attn_keep_bits": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_uint64,
+                                   c_uint64, c_int64, c_void_p, c_void_p]),
+    "enc_attn_fwd_fused_bits": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
+                                        c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
+                                        c_void_p, c_void_p, c_void_p, c_int, c_void_p]),
     "enc_wgemm": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_int64, c_int, c_void_p,
                           c_int64, c_int, c_void_p, c_int64, c_int, c_int, c_void_p, c_void_p]),
     "enc_linear1_bad_fwd": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_void_p,

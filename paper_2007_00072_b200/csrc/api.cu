@@ -55,6 +55,10 @@ struct enc_ctx {
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
+  // fused forward: the attention keep words generated on the side stream beside the QKV
+  // contraction (ENC_OPT_KEEP_AHEAD), joined before the score kernel
+  int keep_ahead = 1;
+  cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction
   uint32_t gemm_tc = 0xFFFFFFFFu;
@@ -254,9 +258,10 @@ int enc_create(enc_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  cudaEvent_t* evs[9] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start, &c->ev_fork,
-                         &c->ev_join, &c->ev_pf,  &c->ev_pfs, &c->ev_bwd};
-  for (int i = 0; i < 9 && e == cudaSuccess; ++i)
+  cudaEvent_t* evs[11] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
+                          &c->ev_fork, &c->ev_join, &c->ev_pf,  &c->ev_pfs,
+                          &c->ev_bwd,  &c->ev_kb_fork, &c->ev_kb_join};
+  for (int i = 0; i < 11 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -297,7 +302,7 @@ void enc_destroy(enc_ctx* c) {
   }
   if (c->lt) lt_destroy(c->lt);
   for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join,
-                         c->ev_pf, c->ev_pfs, c->ev_bwd})
+                         c->ev_pf, c->ev_pfs, c->ev_bwd, c->ev_kb_fork, c->ev_kb_join})
     if (ev) cudaEventDestroy(ev);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side_ws) cudaFree(c->side_ws);
@@ -773,6 +778,41 @@ int enc_attn_fwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   return ENC_OK;
 }
 
+int enc_attn_keep_bits(enc_ctx* ctx, int B, int H, int J, int K, float p, uint64_t seed,
+                       uint64_t subseq, int64_t batch_offset, uint32_t* keep_bits,
+                       enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || J <= 0 || K <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (K % 64) return ENC_EALIGN;
+  if (!keep_bits) return ENC_ENULL;
+  if ((uintptr_t)keep_bits & 7u) return ENC_EALIGN;
+  if (B == 0) return ENC_OK;
+  CK(launch_attn_keep_bits(B, H, J, K, make_philox_key(p, seed, subseq), batch_offset,
+                           keep_bits, (cudaStream_t)stream));
+  ctx->launches += 1;
+  return ENC_OK;
+}
+
+int enc_attn_fwd_fused_bits(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
+                            const void* Kt, const float* mask_bias, float p, uint64_t seed,
+                            uint64_t subseq, int64_t batch_offset, void* Pout, void* A,
+                            const uint32_t* keep_bits, int causal, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(Q, Kt, Pout);
+  if (!keep_bits) return ENC_ENULL;
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if ((uintptr_t)keep_bits & 7u) return ENC_EALIGN;
+  if (B == 0) return ENC_OK;
+  OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
+  CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, P, Kt, P, mask_bias,
+                        make_philox_key(p, seed, subseq), batch_offset, Pout, A,
+                        const_cast<uint32_t*>(keep_bits), (cudaStream_t)stream, causal ? 1 : 0,
+                        1));
+  return ENC_OK;
+}
+
 int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
                        const void* V, const void* Pin, float p, uint64_t seed, uint64_t subseq,
                        int64_t batch_offset, const uint32_t* keep_bits, void* dS,
@@ -829,6 +869,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_GEMM_TC_MASK) {
     ctx->gemm_tc = (uint32_t)value;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_KEEP_AHEAD) {
+    ctx->keep_ahead = value ? 1 : 0;
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_PAIR) {
@@ -983,6 +1027,19 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
       return ENC_EUNSUPPORTED;   // Q, K, V regions not contiguous (cannot happen: J % 128 == 0)
   }
 
+  // fused path: the attention keep words (4.2 MB at config L) are generated on the side
+  // stream while the QKV contraction runs (it leaves the FMA pipe idle), so the fused score
+  // kernel reads them instead of running Philox between its MMA and its epilogue
+  const PhiloxKey pk_attn = make_philox_key(cfg->p_attn, cfg->seed, l4 + 0);
+  uint32_t* kbits = (uint32_t*)at(saved, SL.off[S_KB]);
+  const bool keep_ahead = fused_attn && ctx->keep_ahead && ctx->side && K % 64 == 0;
+  if (keep_ahead) {
+    CK(cudaEventRecord(ctx->ev_kb_fork, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_kb_fork, 0));
+    CK(launch_attn_keep_bits(B, H, J, K, pk_attn, boff, kbits, ctx->side));
+    ctx->launches += 1;
+    CK(cudaEventRecord(ctx->ev_kb_join, ctx->side));
+  }
   // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T (+ bqkv, AIB :550, on the direct path)
   // (cuBLASLt takes a bf16 output's bias in bf16: the bias is rounded to bf16 for the
   // epilogue, R18; the conversion is one tiny kernel)
@@ -1018,13 +1075,13 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // fused + per-(b, h) path: A = dropout(P) is never stored -- the A V (and backward
   // A^T dC) contraction applies the stored keep bits to P while it is in shared memory
   const bool drop_on_load = fused_attn && use_bh(ctx, J, P);
-  const PhiloxKey pk_attn = make_philox_key(cfg->p_attn, cfg->seed, l4 + 0);
-  uint32_t* kbits = (uint32_t*)at(saved, SL.off[S_KB]);
   if (fused_attn) {
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
+    if (keep_ahead) CK(cudaStreamWaitEvent(st, ctx->ev_kb_join, 0));
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
     CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias, pk_attn, boff, Pm,
-                          drop_on_load ? nullptr : A, kbits, st, cfg->causal ? 1 : 0));
+                          drop_on_load ? nullptr : A, kbits, st, cfg->causal ? 1 : 0,
+                          keep_ahead ? 1 : 0));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {

@@ -52,6 +52,7 @@ struct FusedParams {
   uint32_t* keep_bits;     // [B, H, J, K/32] keep-flag words (fwd: written if non-null;
                            // bwd: read instead of recomputing Philox when kBits)
   int write_a;             // fwd: A = dropout(P) stored (0: only P and the keep words)
+  int keep_pre;            // fwd: keep_bits already hold this call's keep words (read them)
 };
 
 __device__ __forceinline__ void qbar(int q) {   // the 8 warps of TMEM lane quarter q
@@ -242,7 +243,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
     const int64_t rowi = (int64_t)bh * prm.J + m0 + r;
     uint32_t kf[kW / 32];
     uint32_t* kbw = prm.keep_bits + rowi * (kK / 32) + cb / 32;
-    if (kBwd && kBits) {
+    if (kBits && (kBwd || prm.keep_pre)) {
       const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(kbw));
       kf[0] = w2.x;
       kf[1] = w2.y;
@@ -550,7 +551,55 @@ cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const 
   return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk);
 }
 
+// The attention keep words (ENC_KEEP_BITS layout) of a [B,H,J,K] call: one thread per 64
+// columns (two words, eight Philox4x32-10 calls).  Launched ahead of the fused forward --
+// in the layer on a side stream beside the QKV contraction, whose tensor-bound tiles leave
+// the FMA pipe idle -- so the score kernel reads the words instead of running Philox
+// between its MMA and its epilogue.
+__global__ void __launch_bounds__(128) keep_bits_kernel(uint32_t* __restrict__ keep_bits,
+                                                        int64_t n2, int K, int64_t g0,
+                                                        PhiloxKey pk) {
+  const bool hiT = pk.T >= 0x8000u;
+  const uint32_t C2 = (hiT ? 0x10000u - pk.T : 0x8000u - pk.T) * 0x10001u;
+  const uint32_t X = hiT ? 0u : 0xFFFFFFFFu;
+  const int w2r = K / 64;   // word pairs per row
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rowi = i / w2r;
+    const int cb = (int)(i - rowi * w2r) * 64;
+    const int64_t grow = g0 + rowi * (K / 8) + cb / 8;
+    uint32_t kf[2];
+    if (pk.T == 0) {
+      kf[0] = kf[1] = 0xFFFFFFFFu;
+    } else {
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t f = 0;
+#pragma unroll 2
+        for (int j = 0; j < 4; ++j) f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, X, 4 * j);
+        kf[c] = f;
+      }
+    }
+    __stcs(reinterpret_cast<uint2*>(keep_bits) + i, make_uint2(kf[0], kf[1]));
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& pk,
+                                  int64_t batch_offset, uint32_t* keep_bits, cudaStream_t st) {
+  if (K % 64) return cudaErrorInvalidValue;
+  const int64_t n2 = (int64_t)B * H * J * (K / 64);
+  if (n2 == 0) return cudaSuccess;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (n2 + 127) / 128;
+  if (grid > 4 * sms) grid = 4 * sms;
+  keep_bits_kernel<<<(int)grid, 128, 0, st>>>(keep_bits, n2, K,
+                                              batch_offset * (int64_t)H * J * (K / 8), pk);
+  return cudaGetLastError();
+}
 
 // K = J = 512 (the whole score row in the 512 TMEM columns), P = 64
 bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
@@ -558,7 +607,7 @@ bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
-                               uint32_t* keep_bits, cudaStream_t st, int causal) {
+                               uint32_t* keep_bits, cudaStream_t st, int causal, int keep_pre) {
   const int K = J;
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
@@ -567,7 +616,7 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,         J,         tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8),
-                  mask_bias, keep_bits, Aout != nullptr};
+                  mask_bias, keep_bits, Aout != nullptr, keep_pre && keep_bits ? 1 : 0};
   if (causal) {   // the masking step: keys k > j of each query row j removed
     if (mask_bias)
       return keep_bits ? launch_persistent(attn_qk_bsb_kernel<true, true, true>, tiles, mq, mk, mp,
@@ -600,7 +649,7 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,       J,       tiles, scale, batch_offset * (int64_t)H * J * (K / 8),
-                  nullptr, const_cast<uint32_t*>(keep_bits), 0};
+                  nullptr, const_cast<uint32_t*>(keep_bits), 0, 0};
   return keep_bits
              ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st,
                                  high_prio)

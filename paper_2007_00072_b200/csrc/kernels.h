@@ -221,7 +221,12 @@ bool attn_fused_supported(int J, int P);
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
-                               uint32_t* keep_bits, cudaStream_t st, int causal = 0);
+                               uint32_t* keep_bits, cudaStream_t st, int causal = 0,
+                               int keep_pre = 0);
+// keep words of the attention dropout (ENC_KEEP_BITS layout) for [B,H,J,K], K % 64 == 0; the
+// fused forward reads them with keep_pre = 1
+cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& pk,
+                                  int64_t batch_offset, uint32_t* keep_bits, cudaStream_t st);
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,

@@ -128,7 +128,8 @@ def enc_set_option(ctx, key, value):
 
 
 (OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT,
- OPT_BWD_SIDE, OPT_ATTN_OVERLAP, OPT_GEMM_TC, OPT_GEMM_PAIR, OPT_GEMM_TC_MASK) = range(11)
+ OPT_BWD_SIDE, OPT_ATTN_OVERLAP, OPT_GEMM_TC, OPT_GEMM_PAIR, OPT_GEMM_TC_MASK,
+ OPT_KEEP_AHEAD) = range(12)
 
 
 def enc_attn_fwd_fused(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq, batch_offset,
@@ -171,3 +172,15 @@ def enc_linear2_dx_bad_bwd(ctx, B, J, I, U, dY2, W2, h, act, p, seed, subseq, ba
     check("enc_linear2_dx_bad_bwd", _abi.load().enc_linear2_dx_bad_bwd(
         ctx.ptr, B, J, I, U, _p(dY2), _p(W2), _p(h), act, p, seed, subseq, batch_offset, _p(dh),
         _p(db1), _stream(stream)))
+
+
+def enc_attn_keep_bits(ctx, B, H, J, K, p, seed, subseq, batch_offset, keep_bits, stream=None):
+    check("enc_attn_keep_bits", _abi.load().enc_attn_keep_bits(
+        ctx.ptr, B, H, J, K, p, seed, subseq, batch_offset, _p(keep_bits), _stream(stream)))
+
+
+def enc_attn_fwd_fused_bits(ctx, B, H, J, P, scale, Q, K, mask_bias, p, seed, subseq,
+                            batch_offset, Pout, A, keep_bits, stream=None, causal=False):
+    check("enc_attn_fwd_fused_bits", _abi.load().enc_attn_fwd_fused_bits(
+        ctx.ptr, B, H, J, P, scale, _p(Q), _p(K), _p(mask_bias), p, seed, subseq, batch_offset,
+        _p(Pout), _p(A), _p(keep_bits), int(causal), _stream(stream)))

@@ -157,3 +157,49 @@ def test_fused_forward_causal(ops, ctx, B, H, masked, p):
     gdS = host(dS)
     assert (gdS[..., np.triu(np.ones((J, J), bool), 1)] == 0).all()
     assert_parity("dS", gdS, dSo, "bf16")
+
+
+@pytest.mark.parametrize("B,H,J,K", [(1, 1, 512, 512), (2, 3, 512, 512), (3, 2, 128, 128),
+                                     (1, 2, 7, 192)])
+@pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
+def test_keep_bits_kernel(ops, ctx, B, H, J, K, p):
+    """enc_attn_keep_bits (the layer's side-stream launch) writes exactly the oracle's mask."""
+    boff, sub = 3, 12
+    bits = torch.full((B, H, J, K // 32), -1, dtype=torch.int32, device="cuda")
+    ops.enc_attn_keep_bits(ctx, B, H, J, K, p, SEED, sub, boff, bits)
+    torch.cuda.synchronize()
+    keep = philox.keep_mask_tensor((B, H, J, K), boff, p, SEED, sub)
+    assert np.array_equal(decode(bits.cpu().numpy(), K), keep)
+
+
+@pytest.mark.parametrize("masked", [False, True])
+@pytest.mark.parametrize("p", [0.1, 0.6])
+def test_fused_forward_given_bits_equals_regenerated(ops, ctx, masked, p):
+    """The fused forward reading precomputed keep words gives bitwise the P / A of the one
+    that runs Philox itself."""
+    B, H, J, P = 2, 3, 512, 64
+    Q = dev(make_tensor((B, H, J, P), 31, "bf16", std=0.8))
+    K = dev(make_tensor((B, H, J, P), 32, "bf16", std=0.8))
+    Mt = None
+    if masked:
+        M = np.zeros((B, J), np.float32)
+        M[:, 300:] = -10000.0
+        Mt = torch.tensor(M, device="cuda")
+    boff, sub = 1, 4
+    out = []
+    for given in (False, True):
+        Pm = torch.empty((B, H, J, J), dtype=torch.bfloat16, device="cuda")
+        A = torch.empty_like(Pm)
+        bits = torch.empty((B, H, J, J // 32), dtype=torch.int32, device="cuda")
+        if given:
+            ops.enc_attn_keep_bits(ctx, B, H, J, J, p, SEED, sub, boff, bits)
+            ops.enc_attn_fwd_fused_bits(ctx, B, H, J, P, 0.125, Q, K, Mt, p, SEED, sub, boff, Pm, A,
+                                        bits)
+        else:
+            ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, Mt, p, SEED, sub, boff, Pm, A,
+                                   keep_bits=bits)
+        torch.cuda.synchronize()
+        out.append((Pm, A, bits))
+    assert torch.equal(out[0][0], out[1][0])
+    assert torch.equal(out[0][1], out[1][1])
+    assert torch.equal(out[0][2], out[1][2])
