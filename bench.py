@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--layers", type=int, default=1,
                     help="encoder layers per step (24 = the BERT-large encoder stack, config 4 "
                          "of BASELINE.json; per-layer gradient all-reduce for N > 1)")
+    ap.add_argument("--opt", action="append", default=[], metavar="KEY=VALUE",
+                    help="extra enc_set_option(KEY, VALUE) on the layer context (repeatable; "
+                         "include/encoder.h ENC_OPT_*)")
     ap.add_argument("--eager", action="store_true",
                     help="launch every step eagerly instead of replaying a CUDA graph")
     return ap.parse_args()
@@ -248,6 +251,9 @@ def main():
                                                             int(args.bwd_side)))
     _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, 7,
                                                             int(args.attn_overlap)))
+    for kv in args.opt:
+        k, v = (int(x) for x in kv.split("="))
+        _abi.check("enc_set_option", _abi.load().enc_set_option(layer.ctx.ptr, k, v))
     inp = make_inputs(dims_global, args.dtype)
     X = torch.tensor(inp["X"][boff:boff + B], device=dev).to(tdt)
     dY = torch.tensor(inp["dY"][boff:boff + B], device=dev).to(tdt)
@@ -592,7 +598,8 @@ def main():
                        "l2": "flushed (512 MB write) between steps" if not args.no_flush
                        else "not flushed", "graph": "eager launches" if args.eager
                        else f"CUDA graph replay (fwd+bwd, {len(parts)} graph(s) per step)",
-                       "attention": attention_desc(args, dims)},
+                       "attention": attention_desc(args, dims),
+                       "options": args.opt or None},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             # ops fused away on this path (no launch of their own) are null

@@ -594,8 +594,11 @@ cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& p
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // one 128-thread block per SM: beside the persistent QKV contraction (1 CTA per SM, 96
+  // registers x 576 threads) a block of 128 x 30 registers still fits, so the two overlap
+  // whichever is placed first
   int64_t grid = (n2 + 127) / 128;
-  if (grid > 4 * sms) grid = 4 * sms;
+  if (grid > sms) grid = sms;
   keep_bits_kernel<<<(int)grid, 128, 0, st>>>(keep_bits, n2, K,
                                               batch_offset * (int64_t)H * J * (K / 8), pk);
   return cudaGetLastError();
