@@ -57,7 +57,7 @@ struct enc_ctx {
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
   // fused forward: the attention keep words generated on the side stream beside the QKV
   // contraction (ENC_OPT_KEEP_AHEAD), joined before the score kernel
-  int keep_ahead = 1;
+  int keep_ahead = 0;   // measured slower at config L (the QKV contraction is slowed more)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction

@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(128) keep_bits_kernel(uint32_t* __restrict__ k
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t f = 0;
-#pragma unroll 2
+#pragma unroll
         for (int j = 0; j < 4; ++j) f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, X, 4 * j);
         kf[c] = f;
       }
@@ -598,7 +598,7 @@ cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& p
   // registers x 576 threads) a block of 128 x 30 registers still fits, so the two overlap
   // whichever is placed first
   int64_t grid = (n2 + 127) / 128;
-  if (grid > sms) grid = sms;
+  if (grid > 2 * sms) grid = 2 * sms;
   keep_bits_kernel<<<(int)grid, 128, 0, st>>>(keep_bits, n2, K,
                                               batch_offset * (int64_t)H * J * (K / 8), pk);
   return cudaGetLastError();

@@ -259,7 +259,7 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {OPT_GEMM_TC: 0},                      # weight contractions on cuBLASLt, BAD separate
     {OPT_GEMM_TC_MASK: (1 << 7) | (1 << 12)},   # only the fused FFN kernels on tcgen05
     {OPT_GEMM_PAIR: 0},                    # single-CTA weight-contraction tiles
-    {11: 0},                               # fused forward runs Philox itself (no keep-ahead)
+    {11: 1},                               # keep words generated ahead on the side stream
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
