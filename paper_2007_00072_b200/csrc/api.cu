@@ -60,8 +60,11 @@ struct enc_ctx {
   int keep_ahead = 0;   // measured slower at config L (the QKV contraction is slowed more)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
-  // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction
-  uint32_t gemm_tc = 0xFFFFFFFFu;
+  // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
+  // Default = the measured selection at configs L and Bb: the two
+  // fused FFN kernels (Linear1 + BAD, Linear2-dX + BAD-bwd) on tcgen05, the plain
+  // contractions on cuBLASLt (its tuned kernels measured 2-8 us faster per contraction)
+  uint32_t gemm_tc = (1u << ENC_OP_GEMM_L1) | (1u << ENC_OP_GEMM_L2_DX);
   int gemm_cg = 0;           // ENC_OPT_GEMM_PAIR 1 (default) -> 0 (auto), 0 -> 1 (single CTAs)
   void* wg_ws = nullptr;     // split-K partial slabs of the fp32 weight-gradient outputs
   void* wg_ws_side = nullptr;   // the same for contractions on the side stream
