@@ -460,6 +460,45 @@ def main():
         except (OSError, ValueError):
             pass
 
+    # ---------------- every operator's in-graph duration and roofline fraction: the step is
+    # captured once more with event-record nodes around every operator (all timing bits
+    # on) and replayed; fused ops against the HBM peak (algorithmic bytes, tally.py),
+    # contractions against the tensor peak (flops).  Not the timed region.
+    op_graph_us, op_frac = {}, {}
+    if not args.eager and world == 1 and stack is None:
+        lib.enc_set_timing(layer.ctx.ptr, (1 << nops) - 1)
+        set_opt(6, 0)   # side-stream overlap off: each op's events bracket only its kernels
+        g_all = torch.cuda.CUDAGraph()
+        s_all = torch.cuda.Stream(dev)
+        s_all.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s_all):
+            step()
+        torch.cuda.current_stream(dev).wait_stream(s_all)
+        with torch.cuda.graph(g_all):
+            step()
+        reps = {n: [] for n in names}
+        for _ in range(5):
+            if not args.no_flush:
+                flush.zero_()
+            g_all.replay()
+            torch.cuda.synchronize()
+            _abi.check("enc_op_times", lib.enc_op_times(layer.ctx.ptr, ms_buf))
+            for i, n in enumerate(names):
+                reps[n].append(ms_buf[i])
+        for n in names:
+            t = statistics.median(reps[n])
+            if t <= 0 or per_op[n] < 0:
+                continue
+            op_graph_us[n] = round(t * 1e3, 2)
+            if n in fused and fused[n]:
+                op_frac[n] = {"bound": "hbm", "frac": round(fused[n] / (t * 1e-3) / 1e9 / hbm_peak, 3)}
+            elif n in flops:
+                op_frac[n] = {"bound": "tensor",
+                              "frac": round(flops[n] / (t * 1e-3) / 1e12 / tc_peak, 3)}
+        set_opt(6, int(args.bwd_side))
+        lib.enc_set_timing(layer.ctx.ptr, 1 << dom_id)
+        del g_all
+
     # ---------------- end to end through the C ABI with host buffers
     Xh = X.cpu().pin_memory()
     dYh = dY.cpu().pin_memory()
@@ -626,6 +665,7 @@ def main():
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
             # ops fused away on this path (no launch of their own) are null
+            "per_op_graph_us": op_graph_us or None, "rooflines": op_frac or None,
             "per_op_us": {n: (round(per_op[n] * 1e3, 2) if per_op[n] >= 0 else None)
                           for n in names},
         }

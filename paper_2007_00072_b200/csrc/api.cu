@@ -1134,11 +1134,9 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
   WgemmArgs l1 = ffn_fwd_args(ctx, d, dtype, cfg, X1, prm->W1, prm->b1, pk_ffn, h, A1);
   if (wgemm_supported(l1)) {
-    {
-      OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 1);
-      CK(launch_wgemm(l1, ctx->num_sms, st));
-    }
-    OpTimer _t(ctx, ENC_OP_BAD_FWD, st, 0);   // fused away
+    // (BAD has no launch of its own: no ENC_OP_BAD_FWD timing on this path)
+    OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 1);
+    CK(launch_wgemm(l1, ctx->num_sms, st));
   } else {
     {
       OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 0);
@@ -1300,9 +1298,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                            g->dW2, U, nullptr, sws)))
           return r;
       }
-      OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 0 : 1);   // fused away
+      // BAD-bwd has no launch of its own: db1's partials are finished with the half's
+      // column sums (timed as ENC_OP_BAD_BWD only when that finalize launches here)
       CK(colsum_finish(w, R, U, U, g->db1, nullptr, nullptr, st));
-      if (!ffn_deferred) CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+      if (!ffn_deferred) {
+        OpTimer _t(ctx, ENC_OP_BAD_BWD, st, 1);
+        CK(launch_colsum_finalize_jobs(ffn_jobs, 2, st));
+      }
     } else {
       {
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DX, st, 0);
