@@ -120,8 +120,10 @@ struct OpTimer {
   int op;
   cudaStream_t st;
   bool on;
-  OpTimer(enc_ctx* c_, int op_, cudaStream_t st_, int launches)
-      : c(c_), op(op_), st(st_), on((c_->timing_mask >> op_) & 1ull) {
+  // active = false: the operator is fused into another kernel on this path (no work of its
+  // own, not timed: enc_op_times reports -1 for it)
+  OpTimer(enc_ctx* c_, int op_, cudaStream_t st_, int launches, bool active = true)
+      : c(c_), op(op_), st(st_), on(active && ((c_->timing_mask >> op_) & 1ull)) {
     c->launches += launches;
     if (on) record(c->ev0[op]);
   }
@@ -1069,7 +1071,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   }
   // AIB (:550): in place on the direct path unless the epilogue added the bias
   {
-    OpTimer _t(ctx, ENC_OP_AIB_FWD, st, direct && bias_done ? 0 : 1);
+    OpTimer _t(ctx, ENC_OP_AIB_FWD, st, direct && bias_done ? 0 : 1, !(direct && bias_done));
     if (!direct)
       CK(launch_aib_fwd(dtype, B, J, H, P, QKV, prm->bqkv, Q, Kt, V, st));
     else if (!bias_done)
@@ -1370,7 +1372,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, fused_attn ? 0 : 1);
+    OpTimer _t(ctx, ENC_OP_GEMM_AV_DA, st, fused_attn ? 0 : 1, !fused_attn);
     if (fused_attn) {
       // dA is produced inside the fused dA + BSB-bwd kernel below
     } else if (tc_attn) {
@@ -1440,7 +1442,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
                          P, (long long)K * P, 0.f, dQ, P, (long long)J * P, BH));
   }
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, tc_attn && !dqdk_one_pass ? 1 : 0);
+    OpTimer _t(ctx, ENC_OP_GEMM_QK_DK, st, tc_attn && !dqdk_one_pass ? 1 : 0, !dqdk_one_pass);
     if (dqdk_one_pass) {
       // computed with dQ above
     } else if (tc_attn)

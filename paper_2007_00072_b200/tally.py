@@ -32,7 +32,7 @@ def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = Fals
     else:
         bsb_f = 3 * BHJK * es + (B * J * f if mask_bias else 0)
         bsb_b = 3 * BHJK * es
-    return {
+    out = {
         "aib_fwd": 0 if direct else 2 * BJ * 3 * I * es + 3 * I * f,
         "bsb_fwd": bsb_f,
         "bdrln_fwd1": 4 * BJI * es + BJ * f + 3 * I * f,
@@ -44,6 +44,15 @@ def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = Fals
         "bsb_bwd": bsb_b,
         "aib_bwd": 0 if direct else 2 * BJ * 3 * I * es + 3 * I * f,
     }
+    if fused_attn:
+        # the attention contractions are HBM-bound (51 flop/B at L): the
+        # per-(b,h) streaming kernels read the [J x K] matrix once (P + keep words, dropout
+        # applied on load; dS for dQ and dK together) and the P-wide operands
+        bits = BHJK // 8
+        out["gemm_av"] = BHJK * es + bits + 2 * BJI * es
+        out["gemm_av_dv"] = BHJK * es + bits + 2 * BJI * es
+        out["gemm_qk_dq"] = BHJK * es + 4 * BJI * es
+    return out
 
 
 def gemm_flops(d) -> dict:
@@ -73,7 +82,8 @@ def step_flops(d) -> int:
 def step_kernel_bytes(d, es: int = 2) -> dict:
     """Algorithmic HBM bytes of every kernel of one fwd+bwd step on the default bf16 path at
     J = 512 (fused score kernels, per-(b,h) contractions with dropout on load, in-place QKV,
-    cuBLASLt weight contractions), for the data-movement tally against the paper's Table A.1
+    Linear1 + BAD and Linear2-dX + BAD-bwd fused tcgen05 kernels, the other weight
+    contractions plain), for the data-movement tally against the paper's Table A.1
     totals (DESIGN.md section 6).  Weights counted once per contraction that reads them;
     fp32 gradient outputs 4 B; BDRLN / BAD masks regenerated, attention mask as 1-bit words."""
     B, J, H, P, I, U = _d(d)
@@ -89,15 +99,13 @@ def step_kernel_bytes(d, es: int = 2) -> dict:
         "av (dropout on load)": s + bits + x + x,
         "gemm_out": x + wo + x,
         "bdrln_fwd1": 4 * x + BJ * f,
-        "gemm_l1": x + w1 + xu,
-        "bad_fwd": 2 * xu,
+        "gemm_l1 + BAD (fused)": x + w1 + 2 * xu,
         "gemm_l2": xu + w1 + x,
         "bdrln_fwd2": 4 * x + BJ * f,
         # backward
         "bdrln_bwd2": 4 * x + BJ * f,
-        "gemm_l2_dx": x + w1 + xu,
+        "gemm_l2_dx + BAD-bwd (fused)": x + w1 + 2 * xu,
         "gemm_l2_dw": x + xu + I * U * f,
-        "bad_bwd": 3 * xu,
         "gemm_l1_dx (+dz2)": xu + w1 + 2 * x,
         "gemm_l1_dw": xu + x + U * I * f,
         "bdrln_bwd1": 4 * x + BJ * f,
