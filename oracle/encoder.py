@@ -285,3 +285,64 @@ def encoder_layer_backward(dY, X, prm, H, cfg: Cfg, saved):
     inter = dict(dz2=dz2, dY2=dY2, dA1=dA1, dh=dh, dX1=dX1, dz1=dz1, dYo=dYo, dC=dC, dA=dA,
                  dV=dV, dS=dS, dQ=dQ, dK=dK, dQKV=dQKV)
     return dX, grads, inter
+
+
+# ----------------------------------------------------------------------------------
+# Encoder-decoder (cross) attention sublayer -- the second workload of SURVEY.md 8(f)4:
+# queries from the decoder stream X [B,J,I], keys and values from the encoder memory
+# Mem [B,K,I] projected by one stacked weight [W^K W^V] (the algebraic "fuse keys and
+# values in encoder/decoder attention"), then the same BSB (site 0) and
+# BDRLN (site 1, residual X, post-LN) as the encoder layer.  K may differ from J.
+# ----------------------------------------------------------------------------------
+def cross_attention_forward(X, Mem, prm, H, cfg: Cfg, mask_bias=None):
+    """prm: Wq [I,I], Wkv [2I,I], Wo [I,I], bq [I], bkv [2I], bo [I], g, be [I].
+    Returns (Y, saved)."""
+    X, Mem = _f(X), _f(Mem)
+    B, J, I = X.shape
+    K = Mem.shape[1]
+    P = I // H
+    scale = 1.0 / np.sqrt(P)
+    sub = lambda site: philox.subsequence(cfg.layer_id, site)   # noqa: E731
+    Qf = _lin(X, prm["Wq"]) + _f(prm["bq"])                      # [B,J,I]
+    KV = _lin(Mem, prm["Wkv"]) + _f(prm["bkv"])                  # [B,K,2I] keys | values
+    Q = Qf.reshape(B, J, H, P).transpose(0, 2, 1, 3)
+    Kh = KV[..., :I].reshape(B, K, H, P).transpose(0, 2, 1, 3)
+    V = KV[..., I:].reshape(B, K, H, P).transpose(0, 2, 1, 3)
+    S = np.matmul(Q, Kh.transpose(0, 1, 3, 2))                   # [B,H,J,K]
+    Pm, A = bsb_fwd(S, mask_bias, scale, cfg.p_attn, cfg.seed, sub(SITE_ATTN), cfg.batch_offset)
+    C = np.matmul(A, V).transpose(0, 2, 1, 3).reshape(B, J, I)
+    Yo = _lin(C, prm["Wo"])
+    Y, xhat, rstd = bdrln_fwd(Yo, prm["bo"], X, prm["g"], prm["be"], cfg.ln_eps, cfg.p_hidden,
+                              cfg.seed, sub(SITE_ATTN_OUT), cfg.batch_offset)
+    saved = dict(Q=Q, K=Kh, V=V, KV=KV, S=S, P=Pm, A=A, C=C, Yo=Yo, xhat=xhat, rstd=rstd, Y=Y)
+    return Y, saved
+
+
+def cross_attention_backward(dY, X, Mem, prm, H, cfg: Cfg, saved):
+    """Returns (dX, dMem, grads) with grads keyed Wq, Wkv, Wo, bq, bkv, bo, g, be (sums over
+    the local batch)."""
+    dY, X, Mem = _f(dY), _f(X), _f(Mem)
+    B, J, I = X.shape
+    K = Mem.shape[1]
+    P = I // H
+    scale = 1.0 / np.sqrt(P)
+    sub = lambda site: philox.subsequence(cfg.layer_id, site)   # noqa: E731
+    sv = saved
+    dz, dYo, dg, dbe, dbo = bdrln_bwd(dY, sv["xhat"], sv["rstd"], prm["g"], cfg.p_hidden,
+                                      cfg.seed, sub(SITE_ATTN_OUT), cfg.batch_offset)
+    dC = np.matmul(dYo, _f(prm["Wo"]))
+    dWo = np.einsum("bji,bjk->ik", dYo, sv["C"])
+    dCbh = dC.reshape(B, J, H, P).transpose(0, 2, 1, 3)
+    dA = np.matmul(dCbh, sv["V"].transpose(0, 1, 3, 2))
+    dV = np.matmul(sv["A"].transpose(0, 1, 3, 2), dCbh)          # [B,H,K,P]
+    dS = bsb_bwd(dA, sv["P"], scale, cfg.p_attn, cfg.seed, sub(SITE_ATTN), cfg.batch_offset)
+    dQ = np.matmul(dS, sv["K"])                                  # [B,H,J,P]
+    dK = np.matmul(dS.transpose(0, 1, 3, 2), sv["Q"])            # [B,H,K,P]
+    dQf = dQ.transpose(0, 2, 1, 3).reshape(B, J, I)
+    dKV = np.concatenate([dK.transpose(0, 2, 1, 3).reshape(B, K, I),
+                          dV.transpose(0, 2, 1, 3).reshape(B, K, I)], axis=-1)
+    dX = np.matmul(dQf, _f(prm["Wq"])) + dz
+    dMem = np.matmul(dKV, _f(prm["Wkv"]))
+    grads = dict(Wq=np.einsum("bjo,bji->oi", dQf, X), Wkv=np.einsum("bko,bki->oi", dKV, Mem),
+                 Wo=dWo, bq=dQf.sum(axis=(0, 1)), bkv=dKV.sum(axis=(0, 1)), bo=dbo, g=dg, be=dbe)
+    return dX, dMem, grads

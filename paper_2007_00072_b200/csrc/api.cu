@@ -57,7 +57,8 @@ struct enc_ctx {
   cudaEvent_t ev_pf = nullptr, ev_pfs = nullptr, ev_bwd = nullptr;
   // fused forward: the attention keep words generated on the side stream beside the QKV
   // contraction (ENC_OPT_KEEP_AHEAD), joined before the score kernel
-  int keep_ahead = 0;   // measured slower at config L (the QKV contraction is slowed more)
+  int keep_ahead = 0;
+  int qkv_fusion = ENC_QKV_STACKED;   // ENC_OPT_QKV_FUSION (Table A.2 algebraic fusion)   // measured slower at config L (the QKV contraction is slowed more)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
@@ -82,6 +83,20 @@ static int wcontract(enc_ctx* ctx, int op, cudaStream_t st, int in_dt, int out_d
                      bool tB, int M, int N, int K, const void* A, int lda, const void* B,
                      int ldb, float beta, void* C, int ldc, const float* bias = nullptr,
                      void* lt_ws = nullptr);
+
+// Groups of stacked Q / K / V weight blocks (block 0 = Q, 1 = K, 2 = V) contracted together
+// under each algebraic-fusion variant of Table A.2
+static void qkv_groups(int mode, int* n, int* start, int* count) {
+  switch (mode) {
+    case ENC_QKV_SEPARATE: *n = 3; start[0] = 0; start[1] = 1; start[2] = 2;
+      count[0] = count[1] = count[2] = 1; return;
+    case ENC_QKV_QK_STACKED: *n = 2; start[0] = 0; count[0] = 2; start[1] = 2; count[1] = 1;
+      return;
+    case ENC_QKV_KV_STACKED: *n = 2; start[0] = 0; count[0] = 1; start[1] = 1; count[1] = 2;
+      return;
+    default: *n = 1; start[0] = 0; count[0] = 3; return;
+  }
+}
 
 // weight contractions: cuBLASLt with per-shape measured algorithm choice, or cuBLAS
 static cublasStatus_t wgemm(enc_ctx* ctx, cudaStream_t st, int in_dt, int out_dt, bool tA,
@@ -876,6 +891,11 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->gemm_tc = (uint32_t)value;
     return ENC_OK;
   }
+  if (key == ENC_OPT_QKV_FUSION) {
+    if (value < ENC_QKV_SEPARATE || value > ENC_QKV_KV_STACKED) return ENC_EINVAL;
+    ctx->qkv_fusion = value;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_KEEP_AHEAD) {
     ctx->keep_ahead = value ? 1 : 0;
     return ENC_OK;
@@ -1045,29 +1065,46 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     ctx->launches += 1;
     CK(cudaEventRecord(ctx->ev_kb_join, ctx->side));
   }
-  // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T (+ bqkv, AIB :550, on the direct path)
-  // (cuBLASLt takes a bf16 output's bias in bf16: the bias is rounded to bf16 for the
-  // epilogue, R18; the conversion is one tiny kernel)
+  // Q,K,V (Table A.1 :549): QKV[BJ,3I] = X Wqkv^T (+ bqkv, AIB :550, on the direct path),
+  // as one contraction per group of stacked weight blocks (algebraic fusion, Table A.2,
+  // Q, K, V separate / QK stacked + V / QKV stacked (default) / Q + KV
+  // stacked), each writing its column blocks of QKV (row stride 3I).  cuBLASLt takes a bf16
+  // output's bias in bf16: rounded to bf16 for its epilogue (R18; one cast kernel).
+  int ngrp = 0, gstart[3], gcount[3];
+  qkv_groups(ctx->qkv_fusion, &ngrp, gstart, gcount);
   bool bias_done = false;
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV, st, 0);
-    if (direct) {   // tcgen05 contraction: the fp32 bias is added in its epilogue
-      r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I,
-                    prm->Wqkv, I, 0.f, QKVs, 3 * I, prm->bqkv);
-      if (r == ENC_OK) bias_done = true;
-      else if (r != ENC_EUNSUPPORTED) return r;
+    void* qkv_out = direct ? QKVs : QKV;
+    bool cast_done = false;
+    for (int gi = 0; gi < ngrp; ++gi) {
+      const int s0 = gstart[gi], nI = gcount[gi] * I;
+      const void* Wg = (const char*)prm->Wqkv + (size_t)s0 * I * I * es;
+      void* Cg = (char*)qkv_out + (size_t)s0 * I * es;
+      bool done = false;
+      if (direct && (gi == 0 || bias_done)) {   // tcgen05: the fp32 bias in its epilogue
+        r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, nI, I, X, I, Wg,
+                      I, 0.f, Cg, 3 * I, prm->bqkv + (size_t)s0 * I);
+        if (r == ENC_OK) done = true;
+        else if (r != ENC_EUNSUPPORTED) return r;
+      }
+      if (!done && direct && (gi == 0 || bias_done) && ctx->lt && ctx->use_lt &&
+          ctx->red_floats >= (size_t)3 * I) {
+        if (!cast_done) {
+          CK(launch_f32_to_bf16(3 * I, prm->bqkv, ctx->red, st));
+          ctx->launches += 1;
+          cast_done = true;
+        }
+        done = wgemm_epi(ctx, st, dtype, dtype, false, true, BJ, nI, I, X, I, Wg, I, Cg, 3 * I,
+                         LT_EPI_BIAS, (float*)((char*)ctx->red + (size_t)s0 * I * 2));
+      }
+      if (gi == 0) bias_done = done;
+      if (done != bias_done) return ENC_EUNSUPPORTED;   // every group the same way
+      if (!done)
+        if ((r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, nI, I, X, I,
+                           Wg, I, 0.f, Cg, 3 * I)))
+          return r;
     }
-    if (!bias_done && direct && ctx->lt && ctx->use_lt && ctx->red_floats >= (size_t)3 * I) {
-      // cuBLASLt takes a bf16 output's bias in bf16 (R18): one cast kernel
-      CK(launch_f32_to_bf16(3 * I, prm->bqkv, ctx->red, st));
-      ctx->launches += 1;
-      bias_done = wgemm_epi(ctx, st, dtype, dtype, false, true, BJ, 3 * I, I, X, I, prm->Wqkv, I,
-                            QKVs, 3 * I, LT_EPI_BIAS, ctx->red);
-    }
-    if (!bias_done)
-      if ((r = wcontract(ctx, ENC_OP_GEMM_QKV, st, dtype, dtype, false, true, BJ, 3 * I, I, X,
-                         I, prm->Wqkv, I, 0.f, direct ? QKVs : QKV, 3 * I)))
-        return r;
   }
   // AIB (:550): in place on the direct path unless the epilogue added the bias
   {
@@ -1459,18 +1496,30 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, wa, st));
   }
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
+  // (algebraic fusion, Table A.2: one dX / dW contraction per group of stacked blocks --
+  // dX accumulates every group onto dz1, dW writes the group's rows of dWqkv)
+  int ngrp = 0, gstart[3], gcount[3];
+  qkv_groups(ctx->qkv_fusion, &ngrp, gstart, gcount);
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
-    if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DX, st, dtype, dtype, false, false, BJ, I, 3 * I, dQKV, 3 * I, prm->Wqkv,
-                       I, 1.f, dX, I)))
-      return r;
+    for (int gi = 0; gi < ngrp; ++gi) {
+      const int s0 = gstart[gi], nI = gcount[gi] * I;
+      if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DX, st, dtype, dtype, false, false, BJ, I, nI,
+                         (const char*)dQKV + (size_t)s0 * I * es, 3 * I,
+                         (const char*)prm->Wqkv + (size_t)s0 * I * I * es, I, 1.f, dX, I)))
+        return r;
+    }
   }
   {
     cudaStream_t ss = fork();
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, ss, 0);
-    if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, ss, dtype, F32, true, false, 3 * I, I, BJ, dQKV, 3 * I, X, I, 0.f,
-                       g->dWqkv, I, nullptr, sws)))
-      return r;
+    for (int gi = 0; gi < ngrp; ++gi) {
+      const int s0 = gstart[gi], nI = gcount[gi] * I;
+      if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, ss, dtype, F32, true, false, nI, I, BJ,
+                         (const char*)dQKV + (size_t)s0 * I * es, 3 * I, X, I, 0.f,
+                         g->dWqkv + (size_t)s0 * I * I, I, nullptr, sws)))
+        return r;
+    }
   }
   if (direct && !bgrad_epi) {
     // bias gradient as a column sum of dQKV (cuBLASLt's BGRAD epilogue on the dW

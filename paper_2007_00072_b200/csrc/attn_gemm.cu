@@ -243,8 +243,12 @@ static cudaError_t launch_tile(dim3 grid, const CUtensorMap& ma, const CUtensorM
 // P-wide operands through map_pop (coordinates (p, h, row, b): row dim 2) with their row
 // strides; [J x K] operands head-major [B,H,J,K] (row dim 1).
 cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, int64_t ldx,
-                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st) {
-  const int K = J;
+                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st,
+                             int Kkeys) {
+  // J query rows, K key rows (self-attention: K = J; encoder-decoder attention: K keys of
+  // the memory sequence)
+  const int K = Kkeys > 0 ? Kkeys : J;
+  if (J % kBM || K % kBM) return cudaErrorInvalidValue;
   AttnGemmParams p{};
   p.H = H;
   CUtensorMap ma, mb, mc;

@@ -149,7 +149,8 @@ cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int 
 // row strides ldx / ldy / ldz (map_pop below; ignored for [J x K] operands).
 bool attn_gemm_supported(int J, int P);
 cudaError_t launch_attn_gemm(int which, int B, int H, int J, int P, const void* X, int64_t ldx,
-                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st);
+                             const void* Y, int64_t ldy, void* Z, int64_t ldz, cudaStream_t st,
+                             int K = 0);   // K keys (0: K = J)
 
 // Hand-written tcgen05 weight contractions with fused epilogues (wgemm.cu).  Row-major
 // C[M,N] = A B: A K-major [M][K] (a_mn = 0) or MN-major [K][M] (a_mn = 1); B K-major [N][K]

@@ -217,6 +217,16 @@ def test_layer_T_fp32_causal(key_padding):
         assert_parity(n, gpu[n], ref[n], "fp32")
 
 
+@pytest.mark.parametrize("fusion", [0, 1, 3])
+def test_layer_T_fp32_qkv_fusion_variants(fusion):
+    """Table A.2's algebraic-fusion variants of the Q/K/V projections
+    compute the same layer: end to end at 1e-5 on the fp32 path."""
+    gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=True, weight_std=0.2,
+                           opts={12: fusion})
+    for n in gpu:
+        assert_parity(n, gpu[n], ref[n], "fp32")
+
+
 def test_layer_T_fp32_no_dropout():
     gpu, ref = _end_to_end(CONFIGS["T"], "fp32", "gelu", key_padding=True, p=0.0,
                            weight_std=0.2)
@@ -260,6 +270,10 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {OPT_GEMM_TC_MASK: (1 << 7) | (1 << 12)},   # only the fused FFN kernels on tcgen05
     {OPT_GEMM_PAIR: 0},                    # single-CTA weight-contraction tiles
     {11: 1},                               # keep words generated ahead on the side stream
+    {12: 0},                               # Table A.2: Q, K, V as separate contractions
+    {12: 1},                               # Table A.2: Q and K stacked, V separate
+    {12: 3},                               # Q, then K and V stacked (P:646 variant)
+    {12: 0, 8: 1},                         # separate, all on the tcgen05 kernel
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
