@@ -46,6 +46,17 @@ class enc_saved_view(ctypes.Structure):
     _fields_ = [(n, c_void_p) for n in SAVED_FIELDS] + [("qkv_ld", c_int64)]
 
 
+XATTN_PARAM_FIELDS = ("Wq", "Wkv", "Wo", "bq", "bkv", "bo", "g", "be")
+
+
+class enc_xattn_params(ctypes.Structure):
+    _fields_ = [(n, c_void_p) for n in XATTN_PARAM_FIELDS]
+
+
+class enc_xattn_grads(ctypes.Structure):
+    _fields_ = [("d" + n, c_void_p) for n in XATTN_PARAM_FIELDS]
+
+
 class enc_opt_segment(ctypes.Structure):
     _fields_ = [("begin", c_int64), ("n", c_int64), ("out", c_void_p), ("dtype", c_int),
                 ("no_decay", c_int)]
@@ -133,6 +144,14 @@ _SIGS = {
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "enc_xattn_sizes": (c_int, [POINTER(enc_dims), c_int, POINTER(c_size_t), POINTER(c_size_t)]),
+    "enc_xattn_forward": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
+                                  POINTER(enc_xattn_params), c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p, c_void_p]),
+    "enc_xattn_backward": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),
+                                   POINTER(enc_xattn_params), c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_void_p, POINTER(enc_xattn_grads),
+                                   c_void_p, c_void_p]),
     "enc_attn_keep_bits": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_uint64,
                                    c_uint64, c_int64, c_void_p, c_void_p]),
     "enc_attn_fwd_fused_bits": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,

@@ -1742,3 +1742,261 @@ int encoder_layer_step_host_pipelined(enc_ctx* ctx, const enc_dims* d, int dtype
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ cross attention
+// Encoder-decoder attention sublayer ("fuse keys and values in
+// encoder/decoder attention"): queries from X [B,J,I], keys and values from the memory
+// Mem [B,K,I] through ONE stacked contraction with [W^K; W^V] -> KV [B,K,2I], then the
+// encoder layer's BSB (site 0, K keys) and BDRLN (site 1, residual X).  Q, K, V are read in
+// place (row strides I and 2I) by the attention contractions: the tiled tcgen05 kernels
+// when bf16, P = 64 and J, K are multiples of 128, else cuBLAS (strided over the heads of
+// each batch element).
+namespace {
+enum XSaved { XS_Q, XS_KV, XS_P, XS_A, XS_C, XS_XH, XS_R, XS_N };
+enum XFwd { XF_S, XF_YO, XF_N };
+enum XBwd { XB_DYO, XB_DC, XB_DA, XB_DS, XB_DQ, XB_DKV, XB_N };
+Layout xsaved_layout(const enc_dims* d, int dtype) {
+  const size_t es = esize(dtype), BJ = (size_t)d->B * d->J, BK = (size_t)d->B * d->K;
+  const size_t s = (size_t)d->B * d->H * d->J * d->K * es;
+  const size_t sz[XS_N] = {BJ * d->I * es, BK * 2 * d->I * es, s, s, BJ * d->I * es,
+                           BJ * d->I * es, BJ * sizeof(float)};
+  return make_layout(sz, XS_N);
+}
+Layout xfwd_layout(const enc_dims* d, int dtype) {
+  const size_t es = esize(dtype), BJ = (size_t)d->B * d->J;
+  const size_t sz[XF_N] = {(size_t)d->B * d->H * d->J * d->K * es, BJ * d->I * es};
+  return make_layout(sz, XF_N);
+}
+Layout xbwd_layout(const enc_dims* d, int dtype) {
+  const size_t es = esize(dtype), BJ = (size_t)d->B * d->J, BK = (size_t)d->B * d->K;
+  const size_t s = (size_t)d->B * d->H * d->J * d->K * es;
+  const size_t sz[XB_N] = {BJ * d->I * es, BJ * d->I * es, s, s, BJ * d->I * es,
+                           BK * 2 * d->I * es};
+  return make_layout(sz, XB_N);
+}
+}  // namespace
+
+static int check_xdims(const enc_dims* d, int dtype) {
+  if (!d) return ENC_ENULL;
+  if (!valid_dtype(dtype)) return ENC_EDTYPE;
+  if (d->B < 0 || d->J <= 0 || d->K <= 0 || d->H <= 0 || d->P <= 0) return ENC_EINVAL;
+  if (d->W != d->P || d->I != d->H * d->P) return ENC_EINVAL;
+  if (d->I % 8 || d->K % 8 || d->P % 8) return ENC_EALIGN;
+  if (!rowop_supported(d->K) || !rowop_supported(d->I) || !bdrln_bwd_supported(d->I, dtype))
+    return ENC_EUNSUPPORTED;
+  if ((int64_t)d->B * (d->J > d->K ? d->J : d->K) * 2 * d->I / 8 >= INT32_MAX ||
+      (int64_t)d->B * d->H * d->J >= INT32_MAX)
+    return ENC_EUNSUPPORTED;
+  return ENC_OK;
+}
+
+// One attention contraction of the cross-attention sublayer (which = ENC_AG_*): X, Y, Z as
+// in enc_attn_gemm, P-wide operands token-major with row strides ldx / ldy / ldz, [J x K]
+// operands head-major [B,H,J,K].
+static int xcontract(enc_ctx* ctx, int which, int dtype, int B, int H, int J, int K, int P,
+                     const void* X, int64_t ldx, const void* Y, int64_t ldy, void* Z, int64_t ldz,
+                     cudaStream_t st) {
+  if (dtype == ENC_BF16 && ctx->attn_tc && P == 64 && J % 128 == 0 && K % 128 == 0) {
+    CK(launch_attn_gemm(which, B, H, J, P, X, ldx, Y, ldy, Z, ldz, st, K));
+    ctx->launches += 1;
+    return ENC_OK;
+  }
+  const size_t es = esize(dtype);
+  const long long jk = (long long)J * K;
+  for (int b = 0; b < B; ++b) {
+    auto tok = [&](const void* p, int rows, int64_t ld) {   // batch b of a token-major operand
+      return (const char*)p + (size_t)b * rows * ld * es;
+    };
+    auto hm = [&](const void* p) { return (const char*)p + (size_t)b * H * jk * es; };
+    cublasStatus_t s = CUBLAS_STATUS_SUCCESS;
+    switch (which) {
+      case ENC_AG_QK:   // S[J,K] = Q[J,P] K[K,P]^T
+      case ENC_AG_DA:   // dA[J,K] = dC[J,P] V[K,P]^T
+        s = gemm_rm_strided(ctx->blas, dtype, false, true, J, K, P, 1.f, tok(X, J, ldx), (int)ldx,
+                            P, tok(Y, K, ldy), (int)ldy, P, 0.f, (void*)hm(Z), K, jk, H);
+        break;
+      case ENC_AG_AV:   // C[J,P] = A[J,K] V[K,P]
+      case ENC_AG_DQ:   // dQ[J,P] = dS[J,K] K[K,P]
+        s = gemm_rm_strided(ctx->blas, dtype, false, false, J, P, K, 1.f, hm(X), K, jk,
+                            tok(Y, K, ldy), (int)ldy, P, 0.f, (void*)tok(Z, J, ldz), (int)ldz, P,
+                            H);
+        break;
+      case ENC_AG_DV:   // dV[K,P] = A[J,K]^T dC[J,P]
+      case ENC_AG_DK:   // dK[K,P] = dS[J,K]^T Q[J,P]
+        s = gemm_rm_strided(ctx->blas, dtype, true, false, K, P, J, 1.f, hm(X), K, jk,
+                            tok(Y, J, ldy), (int)ldy, P, 0.f, (void*)tok(Z, K, ldz), (int)ldz, P,
+                            H);
+        break;
+      default:
+        return ENC_EINVAL;
+    }
+    if (s != CUBLAS_STATUS_SUCCESS) return ENC_ECUBLAS;
+  }
+  return ENC_OK;
+}
+
+// C[rows, N] = A W^T + bias, the bias in the contraction epilogue where available, else a
+// row-bias pass
+static int linear_bias(enc_ctx* ctx, int op, cudaStream_t st, int dtype, int rows, int N, int Kd,
+                       const void* A, const void* W, const float* bias, void* C) {
+  int r = wcontract(ctx, op, st, dtype, dtype, false, true, rows, N, Kd, A, Kd, W, Kd, 0.f, C, N,
+                    bias);
+  if (r == ENC_OK) return ENC_OK;
+  if (r != ENC_EUNSUPPORTED) return r;
+  if ((r = wcontract(ctx, op, st, dtype, dtype, false, true, rows, N, Kd, A, Kd, W, Kd, 0.f, C,
+                     N)))
+    return r;
+  CK(launch_bias_rows(dtype, rows, N, C, bias, st));
+  ctx->launches += 1;
+  return ENC_OK;
+}
+
+extern "C" {
+
+int enc_xattn_sizes(const enc_dims* d, int dtype, size_t* saved_bytes, size_t* scratch_bytes) {
+  int r = check_xdims(d, dtype);
+  if (r) return r;
+  if (saved_bytes) *saved_bytes = xsaved_layout(d, dtype).total;
+  if (scratch_bytes) {
+    const size_t f = xfwd_layout(d, dtype).total, b = xbwd_layout(d, dtype).total;
+    *scratch_bytes = f > b ? f : b;
+  }
+  return ENC_OK;
+}
+
+static int check_xparams(const enc_xattn_params* p) {
+  if (!p) return ENC_ENULL;
+  CHECK_PTRS(p->Wq, p->Wkv, p->Wo, p->bq, p->bkv, p->bo, p->g, p->be);
+  return ENC_OK;
+}
+
+int enc_xattn_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                      const enc_xattn_params* prm, const void* X, const void* Mem,
+                      const float* mask_bias, void* Y, void* saved, void* scratch,
+                      enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_xdims(d, dtype);
+  if (r) return r;
+  if ((r = check_cfg(cfg))) return r;
+  if (cfg->causal) return ENC_EINVAL;   // causal masking needs J == K (self-attention)
+  if ((r = check_xparams(prm))) return r;
+  CHECK_PTRS(X, Mem, Y, saved, scratch);
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if (d->B == 0) return ENC_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CB(cublasSetStream(ctx->blas, st));
+  const int B = d->B, J = d->J, K = d->K, H = d->H, P = d->P, I = d->I;
+  const Layout SL = xsaved_layout(d, dtype), FL = xfwd_layout(d, dtype);
+  void *Q = at(saved, SL.off[XS_Q]), *KV = at(saved, SL.off[XS_KV]);
+  void *Pm = at(saved, SL.off[XS_P]), *A = at(saved, SL.off[XS_A]), *C = at(saved, SL.off[XS_C]);
+  void* xh = at(saved, SL.off[XS_XH]);
+  float* rs = (float*)at(saved, SL.off[XS_R]);
+  void *S = at(scratch, FL.off[XF_S]), *Yo = at(scratch, FL.off[XF_YO]);
+  const size_t es = esize(dtype);
+  const uint64_t l4 = 4ull * cfg->layer_id;
+  const float scale = 1.0f / sqrtf((float)P);
+  // Q = X Wq^T + bq;  [K | V] = Mem [Wk; Wv]^T + bkv (one stacked contraction)
+  if ((r = linear_bias(ctx, ENC_OP_GEMM_QKV, st, dtype, B * J, I, I, X, prm->Wq, prm->bq, Q)))
+    return r;
+  if ((r = linear_bias(ctx, ENC_OP_GEMM_QKV, st, dtype, B * K, 2 * I, I, Mem, prm->Wkv, prm->bkv,
+                       KV)))
+    return r;
+  // S = Q K^T per (b, h), BSB (site 0), C = A V
+  if ((r = xcontract(ctx, ENC_AG_QK, dtype, B, H, J, K, P, Q, I, KV, 2 * I, S, 0, st))) return r;
+  CK(launch_bsb_fwd(dtype, B, H, J, K, scale, S, mask_bias,
+                    make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), cfg->batch_offset, Pm, A, st));
+  ctx->launches += 1;
+  if ((r = xcontract(ctx, ENC_AG_AV, dtype, B, H, J, K, P, A, 0, (char*)KV + (size_t)I * es,
+                     2 * I, C, I, st)))
+    return r;
+  // Out, BDRLN (site 1) with the residual X
+  if ((r = wcontract(ctx, ENC_OP_GEMM_OUT, st, dtype, dtype, false, true, B * J, I, I, C, I,
+                     prm->Wo, I, 0.f, Yo, I)))
+    return r;
+  CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g, prm->be, cfg->ln_eps,
+                      make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), cfg->batch_offset, Y, xh,
+                      rs, st));
+  ctx->launches += 1;
+  return ENC_OK;
+}
+
+int enc_xattn_backward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_cfg* cfg,
+                       const enc_xattn_params* prm, const void* X, const void* Mem,
+                       const void* saved, const void* dY, void* dX, void* dMem,
+                       const enc_xattn_grads* g, void* scratch, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  int r = check_xdims(d, dtype);
+  if (r) return r;
+  if ((r = check_cfg(cfg))) return r;
+  if (cfg->causal) return ENC_EINVAL;
+  if ((r = check_xparams(prm))) return r;
+  if (!g) return ENC_ENULL;
+  CHECK_PTRS(X, Mem, saved, dY, dX, dMem, scratch, g->dWq, g->dWkv, g->dWo, g->dbq, g->dbkv,
+             g->dbo, g->dg, g->dbe);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = d->B, J = d->J, K = d->K, H = d->H, P = d->P, I = d->I;
+  if (B == 0) {
+    const size_t n[8] = {(size_t)I * I, (size_t)2 * I * I, (size_t)I * I, (size_t)I,
+                         (size_t)2 * I, (size_t)I, (size_t)I, (size_t)I};
+    float* p[8] = {g->dWq, g->dWkv, g->dWo, g->dbq, g->dbkv, g->dbo, g->dg, g->dbe};
+    for (int i = 0; i < 8; ++i) CK(cudaMemsetAsync(p[i], 0, n[i] * sizeof(float), st));
+    return ENC_OK;
+  }
+  CB(cublasSetStream(ctx->blas, st));
+  const size_t es = esize(dtype);
+  const Layout SL = xsaved_layout(d, dtype), BL = xbwd_layout(d, dtype);
+  void* sv = (void*)saved;
+  void *Q = at(sv, SL.off[XS_Q]), *KV = at(sv, SL.off[XS_KV]);
+  void *Pm = at(sv, SL.off[XS_P]), *A = at(sv, SL.off[XS_A]), *C = at(sv, SL.off[XS_C]);
+  void* xh = at(sv, SL.off[XS_XH]);
+  float* rs = (float*)at(sv, SL.off[XS_R]);
+  void *dYo = at(scratch, BL.off[XB_DYO]), *dC = at(scratch, BL.off[XB_DC]);
+  void *dA = at(scratch, BL.off[XB_DA]), *dS = at(scratch, BL.off[XB_DS]);
+  void *dQ = at(scratch, BL.off[XB_DQ]), *dKV = at(scratch, BL.off[XB_DKV]);
+  const uint64_t l4 = 4ull * cfg->layer_id;
+  const float scale = 1.0f / sqrtf((float)P);
+  const ReduceWs ws = ws_of(ctx);
+  const int F32 = ENC_FP32;
+  // BDRLN-bwd (site 1): dz -> dX (residual), dYo; dg, dbe, dbo
+  CK(launch_bdrln_bwd(dtype, B, J, I, dY, xh, rs, prm->g,
+                      make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), cfg->batch_offset, dX,
+                      dYo, g->dg, g->dbe, g->dbo, ws, st));
+  ctx->launches += 2;
+  // Out dX, dW
+  if ((r = wcontract(ctx, ENC_OP_GEMM_OUT_DX, st, dtype, dtype, false, false, B * J, I, I, dYo, I,
+                     prm->Wo, I, 0.f, dC, I)))
+    return r;
+  if ((r = wcontract(ctx, ENC_OP_GEMM_OUT_DW, st, dtype, F32, true, false, I, I, B * J, dYo, I, C,
+                     I, 0.f, g->dWo, I)))
+    return r;
+  // dA = dC V^T, dV = A^T dC (into the V half of dKV), BSB-bwd, dQ = dS K, dK = dS^T Q
+  char* V = (char*)KV + (size_t)I * es;
+  if ((r = xcontract(ctx, ENC_AG_DA, dtype, B, H, J, K, P, dC, I, V, 2 * I, dA, 0, st))) return r;
+  if ((r = xcontract(ctx, ENC_AG_DV, dtype, B, H, J, K, P, A, 0, dC, I,
+                     (char*)dKV + (size_t)I * es, 2 * I, st)))
+    return r;
+  CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
+                    make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), cfg->batch_offset, dS, st));
+  ctx->launches += 1;
+  if ((r = xcontract(ctx, ENC_AG_DQ, dtype, B, H, J, K, P, dS, 0, KV, 2 * I, dQ, I, st))) return r;
+  if ((r = xcontract(ctx, ENC_AG_DK, dtype, B, H, J, K, P, dS, 0, Q, I, dKV, 2 * I, st))) return r;
+  // bias gradients (column sums), then dX += dQ Wq (beta = 1 onto dz), dMem = dKV [Wk; Wv]
+  CK(launch_colsum(dtype, B * J, I, dQ, g->dbq, ws, st));
+  CK(launch_colsum(dtype, B * K, 2 * I, dKV, g->dbkv, ws, st));
+  ctx->launches += 4;
+  if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DX, st, dtype, dtype, false, false, B * J, I, I, dQ, I,
+                     prm->Wq, I, 1.f, dX, I)))
+    return r;
+  if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DX, st, dtype, dtype, false, false, B * K, I, 2 * I, dKV,
+                     2 * I, prm->Wkv, I, 0.f, dMem, I)))
+    return r;
+  if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, st, dtype, F32, true, false, I, I, B * J, dQ, I, X,
+                     I, 0.f, g->dWq, I)))
+    return r;
+  if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, st, dtype, F32, true, false, 2 * I, I, B * K, dKV,
+                     2 * I, Mem, I, 0.f, g->dWkv, I)))
+    return r;
+  return ENC_OK;
+}
+
+}  // extern "C"

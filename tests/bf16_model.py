@@ -86,3 +86,55 @@ def layer(X, prm, H, cfg, mask_bias=None, dY=None):
                  ("be2", dbe2)):
         out["d" + n] = v
     return out
+
+
+def cross_attention(X, Mem, prm, H, cfg, mask_bias=None, dY=None):
+    """The encoder-decoder attention sublayer (oracle cross_attention_*) with bf16 storage at
+    the CUDA path's storage points: Q, KV, S, P, A, C, Yo, Y, xhat; dz, dYo, dC, dA, dV, dS,
+    dQ, dK, dX, dMem (the unfused attention path stores S, A, dA)."""
+    X, Mem = np.asarray(X, np.float64), np.asarray(Mem, np.float64)
+    W = {k: np.asarray(v, np.float64) for k, v in prm.items()}
+    B, J, I = X.shape
+    K = Mem.shape[1]
+    P = I // H
+    sc = 1.0 / np.sqrt(P)
+    sub = lambda site: philox.subsequence(cfg.layer_id, site)  # noqa: E731
+    seed, boff = cfg.seed, cfg.batch_offset
+    Qf = r(X @ W["Wq"].T + W["bq"])
+    KV = r(Mem @ W["Wkv"].T + W["bkv"])
+    Q = Qf.reshape(B, J, H, P).transpose(0, 2, 1, 3)
+    Kh = KV[..., :I].reshape(B, K, H, P).transpose(0, 2, 1, 3)
+    V = KV[..., I:].reshape(B, K, H, P).transpose(0, 2, 1, 3)
+    S = r(Q @ Kh.transpose(0, 1, 3, 2))
+    Pm, A = E.bsb_fwd(S, mask_bias, sc, cfg.p_attn, seed, sub(0), boff)
+    Pm, A = r(Pm), r(A)
+    C = r((A @ V).transpose(0, 2, 1, 3).reshape(B, J, I))
+    Yo = r(C @ W["Wo"].T)
+    Y, xh, rs = E.bdrln_fwd(Yo, W["bo"], X, W["g"], W["be"], cfg.ln_eps, cfg.p_hidden, seed,
+                            sub(1), boff)
+    Y, xh = r(Y), r(xh)
+    out = {"Y": Y}
+    if dY is None:
+        return out
+    dY = np.asarray(dY, np.float64)
+    dz, dYo, dg, dbe, dbo = E.bdrln_bwd(dY, xh, rs, W["g"], cfg.p_hidden, seed, sub(1), boff)
+    dz, dYo = r(dz), r(dYo)
+    dC = r(dYo @ W["Wo"])
+    dWo = np.einsum("bji,bjk->ik", dYo, C)
+    dCbh = dC.reshape(B, J, H, P).transpose(0, 2, 1, 3)
+    dA = r(dCbh @ V.transpose(0, 1, 3, 2))
+    dV = r(A.transpose(0, 1, 3, 2) @ dCbh)
+    dS = r(E.bsb_bwd(dA, Pm, sc, cfg.p_attn, seed, sub(0), boff))
+    dQ = r(dS @ Kh)
+    dK = r(dS.transpose(0, 1, 3, 2) @ Q)
+    dQf = dQ.transpose(0, 2, 1, 3).reshape(B, J, I)
+    dKV = np.concatenate([dK.transpose(0, 2, 1, 3).reshape(B, K, I),
+                          dV.transpose(0, 2, 1, 3).reshape(B, K, I)], axis=-1)
+    out["dX"] = r(dQf @ W["Wq"] + dz)
+    out["dMem"] = r(dKV @ W["Wkv"])
+    g = {"Wq": np.einsum("bjo,bji->oi", dQf, X), "Wkv": np.einsum("bko,bki->oi", dKV, Mem),
+         "Wo": dWo, "bq": dQf.sum(axis=(0, 1)), "bkv": dKV.sum(axis=(0, 1)), "bo": dbo, "g": dg,
+         "be": dbe}
+    for n, v in g.items():
+        out["d" + n] = v
+    return out
