@@ -189,7 +189,17 @@ def _stagewise(dims, dtype, act, key_padding, opts=None, **kw):
               ("dK", b["dK"], b["dS"].transpose(0, 1, 3, 2) @ s["Q"])]
     dQKVo, dbqkvo = E.aib_bwd(b["dQ"], b["dK"], b["dV"])
     pairs += [("dQKV", b["dQKV"], dQKVo), ("dbqkv", g["bqkv"], dbqkvo)]
-    pairs += [("dX", dX, b["dQKV"] @ W["Wqkv"] + dz1o),
+    # Table A.2 variants with several Q/K/V groups accumulate dX group by group onto the
+    # bf16 dX buffer (one rounding per group): the reference follows the same sequence
+    groups = {0: [(0, 1), (1, 1), (2, 1)], 1: [(0, 2), (2, 1)], 3: [(0, 1), (1, 2)]}.get(
+        (opts or {}).get(12, 2), [(0, 3)])
+    dXref = dz1o
+    for gi, (s0, c) in enumerate(groups):
+        blk = slice(s0 * I, (s0 + c) * I)
+        dXref = dXref + b["dQKV"][..., blk] @ W["Wqkv"][blk]
+        if dtype == "bf16" and len(groups) > 1 and gi + 1 < len(groups):
+            dXref = bf16_round(dXref.astype(np.float32)).astype(np.float64)
+    pairs += [("dX", dX, dXref),
               ("dWqkv", g["Wqkv"], np.einsum("bjo,bji->oi", b["dQKV"], X))]
     return pairs, fp32_pairs
 
