@@ -194,6 +194,8 @@ def _stagewise(dims, dtype, act, key_padding, opts=None, **kw):
     groups = {0: [(0, 1), (1, 1), (2, 1)], 1: [(0, 2), (2, 1)], 3: [(0, 1), (1, 2)]}.get(
         (opts or {}).get(12, 2), [(0, 3)])
     dXref = dz1o
+    if dtype == "bf16" and len(groups) > 1:   # dz1 is stored in the bf16 dX buffer first
+        dXref = bf16_round(dXref.astype(np.float32)).astype(np.float64)
     for gi, (s0, c) in enumerate(groups):
         blk = slice(s0 * I, (s0 + c) * I)
         dXref = dXref + b["dQKV"][..., blk] @ W["Wqkv"][blk]
