@@ -58,7 +58,9 @@ struct enc_ctx {
   // fused forward: the attention keep words generated on the side stream beside the QKV
   // contraction (ENC_OPT_KEEP_AHEAD), joined before the score kernel
   int keep_ahead = 0;
-  int qkv_fusion = ENC_QKV_STACKED;   // ENC_OPT_QKV_FUSION (Table A.2 algebraic fusion)   // measured slower at config L (the QKV contraction is slowed more)
+  int qkv_fusion = ENC_QKV_STACKED;   // ENC_OPT_QKV_FUSION (Table A.2 algebraic fusion)
+  int qkv_fusion_bwd = ENC_QKV_STACKED;   // its backward dX / dW grouping
+  int bdrln_variant = 0;   // ENC_OPT_BDRLN_VARIANT (kernel / warps per row of BDRLN, -bwd)   // measured slower at config L (the QKV contraction is slowed more)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
@@ -894,6 +896,19 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   if (key == ENC_OPT_QKV_FUSION) {
     if (value < ENC_QKV_SEPARATE || value > ENC_QKV_KV_STACKED) return ENC_EINVAL;
     ctx->qkv_fusion = value;
+    ctx->qkv_fusion_bwd = value;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_QKV_FUSION_BWD) {
+    if (value < ENC_QKV_SEPARATE || value > ENC_QKV_KV_STACKED) return ENC_EINVAL;
+    ctx->qkv_fusion_bwd = value;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_BDRLN_VARIANT) {
+    for (int site = 0; site < 4; ++site)
+      if (((value >> (4 * site)) & 15) > 4) return ENC_EINVAL;
+    if (value < 0 || value >= (1 << 16)) return ENC_EINVAL;
+    ctx->bdrln_variant = value;
     return ENC_OK;
   }
   if (key == ENC_OPT_KEEP_AHEAD) {
@@ -1166,7 +1181,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD1, st, 1);
     CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
-                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st));
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st,
+                        ctx->bdrln_variant & 15));
   }
   // Linear (:559) + BAD (:560-562).  The activation input h = X1 W1^T + b1 is kept for the
   // backward (saved.h); on the tcgen05 path BAD runs in the contraction's epilogue
@@ -1196,7 +1212,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD2, st, 1);
     CK(launch_bdrln_fwd(dtype, B, J, I, Y2, prm->b2, X1, prm->g2, prm->be2, cfg->ln_eps,
-                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st));
+                        make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st,
+                        (ctx->bdrln_variant >> 4) & 15));
   }
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1313,7 +1330,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     w.defer = &ffn_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dY, xh2, r2, prm->g2,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, dX1, dY2, g->dg2,
-                        g->dbe2, g->db2, w, st));
+                        g->dbe2, g->db2, w, st, (ctx->bdrln_variant >> 8) & 15));
   }
   // Linear2 dX (:573) + BAD-bwd (:576-578) in one tcgen05 kernel on the bf16 path (dA1 never
   // reaches HBM; db1 from its epilogue's column partials), else the contraction into dA1 and
@@ -1390,7 +1407,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     w.defer = &att_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dX1, xh1, r1, prm->g1,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, dX, dYo, g->dg1,
-                        g->dbe1, g->dbo, w, st));
+                        g->dbe1, g->dbo, w, st, (ctx->bdrln_variant >> 12) & 15));
   }
   const ReduceWs wa = after(att_jobs[0]);   // the rest of the half reduces past those partials
   // Out dX (:586), dW (:587)
@@ -1499,7 +1516,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // (algebraic fusion, Table A.2: one dX / dW contraction per group of stacked blocks --
   // dX accumulates every group onto dz1, dW writes the group's rows of dWqkv)
   int ngrp = 0, gstart[3], gcount[3];
-  qkv_groups(ctx->qkv_fusion, &ngrp, gstart, gcount);
+  qkv_groups(ctx->qkv_fusion_bwd, &ngrp, gstart, gcount);
   {
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DX, st, 0);
     for (int gi = 0; gi < ngrp; ++gi) {

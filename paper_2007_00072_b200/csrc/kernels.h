@@ -107,23 +107,26 @@ cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, c
 cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, const float* bias,
                              const void* R, const float* gamma, const float* beta, float eps,
                              const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                             float* rstd, cudaStream_t st);
+                             float* rstd, cudaStream_t st, int variant = 0);
+// variant: 0 = the default kernel for I, 1 = warp-per-row, 2 / 3 / 4 = row-group kernels with
+// that many warps per row (when it divides the row; else the default)
 cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, const void* xhat,
                              const float* rstd, const float* gamma, const PhiloxKey& pk,
                              int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
-                             float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st);
+                             float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st,
+                             int variant = 0);
 
 // Row-group BDRLN variants (ops_ln_rg.cu): 4 warps per row, persistent, TMA row ring.
 bool bdrln_rg_supported(int I);
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
                                 const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                                float* rstd, cudaStream_t st);
+                                float* rstd, cudaStream_t st, int gw = 0);
 cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut,
                                 const void* xhat, const float* rstd, const float* gamma,
                                 const PhiloxKey& pk, int64_t batch_offset, void* dz,
                                 void* dYpre, float* dgamma, float* dbeta, float* dbias,
-                                const ReduceWs& ws, cudaStream_t st);
+                                const ReduceWs& ws, cudaStream_t st, int gw = 0);
 
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* h,

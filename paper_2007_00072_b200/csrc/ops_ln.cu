@@ -94,12 +94,12 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
 cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, const float* bias,
                              const void* R, const float* gamma, const float* beta, float eps,
                              const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                             float* rstd, cudaStream_t st) {
+                             float* rstd, cudaStream_t st, int variant) {
   const int rows = B * J;
   if (rows == 0) return cudaSuccess;
-  if (bdrln_rg_supported(I))
+  if (variant != 1 && bdrln_rg_supported(I))
     return launch_bdrln_fwd_rg(dtype, B, J, I, Y, bias, R, gamma, beta, eps, pk, batch_offset,
-                               out, xhat, rstd, st);
+                               out, xhat, rstd, st, variant);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const int grid = (rows + 7) / 8;
@@ -284,16 +284,17 @@ bool bdrln_bwd_supported(int I, int dtype) {
 cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, const void* xhat,
                              const float* rstd, const float* gamma, const PhiloxKey& pk,
                              int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
-                             float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st) {
+                             float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st,
+                             int variant) {
   const int rows = B * J;
   if (rows == 0) {
     cudaMemsetAsync(dgamma, 0, sizeof(float) * I, st);
     cudaMemsetAsync(dbeta, 0, sizeof(float) * I, st);
     return cudaMemsetAsync(dbias, 0, sizeof(float) * I, st);
   }
-  if (bdrln_rg_supported(I))
+  if (variant != 1 && bdrln_rg_supported(I))
     return launch_bdrln_bwd_rg(dtype, B, J, I, dOut, xhat, rstd, gamma, pk, batch_offset, dz,
-                               dYpre, dgamma, dbeta, dbias, ws, st);
+                               dYpre, dgamma, dbeta, dbias, ws, st, variant);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   int G = (rows + kLnBwdWarps - 1) / kLnBwdWarps;

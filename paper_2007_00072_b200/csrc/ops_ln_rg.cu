@@ -338,6 +338,11 @@ static int rg_gw(int nc) {
   if (nc == 128) return 2;   // I = 1024: two warps x two chunks per lane (measured faster than 4 x 1)
   return (nc % 96 == 0 && nc / 3 <= 64) ? 3 : 4;
 }
+// a requested warps-per-row count is usable when it splits the row's chunks evenly into at
+// most two chunks per lane (the compiled CPW variants)
+static bool rg_gw_valid(int nc, int gw) {
+  return (gw == 2 || gw == 3 || gw == 4) && nc % gw == 0 && nc / gw <= 64;
+}
 #define ENC_GW_DISPATCH(gw, ...)                               \
   do {                                                         \
     if ((gw) == 2) { constexpr int GW = 2; __VA_ARGS__; }      \
@@ -353,13 +358,13 @@ static int rg_gw(int nc) {
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
                                 const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                                float* rstd, cudaStream_t st) {
+                                float* rstd, cudaStream_t st, int gw_req) {
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false);
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
-  const int gw = rg_gw(nc);
+  const int gw = rg_gw_valid(nc, gw_req) ? gw_req : rg_gw(nc);
   ENC_GW_DISPATCH(gw, ENC_CPW_DISPATCH(nc / gw, ENC_STG_DISPATCH(stg, {
     constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
@@ -381,7 +386,7 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
                                 const void* xhat, const float* rstd, const float* gamma,
                                 const PhiloxKey& pk, int64_t batch_offset, void* dz,
                                 void* dYpre, float* dgamma, float* dbeta, float* dbias,
-                                const ReduceWs& ws, cudaStream_t st) {
+                                const ReduceWs& ws, cudaStream_t st, int gw_req) {
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
@@ -389,7 +394,7 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
   const int cap = (int)(ws.cap_floats / (size_t)(3 * I));
   int G = 1;
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
-  const int gw = rg_gw(nc);
+  const int gw = rg_gw_valid(nc, gw_req) ? gw_req : rg_gw(nc);
   ENC_GW_DISPATCH(gw, ENC_CPW_DISPATCH(nc / gw, ENC_STG_DISPATCH(stg, {
     constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
