@@ -288,6 +288,8 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {12: 0, 8: 1},                         # separate, all on the tcgen05 kernel
     {14: 0x1111},                          # BDRLN / BDRLN-bwd one warp per row
     {14: 0x4242},                          # BDRLN row groups of 2 / 4 warps per site
+    {14: 0x1111},                          # BDRLN / BDRLN-bwd one warp per row
+    {14: 0x4242},                          # BDRLN row groups of 2 / 4 warps per site
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
