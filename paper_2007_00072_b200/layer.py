@@ -195,7 +195,14 @@ class EncoderLayer:
         """Set the context's options from a configuration file written by the SSSP
         configuration selection (config_select.emit_configuration; "used to
         automatically define tensor layouts at the start of training")."""
+        import json
         from .config_select import load_configuration
+        with open(fname) as f:
+            doc = json.load(f)
+        if "chosen_options" in doc:   # per-operator selection (tools/select_config.py)
+            for k, v in doc["chosen_options"].items():
+                check("enc_set_option", self.lib.enc_set_option(self.ctx.ptr, int(k), int(v)))
+            return doc["chosen_knobs"]
         _path, _total, knobs = load_configuration(fname)
         for k, v in knobs.items():
             check("enc_set_option",
