@@ -155,12 +155,19 @@ def sweeps(I):
     gw = [0, 1] + [g for g in (2, 3, 4) if (I // 8) % g == 0 and (I // 8) // g <= 64]
     for fus in range(4):
         for impl in (0, 1):
+            for direct in (1, 0):
+                k = default_knobs()
+                k["fus"] = k["fus_bwd"] = fus
+                k["direct"] = direct
+                for op in OPID:
+                    k["tc:" + op] = impl
+                k["bd:bdrln_fwd1"] = k["bd:bdrln_fwd2"] = gw[(2 * fus + impl) % len(gw)]
+                k["bd:bdrln_bwd1"] = k["bd:bdrln_bwd2"] = gw[(2 * fus + impl + 1) % len(gw)]
+                out.append(k)
+        for dx, dw in ((0, 1), (1, 0)):   # mixed backward Q/K/V contractions
             k = default_knobs()
-            k["fus"] = k["fus_bwd"] = fus
-            for op in OPID:
-                k["tc:" + op] = impl
-            k["bd:bdrln_fwd1"] = k["bd:bdrln_fwd2"] = gw[(2 * fus + impl) % len(gw)]
-            k["bd:bdrln_bwd1"] = k["bd:bdrln_bwd2"] = gw[(2 * fus + impl + 1) % len(gw)]
+            k["fus_bwd"] = fus
+            k["tc:gemm_qkv_dx"], k["tc:gemm_qkv_dw"] = dx, dw
             out.append(k)
     for path in ATTN:
         for direct in ((0,) if path == "cublas" else (0, 1)):
@@ -235,7 +242,7 @@ def main():
 
     # tune cuBLASLt once for every shape (explicit tuning pass, then off)
     eops.enc_set_option(layer.ctx, 3, 1)
-    for k in (default_knobs(),) + tuple(s for s in sweeps(I)[:8]):
+    for k in (default_knobs(),) + tuple(s for s in sweeps(I)[:24]):
         apply(k)
         step()
     torch.cuda.synchronize()
