@@ -373,6 +373,8 @@ def main():
              "sssp_vs_best": measured["sssp"] / measured[best],
              "sssp_vs_default": measured["sssp"] / measured["default"],
              "operators": [o for o, _ in op_list],
+             "cost_table_us": [[op, cid, ain, aout, round(c, 2)]
+                               for op, cid, ain, aout, c, _kn in rows],
              "configurations": len(configs), "nodes": len(sg.nodes()),
              "edges": sum(len(e) for e in sg.edges)}
     emit_configuration(path, total, a.out, extra)
