@@ -196,7 +196,7 @@ def gemm_desc(args) -> str:
 
 def attention_desc(args, dims) -> str:
     backend = args.attn_backend
-    if backend == "fused" and not (dims.J == 512 and dims.P == 64 and args.dtype == "bf16"):
+    if backend == "fused" and not (dims.J in (128, 512) and dims.P == 64 and args.dtype == "bf16"):
         backend = "tc" if args.dtype == "bf16" else "cublas"   # what the library selects
     return {"fused": "fused tcgen05 QK^T+BSB / dA+BSB-bwd (S, dA in TMEM), dropout on load in "
                      "the per-(b,h) A.V / A^T.dC contractions",

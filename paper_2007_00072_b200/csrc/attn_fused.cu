@@ -604,13 +604,19 @@ cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& p
   return cudaGetLastError();
 }
 
-// K = J = 512 (the whole score row in the 512 TMEM columns), P = 64
-bool attn_fused_supported(int J, int P) { return P == 64 && J == kK; }
+// K = J = 512 (the whole score row in the 512 TMEM columns), or J = K = 128 (attn_short.cu),
+// P = 64
+bool attn_fused_supported(int J, int P) {
+  return (P == 64 && J == kK) || attn_short_supported(J, P);
+}
 
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
                                uint32_t* keep_bits, cudaStream_t st, int causal, int keep_pre) {
+  if (attn_short_supported(J, P))
+    return launch_attn_qk_bsb_short(B, H, J, P, scale, Q, ldq, Kt, ldk, mask_bias, pk,
+                                    batch_offset, Pout, Aout, keep_bits, st, causal, keep_pre);
   const int K = J;
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
@@ -645,6 +651,9 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
                                 const PhiloxKey& pk, int64_t batch_offset,
                                 const uint32_t* keep_bits, void* dS, cudaStream_t st,
                                 bool high_prio) {
+  if (attn_short_supported(J, P))
+    return launch_attn_da_bsbb_short(B, H, J, P, scale, dC, lddc, V, ldv, Pin, pk, batch_offset,
+                                     keep_bits, dS, st, high_prio);
   const int K = J;
   CUtensorMap mc, mv, mp, ms;
   bool ok = map_pop(&mc, dC, B, H, J, P, lddc, kRows) && map_pop(&mv, V, B, H, K, P, ldv, 256) &&

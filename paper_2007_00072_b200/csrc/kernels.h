@@ -217,8 +217,22 @@ cudaError_t launch_attn_dqdk_bh(int B, int H, int J, int P, const void* dS, cons
                                 cudaStream_t st);
 
 // Fused tcgen05 score kernels (attn_fused.cu): QK^T + BSB (writes P, A) and dC V^T +
-// BSB-bwd (writes dS), bf16, P == 64, J == 512.
+// BSB-bwd (writes dS), bf16, P == 64, J == 512 (one 128-row tile per CTA round) or J == 128
+// (attn_short.cu: whole (b, h) pairs pipelined through TMEM slots; dispatched by the two
+// launchers below).
 bool attn_fused_supported(int J, int P);
+bool attn_short_supported(int J, int P);
+cudaError_t launch_attn_qk_bsb_short(int B, int H, int J, int P, float scale, const void* Q,
+                                     int64_t ldq, const void* Kt, int64_t ldk,
+                                     const float* mask_bias, const PhiloxKey& pk,
+                                     int64_t batch_offset, void* Pout, void* Aout,
+                                     uint32_t* keep_bits, cudaStream_t st, int causal,
+                                     int keep_pre);
+cudaError_t launch_attn_da_bsbb_short(int B, int H, int J, int P, float scale, const void* dC,
+                                      int64_t lddc, const void* V, int64_t ldv, const void* Pin,
+                                      const PhiloxKey& pk, int64_t batch_offset,
+                                      const uint32_t* keep_bits, void* dS, cudaStream_t st,
+                                      bool high_prio);
 // keep_bits: [B,H,J,K/32] keep-flag words (layout in include/encoder.h), written by the
 // forward when non-null and read by the backward instead of recomputing Philox when non-null.
 // Q, K (fwd) and dC, V (bwd) are P-wide operands with row strides ldq, ldk, lddc, ldv.

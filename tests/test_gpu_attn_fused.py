@@ -35,7 +35,13 @@ def host(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512), (3, 2, 512)])
+# J = 128: the short-row kernels (attn_short.cu), (b, h) pairs pipelined through 3 TMEM
+# slots; (64, 12) gives > 3 pairs per CTA (slot reuse, barrier phase wrap), (5, 2) fewer
+# pairs than SMs
+SHORT = [(1, 1, 128), (5, 2, 128), (64, 12, 128)]
+
+
+@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512), (3, 2, 512)] + SHORT)
 @pytest.mark.parametrize("masked", [False, True])
 @pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
 @pytest.mark.parametrize("store_a", [True, False])
@@ -76,7 +82,7 @@ def test_fused_forward(ops, ctx, B, H, J, masked, p, store_a):
     assert np.allclose(gP.sum(-1), 1.0, atol=2e-2)
 
 
-@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512)])
+@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512)] + SHORT)
 @pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
 @pytest.mark.parametrize("stored", [False, True])
 def test_fused_backward(ops, ctx, B, H, J, p, stored):
@@ -105,10 +111,10 @@ def test_fused_backward(ops, ctx, B, H, J, p, stored):
     assert_parity("dS", g, dSo, "bf16")
 
 
-@pytest.mark.parametrize("J,P", [(256, 64), (384, 64), (512, 32)])
+@pytest.mark.parametrize("J,P", [(256, 64), (384, 64), (512, 32), (128, 32), (640, 64)])
 def test_fused_unsupported_shapes(ops, ctx, J, P):
-    """The fused kernels hold a whole 512-key score row in TMEM; other shapes are refused
-    (the layer then takes the unfused tcgen05 path)."""
+    """The fused kernels hold a whole 512-key score row (or whole 128 x 128 score matrices)
+    in TMEM; other shapes are refused (the layer then takes the unfused tcgen05 path)."""
     from paper_2007_00072_b200._abi import EncError
     x = torch.zeros((1, 1, J, P), dtype=torch.bfloat16, device="cuda")
     o = torch.zeros((1, 1, J, J), dtype=torch.bfloat16, device="cuda")
@@ -119,12 +125,13 @@ def test_fused_unsupported_shapes(ops, ctx, J, P):
 @pytest.mark.parametrize("B,H", [(1, 2), (2, 3)])
 @pytest.mark.parametrize("masked", [False, True])
 @pytest.mark.parametrize("p", [0.1, 0.0])
-def test_fused_forward_causal(ops, ctx, B, H, masked, p):
+@pytest.mark.parametrize("J", [512, 128])
+def test_fused_forward_causal(ops, ctx, B, H, masked, p, J):
     """Causal masking step (R22) inside the fused kernel: P is
     exactly zero above the diagonal (whole 32-column chunks and 64-column warp slices are
     fully masked for the early rows) and matches the oracle's causal BSB elsewhere; the
     fused backward run on that P matches the oracle's BSB-bwd."""
-    J, P = 512, 64
+    P = 64
     Q = make_tensor((B, H, J, P), 31, "bf16", std=0.8)
     K = make_tensor((B, H, J, P), 32, "bf16", std=0.8)
     M = None
@@ -174,16 +181,17 @@ def test_keep_bits_kernel(ops, ctx, B, H, J, K, p):
 
 @pytest.mark.parametrize("masked", [False, True])
 @pytest.mark.parametrize("p", [0.1, 0.6])
-def test_fused_forward_given_bits_equals_regenerated(ops, ctx, masked, p):
+@pytest.mark.parametrize("J", [512, 128])
+def test_fused_forward_given_bits_equals_regenerated(ops, ctx, masked, p, J):
     """The fused forward reading precomputed keep words gives bitwise the P / A of the one
     that runs Philox itself."""
-    B, H, J, P = 2, 3, 512, 64
+    B, H, P = 2, 3, 64
     Q = dev(make_tensor((B, H, J, P), 31, "bf16", std=0.8))
     K = dev(make_tensor((B, H, J, P), 32, "bf16", std=0.8))
     Mt = None
     if masked:
         M = np.zeros((B, J), np.float32)
-        M[:, 300:] = -10000.0
+        M[:, J * 3 // 5:] = -10000.0
         Mt = torch.tensor(M, device="cuda")
     boff, sub = 1, 4
     out = []

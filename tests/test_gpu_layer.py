@@ -47,7 +47,7 @@ def _paths(dims, dtype, opts=None):
     o = {OPT_ATTN_TC: 1, OPT_ATTN_FUSED: 1, OPT_ATTN_BH: 1, OPT_QKV_DIRECT: 1}
     o.update(opts or {})
     tc = bool(o[OPT_ATTN_TC]) and dtype == "bf16" and dims.P == 64 and dims.J % 128 == 0
-    fused = tc and bool(o[OPT_ATTN_FUSED]) and dims.J == 512
+    fused = tc and bool(o[OPT_ATTN_FUSED]) and dims.J in (128, 512)
     bh = bool(o[OPT_ATTN_BH]) and dims.P == 64 and dims.J % 128 == 0 and dims.J <= 512
     return {"tc": tc, "fused": fused, "drop_on_load": fused and bh}
 
@@ -288,8 +288,6 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {12: 0, 8: 1},                         # separate, all on the tcgen05 kernel
     {14: 0x1111},                          # BDRLN / BDRLN-bwd one warp per row
     {14: 0x4242},                          # BDRLN row groups of 2 / 4 warps per site
-    {14: 0x1111},                          # BDRLN / BDRLN-bwd one warp per row
-    {14: 0x4242},                          # BDRLN row groups of 2 / 4 warps per site
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
@@ -299,10 +297,25 @@ def test_layer_bf16_stagewise_paths(opts):
         assert_parity(n, g, o, "bf16")
 
 
+@pytest.mark.parametrize("opts", [
+    None,                                  # short-row fused score kernels, dropout on load
+    {OPT_ATTN_BH: 0},                      # short-row fused kernels + tiled A.V (A stored)
+    {OPT_ATTN_FUSED: 0},                   # tiled QK^T + BSB kernels + per-(b,h)
+    {11: 1},                               # keep words generated ahead on the side stream
+])
+def test_layer_bf16_stagewise_paths_short(opts):
+    """The attention-path options at the short-row shape J = 128 (config Bb's J, P)."""
+    pairs, f32 = _stagewise(Dims(B=3, J=128, H=4, P=64, U=512), "bf16", "gelu", True,
+                            opts=opts, weight_std=0.06)
+    for n, g, o in pairs + f32:
+        assert_parity(n, g, o, "bf16")
+
+
 @pytest.mark.parametrize("dims,opts", [
     (Dims(B=2, J=512, H=2, P=64, U=512), None),               # fused score kernels
     (Dims(B=2, J=512, H=2, P=64, U=512), {OPT_ATTN_FUSED: 0}),  # tiled QK^T + BSB kernel
-    (Dims(B=3, J=128, H=4, P=64, U=512), None),               # short-row BSB kernels
+    (Dims(B=3, J=128, H=4, P=64, U=512), None),               # short-row fused kernels
+    (Dims(B=3, J=128, H=4, P=64, U=512), {OPT_ATTN_FUSED: 0}),  # short-row tiled BSB
     (Dims(B=2, J=64, H=4, P=16, U=256), None),                # cuBLAS attention path
 ])
 def test_layer_bf16_stagewise_causal(dims, opts):
