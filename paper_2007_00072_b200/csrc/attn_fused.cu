@@ -299,17 +299,11 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
             for (int i = 0; i < kSub; ++i)
               if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
           }
-          m = v[0];
-#pragma unroll
-          for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
+          m = tree_max<kSub>(v);
           const float mr = m == -INFINITY ? 0.f : m;
-          float l = 0.f;
 #pragma unroll
-          for (int i = 0; i < kSub; ++i) {
-            v[i] = tc::ex2(v[i] - mr);
-            l += v[i];
-          }
-          lc[ch] = l;
+          for (int i = 0; i < kSub; ++i) v[i] = tc::ex2(v[i] - mr);
+          lc[ch] = tree_sum<kSub>(v);
           tc::tmem_st16(trow + ch * kSub, v);
         } else {
           tc::tmem_ld32(trow + ch * kSub, v);
@@ -318,19 +312,12 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
             for (int i = 0; i < kSub; ++i)
               if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
           }
-          m = v[0];
-#pragma unroll
-          for (int i = 1; i < kSub; ++i) m = fmaxf(m, v[i]);
-          m *= c;   // c > 0
+          m = tree_max<kSub>(v) * c;   // c > 0
           // a fully masked chunk (causal) has m = -inf: exponentiate against 0 instead
           const float mz = (kCausal && m == -INFINITY) ? 0.f : m;
-          float l = 0.f;
 #pragma unroll
-          for (int i = 0; i < kSub; ++i) {
-            v[i] = tc::ex2(fmaf(v[i], c, -mz));
-            l += v[i];
-          }
-          lc[ch] = l;
+          for (int i = 0; i < kSub; ++i) v[i] = tc::ex2(fmaf(v[i], c, -mz));
+          lc[ch] = tree_sum<kSub>(v);
           tc::tmem_st32(trow + ch * kSub, v);
         }
         mc[ch] = m;
@@ -404,7 +391,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
       mbar_wait_sleep(&p_full[warp], it & 1);
       TRACE(3);
-      float dot = 0.f;
+      float dacc[4] = {0.f, 0.f, 0.f, 0.f};   // four partial sums
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
         tc::tmem_ld32(trow + ch * 32, v);
@@ -416,9 +403,11 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
               *reinterpret_cast<const uint4*>(own + tc::sw128(lane, ch * 4 + j)), p);
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            dot = fmaf(((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u], dot);
+            dacc[u & 3] = fmaf(((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u],
+                               dacc[u & 3]);
         }
       }
+      const float dot = (dacc[0] + dacc[1]) + (dacc[2] + dacc[3]);
       // row statistics alternate between the .x / .y slots by tile parity: a slot is
       // rewritten two tiles later, after every warp of the quarter passed the next barrier
       float* st = reinterpret_cast<float*>(stats) + (it & 1);

@@ -216,20 +216,14 @@ __global__ void __launch_bounds__(kFThreads, 1) attn_qk_bsb_short_kernel(
           for (int k = 0; k < 32; ++k)
             if (ch * 32 + k > r) v[k] = -INFINITY;
         }
-        float m = v[0];
-#pragma unroll
-        for (int k = 1; k < 32; ++k) m = fmaxf(m, v[k]);
+        float m = tree_max<32>(v);
         if (!kMask) m *= c;   // c > 0: scale after the max
         // a fully masked chunk has m = -inf: exponentiate against 0 instead
         const float mz = m == -INFINITY ? 0.f : m;
-        float l = 0.f;
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          v[k] = tc::ex2(kMask ? v[k] - mz : fmaf(v[k], c, -mz));
-          l += v[k];
-        }
+        for (int k = 0; k < 32; ++k) v[k] = tc::ex2(kMask ? v[k] - mz : fmaf(v[k], c, -mz));
         mc[ch] = m;
-        lc[ch] = l;
+        lc[ch] = tree_sum<32>(v);
         tc::tmem_st32(trow + ch * 32, v);
       }
       tc::tmem_wait_st();
@@ -289,11 +283,19 @@ __global__ void __launch_bounds__(kFThreads, 1) attn_qk_bsb_short_kernel(
 }
 
 // ------------------------------------------------------------------ backward
-constexpr int kBSlots = 3;
+// Three epilogue groups (TMEM slots), with the loads decoupled from them: a 2-stage ring of
+// dC / V operand tiles (free once the MMA read them) and a 5-deep ring of P tiles (free once
+// the dS written over them has been read out by the TMA store), each filled by its own
+// producer thread, so up to two tiles' P loads are in flight beside the three epilogues.
+constexpr int kBSlots = 3;                   // TMEM slots = epilogue groups
+constexpr int kBOps = 2;                     // dC / V operand stages
+constexpr int kBPs = 5;                      // P / dS tile buffers
 constexpr int kBThreads = 32 * (4 + 4 * kBSlots);
 constexpr uint32_t kPBytes = kS * kS * 2;    // P / dS tile (32 KB): [4 quarters][2 halves][32 x 128 B]
-constexpr uint32_t kBSlotBytes = 2 * kOpBytes + kPBytes;
-constexpr size_t kBSmem = 1024 + (size_t)kBSlots * kBSlotBytes + 256;
+constexpr uint32_t kBOpOff = kBPs * kPBytes;
+constexpr uint32_t kBBarOff = kBOpOff + kBOps * 2 * kOpBytes;
+constexpr size_t kBSmem = 1024 + kBBarOff + 8 * (2 * kBOps + 2 * kBPs + 2 * kBSlots) + 16;
+static_assert(kBSmem <= 232448, "smem");
 
 __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
     const __grid_constant__ CUtensorMap mapdC, const __grid_constant__ CUtensorMap mapV,
@@ -301,22 +303,32 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
     ShortParams prm, PhiloxKey pk) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* base = tc::align1024(smem_raw);
-  uint64_t* op_full = reinterpret_cast<uint64_t*>(base + kBSlots * kBSlotBytes);
-  uint64_t* slot_free = op_full + kBSlots;    // MMA done (1) + the 4 warps' dS stores read (4)
-  uint64_t* tm_full = slot_free + kBSlots;
+  uint64_t* op_full = reinterpret_cast<uint64_t*>(base + kBBarOff);
+  uint64_t* op_empty = op_full + kBOps;       // MMA read the operands
+  uint64_t* p_full = op_empty + kBOps;
+  uint64_t* p_free = p_full + kBPs;           // the 4 warps' dS stores have read the buffer
+  uint64_t* tm_full = p_free + kBPs;
   uint64_t* tm_empty = tm_full + kBSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + kBSlots);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int H = prm.H;
+  const int G = (int)gridDim.x;
+  const int ntiles = prm.tiles > (int)blockIdx.x ? (prm.tiles - (int)blockIdx.x + G - 1) / G : 0;
 
   if (threadIdx.x == 0) {
     tc::prefetch_tmap(&mapdC);
     tc::prefetch_tmap(&mapV);
     tc::prefetch_tmap(&mapP);
     tc::prefetch_tmap(&mapdS);
-    for (int s = 0; s < kBSlots; ++s) {
+    for (int s = 0; s < kBOps; ++s) {
       mbar_init(&op_full[s], 1);
-      mbar_init(&slot_free[s], 5);
+      mbar_init(&op_empty[s], 1);
+    }
+    for (int s = 0; s < kBPs; ++s) {
+      mbar_init(&p_full[s], 1);
+      mbar_init(&p_free[s], 4);
+    }
+    for (int s = 0; s < kBSlots; ++s) {
       mbar_init(&tm_full[s], 1);
       mbar_init(&tm_empty[s], 4);
     }
@@ -330,41 +342,49 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
 
   if (warp == 0) {
     if (lane == 0) {
-      auto load = [&](int t, int s) {
+      // ---------------------------------------------------------- operands + MMA
+      auto load = [&](int i) {
+        const int t = (int)blockIdx.x + i * G, s = i % kBOps;
         const int b = t / H, h = t - b * H;
-        unsigned char* a = base + s * kBSlotBytes;
-        mbar_arrive_expect_tx(&op_full[s], kBSlotBytes);
+        unsigned char* a = base + kBOpOff + s * 2 * kOpBytes;
+        mbar_arrive_expect_tx(&op_full[s], 2 * kOpBytes);
         tc::tma_load_4d(a, &mapdC, &op_full[s], 0, h, 0, b);             // dC rows 0..127
         tc::tma_load_4d(a + kOpBytes, &mapV, &op_full[s], 0, h, 0, b);   // V rows 0..127
-        unsigned char* pt = a + 2 * kOpBytes;
+      };
+      for (int i = 0; i < ntiles && i < kBOps; ++i) load(i);
+      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kS, kS, false, false);
+      for (int i = 0; i < ntiles; ++i) {
+        const int so = i % kBOps, st = i % kBSlots;
+        mbar_wait(&tm_empty[st], ((uint32_t)(i / kBSlots) & 1u) ^ 1u);
+        mbar_wait(&op_full[so], (uint32_t)(i / kBOps) & 1u);
+        tc::fence_after_sync();
+        const uint32_t a0 = smem_u32(base + kBOpOff + so * 2 * kOpBytes), b0 = a0 + kOpBytes;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16(tmem + st * kS, tc::smem_desc(a0 + k * 32, 16, 1024),
+                       tc::smem_desc(b0 + k * 32, 16, 1024), idesc, k != 0);
+        tc::mma_commit(&tm_full[st]);
+        tc::mma_commit(&op_empty[so]);
+        if (i + kBOps < ntiles) {   // the stage is free once these MMAs have read it
+          mbar_wait(&op_empty[so], (uint32_t)(i / kBOps) & 1u);
+          load(i + kBOps);
+        }
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {
+      // ---------------------------------------------------------- P tiles
+      for (int i = 0; i < ntiles; ++i) {
+        const int t = (int)blockIdx.x + i * G, sp = i % kBPs;
+        const int b = t / H, h = t - b * H;
+        mbar_wait(&p_free[sp], ((uint32_t)(i / kBPs) & 1u) ^ 1u);
+        mbar_arrive_expect_tx(&p_full[sp], kPBytes);
+        unsigned char* pt = base + sp * kPBytes;
 #pragma unroll
         for (int qq = 0; qq < 4; ++qq)
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf)
-            tc::tma_load_4d(pt + (qq * 2 + hf) * 4096, &mapP, &op_full[s], hf * 64, qq * 32, h, b);
-      };
-      int i = 0;
-      for (int t = blockIdx.x; t < prm.tiles && i < kBSlots; t += gridDim.x, ++i) load(t, i);
-      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kS, kS, false, false);
-      i = 0;
-      for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++i) {
-        const int s = i % kBSlots;
-        const uint32_t ph = (uint32_t)(i / kBSlots) & 1u;
-        mbar_wait(&tm_empty[s], ph ^ 1u);
-        mbar_wait(&op_full[s], ph);
-        tc::fence_after_sync();
-        const uint32_t a0 = smem_u32(base + s * kBSlotBytes), b0 = a0 + kOpBytes;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma_bf16(tmem + s * kS, tc::smem_desc(a0 + k * 32, 16, 1024),
-                       tc::smem_desc(b0 + k * 32, 16, 1024), idesc, k != 0);
-        tc::mma_commit(&tm_full[s]);
-        tc::mma_commit(&slot_free[s]);
-        const int tn = t + kBSlots * (int)gridDim.x;
-        if (tn < prm.tiles) {   // operands read by the MMA and dS stored out of the slot
-          mbar_wait(&slot_free[s], ph);
-          load(tn, s);
-        }
+            tc::tma_load_4d(pt + (qq * 2 + hf) * 4096, &mapP, &p_full[sp], hf * 64, qq * 32, h, b);
       }
     }
   } else if (warp >= 4) {
@@ -375,11 +395,10 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
     const bool hiT = pk.T >= 0x8000u;
     const uint32_t C2 = (hiT ? 0x10000u - pk.T : 0x8000u - pk.T) * 0x10001u;
     const uint32_t X = hiT ? 0u : 0xFFFFFFFFu;
-    int i = s;
-    for (int t = blockIdx.x + s * (int)gridDim.x; t < prm.tiles;
-         t += kBSlots * (int)gridDim.x, i += kBSlots) {
+    int pending = -1;   // P buffer whose dS store this warp has not yet released
+    for (int i = s; i < ntiles; i += kBSlots) {
+      const int t = (int)blockIdx.x + i * G, sp = i % kBPs;
       const int b = t / H, h = t - b * H;
-      const uint32_t ph = (uint32_t)(i / kBSlots) & 1u;
       const int64_t rowi = (int64_t)t * kS + r;
       uint32_t kf[4];
       if (prm.keep_bits) {
@@ -388,12 +407,16 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
       } else {
         row_flags(kf, prm.g0 + rowi * (kS / 8), pk, C2, X);
       }
-      mbar_wait_sleep(&tm_full[s], ph, 20000u);
-      mbar_wait(&op_full[s], ph);   // P landed (TMA) -- also implied by tm_full
+      if (pending >= 0 && lane == 0) {   // release the previous tile's buffer (deferred)
+        tc::bulk_wait_read<0>();
+        mbar_arrive(&p_free[pending]);
+      }
+      mbar_wait_sleep(&tm_full[s], (uint32_t)(i / kBSlots) & 1u, 20000u);
+      mbar_wait(&p_full[sp], (uint32_t)(i / kBPs) & 1u);
       tc::fence_after_sync();
-      unsigned char* pt = base + s * kBSlotBytes + 2 * kOpBytes + q * 2 * 4096;
-      // pass 1: dot = sum_k keep_k dA_k P_k
-      float v[32], dot = 0.f;
+      unsigned char* pt = base + sp * kPBytes + q * 2 * 4096;
+      // pass 1: dot = sum_k keep_k dA_k P_k (four partial sums)
+      float v[32], dacc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         tc::tmem_ld32(trow + ch * 32, v);
@@ -405,9 +428,11 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
               *reinterpret_cast<const uint4*>(half + tc::sw128(lane, (ch & 1) * 4 + j)), p);
 #pragma unroll
           for (int u = 0; u < 8; ++u)
-            dot = fmaf(((kf[ch] >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u], dot);
+            dacc[u & 3] = fmaf(((kf[ch] >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u],
+                               dacc[u & 3]);
         }
       }
+      const float dot = (dacc[0] + dacc[1]) + (dacc[2] + dacc[3]);
       const float nDs = -dot * ss;
       // pass 2: dS = P (keep ? scale s dA : 0) - scale s dot P, in place of P
 #pragma unroll
@@ -436,9 +461,8 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
         tc::tma_store_4d(&mapdS, pt, 0, q * 32, h, b);
         tc::tma_store_4d(&mapdS, pt + 4096, 64, q * 32, h, b);
         tc::bulk_commit();
-        tc::bulk_wait_read<0>();
-        mbar_arrive(&slot_free[s]);
       }
+      pending = sp;
       __syncwarp();
     }
     if (lane == 0) tc::bulk_wait<0>();

@@ -169,6 +169,19 @@ __device__ __forceinline__ void dropout8(float v[8], uint64_t g, const PhiloxKey
   for (int j = 0; j < 8; ++j) v[j] *= m[j];
 }
 
+// ---------------------------------------------------------------- thread-local reductions
+// pairwise trees over N (power of 2) register values: log2(N) dependent steps instead of N
+template <int N>
+__device__ __forceinline__ float tree_sum(const float* v) {
+  if constexpr (N == 1) return v[0];
+  else return tree_sum<N / 2>(v) + tree_sum<N / 2>(v + N / 2);
+}
+template <int N>
+__device__ __forceinline__ float tree_max(const float* v) {
+  if constexpr (N == 1) return v[0];
+  else return fmaxf(tree_max<N / 2>(v), tree_max<N / 2>(v + N / 2));
+}
+
 // ---------------------------------------------------------------- warp reductions
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
