@@ -143,6 +143,9 @@ _SIGS = {
     "enc_attn_bwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),
+    "enc_attn_bwd_fused_dc": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_uint64,
+                                      c_uint64, c_int64, c_void_p, c_void_p, c_void_p]),
     "enc_bei": (c_int, [c_void_p, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "enc_xattn_sizes": (c_int, [POINTER(enc_dims), c_int, POINTER(c_size_t), POINTER(c_size_t)]),
     "enc_xattn_forward": (c_int, [c_void_p, POINTER(enc_dims), c_int, POINTER(enc_cfg),

@@ -60,7 +60,8 @@ struct enc_ctx {
   int keep_ahead = 0;
   int qkv_fusion = ENC_QKV_STACKED;   // ENC_OPT_QKV_FUSION (Table A.2 algebraic fusion)
   int qkv_fusion_bwd = ENC_QKV_STACKED;   // its backward dX / dW grouping
-  int bdrln_variant = 0;   // ENC_OPT_BDRLN_VARIANT (kernel / warps per row of BDRLN, -bwd)   // measured slower at config L (the QKV contraction is slowed more)
+  int bdrln_variant = 0;   // ENC_OPT_BDRLN_VARIANT (kernel / warps per row of BDRLN, -bwd)
+  int attn_dc = 1;         // ENC_OPT_ATTN_DC (fused BSB-bwd row term from C, R26)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
@@ -408,7 +409,7 @@ static int check_cfg(const enc_cfg* c) {
 // ------------------------------------------------------------------ buffer layouts
 namespace {
 enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_KB,
-               S_N };
+               S_CLO, S_N };
 enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y2, F_N };
 enum BwdId { B_PTR, B_DY2, B_DA1, B_DH, B_DX1, B_DYO, B_DC, B_DA, B_DS, B_DQ, B_DK, B_DV, B_DQKV, B_N };
 
@@ -448,8 +449,9 @@ static Sizes sizes_of(const enc_dims* d, int dtype) {
 }
 static Layout saved_layout(const enc_dims* d, int dtype) {
   const Sizes s = sizes_of(d, dtype);
-  const size_t sz[S_N] = {s.BJI, s.BJI, s.BJI, s.BHJK, s.BHJK, s.BJI, s.BJI,
-                          s.BJI, s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ, s.KB};
+  // S_CLO: the attention output's rounding residual (bf16 path, R26)
+  const size_t sz[S_N] = {s.BJI, s.BJI, s.BJI, s.BHJK, s.BHJK, s.BJI, s.BJI, s.BJI,
+                          s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ,   s.KB,  s.BJI};
   return make_layout(sz, S_N);
 }
 static Layout fwd_layout(const enc_dims* d, int dtype) {
@@ -531,11 +533,18 @@ static bool qkv_direct(const enc_ctx* ctx, const enc_dims* d, int dtype) {
 
 // The attention-path flags a forward wrote `saved` with (Q/K/V in place or permuted, fused
 // score kernels, A stored or applied on load): the backward must read it the same way
+// The fused BSB-bwd takes its row term from C = C_hi + C_lo (R26) when the forward wrote the
+// low word: fused score path with A.V on the per-(b,h) kernel, J = K = 512
+static bool dc_term_of(const enc_ctx* ctx, bool fused_attn, int J, int P) {
+  return fused_attn && use_bh(ctx, J, P) && ctx->attn_dc && !attn_short_supported(J, P);
+}
+
 static uint32_t path_flags(const enc_ctx* ctx, const enc_dims* d, int dtype) {
   const bool tc = tc_attn_of(ctx, dtype, d->J, d->P);
   const bool fused = tc && ctx->attn_fused && attn_fused_supported(d->J, d->P);
   return (qkv_direct(ctx, d, dtype) ? 1u : 0u) | (tc ? 2u : 0u) | (fused ? 4u : 0u) |
-         (fused && use_bh(ctx, d->J, d->P) ? 8u : 0u) | 0x100u;
+         (fused && use_bh(ctx, d->J, d->P) ? 8u : 0u) |
+         (dc_term_of(ctx, fused, d->J, d->P) ? 16u : 0u) | 0x100u;
 }
 
 int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
@@ -851,6 +860,22 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   return ENC_OK;
 }
 
+int enc_attn_bwd_fused_dc(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
+                          const void* V, const void* Pin, const void* C_hi, const void* C_lo,
+                          float p, uint64_t seed, uint64_t subseq, int64_t batch_offset,
+                          const uint32_t* keep_bits, void* dS, enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (!attn_fused_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(dC, V, Pin, C_hi, C_lo, dS);
+  if (B == 0) return ENC_OK;
+  OpTimer _t(ctx, ENC_OP_BSB_BWD, (cudaStream_t)stream, 1);
+  CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, (int64_t)H * P, V, P, Pin,
+                         make_philox_key(p, seed, subseq), batch_offset, keep_bits, dS,
+                         (cudaStream_t)stream, false, C_hi, C_lo, (int64_t)H * P));
+  return ENC_OK;
+}
+
 int enc_set_option(enc_ctx* ctx, int key, int value) {
   if (!ctx) return ENC_ENULL;
   if (key == ENC_OPT_ATTN_TC) {
@@ -913,6 +938,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_KEEP_AHEAD) {
     ctx->keep_ahead = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_ATTN_DC) {
+    ctx->attn_dc = value ? 1 : 0;
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_PAIR) {
@@ -1161,7 +1190,10 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   {
     OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
     if (drop_on_load) {
-      CK(launch_attn_av_bh(B, H, J, P, Pm, V, ldqkv, C, I, kbits, pk_attn.scale, st));
+      // (+ the fp32 result's low bf16 word for the backward's row term, R26)
+      CK(launch_attn_av_bh(B, H, J, P, Pm, V, ldqkv, C, I, kbits, pk_attn.scale, st,
+                           dc_term_of(ctx, fused_attn, J, P) ? at(saved, SL.off[S_CLO])
+                                                             : nullptr));
     } else if (tc_attn) {
       CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, 0, V, ldqkv, C, I, st));
     } else {
@@ -1469,10 +1501,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   // BSB-bwd (:590)
   {
     OpTimer _t(ctx, ENC_OP_BSB_BWD, st, 1);
+    const bool dc_term = dc_term_of(ctx, fused_attn, J, P);
     if (fused_attn)  // Gamma dX1 (:588) + BSB-bwd (:590): dA stays in TMEM
       CK(launch_attn_da_bsbb(B, H, J, P, scale, dC, I, V, ldqkv, Pm,
                              make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff,
-                             (const uint32_t*)at(sv, SL.off[S_KB]), dS, st, overlap));
+                             (const uint32_t*)at(sv, SL.off[S_KB]), dS, st, overlap,
+                             dc_term ? C : nullptr, dc_term ? at(sv, SL.off[S_CLO]) : nullptr,
+                             I));
     else
       CK(launch_bsb_bwd(dtype, B, H, J, K, scale, dA, Pm,
                         make_philox_key(cfg->p_attn, cfg->seed, l4 + 0), boff, dS, st));

@@ -47,6 +47,11 @@ struct BhParams {
   // MMA, and the epilogue multiplies the fp32 accumulators by out_scale (= s)
   const uint32_t* keep;   // [B*H*J, K/32] ENC_KEEP_BITS words, or null (X used as is)
   float out_scale;
+  // optional (row output only): the rounding residual lo = bf16(acc - float(bf16(acc))) of
+  // every stored element, same layout as the row output (the attention output's low word
+  // for the backward's row term, R26)
+  __nv_bfloat16* lo_r;
+  int64_t ld_lo;
 };
 
 // 0xFFFF / 0x0000 per 16-bit half from the sign bits 15 and 31 (prmt sign replication)
@@ -279,6 +284,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
           w.w = Chunk<__nv_bfloat16>::pack2(v[8 * ch + 6], v[8 * ch + 7]);
           *reinterpret_cast<uint4*>(buf + tc::sw128(lane, ch)) = w;
         }
+        if (is_r && p.lo_r != nullptr) {
+          // lane = row; its 64 columns are 128 contiguous bytes of the [B,J,H,P] rows
+          __nv_bfloat16* lo = p.lo_r + ((int64_t)b * (nt * 128) + t * 128 + q * 32 + lane) *
+                                           p.ld_lo + h * 64;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            float r8[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const float hi = __bfloat162float(__float2bfloat16_rn(v[8 * ch + u]));
+              r8[u] = v[8 * ch + u] - hi;
+            }
+            uint4 w;
+            w.x = Chunk<__nv_bfloat16>::pack2(r8[0], r8[1]);
+            w.y = Chunk<__nv_bfloat16>::pack2(r8[2], r8[3]);
+            w.z = Chunk<__nv_bfloat16>::pack2(r8[4], r8[5]);
+            w.w = Chunk<__nv_bfloat16>::pack2(r8[6], r8[7]);
+            *reinterpret_cast<uint4*>(lo + ch * 8) = w;
+          }
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -381,9 +406,13 @@ bool attn_bh_supported(int J, int P) { return P == 64 && J % 128 == 0 && J >= 12
 static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const void* Yr,
                              int64_t ldyr, const void* Yc, int64_t ldyc, void* Or, int64_t ldor,
                              void* Oc, int64_t ldoc, float* ps_r, float* ps_c, int ps_ld,
-                             const uint32_t* keep, float out_scale, cudaStream_t st) {
+                             const uint32_t* keep, float out_scale, cudaStream_t st,
+                             void* lo_r = nullptr) {
   if (!attn_bh_supported(J, P)) return cudaErrorInvalidValue;
+  if (lo_r && (((uintptr_t)lo_r & 15u) || ldor % 8)) return cudaErrorInvalidValue;
   BhParams p{};
+  p.lo_r = (__nv_bfloat16*)lo_r;
+  p.ld_lo = ldor;
   p.H = H;
   p.nt = J / 128;
   p.units = B * H;
@@ -418,9 +447,9 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
 
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
                               int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
-                              float scale, cudaStream_t st) {
+                              float scale, cudaStream_t st, void* C_lo) {
   return bh_launch(B, H, J, P, A, V, ldv, nullptr, 0, C, ldc, nullptr, 0, nullptr, nullptr, 0,
-                   keep, keep ? scale : 1.f, st);
+                   keep, keep ? scale : 1.f, st, C_lo);
 }
 
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,

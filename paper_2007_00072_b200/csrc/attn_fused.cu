@@ -22,12 +22,20 @@
 // 64-B-swizzled [32 x 32] tile pair and written by TMA stores.
 // Backward epilogue: each warp TMA-loads its own [32 x 64] P sub-tile (one tile ahead, its
 // own mbarrier), pass 1 sum_k dropout(dA)*P with the keep bits kept in registers, pass 2
-// dS written in place of the P sub-tile and stored by TMA.
+// dS written in place of the P sub-tile and stored by TMA.  With the forward's attention
+// output C given (kDC, R26), the row term sum_k dP*P is the identity
+// sum_p dC*C (C = A V, A = dropout(P)), formed from dC and C (fp32 as two bf16 words,
+// C_hi by TMA with the operands) while the MMA runs: pass 1, its wait for P and its
+// cross-warp barrier disappear and the epilogue is one pass over TMEM (measured at config L:
+// 53 -> 45 us alone, 48 -> 39 us in the layer's graph).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <type_traits>
 
 #include "kernels.h"
 #include "tc_gemm.cuh"
@@ -53,7 +61,20 @@ struct FusedParams {
                            // bwd: read instead of recomputing Philox when kBits)
   int write_a;             // fwd: A = dropout(P) stored (0: only P and the keep words)
   int keep_pre;            // fwd: keep_bits already hold this call's keep words (read them)
+  // bwd kDC: dC and the forward's attention output C = C_hi + C_lo ([B,J,H,P] rows)
+  const __nv_bfloat16* dc;
+  const __nv_bfloat16* chi;
+  const __nv_bfloat16* clo;
+  int64_t ld_dc, ld_c;
 };
+
+__device__ __forceinline__ uint4 ld_nc4(const __nv_bfloat16* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
 
 __device__ __forceinline__ void qbar(int q) {   // the 8 warps of TMEM lane quarter q
   asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(kSlices * 32) : "memory");
@@ -138,15 +159,18 @@ __device__ __forceinline__ void trace_ev(int warp, int lane, int it, int e) {
 constexpr uint32_t kOpA = 0, kOpB = 16384, kOpX = 81920;
 constexpr uint32_t kStats = kOpX + kWarps * 4096;
 constexpr uint32_t kBars = kStats + 2 * kSlices * kRows * 8;
-constexpr size_t kSmem = 1024 + kBars + (4 + kWarps) * 8 + 16;
+constexpr uint32_t kLoX = kBars + 512;                     // bwd kDC: [2][4][32] float
+constexpr size_t kSmem = 1024 + kLoX + 2 * 4 * 32 * 4;
 static_assert(kSmem <= 227 * 1024, "smem");
 static_assert(kW == 64, "two keep-flag words per thread");
 
-template <bool kBwd, bool kMask, bool kBits, bool kCausal = false>
+template <bool kBwd, bool kMask, bool kBits, bool kCausal = false, bool kDC = false>
 __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtensorMap& mapB,
                                            const CUtensorMap& mapP, const CUtensorMap& mapO1,
                                            const CUtensorMap& mapO2, const FusedParams& prm,
-                                           const PhiloxKey& pk, unsigned char* base) {
+                                           const PhiloxKey& pk, unsigned char* base,
+                                           const CUtensorMap* mapC = nullptr) {
+  static_assert(!kDC || kBwd, "kDC is a backward variant");
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int q = warp & 3;             // TMEM lane quarter
@@ -165,7 +189,10 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   uint64_t* tm_full = op_full + 2;
   uint64_t* tm_empty = op_full + 3;
   uint64_t* p_full = op_full + 4;                              // [32] (bwd, per warp)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(op_full + 4 + kWarps);
+  uint64_t* dbar = op_full + 4 + kWarps;                       // (kDC) [4 quarters][2]
+  uint64_t* d_done = op_full + 12 + kWarps;                    // (kDC) dC / C_hi tiles read
+  float* lo_x = reinterpret_cast<float*>(base + kLoX);         // (kDC) [2][4][32]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(op_full + 13 + kWarps);
   unsigned char* own = base + kOpX + warp * 4096;              // this warp's 4 KB region
 
   auto tile_coords = [&](int t, int& b, int& h, int& m0, int& bh) {
@@ -177,7 +204,8 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   auto load_operands = [&](int t) {
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
-    mbar_arrive_expect_tx(op_full, (uint32_t)(kRows + kK) * 128);
+    mbar_arrive_expect_tx(op_full, (uint32_t)(kRows + kK + (kDC ? kRows : 0)) * 128);
+    if (kDC) tc::tma_load_4d(base + kStats, mapC, op_full, 0, h, m0, b);   // C_hi rows m0..
     // P-wide operand maps (map_pop): coordinates (p, h, row, b)
     tc::tma_load_4d(base + kOpA, &mapA, op_full, 0, h, m0, b);          // Q / dC rows m0..
     tc::tma_load_4d(base + kOpB, &mapB, op_full, 0, h, 0, b);           // K or V rows 0..255
@@ -196,10 +224,15 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
     tc::prefetch_tmap(&mapO1);
     if (kBwd) tc::prefetch_tmap(&mapP);
     if (!kBwd) tc::prefetch_tmap(&mapO2);
+    if (kDC) tc::prefetch_tmap(mapC);
     mbar_init(op_full, 1);
     mbar_init(op_empty, 1);
     mbar_init(tm_full, 1);
     mbar_init(tm_empty, kWarps);
+    if (kDC) {
+      for (int i = 0; i < 8; ++i) mbar_init(&dbar[i], kSlices * 32);
+      mbar_init(d_done, kWarps);
+    }
     fence_mbar_init();
   }
   if (kBwd && lane == 0) {
@@ -215,7 +248,6 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
 
   if (leader && blockIdx.x < prm.tiles) load_operands(blockIdx.x);
   if (kBwd && lane == 0 && blockIdx.x < prm.tiles) load_psub(blockIdx.x);
-
   int it = 0;
   for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
     int b, h, m0, bh;
@@ -263,11 +295,53 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     }
     TRACE(1);
+    float Dc = 0.f;
+    if constexpr (kDC) {
+      // D_r = sum_p dC[r,p] (C_hi[r,p] + C_lo[r,p]).  C_hi part: per thread over its whole row
+      // from the dC and C_hi tiles in shared memory.  C_lo part (a 2^-9 correction): warp
+      // (q, s) forms it for rows 32q + 4s .. +3 from ONE coalesced 16-B load per lane (lane l:
+      // row 4s + l/8, p-chunk l%8; issued before the C_hi part, which covers its latency), a
+      // 3-step shuffle reduction over the row's 8 lanes, and hands the 4 sums to the quarter
+      // through lo_x behind the quarter's per-parity mbarrier (read before pass 2)
+      const int lrow = m0 + q * 32 + 4 * slice + (lane >> 3);
+      const uint4 ul = ld_nc4(prm.clo + ((int64_t)b * prm.J + lrow) * prm.ld_c + h * 64 +
+                              (lane & 7) * 8);
+      mbar_wait(op_full, it & 1);
+      float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float x[8], y[8];
+        Chunk<__nv_bfloat16>::unpack(
+            *reinterpret_cast<const uint4*>(base + kOpA + tc::sw128(r, c)), x);
+        Chunk<__nv_bfloat16>::unpack(
+            *reinterpret_cast<const uint4*>(base + kStats + tc::sw128(r, c)), y);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dacc[u & 3] = fmaf(x[u], y[u], dacc[u & 3]);
+      }
+      Dc = (dacc[0] + dacc[1]) + (dacc[2] + dacc[3]);
+      {
+        float xd[8], xl[8];
+        Chunk<__nv_bfloat16>::unpack(*reinterpret_cast<const uint4*>(
+                                         base + kOpA + tc::sw128(lrow - m0, lane & 7)), xd);
+        Chunk<__nv_bfloat16>::unpack(ul, xl);
+        float part = 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) part = fmaf(xd[u], xl[u], part);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 1);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 2);
+        part += __shfl_xor_sync(0xFFFFFFFFu, part, 4);
+        if ((lane & 7) == 0) lo_x[((it & 1) * 4 + q) * 32 + 4 * slice + (lane >> 3)] = part;
+        mbar_arrive(&dbar[q * 2 + (it & 1)]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_done);
+    }
     mbar_wait_sleep(tm_full, it & 1);
     tc::fence_after_sync();
     TRACE(2);
     if (leader && t + (int)gridDim.x < prm.tiles) {   // operands free: prefetch the next tile
       mbar_wait(op_empty, it & 1);
+      if (kDC) mbar_wait(d_done, it & 1);   // every warp has read dC and C_hi
       load_operands(t + gridDim.x);
     }
     float v[32];
@@ -388,39 +462,45 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       }
       TRACE(5);
     } else {
-      // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
       mbar_wait_sleep(&p_full[warp], it & 1);
       TRACE(3);
-      float dacc[4] = {0.f, 0.f, 0.f, 0.f};   // four partial sums
-#pragma unroll
-      for (int ch = 0; ch < kW / 32; ++ch) {
-        tc::tmem_ld32(trow + ch * 32, v);
-        const uint32_t f = kf[ch];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float p[8];
-          Chunk<__nv_bfloat16>::unpack(
-              *reinterpret_cast<const uint4*>(own + tc::sw128(lane, ch * 4 + j)), p);
-#pragma unroll
-          for (int u = 0; u < 8; ++u)
-            dacc[u & 3] = fmaf(((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u],
-                               dacc[u & 3]);
-        }
-      }
-      const float dot = (dacc[0] + dacc[1]) + (dacc[2] + dacc[3]);
-      // row statistics alternate between the .x / .y slots by tile parity: a slot is
-      // rewritten two tiles later, after every warp of the quarter passed the next barrier
-      float* st = reinterpret_cast<float*>(stats) + (it & 1);
-      st[2 * (slice * kRows + r)] = dot;
-      TRACE(4);
-      qbar(q);
-      TRACE(5);
-      float D = 0.f;
-#pragma unroll
-      for (int s2 = 0; s2 < kSlices; ++s2) D += st[2 * (s2 * kRows + r)];
       // dS = scale * P * (dP - D'),  dP = keep ? sc * dA : 0,  D' = sc * dot
       const float ss = prm.c * pk.scale;        // scale * dropout scale
-      const float nDs = -D * ss;                // -scale * D'
+      float nDs;                                // -scale * D'
+      if constexpr (kDC) {
+        mbar_wait(&dbar[q * 2 + (it & 1)], (it >> 1) & 1);
+        nDs = -(Dc + lo_x[((it & 1) * 4 + q) * 32 + lane]) * prm.c;   // D' includes sc
+      } else {
+        // pass 1: dot = sum_k keep_k * dA_k * P_k over this slice (x dropout scale below)
+        float dacc[4] = {0.f, 0.f, 0.f, 0.f};   // four partial sums
+#pragma unroll
+        for (int ch = 0; ch < kW / 32; ++ch) {
+          tc::tmem_ld32(trow + ch * 32, v);
+          const uint32_t f = kf[ch];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            float p[8];
+            Chunk<__nv_bfloat16>::unpack(
+                *reinterpret_cast<const uint4*>(own + tc::sw128(lane, ch * 4 + j)), p);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              dacc[u & 3] = fmaf(((f >> flag_bit(j, u)) & 1u) ? v[8 * j + u] : 0.f, p[u],
+                                 dacc[u & 3]);
+          }
+        }
+        const float dot = (dacc[0] + dacc[1]) + (dacc[2] + dacc[3]);
+        // row statistics alternate between the .x / .y slots by tile parity: a slot is
+        // rewritten two tiles later, after every warp of the quarter passed the next barrier
+        float* st = reinterpret_cast<float*>(stats) + (it & 1);
+        st[2 * (slice * kRows + r)] = dot;
+        TRACE(4);
+        qbar(q);
+        TRACE(5);
+        float D = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < kSlices; ++s2) D += st[2 * (s2 * kRows + r)];
+        nDs = -D * ss;
+      }
       // pass 2: dS over the P sub-tile in place
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
@@ -471,17 +551,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_kernel(
     FusedParams prm, PhiloxKey pk) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   fused_body<false, kMask, kBits, kCausal>(mapQ, mapK, mapQ, mapP, mapA, prm, pk,
-                                  tc::align1024(smem_raw));
+                                           tc::align1024(smem_raw));
 }
 
-template <bool kBits>
+template <bool kBits, bool kDC>
 __global__ void __launch_bounds__(kThreads, 1) attn_da_bsbb_kernel(
     const __grid_constant__ CUtensorMap mapdC, const __grid_constant__ CUtensorMap mapV,
     const __grid_constant__ CUtensorMap mapP, const __grid_constant__ CUtensorMap mapdS,
-    FusedParams prm, PhiloxKey pk) {
+    FusedParams prm, PhiloxKey pk, const __grid_constant__ CUtensorMap mapC) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  fused_body<true, false, kBits>(mapdC, mapV, mapP, mapdS, mapdS, prm, pk,
-                                 tc::align1024(smem_raw));
+  fused_body<true, false, kBits, false, kDC>(mapdC, mapV, mapP, mapdS, mapdS, prm, pk,
+                                             tc::align1024(smem_raw), &mapC);
 }
 
 bool map4(CUtensorMap* m, const void* ptr, const uint64_t d[4], const uint64_t s[3],
@@ -516,10 +596,15 @@ int persistent_grid(int tiles) {
 template <typename Kern>
 cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const CUtensorMap& b,
                               const CUtensorMap& c, const CUtensorMap& d, const FusedParams& prm,
-                              const PhiloxKey& pk, cudaStream_t st, bool high_prio = false) {
+                              const PhiloxKey& pk, cudaStream_t st, bool high_prio = false,
+                              const CUtensorMap* e = nullptr) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
   if (!high_prio) {
-    kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk);
+    if constexpr (std::is_invocable_v<Kern, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                                      FusedParams, PhiloxKey, CUtensorMap>)
+      kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk, *e);
+    else
+      kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk);
     return cudaGetLastError();
   }
   // the persistent kernel assumes all of its CTAs are resident at once: when a kernel on
@@ -537,7 +622,11 @@ cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const 
   at[0].val.priority = greatest;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk);
+  if constexpr (std::is_invocable_v<Kern, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
+                                    FusedParams, PhiloxKey, CUtensorMap>)
+    return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk, *e);
+  else
+    return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk);
 }
 
 // The attention keep words (ENC_KEEP_BITS layout) of a [B,H,J,K] call: one thread per 64
@@ -639,7 +728,8 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,
                                 const uint32_t* keep_bits, void* dS, cudaStream_t st,
-                                bool high_prio) {
+                                bool high_prio, const void* Chi, const void* Clo,
+                                int64_t ldc) {
   if (attn_short_supported(J, P))
     return launch_attn_da_bsbb_short(B, H, J, P, scale, dC, lddc, V, ldv, Pin, pk, batch_offset,
                                      keep_bits, dS, st, high_prio);
@@ -648,14 +738,26 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
   bool ok = map_pop(&mc, dC, B, H, J, P, lddc, kRows) && map_pop(&mv, V, B, H, K, P, ldv, 256) &&
             map_bhrc(&mp, Pin, B, H, J, K, 64, 32) && map_bhrc(&ms, dS, B, H, J, K, 64, 32);
   if (!ok) return cudaErrorInvalidValue;
+  const bool dc = Chi && Clo;
+  if (dc && (((uintptr_t)dC | (uintptr_t)Chi | (uintptr_t)Clo) & 15u || lddc % 8 || ldc % 8))
+    return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,       J,       tiles, scale, batch_offset * (int64_t)H * J * (K / 8),
-                  nullptr, const_cast<uint32_t*>(keep_bits), 0, 0};
-  return keep_bits
-             ? launch_persistent(attn_da_bsbb_kernel<true>, tiles, mc, mv, mp, ms, prm, pk, st,
-                                 high_prio)
-             : launch_persistent(attn_da_bsbb_kernel<false>, tiles, mc, mv, mp, ms, prm, pk, st,
-                                 high_prio);
+                  nullptr, const_cast<uint32_t*>(keep_bits), 0, 0,
+                  (const __nv_bfloat16*)dC, (const __nv_bfloat16*)Chi,
+                  (const __nv_bfloat16*)Clo, lddc, ldc};
+  if (dc) {   // the C_hi tile arrives with the operands (C_lo is read by the warps)
+    CUtensorMap mC;
+    if (!map_pop(&mC, Chi, B, H, J, P, ldc, kRows)) return cudaErrorInvalidValue;
+    return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true, true>, tiles, mc, mv, mp, ms,
+                                         prm, pk, st, high_prio, &mC)
+                     : launch_persistent(attn_da_bsbb_kernel<false, true>, tiles, mc, mv, mp, ms,
+                                         prm, pk, st, high_prio, &mC);
+  }
+  return keep_bits ? launch_persistent(attn_da_bsbb_kernel<true, false>, tiles, mc, mv, mp, ms,
+                                       prm, pk, st, high_prio, &mc)
+                   : launch_persistent(attn_da_bsbb_kernel<false, false>, tiles, mc, mv, mp, ms,
+                                       prm, pk, st, high_prio, &mc);
 }
 
 #ifdef ENC_FUSED_TRACE

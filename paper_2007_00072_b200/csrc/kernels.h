@@ -207,7 +207,7 @@ bool attn_bh_supported(int J, int P);
 // ENC_KEEP_BITS words while the block is in shared memory; the result is scaled by `scale`.
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
                               int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
-                              float scale, cudaStream_t st);
+                              float scale, cudaStream_t st, void* C_lo = nullptr);
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
                               int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
                               const uint32_t* keep, float scale, cudaStream_t st);
@@ -249,7 +249,8 @@ cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const v
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,
                                 const uint32_t* keep_bits, void* dS, cudaStream_t st,
-                                bool high_prio = false);
+                                bool high_prio = false, const void* Chi = nullptr,
+                                const void* Clo = nullptr, int64_t ldc = 0);
 
 // Pointer tables for the two-level-strided batched GEMMs of the attention (A.V forward,
 // dA/dV backward): the operand [B,J,H,P] with row stride I per (b,h) pair.

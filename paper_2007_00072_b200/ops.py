@@ -129,7 +129,7 @@ def enc_set_option(ctx, key, value):
 
 (OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT,
  OPT_BWD_SIDE, OPT_ATTN_OVERLAP, OPT_GEMM_TC, OPT_GEMM_PAIR, OPT_GEMM_TC_MASK,
- OPT_KEEP_AHEAD, OPT_QKV_FUSION, OPT_QKV_FUSION_BWD, OPT_BDRLN_VARIANT) = range(15)
+ OPT_KEEP_AHEAD, OPT_QKV_FUSION, OPT_QKV_FUSION_BWD, OPT_BDRLN_VARIANT, OPT_ATTN_DC) = range(16)
 QKV_SEPARATE, QKV_QK_STACKED, QKV_STACKED, QKV_KV_STACKED = range(4)
 
 
@@ -145,6 +145,13 @@ def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batc
     check("enc_attn_bwd_fused", _abi.load().enc_attn_bwd_fused(
         ctx.ptr, B, H, J, P, scale, _p(dC), _p(V), _p(Pin), p, seed, subseq, batch_offset,
         _p(keep_bits), _p(dS), _stream(stream)))
+
+
+def enc_attn_bwd_fused_dc(ctx, B, H, J, P, scale, dC, V, Pin, C_hi, C_lo, p, seed, subseq,
+                          batch_offset, dS, keep_bits=None, stream=None):
+    check("enc_attn_bwd_fused_dc", _abi.load().enc_attn_bwd_fused_dc(
+        ctx.ptr, B, H, J, P, scale, _p(dC), _p(V), _p(Pin), _p(C_hi), _p(C_lo), p, seed,
+        subseq, batch_offset, _p(keep_bits), _p(dS), _stream(stream)))
 
 
 def enc_wgemm(ctx, A, B, C, tA=False, tB=False, beta=0, bias=None, M=None, N=None, K=None,

@@ -111,6 +111,42 @@ def test_fused_backward(ops, ctx, B, H, J, p, stored):
     assert_parity("dS", g, dSo, "bf16")
 
 
+@pytest.mark.parametrize("B,H,J", [(1, 1, 512), (2, 3, 512), (8, 16, 512)] + SHORT)
+@pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
+@pytest.mark.parametrize("stored", [False, True])
+def test_fused_backward_dc(ops, ctx, B, H, J, p, stored):
+    """enc_attn_bwd_fused_dc: the BSB-bwd row term from the attention output C = A V
+    (R26) -- C built here from the oracle's keep mask in fp64 and split into the
+    two bf16 words the layer stores (C_hi, C_lo); dS must match the oracle's BSB-bwd (which
+    forms sum_k dP P) within the bf16 tolerance, dropped elements included."""
+    P = 64
+    dC = make_tensor((B, J, H, P), 41, "bf16")          # [B,J,H,P]
+    V = make_tensor((B, H, J, P), 42, "bf16")
+    Pm = make_positive_rows((B, H, J, J), 43, "bf16")
+    boff, sub, scale = 5, 4, 0.125
+    keep = philox.keep_mask_tensor((B, H, J, J), boff, p, SEED, sub).astype(np.float64)
+    A = Pm.astype(np.float64) * keep * philox.dropout_scale(p)
+    C = np.ascontiguousarray(np.einsum("bhjk,bhkp->bjhp", A, V.astype(np.float64)))
+    bits = None
+    if stored:
+        bits = torch.zeros((B, H, J, J // 32), dtype=torch.int32, device="cuda")
+        q = dev(make_tensor((B, H, J, P), 44, "bf16"))
+        junk = torch.empty((B, H, J, J), dtype=torch.bfloat16, device="cuda")
+        ops.enc_attn_fwd_fused(ctx, B, H, J, P, scale, q, q, None, p, SEED, sub, boff, junk,
+                               None, keep_bits=bits)
+    dS = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
+    C_hi = torch.tensor(C, dtype=torch.float64).to(torch.bfloat16)
+    C_lo = (torch.tensor(C, dtype=torch.float64) - C_hi.double()).to(torch.bfloat16)
+    ops.enc_attn_bwd_fused_dc(ctx, B, H, J, P, scale, dev(dC), dev(V), dev(Pm), C_hi.cuda(),
+                              C_lo.cuda(), p, SEED, sub, boff, dS, keep_bits=bits)
+    torch.cuda.synchronize()
+    dA = dC.astype(np.float64).transpose(0, 2, 1, 3) @ V.astype(np.float64).transpose(0, 1, 3, 2)
+    dSo = E.bsb_bwd(dA, Pm, scale, p, SEED, sub, boff)
+    g = host(dS)
+    assert np.isfinite(g).all()
+    assert_parity("dS", g, dSo, "bf16")
+
+
 @pytest.mark.parametrize("J,P", [(256, 64), (384, 64), (512, 32), (128, 32), (640, 64)])
 def test_fused_unsupported_shapes(ops, ctx, J, P):
     """The fused kernels hold a whole 512-key score row (or whole 128 x 128 score matrices)

@@ -32,6 +32,7 @@ def main():
     Q = torch.randn((B, H, J, P), device=dev, generator=g).to(bf)
     K = torch.randn((B, H, J, P), device=dev, generator=g).to(bf)
     dC = torch.randn((B, J, H, P), device=dev, generator=g).to(bf)
+    Cm = torch.randn((B, J, H, P), device=dev, generator=g).to(bf)
     M = torch.zeros((B, J), device=dev) if args.mask else None
     Pm = torch.empty((B, H, J, J), device=dev, dtype=bf)
     A = torch.empty_like(Pm)
@@ -57,16 +58,26 @@ def main():
         "bwd": (lambda: ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, args.p, seed, 0,
                                                0, dS, keep_bits=bits),
                 2 * x_bytes + 2 * s_bytes + k_bytes),
+        "bwd_dc": (lambda: ops.enc_attn_bwd_fused_dc(ctx, B, H, J, P, 0.125, dC, K, Pm, Cm, Cm, args.p,
+                                                     seed, 0, 0, dS, keep_bits=bits),
+                   4 * x_bytes + 2 * s_bytes + k_bytes),
     }
     only = [v for v in args.only.split(",") if v] or list(variants)
     for name in only:
         fn, byts = variants[name]
+        fn()   # bits for the backward variants (and warm-up)
+        torch.cuda.synchronize()
+        # the launch replayed from a CUDA graph: no host-side tensor-map encoding inside
+        # the events
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
         ts = []
         for _ in range(args.reps):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            fn()
+            gr.replay()
             e1.record(st)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
