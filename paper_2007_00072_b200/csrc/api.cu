@@ -62,6 +62,7 @@ struct enc_ctx {
   int qkv_fusion_bwd = ENC_QKV_STACKED;   // its backward dX / dW grouping
   int bdrln_variant = 0;   // ENC_OPT_BDRLN_VARIANT (kernel / warps per row of BDRLN, -bwd)
   int attn_dc = 1;         // ENC_OPT_ATTN_DC (fused BSB-bwd row term from C, R26)
+  int mask_bytes = 1;      // ENC_OPT_MASK_BYTES (BDRLN / BAD keep bytes stored, R27)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
@@ -409,12 +410,12 @@ static int check_cfg(const enc_cfg* c) {
 // ------------------------------------------------------------------ buffer layouts
 namespace {
 enum SavedId { S_Q, S_K, S_V, S_P, S_A, S_C, S_X1, S_XH1, S_H, S_A1, S_XH2, S_R1, S_R2, S_KB,
-               S_CLO, S_N };
+               S_CLO, S_KB1, S_KBF, S_KB2, S_N };
 enum FwdId { F_PTR, F_QKV, F_S, F_YO, F_Y2, F_N };
 enum BwdId { B_PTR, B_DY2, B_DA1, B_DH, B_DX1, B_DYO, B_DC, B_DA, B_DS, B_DQ, B_DK, B_DV, B_DQKV, B_N };
 
 struct Layout {
-  size_t off[16];
+  size_t off[20];
   size_t total;
 };
 
@@ -432,7 +433,7 @@ static Layout make_layout(const size_t* sizes, int n) {
 }
 
 struct Sizes {
-  size_t BJI, BJU, BHJK, BJ3I, BJ, ptr, KB;
+  size_t BJI, BJU, BHJK, BJ3I, BJ, ptr, KB, KBI, KBU;
 };
 static Sizes sizes_of(const enc_dims* d, int dtype) {
   const size_t es = esize(dtype);
@@ -445,13 +446,17 @@ static Sizes sizes_of(const enc_dims* d, int dtype) {
   s.BJ = BJ * sizeof(float);
   s.ptr = (size_t)5 * d->B * d->H * sizeof(void*);
   s.KB = (size_t)d->B * d->H * d->J * ((d->K + 31) / 32) * sizeof(uint32_t);  // keep-flag words
+  s.KBI = BJ * (size_t)(d->I / 8);   // keep bytes of a hidden-size dropout site (R27)
+  s.KBU = BJ * (size_t)(d->U / 8);   // keep bytes of the FFN dropout site
   return s;
 }
 static Layout saved_layout(const enc_dims* d, int dtype) {
   const Sizes s = sizes_of(d, dtype);
   // S_CLO: the attention output's rounding residual (bf16 path, R26)
+  // S_KB1 / S_KBF / S_KB2: keep bytes of BDRLN site 1, BAD, BDRLN site 2 (R27)
   const size_t sz[S_N] = {s.BJI, s.BJI, s.BJI, s.BHJK, s.BHJK, s.BJI, s.BJI, s.BJI,
-                          s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ,   s.KB,  s.BJI};
+                          s.BJU, s.BJU, s.BJI, s.BJ,   s.BJ,   s.KB,  s.BJI, s.KBI,
+                          s.KBU, s.KBI};
   return make_layout(sz, S_N);
 }
 static Layout fwd_layout(const enc_dims* d, int dtype) {
@@ -539,12 +544,20 @@ static bool dc_term_of(const enc_ctx* ctx, bool fused_attn, int J, int P) {
   return fused_attn && use_bh(ctx, J, P) && ctx->attn_dc && !attn_short_supported(J, P);
 }
 
+// The forward stores keep bytes (R27) of both BDRLN sites when ENC_OPT_MASK_BYTES is on, and
+// of BAD when it also runs in the Linear1 contraction's epilogue
+static bool bad_bytes_of(const enc_ctx* ctx, const enc_dims* d, int dtype) {
+  return ctx->mask_bytes && dtype == ENC_BF16 && ((ctx->gemm_tc >> ENC_OP_GEMM_L1) & 1u) &&
+         d->U % 8 == 0 && d->I % 8 == 0;
+}
+
 static uint32_t path_flags(const enc_ctx* ctx, const enc_dims* d, int dtype) {
   const bool tc = tc_attn_of(ctx, dtype, d->J, d->P);
   const bool fused = tc && ctx->attn_fused && attn_fused_supported(d->J, d->P);
   return (qkv_direct(ctx, d, dtype) ? 1u : 0u) | (tc ? 2u : 0u) | (fused ? 4u : 0u) |
          (fused && use_bh(ctx, d->J, d->P) ? 8u : 0u) |
-         (dc_term_of(ctx, fused, d->J, d->P) ? 16u : 0u) | 0x100u;
+         (dc_term_of(ctx, fused, d->J, d->P) ? 16u : 0u) | (ctx->mask_bytes ? 32u : 0u) |
+         (bad_bytes_of(ctx, d, dtype) ? 64u : 0u) | 0x100u;
 }
 
 int enc_saved_views(enc_ctx* ctx, const enc_dims* d, int dtype, void* saved, enc_saved_view* v) {
@@ -944,6 +957,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->attn_dc = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_MASK_BYTES) {
+    ctx->mask_bytes = value ? 1 : 0;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_GEMM_PAIR) {
     ctx->gemm_cg = value ? 0 : 1;
     return ENC_OK;
@@ -1214,12 +1231,14 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD1, st, 1);
     CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st,
-                        ctx->bdrln_variant & 15));
+                        ctx->bdrln_variant & 15,
+                        ctx->mask_bytes ? (uint8_t*)at(saved, SL.off[S_KB1]) : nullptr));
   }
   // Linear (:559) + BAD (:560-562).  The activation input h = X1 W1^T + b1 is kept for the
   // backward (saved.h); on the tcgen05 path BAD runs in the contraction's epilogue
   const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
   WgemmArgs l1 = ffn_fwd_args(ctx, d, dtype, cfg, X1, prm->W1, prm->b1, pk_ffn, h, A1);
+  if (bad_bytes_of(ctx, d, dtype)) l1.kb_out = (uint8_t*)at(saved, SL.off[S_KBF]);
   if (wgemm_supported(l1)) {
     // (BAD has no launch of its own: no ENC_OP_BAD_FWD timing on this path)
     OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 1);
@@ -1245,7 +1264,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD2, st, 1);
     CK(launch_bdrln_fwd(dtype, B, J, I, Y2, prm->b2, X1, prm->g2, prm->be2, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st,
-                        (ctx->bdrln_variant >> 4) & 15));
+                        (ctx->bdrln_variant >> 4) & 15,
+                        ctx->mask_bytes ? (uint8_t*)at(saved, SL.off[S_KB2]) : nullptr));
   }
   {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -1362,7 +1382,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     w.defer = &ffn_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dY, xh2, r2, prm->g2,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, dX1, dY2, g->dg2,
-                        g->dbe2, g->db2, w, st, (ctx->bdrln_variant >> 8) & 15));
+                        g->dbe2, g->db2, w, st, (ctx->bdrln_variant >> 8) & 15,
+                        ctx->mask_bytes ? (const uint8_t*)at(sv, SL.off[S_KB2]) : nullptr));
   }
   // Linear2 dX (:573) + BAD-bwd (:576-578) in one tcgen05 kernel on the bf16 path (dA1 never
   // reaches HBM; db1 from its epilogue's column partials), else the contraction into dA1 and
@@ -1373,6 +1394,7 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     ReduceWs w = after(ffn_jobs[0]);
     w.defer = &ffn_jobs[1];
     WgemmArgs l2 = ffn_bwd_args(ctx, d, dtype, cfg, dY2, prm->W2, h, pk_ffn, dh, w.partials);
+    if (bad_bytes_of(ctx, d, dtype)) l2.kb_in = (const uint8_t*)at(sv, SL.off[S_KBF]);
     const int R = wgemm_partial_rows(l2);
     if (wgemm_supported(l2) && (size_t)R * U <= w.cap_floats) {
       {
@@ -1439,7 +1461,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     w.defer = &att_jobs[0];
     CK(launch_bdrln_bwd(dtype, B, J, I, dX1, xh1, r1, prm->g1,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, dX, dYo, g->dg1,
-                        g->dbe1, g->dbo, w, st, (ctx->bdrln_variant >> 12) & 15));
+                        g->dbe1, g->dbo, w, st, (ctx->bdrln_variant >> 12) & 15,
+                        ctx->mask_bytes ? (const uint8_t*)at(sv, SL.off[S_KB1]) : nullptr));
   }
   const ReduceWs wa = after(att_jobs[0]);   // the rest of the half reduces past those partials
   // Out dX (:586), dW (:587)

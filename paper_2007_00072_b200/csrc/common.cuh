@@ -160,6 +160,46 @@ __device__ __forceinline__ void keep_mul8(uint64_t g, const PhiloxKey& pk, float
   }
 }
 
+// Keep bytes (R27): the 8 keep flags of chunk g as one byte, bit u = element u of
+// the chunk, stored by a forward site so its backward reads 1 byte per 8 elements instead
+// of re-running Philox.  keep_byte_mul8 also returns the multipliers of keep_mul8.
+__device__ __forceinline__ uint32_t keep_byte_mul8(uint64_t g, const PhiloxKey& pk, float m[8]) {
+  if (pk.T == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) m[j] = pk.scale;
+    return 0xFFu;
+  }
+  const uint4 w = philox4x32_10(g, pk);
+  const uint32_t T16 = pk.T << 16;
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  uint32_t b = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool lo = (wv[i] << 16) >= T16, hi = wv[i] >= T16;
+    m[2 * i] = lo ? pk.scale : 0.f;
+    m[2 * i + 1] = hi ? pk.scale : 0.f;
+    b |= (lo ? 1u : 0u) << (2 * i);
+    b |= (hi ? 1u : 0u) << (2 * i + 1);
+  }
+  return b;
+}
+__device__ __forceinline__ void mul8_from_byte(uint32_t b, float scale, float m[8]) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) m[j] = ((b >> j) & 1u) ? scale : 0.f;
+}
+// multipliers of chunk ci (index within the site, Philox chunk g0 + ci): read from the
+// site's stored keep bytes (kb_in), else from Philox -- and then stored to kb_out if given
+__device__ __forceinline__ void keep_mul8_io(int64_t g0, int64_t ci, const PhiloxKey& pk,
+                                             uint8_t* kb_out, const uint8_t* kb_in, float m[8]) {
+  if (kb_in != nullptr) {
+    mul8_from_byte(__ldg(kb_in + ci), pk.scale, m);
+  } else if (kb_out != nullptr) {
+    kb_out[ci] = (uint8_t)keep_byte_mul8((uint64_t)(g0 + ci), pk, m);
+  } else {
+    keep_mul8((uint64_t)(g0 + ci), pk, m);
+  }
+}
+
 // v[j] = keep_j ? v[j] * scale : 0
 __device__ __forceinline__ void dropout8(float v[8], uint64_t g, const PhiloxKey& pk) {
   if (pk.T == 0) return;

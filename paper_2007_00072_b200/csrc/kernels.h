@@ -107,26 +107,32 @@ cudaError_t launch_bsb_bwd(int dtype, int B, int H, int J, int K, float scale, c
 cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, const float* bias,
                              const void* R, const float* gamma, const float* beta, float eps,
                              const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                             float* rstd, cudaStream_t st, int variant = 0);
+                             float* rstd, cudaStream_t st, int variant = 0,
+                             uint8_t* kb_out = nullptr, const uint8_t* kb_in = nullptr);
 // variant: 0 = the default kernel for I, 1 = warp-per-row, 2 / 3 / 4 = row-group kernels with
-// that many warps per row (when it divides the row; else the default)
+// that many warps per row (when it divides the row; else the default).
+// kb_out / kb_in (optional, [B*J][I/8] bytes, R27): the forward stores the keep
+// byte of every 8-element chunk it used; a backward (or forward) given them reads them
+// instead of evaluating Philox -- same mask, same results.
 cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, const void* xhat,
                              const float* rstd, const float* gamma, const PhiloxKey& pk,
                              int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
                              float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st,
-                             int variant = 0);
+                             int variant = 0, const uint8_t* kb_in = nullptr);
 
 // Row-group BDRLN variants (ops_ln_rg.cu): 4 warps per row, persistent, TMA row ring.
 bool bdrln_rg_supported(int I);
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
                                 const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                                float* rstd, cudaStream_t st, int gw = 0);
+                                float* rstd, cudaStream_t st, int gw = 0,
+                                uint8_t* kb_out = nullptr, const uint8_t* kb_in = nullptr);
 cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut,
                                 const void* xhat, const float* rstd, const float* gamma,
                                 const PhiloxKey& pk, int64_t batch_offset, void* dz,
                                 void* dYpre, float* dgamma, float* dbeta, float* dbias,
-                                const ReduceWs& ws, cudaStream_t st, int gw = 0);
+                                const ReduceWs& ws, cudaStream_t st, int gw = 0,
+                                const uint8_t* kb_in = nullptr);
 
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* h,
@@ -173,6 +179,10 @@ struct WgemmArgs {
   int act = 0;
   PhiloxKey pk{};
   int64_t g0 = 0;                // Philox chunk index of element (0, 0)
+  // keep bytes ([M][N/8], R27): EPI_BAD_FWD stores them (kb_out), EPI_BAD_BWD reads
+  // them instead of evaluating Philox (kb_in)
+  uint8_t* kb_out = nullptr;
+  const uint8_t* kb_in = nullptr;
   void* ws = nullptr; size_t ws_bytes = 0;   // split-K slabs (fp32 EPI_STORE outputs)
   int cg = 0;                    // 0 = CTA pairs (cta_group::2) where M > 128, 1 = single CTAs
 };

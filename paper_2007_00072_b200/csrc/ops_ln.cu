@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
     const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
-    PhiloxKey pk) {
+    PhiloxKey pk, uint8_t* __restrict__ kb_out, const uint8_t* __restrict__ kb_in) {
   using C = Chunk<T>;
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
       C::unpack(rr[i], z[i]);
       load_f32x8(bias + ch * 8, b);
       float m[8];
-      keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+      keep_mul8_io(g0, (int64_t)row * nc + ch, pk, kb_out, kb_in, m);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         z[i][j] = fmaf(y[j] + b[j], m[j], z[i][j]);
@@ -94,12 +94,13 @@ __global__ void __launch_bounds__(256) bdrln_fwd_kernel(
 cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, const float* bias,
                              const void* R, const float* gamma, const float* beta, float eps,
                              const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                             float* rstd, cudaStream_t st, int variant) {
+                             float* rstd, cudaStream_t st, int variant, uint8_t* kb_out,
+                             const uint8_t* kb_in) {
   const int rows = B * J;
   if (rows == 0) return cudaSuccess;
   if (variant != 1 && bdrln_rg_supported(I))
     return launch_bdrln_fwd_rg(dtype, B, J, I, Y, bias, R, gamma, beta, eps, pk, batch_offset,
-                               out, xhat, rstd, st, variant);
+                               out, xhat, rstd, st, variant, kb_out, kb_in);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   const int grid = (rows + 7) / 8;
@@ -107,11 +108,11 @@ cudaError_t launch_bdrln_fwd(int dtype, int B, int J, int I, const void* Y, cons
     if (dtype == 0)
       bdrln_fwd_kernel<__nv_bfloat16, CPL><<<grid, 256, 0, st>>>(
           (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
-          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk);
+          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out, kb_in);
     else
       bdrln_fwd_kernel<float, CPL><<<grid, 256, 0, st>>>(
           (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat, rstd,
-          rows, I, eps, g0, pk);
+          rows, I, eps, g0, pk, kb_out, kb_in);
   });
   return cudaGetLastError();
 }
@@ -129,7 +130,8 @@ template <typename T, int CPL>
 __global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
-    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk, int kLnBwdStages) {
+    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk, int kLnBwdStages,
+    const uint8_t* __restrict__ kb_in) {
   using C = Chunk<T>;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
@@ -193,6 +195,12 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
       }
     }
     const float rs = __ldg(rstd + row);
+    uint32_t kb[CPL];   // stored keep bytes (R27), loaded early with rstd
+#pragma unroll
+    for (int i = 0; i < CPL; ++i)
+      kb[i] = (kb_in != nullptr && lane + 32 * i < nc)
+                  ? (uint32_t)__ldg(kb_in + (int64_t)row * nc + lane + 32 * i)
+                  : 0u;
     const int64_t base = (int64_t)row * I;
     float go[CPL][8], xh[CPL][8];
     float s1 = 0.f, s2 = 0.f;
@@ -221,7 +229,10 @@ __global__ void __launch_bounds__(kLnBwdWarps * 32, 1) bdrln_bwd_kernel(
       const int ch = lane + 32 * i;
       if (ch < nc) {
         float d[8], y[8], m[8];
-        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+        if (kb_in != nullptr)
+          mul8_from_byte(kb[i], pk.scale, m);
+        else
+          keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           d[j] = rs * (go[i][j] - mg - xh[i][j] * mgx);
@@ -285,7 +296,7 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
                              const float* rstd, const float* gamma, const PhiloxKey& pk,
                              int64_t batch_offset, void* dz, void* dYpre, float* dgamma,
                              float* dbeta, float* dbias, const ReduceWs& ws, cudaStream_t st,
-                             int variant) {
+                             int variant, const uint8_t* kb_in) {
   const int rows = B * J;
   if (rows == 0) {
     cudaMemsetAsync(dgamma, 0, sizeof(float) * I, st);
@@ -294,7 +305,7 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
   }
   if (variant != 1 && bdrln_rg_supported(I))
     return launch_bdrln_bwd_rg(dtype, B, J, I, dOut, xhat, rstd, gamma, pk, batch_offset, dz,
-                               dYpre, dgamma, dbeta, dbias, ws, st, variant);
+                               dYpre, dgamma, dbeta, dbias, ws, st, variant, kb_in);
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
   int G = (rows + kLnBwdWarps - 1) / kLnBwdWarps;
@@ -312,13 +323,14 @@ cudaError_t launch_bdrln_bwd(int dtype, int B, int J, int I, const void* dOut, c
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<G, kLnBwdWarps * 32, smem, st>>>(
             (const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat, rstd, gamma,
-            (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, stages);
+            (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, stages,
+            kb_in);
       } else {
         auto kern = bdrln_bwd_kernel<float, CPL>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<G, kLnBwdWarps * 32, smem, st>>>((const float*)dOut, (const float*)xhat, rstd,
                                                 gamma, (float*)dz, (float*)dYpre, ws.partials,
-                                                rows, I, g0, pk, stages);
+                                                rows, I, g0, pk, stages, kb_in);
       }
     }
   });

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd
     const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
-    PhiloxKey pk) {
+    PhiloxKey pk, uint8_t* __restrict__ kb_out, const uint8_t* __restrict__ kb_in) {
   using C = Chunk<T>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd
         float y[8], m[8];
         C::unpack(C::ld_smem(sy + ch * 8), y);
         C::unpack(C::ld_smem(sr + ch * 8), z[i]);
-        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+        keep_mul8_io(g0, (int64_t)row * nc + ch, pk, kb_out, kb_in, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           z[i][j] = fmaf(y[j] + pb[i][j], m[j], z[i][j]);
@@ -166,7 +166,8 @@ template <typename T, int CPW, int STG, int GW>
 __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd_rg_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
-    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk) {
+    float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk,
+    const uint8_t* __restrict__ kb_in) {
   using C = Chunk<T>;
   extern __shared__ __align__(128) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -201,6 +202,12 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd
   for (int row = first; row < rows; row += stride, ++k) {
     const int s = k % STG;
     const float rs = __ldg(rstd + row);   // issued early: used after the row reduction
+    uint32_t kb[CPW];                     // stored keep bytes (R27), issued early as well
+#pragma unroll
+    for (int i = 0; i < CPW; ++i)
+      kb[i] = (kb_in != nullptr && lane + 32 * i < ncq)
+                  ? (uint32_t)__ldg(kb_in + (int64_t)row * nc + w * ncq + lane + 32 * i)
+                  : 0u;
     mbar_wait(&bar[s], (uint32_t)(k / STG) & 1u);
     const T* sg = ring_row<T, 2, STG>(smem, I, g, s, 0);
     const T* sx = ring_row<T, 2, STG>(smem, I, g, s, 1);
@@ -253,7 +260,10 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd
       if (cq < ncq) {
         const int ch = w * ncq + cq;
         float d[8], y[8], m[8];
-        keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
+        if (kb_in != nullptr)
+          mul8_from_byte(kb[i], pk.scale, m);
+        else
+          keep_mul8((uint64_t)(g0 + (int64_t)row * nc + ch), pk, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           d[j] = rs * (go[i][j] - mg - xh[i][j] * mgx);
@@ -358,7 +368,8 @@ static bool rg_gw_valid(int nc, int gw) {
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
                                 const PhiloxKey& pk, int64_t batch_offset, void* out, void* xhat,
-                                float* rstd, cudaStream_t st, int gw_req) {
+                                float* rstd, cudaStream_t st, int gw_req, uint8_t* kb_out,
+                                const uint8_t* kb_in) {
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
@@ -371,12 +382,12 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
       auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
       kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
           (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
-          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk);
+          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out, kb_in);
     } else {
       auto kern = bdrln_fwd_rg_kernel<float, CPW, STG, GW>;
       kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
           (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat, rstd,
-          rows, I, eps, g0, pk);
+          rows, I, eps, g0, pk, kb_out, kb_in);
     }
   })));
   return cudaGetLastError();
@@ -386,7 +397,8 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
                                 const void* xhat, const float* rstd, const float* gamma,
                                 const PhiloxKey& pk, int64_t batch_offset, void* dz,
                                 void* dYpre, float* dgamma, float* dbeta, float* dbias,
-                                const ReduceWs& ws, cudaStream_t st, int gw_req) {
+                                const ReduceWs& ws, cudaStream_t st, int gw_req,
+                                const uint8_t* kb_in) {
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
@@ -403,13 +415,13 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
       if (G > cap) G = cap;
       kern<<<G, thr, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
                                  rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
-                                 ws.partials, rows, I, g0, pk);
+                                 ws.partials, rows, I, g0, pk, kb_in);
     } else {
       auto kern = bdrln_bwd_rg_kernel<float, CPW, STG, GW>;
       G = rg_grid(kern, rows, smem, thr);
       if (G > cap) G = cap;
       kern<<<G, thr, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
-                                 (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk);
+                                 (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk, kb_in);
     }
   })));
   cudaError_t e = cudaGetLastError();

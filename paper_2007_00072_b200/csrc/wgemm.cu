@@ -66,6 +66,8 @@ struct Params {
   PhiloxKey pk;           // BAD epilogues (site 2)
   int64_t g0;             // Philox chunk index of element (0, 0): batch_offset * J * N / 8
   float* partials;        // EPI_BAD_BWD: [ceil(M/128) * 4][N] column partial sums of dh
+  uint8_t* kb_out;        // EPI_BAD_FWD: keep bytes [M][N/8] written (or null)
+  const uint8_t* kb_in;   // EPI_BAD_BWD: keep bytes [M][N/8] read instead of Philox (or null)
 };
 
 // byte offset of 16-B chunk c (0..3) of row r in a [32 x 64 B] SWIZZLE_64B tile
@@ -422,6 +424,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // h = acc + b1 (stored, bf16); A1 = keep ? act(h) * s : 0 from the stored h
           PhiloxKey pkh = p.pk;
           pkh.scale *= 0.5f;   // act_f2 returns 2 act(h)
+          const int64_t ci0 = (int64_t)row * (p.N >> 3) + (col >> 3);   // first chunk
+          uint32_t kw = 0;                                              // its 4 keep bytes
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, hb[8], m[8], a[8];
@@ -430,10 +434,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 8; ++i) hb[i] = v[8 * j + i] + b[i];
             o0[j] = pack_bf16x8(hb);
             unpack_bf16x8(o0[j], hb);
-            keep_mul8((uint64_t)(p.g0 + (int64_t)row * (p.N >> 3) + ((col >> 3) + j)), pkh, m);
+            if (p.kb_out != nullptr)
+              kw |= keep_byte_mul8((uint64_t)(p.g0 + ci0 + j), pkh, m) << (8 * j);
+            else
+              keep_mul8((uint64_t)(p.g0 + ci0 + j), pkh, m);
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = act_f2<ACT>(hb[i]) * m[i];
             o1[j] = pack_bf16x8(a);
+          }
+          if (p.kb_out != nullptr && row < p.M && col < p.N) {
+            if ((p.N & 31) == 0) {   // whole, 4-B aligned words
+              *reinterpret_cast<uint32_t*>(p.kb_out + ci0) = kw;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (col + 8 * j < p.N) p.kb_out[ci0 + j] = (uint8_t)(kw >> (8 * j));
+            }
           }
         }
         if (EPI != EPI_BAD_BWD) {
@@ -454,11 +470,25 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         } else {   // EPI_BAD_BWD
           // dh = keep ? acc * s * act'(h) : 0, written over h in the staging buffer
+          const int64_t ci0 = (int64_t)row * (p.N >> 3) + (col >> 3);   // first chunk
+          uint32_t kw = 0;
+          if (p.kb_in != nullptr && row < p.M && col < p.N) {
+            if ((p.N & 31) == 0) {
+              kw = __ldg(reinterpret_cast<const uint32_t*>(p.kb_in + ci0));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                if (col + 8 * j < p.N) kw |= (uint32_t)__ldg(p.kb_in + ci0 + j) << (8 * j);
+            }
+          }
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float h8[8], m[8];
             unpack_bf16x8(*reinterpret_cast<const uint4*>(sb + sw64(lane, j)), h8);
-            keep_mul8((uint64_t)(p.g0 + (int64_t)row * (p.N >> 3) + ((col >> 3) + j)), p.pk, m);
+            if (p.kb_in != nullptr)
+              mul8_from_byte(kw >> (8 * j), p.pk.scale, m);
+            else
+              keep_mul8((uint64_t)(p.g0 + ci0 + j), p.pk, m);
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[8 * j + i] = v[8 * j + i] * m[i] * act_df<ACT>(h8[i]);
             *reinterpret_cast<uint4*>(sb + sw64(lane, j)) = pack_bf16x8(v + 8 * j);
@@ -664,6 +694,8 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
   p.pk = g.pk;
   p.g0 = g.g0;
   p.partials = g.partials;
+  p.kb_out = g.kb_out;
+  p.kb_in = g.kb_in;
 
   CUtensorMap ma, mb, mc, mc2, mx;
   bool ok = true;

@@ -421,3 +421,35 @@ def test_attn_overlap_option_bitwise(graph):
         out.append((dX.cpu(), layer.grad_flat.cpu()))
     assert torch.equal(out[0][0], out[1][0])
     assert torch.equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("dtype,dims,variant", [
+    ("bf16", Dims(B=2, J=512, H=4, P=64, U=1024), 0),        # row-group BDRLN kernels
+    ("bf16", Dims(B=2, J=512, H=4, P=64, U=1024), 0x1111),   # one warp per row at every site
+    ("bf16", Dims(B=3, J=128, H=2, P=64, U=264), 0),         # U % 32 != 0: ragged keep words
+    ("fp32", Dims(B=2, J=16, H=2, P=8, U=64), 0),            # fp32: BDRLN bytes, BAD separate
+])
+def test_mask_bytes_option_bitwise(dtype, dims, variant):
+    """ENC_OPT_MASK_BYTES (R27): the forward stores the BDRLN / BAD keep flags as
+    bytes and the backward reads them instead of re-running Philox -- Y, dX and every
+    gradient are bitwise those of the regenerating backward (the masks are the same)."""
+    from paper_2007_00072_b200 import ops
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    prm = make_params(dims, dtype, "parity", weight_std=0.05)
+    inp = make_inputs(dims, dtype, key_padding=True)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    X = torch.tensor(inp["X"], device="cuda").to(tdt)
+    dY = torch.tensor(inp["dY"], device="cuda").to(tdt)
+    M = torch.tensor(inp["mask_bias"], device="cuda")
+    out = []
+    for mb in (0, 1):
+        layer = EncoderLayer(dims, dtype, LayerCfg())
+        ops.enc_set_option(layer.ctx, ops.OPT_MASK_BYTES, mb)
+        ops.enc_set_option(layer.ctx, ops.OPT_BDRLN_VARIANT, variant)
+        layer.set_params(prm)
+        Y = layer.forward(X, M).clone()
+        dX = layer.backward(X, dY).clone()
+        torch.cuda.synchronize()
+        out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu()))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
