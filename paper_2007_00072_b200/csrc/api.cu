@@ -9,6 +9,7 @@
 
 #include <climits>
 
+#include <atomic>
 #include <mutex>
 #include <new>
 #include <unordered_map>
@@ -18,6 +19,20 @@
 #include "kernels.h"
 
 using namespace enc;
+
+// ENC_OPT_PDL (process-wide: the launch helpers have no context): programmatic dependent
+// launch of the kernels that call pdl_wait() (kernels.h launch_k)
+static std::atomic<int> g_pdl{-1};
+bool enc::pdl_enabled() {
+  int v = g_pdl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("ENC_PDL");
+    v = (e && atoi(e) == 0) ? 0 : 1;
+    g_pdl.store(v, std::memory_order_relaxed);
+  }
+  return v != 0;
+}
+void enc::pdl_set(bool on) { g_pdl.store(on ? 1 : 0, std::memory_order_relaxed); }
 
 struct enc_ctx {
   int device = 0;
@@ -944,7 +959,7 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_BDRLN_VARIANT) {
     for (int site = 0; site < 4; ++site)
-      if (((value >> (4 * site)) & 15) > 4) return ENC_EINVAL;
+      if (((value >> (4 * site)) & 15) > 5) return ENC_EINVAL;
     if (value < 0 || value >= (1 << 16)) return ENC_EINVAL;
     ctx->bdrln_variant = value;
     return ENC_OK;
@@ -959,6 +974,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
   }
   if (key == ENC_OPT_MASK_BYTES) {
     ctx->mask_bytes = value ? 1 : 0;
+    return ENC_OK;
+  }
+  if (key == ENC_OPT_PDL) {
+    pdl_set(value != 0);
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_PAIR) {

@@ -91,6 +91,17 @@ __device__ __forceinline__ void load_f32x8(const float* p, float v[8]) {
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with the programmatic-serialization attribute (launch_k, kernels.h) may
+// start while its stream predecessor is still running: everything before pdl_wait() (barrier
+// init, parameter loads, descriptor prefetch) overlaps the predecessor's tail; pdl_wait()
+// returns once the predecessor has completed and its writes are visible.  Without the
+// attribute both are no-ops.  pdl_trigger() lets the successor's CTAs launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- Philox4x32-10
 // Salmon et al. SC'11 (Random123); same ctr/key/word layout as cuRAND's
 // curand_init(seed, subseq, 4*g) + curand4() (R5).  The ten round keys and the

@@ -73,6 +73,27 @@ cudaError_t launch_colsum_finalize_jobs(const ColsumJob* jobs, int n, cudaStream
 
 PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq);
 
+// Programmatic dependent launch (ENC_OPT_PDL): launch_k launches `kern` with the
+// programmatic-serialization attribute when pdl_enabled() (kernels that call pdl_wait()
+// before reading what their stream predecessor wrote), else as a plain launch.
+bool pdl_enabled();
+void pdl_set(bool on);
+template <typename Kern, typename... Args>
+cudaError_t launch_k(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // dtype: 0 = bf16, 1 = fp32 (enc_dtype).  All return cudaSuccess or the launch error;
 // shape support is checked by the caller (api.cu) through *_supported().
 bool rowop_supported(int n_per_row);  // BSB (K), BDRLN (I): chunks-per-lane variants

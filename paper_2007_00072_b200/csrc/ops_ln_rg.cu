@@ -21,7 +21,8 @@
 namespace enc {
 namespace {
 
-constexpr int kGroups = 4;              // row groups per CTA
+constexpr int kGroups = 4;              // row groups per CTA (NG of the default variants)
+constexpr int kWideGroups = 8;          // NG of the wide variant: 8 groups x GW warps per CTA
 constexpr int kGWarps = 4;              // most warps per row group (header sizing)
 constexpr int kRgMaxStages = 4;
 
@@ -30,9 +31,9 @@ __device__ __forceinline__ void gbar(int group) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "r"(GW * 32) : "memory");
 }
 
-// shared layout: mbar[group][stage] (128 B) | red2[group][stage][4] float4 (1 KB) |
+// shared layout: mbar[group][stage] (256 B) | red[group][stage][GW] float4 |
 // ring[group][stage][ntens][I] T | (bwd, after the loop) colsum[group][3][I] float
-constexpr int kRgHdr = 128 + kGroups * kRgMaxStages * kGWarps * 16;
+constexpr int kRgHdr = 256 + kWideGroups * kRgMaxStages * kGWarps * 16;
 
 template <typename T, int NT, int STG>
 __device__ __forceinline__ T* ring_row(unsigned char* smem, int I, int g, int s, int t) {
@@ -40,8 +41,9 @@ __device__ __forceinline__ T* ring_row(unsigned char* smem, int I, int g, int s,
 }
 
 // ------------------------------------------------------------------ forward
-template <typename T, int CPW, int STG, int GW>
-__global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd_rg_kernel(
+template <typename T, int CPW, int STG, int GW, int NG = kGroups>
+__global__ void __launch_bounds__(NG * GW * 32, NG * GW * 32 > 512 ? 1 : (CPW == 1 ? 2 : 1))
+bdrln_fwd_rg_kernel(
     const T* __restrict__ Y, const float* __restrict__ bias, const T* __restrict__ R,
     const float* __restrict__ gamma, const float* __restrict__ beta, T* __restrict__ out,
     T* __restrict__ xhat, float* __restrict__ rstd_out, int rows, int I, float eps, int64_t g0,
@@ -53,13 +55,26 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd
   const int nc = I >> 3, ncq = nc / GW;          // chunks per row, per quarter
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
-  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * GW;
-  const int stride = gridDim.x * kGroups;
-  const int first = blockIdx.x * kGroups + g;
+  float4* red = reinterpret_cast<float4*>(smem + 256) + (size_t)g * STG * GW;
+  const int stride = gridDim.x * NG;
+  const int first = blockIdx.x * NG + g;
   const bool leader = (w == 0 && lane == 0);
+  // this lane's columns are the same for every row: parameters into registers once (before
+  // pdl_wait: they are not written by the stream predecessor)
+  float pb[CPW][8], pg[CPW][8], pe[CPW][8];
+#pragma unroll
+  for (int i = 0; i < CPW; ++i) {
+    const int ch = w * ncq + min(lane + 32 * i, ncq - 1);
+    load_f32x8(bias + ch * 8, pb[i]);
+    load_f32x8(gamma + ch * 8, pg[i]);
+    load_f32x8(beta + ch * 8, pe[i]);
+  }
   if (leader) {
     for (int s = 0; s < STG; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
+  }
+  pdl_wait();
+  if (leader) {
     for (int s = 0; s < STG; ++s) {
       const int r = first + s * stride;
       if (r < rows) {
@@ -68,15 +83,6 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd
         bulk_g2s(ring_row<T, 2, STG>(smem, I, g, s, 1), R + (int64_t)r * I, row_bytes, &bar[s]);
       }
     }
-  }
-  // this lane's columns are the same for every row: parameters into registers once
-  float pb[CPW][8], pg[CPW][8], pe[CPW][8];
-#pragma unroll
-  for (int i = 0; i < CPW; ++i) {
-    const int ch = w * ncq + min(lane + 32 * i, ncq - 1);
-    load_f32x8(bias + ch * 8, pb[i]);
-    load_f32x8(gamma + ch * 8, pg[i]);
-    load_f32x8(beta + ch * 8, pe[i]);
   }
   gbar<GW>(g);
   int k = 0;
@@ -162,8 +168,9 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_fwd
 }
 
 // ------------------------------------------------------------------ backward
-template <typename T, int CPW, int STG, int GW>
-__global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd_rg_kernel(
+template <typename T, int CPW, int STG, int GW, int NG = kGroups>
+__global__ void __launch_bounds__(NG * GW * 32, NG * GW * 32 > 512 ? 1 : (CPW == 1 ? 2 : 1))
+bdrln_bwd_rg_kernel(
     const T* __restrict__ dOut, const T* __restrict__ xhat, const float* __restrict__ rstd,
     const float* __restrict__ gamma, T* __restrict__ dz, T* __restrict__ dYpre,
     float* __restrict__ partials, int rows, int I, int64_t g0, PhiloxKey pk,
@@ -176,13 +183,16 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd
   const uint32_t row_bytes = (uint32_t)I * sizeof(T);
   const float inv_n = 1.f / (float)I;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem) + g * STG;
-  float4* red = reinterpret_cast<float4*>(smem + 128) + (size_t)g * STG * GW;
-  const int stride = gridDim.x * kGroups;
-  const int first = blockIdx.x * kGroups + g;
+  float4* red = reinterpret_cast<float4*>(smem + 256) + (size_t)g * STG * GW;
+  const int stride = gridDim.x * NG;
+  const int first = blockIdx.x * NG + g;
   const bool leader = (w == 0 && lane == 0);
   if (leader) {
     for (int s = 0; s < STG; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
+  }
+  pdl_wait();   // dOut is the stream predecessor's output
+  if (leader) {
     for (int s = 0; s < STG; ++s) {
       const int r = first + s * stride;
       if (r < rows) {
@@ -297,36 +307,38 @@ __global__ void __launch_bounds__(kGroups * GW * 32, CPW == 1 ? 2 : 1) bdrln_bwd
   }
   __syncthreads();
   float* outp = partials + (int64_t)blockIdx.x * 3 * I;
-  for (int c = threadIdx.x; c < 3 * I; c += (kGroups * GW * 32)) {
+  for (int c = threadIdx.x; c < 3 * I; c += (NG * GW * 32)) {
     float v = colsum[c];
 #pragma unroll
-    for (int q = 1; q < kGroups; ++q) v += colsum[(size_t)q * 3 * I + c];
+    for (int q = 1; q < NG; ++q) v += colsum[(size_t)q * 3 * I + c];
     outp[c] = v;
   }
 }
 
-// ring depth: 4 stages when the ring stays within ~96 KB (two CTAs per SM), else 2
-int rg_stages(int I, size_t es) {
-  return (size_t)kGroups * 4 * 2 * I * es <= 96 * 1024 ? 4 : 2;
+// ring depth: 4 stages when the ring stays within ~96 KB (two CTAs per SM; the wide
+// variant, one CTA per SM: 160 KB), else 2
+int rg_stages(int I, size_t es, int ng = kGroups) {
+  const size_t cap = ng == kWideGroups ? 160 * 1024 : 96 * 1024;
+  return (size_t)ng * 4 * 2 * I * es <= cap ? 4 : 2;
 }
 
-size_t rg_smem(int I, size_t es, bool bwd) {
-  const size_t ring = (size_t)kGroups * rg_stages(I, es) * 2 * I * es;
-  const size_t cols = bwd ? (size_t)kGroups * 3 * I * sizeof(float) : 0;
+size_t rg_smem(int I, size_t es, bool bwd, int ng = kGroups) {
+  const size_t ring = (size_t)ng * rg_stages(I, es, ng) * 2 * I * es;
+  const size_t cols = bwd ? (size_t)ng * 3 * I * sizeof(float) : 0;
   return kRgHdr + (ring > cols ? ring : cols);
 }
 
 // persistent grid: as many CTAs as can be resident (occupancy query), at most one group
 // per row
 template <typename Kern>
-int rg_grid(Kern kern, int rows, size_t smem, int threads) {
+int rg_grid(Kern kern, int rows, size_t smem, int threads, int ng = kGroups) {
   int dev = 0, sms = 148, per_sm = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
   if (per_sm < 1) per_sm = 1;
-  int G = (rows + kGroups - 1) / kGroups;
+  int G = (rows + ng - 1) / ng;
   if (G > per_sm * sms) G = per_sm * sms;
   return G < 1 ? 1 : G;
 }
@@ -364,6 +376,10 @@ static bool rg_gw_valid(int nc, int gw) {
     if ((stg) == 4) { constexpr int STG = 4; __VA_ARGS__; }    \
     else { constexpr int STG = 2; __VA_ARGS__; }               \
   } while (0)
+// wide variant (ENC_OPT_BDRLN_VARIANT 5): 8 row groups of nc/32 warps (one chunk per lane),
+// up to 1024 threads in one CTA per SM -- twice the resident warps of the default for the
+// same one partial row per CTA in the backward
+static bool rg_wide_valid(int nc) { return nc % 32 == 0 && nc / 32 >= 2 && nc / 32 <= 4; }
 
 cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, const float* bias,
                                 const void* R, const float* gamma, const float* beta, float eps,
@@ -373,6 +389,27 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
+  if (gw_req == 5 && rg_wide_valid(nc)) {
+    constexpr int NG = kWideGroups;
+    const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false, NG);
+    const int stg = rg_stages(I, dtype == 0 ? 2 : 4, NG);
+    ENC_GW_DISPATCH(nc / 32, ENC_STG_DISPATCH(stg, {
+      constexpr int thr = NG * GW * 32;
+      if (dtype == 0) {
+        auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, 1, STG, GW, NG>;
+        launch_k(kern, rg_grid(kern, rows, smem, thr, NG), thr, smem, st,
+                 (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
+                 (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out,
+                 kb_in);
+      } else {
+        auto kern = bdrln_fwd_rg_kernel<float, 1, STG, GW, NG>;
+        kern<<<rg_grid(kern, rows, smem, thr, NG), thr, smem, st>>>(
+            (const float*)Y, bias, (const float*)R, gamma, beta, (float*)out, (float*)xhat,
+            rstd, rows, I, eps, g0, pk, kb_out, kb_in);
+      }
+    }));
+    return cudaGetLastError();
+  }
   const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, false);
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
   const int gw = rg_gw_valid(nc, gw_req) ? gw_req : rg_gw(nc);
@@ -380,9 +417,10 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
     constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
       auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
-      kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
-          (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
-          (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out, kb_in);
+      launch_k(kern, rg_grid(kern, rows, smem, thr), thr, smem, st,
+               (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
+               (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out,
+               kb_in);
     } else {
       auto kern = bdrln_fwd_rg_kernel<float, CPW, STG, GW>;
       kern<<<rg_grid(kern, rows, smem, thr), thr, smem, st>>>(
@@ -402,9 +440,35 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
   const int rows = B * J;
   const int nc = I / 8;
   const int64_t g0 = batch_offset * (int64_t)J * nc;
-  const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, true);
   const int cap = (int)(ws.cap_floats / (size_t)(3 * I));
   int G = 1;
+  if (gw_req == 5 && rg_wide_valid(nc)) {
+    constexpr int NG = kWideGroups;
+    const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, true, NG);
+    const int stg = rg_stages(I, dtype == 0 ? 2 : 4, NG);
+    ENC_GW_DISPATCH(nc / 32, ENC_STG_DISPATCH(stg, {
+      constexpr int thr = NG * GW * 32;
+      if (dtype == 0) {
+        auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, 1, STG, GW, NG>;
+        G = rg_grid(kern, rows, smem, thr, NG);
+        if (G > cap) G = cap;
+        launch_k(kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
+                 (const __nv_bfloat16*)xhat, rstd, gamma, (__nv_bfloat16*)dz,
+                 (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, kb_in);
+      } else {
+        auto kern = bdrln_bwd_rg_kernel<float, 1, STG, GW, NG>;
+        G = rg_grid(kern, rows, smem, thr, NG);
+        if (G > cap) G = cap;
+        kern<<<G, thr, smem, st>>>((const float*)dOut, (const float*)xhat, rstd, gamma,
+                                   (float*)dz, (float*)dYpre, ws.partials, rows, I, g0, pk,
+                                   kb_in);
+      }
+    }));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return colsum_finish(ws, G, 3 * I, I, dgamma, dbeta, dbias, st);
+  }
+  const size_t smem = rg_smem(I, dtype == 0 ? 2 : 4, true);
   const int stg = rg_stages(I, dtype == 0 ? 2 : 4);
   const int gw = rg_gw_valid(nc, gw_req) ? gw_req : rg_gw(nc);
   ENC_GW_DISPATCH(gw, ENC_CPW_DISPATCH(nc / gw, ENC_STG_DISPATCH(stg, {
@@ -413,9 +477,9 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
       auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
       G = rg_grid(kern, rows, smem, thr);
       if (G > cap) G = cap;
-      kern<<<G, thr, smem, st>>>((const __nv_bfloat16*)dOut, (const __nv_bfloat16*)xhat,
-                                 rstd, gamma, (__nv_bfloat16*)dz, (__nv_bfloat16*)dYpre,
-                                 ws.partials, rows, I, g0, pk, kb_in);
+      launch_k(kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
+               (const __nv_bfloat16*)xhat, rstd, gamma, (__nv_bfloat16*)dz,
+               (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, kb_in);
     } else {
       auto kern = bdrln_bwd_rg_kernel<float, CPW, STG, GW>;
       G = rg_grid(kern, rows, smem, thr);

@@ -288,6 +288,7 @@ def test_layer_small_bf16_stagewise(dims, act, kp):
     {12: 0, 8: 1},                         # separate, all on the tcgen05 kernel
     {14: 0x1111},                          # BDRLN / BDRLN-bwd one warp per row
     {14: 0x4242},                          # BDRLN row groups of 2 / 4 warps per site
+    {14: 0x5555},                          # wide row-group BDRLN kernels (8 groups per CTA)
 ])
 def test_layer_bf16_stagewise_paths(opts):
     """Every attention-path option combination at a fused-capable shape (J = 512)."""
@@ -426,6 +427,7 @@ def test_attn_overlap_option_bitwise(graph):
 @pytest.mark.parametrize("dtype,dims,variant", [
     ("bf16", Dims(B=2, J=512, H=4, P=64, U=1024), 0),        # row-group BDRLN kernels
     ("bf16", Dims(B=2, J=512, H=4, P=64, U=1024), 0x1111),   # one warp per row at every site
+    ("bf16", Dims(B=2, J=512, H=4, P=64, U=1024), 0x5555),   # wide row-group kernels
     ("bf16", Dims(B=3, J=128, H=2, P=64, U=264), 0),         # U % 32 != 0: ragged keep words
     ("fp32", Dims(B=2, J=16, H=2, P=8, U=64), 0),            # fp32: BDRLN bytes, BAD separate
 ])
