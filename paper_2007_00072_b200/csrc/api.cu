@@ -22,17 +22,18 @@ using namespace enc;
 
 // ENC_OPT_PDL (process-wide: the launch helpers have no context): programmatic dependent
 // launch of the kernels that call pdl_wait() (kernels.h launch_k)
+static constexpr int kPdlDefault = PDL_LN | PDL_ATTN_BH | PDL_WGEMM;   // measured at L (DESIGN 8.6)
 static std::atomic<int> g_pdl{-1};
-bool enc::pdl_enabled() {
+bool enc::pdl_enabled(int cls) {
   int v = g_pdl.load(std::memory_order_relaxed);
   if (v < 0) {
     const char* e = getenv("ENC_PDL");
-    v = (e && atoi(e) == 0) ? 0 : 1;
+    v = e ? (int)strtol(e, nullptr, 0) : kPdlDefault;
     g_pdl.store(v, std::memory_order_relaxed);
   }
-  return v != 0;
+  return (v & cls) != 0;
 }
-void enc::pdl_set(bool on) { g_pdl.store(on ? 1 : 0, std::memory_order_relaxed); }
+void enc::pdl_set(int mask) { g_pdl.store(mask, std::memory_order_relaxed); }
 
 struct enc_ctx {
   int device = 0;
@@ -977,7 +978,8 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   if (key == ENC_OPT_PDL) {
-    pdl_set(value != 0);
+    if (value < 0 || value > 31) return ENC_EINVAL;
+    pdl_set(value);
     return ENC_OK;
   }
   if (key == ENC_OPT_GEMM_PAIR) {

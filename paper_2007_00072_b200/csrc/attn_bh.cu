@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // operands are the stream predecessor's outputs
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -392,7 +393,7 @@ cudaError_t launch_bh(const CUtensorMap* m, const BhParams& p, cudaStream_t st) 
   cudaFuncSetAttribute(attn_bh_kernel<STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)smem);
   const int grid = p.units < sm_count() ? p.units : sm_count();
-  attn_bh_kernel<STAGES><<<grid, kThreads, smem, st>>>(m[0], m[1], m[2], m[3], m[4], p);
+  launch_k(PDL_ATTN_BH, attn_bh_kernel<STAGES>, grid, kThreads, smem, st, m[0], m[1], m[2], m[3], m[4], p);
   return cudaGetLastError();
 }
 

@@ -245,6 +245,7 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + cb;
+  pdl_wait();   // operands are the stream predecessor's outputs
 
   if (leader && blockIdx.x < prm.tiles) load_operands(blockIdx.x);
   if (kBwd && lane == 0 && blockIdx.x < prm.tiles) load_psub(blockIdx.x);
@@ -599,29 +600,28 @@ cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const 
                               const PhiloxKey& pk, cudaStream_t st, bool high_prio = false,
                               const CUtensorMap* e = nullptr) {
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-  if (!high_prio) {
-    if constexpr (std::is_invocable_v<Kern, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
-                                      FusedParams, PhiloxKey, CUtensorMap>)
-      kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk, *e);
-    else
-      kern<<<persistent_grid(tiles), kThreads, kSmem, st>>>(a, b, c, d, prm, pk);
-    return cudaGetLastError();
-  }
-  // the persistent kernel assumes all of its CTAs are resident at once: when a kernel on
-  // another stream is ready at the same moment (the layer's dV beside the fused backward),
-  // the block scheduler must place this one's CTAs first
-  int least = 0, greatest = 0;
-  cudaDeviceGetStreamPriorityRange(&least, &greatest);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(persistent_grid(tiles));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributePriority;
-  at[0].val.priority = greatest;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (high_prio) {
+    // the persistent kernel assumes all of its CTAs are resident at once: when a kernel on
+    // another stream is ready at the same moment (the layer's dV beside the fused backward),
+    // the block scheduler must place this one's CTAs first
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    at[na].id = cudaLaunchAttributePriority;
+    at[na++].val.priority = greatest;
+  }
+  if (pdl_enabled(PDL_ATTN_FUSED)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   if constexpr (std::is_invocable_v<Kern, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap,
                                     FusedParams, PhiloxKey, CUtensorMap>)
     return cudaLaunchKernelEx(&cfg, kern, a, b, c, d, prm, pk, *e);

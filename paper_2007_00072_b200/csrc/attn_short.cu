@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(kFThreads, 1) attn_qk_bsb_short_kernel(
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // operands are the stream predecessor's outputs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -339,6 +340,7 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // operands are the stream predecessor's outputs
 
   if (warp == 0) {
     if (lane == 0) {
@@ -504,15 +506,20 @@ cudaError_t launch_short(Kern kern, int tiles, size_t smem, int threads, cudaStr
   cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   if (high_prio) {   // placed ahead of a kernel made ready on another stream (layer dV)
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    at[0].id = cudaLaunchAttributePriority;
-    at[0].val.priority = greatest;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributePriority;
+    at[na++].val.priority = greatest;
   }
+  if (pdl_enabled(PDL_ATTN_FUSED)) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

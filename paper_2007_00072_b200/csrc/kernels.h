@@ -74,12 +74,14 @@ cudaError_t launch_colsum_finalize_jobs(const ColsumJob* jobs, int n, cudaStream
 PhiloxKey make_philox_key(float p, uint64_t seed, uint64_t subseq);
 
 // Programmatic dependent launch (ENC_OPT_PDL): launch_k launches `kern` with the
-// programmatic-serialization attribute when pdl_enabled() (kernels that call pdl_wait()
-// before reading what their stream predecessor wrote), else as a plain launch.
-bool pdl_enabled();
-void pdl_set(bool on);
+// programmatic-serialization attribute when pdl_enabled(cls) (kernels that call pdl_wait()
+// before reading what their stream predecessor wrote), else as a plain launch.  cls: the
+// kernel class bit (PDL_* below) of the ENC_OPT_PDL mask.
+enum { PDL_LN = 1, PDL_ATTN_FUSED = 2, PDL_ATTN_BH = 4, PDL_WGEMM = 8, PDL_FINAL = 16 };
+bool pdl_enabled(int cls);
+void pdl_set(int mask);
 template <typename Kern, typename... Args>
-cudaError_t launch_k(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+cudaError_t launch_k(int cls, Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
@@ -90,7 +92,7 @@ cudaError_t launch_k(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl_enabled(cls) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
     const float* __restrict__ partials, int R, int ncols, int nper, float* out0, float* out1,
     float* out2) {
   __shared__ float sm[kFinY][33];
+  pdl_wait();   // the partials are the stream predecessor's outputs
   const int c = blockIdx.x * 32 + threadIdx.x;
   float s = 0.f;
   if (c < ncols) {
@@ -381,9 +382,8 @@ __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_kernel(
 cudaError_t launch_colsum_finalize(const float* partials, int R, int ncols, int nper,
                                    float* out0, float* out1, float* out2, cudaStream_t st) {
   dim3 block(32, kFinY);
-  colsum_finalize_kernel<<<(ncols + 31) / 32, block, 0, st>>>(partials, R, ncols, nper, out0,
-                                                              out1, out2);
-  return cudaGetLastError();
+  return launch_k(PDL_FINAL, colsum_finalize_kernel, (ncols + 31) / 32, block, 0, st, partials, R, ncols,
+                  nper, out0, out1, out2);
 }
 
 cudaError_t colsum_finish(const ReduceWs& ws, int R, int ncols, int nper, float* out0,
@@ -409,6 +409,7 @@ struct ColsumJobs4 {
 
 __global__ void __launch_bounds__(32 * kFinY) colsum_finalize_jobs_kernel(ColsumJobs4 js) {
   __shared__ float sm[kFinY][33];
+  pdl_wait();
   int k = 0;
   while (k < 3 && (int)blockIdx.x >= js.first_block[k + 1]) ++k;
   const ColsumJob& jb = js.j[k];
@@ -453,7 +454,7 @@ cudaError_t launch_colsum_finalize_jobs(const ColsumJob* jobs, int n, cudaStream
   js.first_block[4] = nb;
   if (nb == 0) return cudaSuccess;
   dim3 block(32, kFinY);
-  colsum_finalize_jobs_kernel<<<nb, block, 0, st>>>(js);
+  launch_k(PDL_FINAL, colsum_finalize_jobs_kernel, nb, block, 0, st, js);
   return cudaGetLastError();
 }
 

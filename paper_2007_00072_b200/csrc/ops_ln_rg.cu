@@ -397,7 +397,7 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
       constexpr int thr = NG * GW * 32;
       if (dtype == 0) {
         auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, 1, STG, GW, NG>;
-        launch_k(kern, rg_grid(kern, rows, smem, thr, NG), thr, smem, st,
+        launch_k(PDL_LN, kern, rg_grid(kern, rows, smem, thr, NG), thr, smem, st,
                  (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
                  (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out,
                  kb_in);
@@ -417,7 +417,7 @@ cudaError_t launch_bdrln_fwd_rg(int dtype, int B, int J, int I, const void* Y, c
     constexpr int thr = kGroups * GW * 32;
     if (dtype == 0) {
       auto kern = bdrln_fwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
-      launch_k(kern, rg_grid(kern, rows, smem, thr), thr, smem, st,
+      launch_k(PDL_LN, kern, rg_grid(kern, rows, smem, thr), thr, smem, st,
                (const __nv_bfloat16*)Y, bias, (const __nv_bfloat16*)R, gamma, beta,
                (__nv_bfloat16*)out, (__nv_bfloat16*)xhat, rstd, rows, I, eps, g0, pk, kb_out,
                kb_in);
@@ -452,7 +452,7 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
         auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, 1, STG, GW, NG>;
         G = rg_grid(kern, rows, smem, thr, NG);
         if (G > cap) G = cap;
-        launch_k(kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
+        launch_k(PDL_LN, kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
                  (const __nv_bfloat16*)xhat, rstd, gamma, (__nv_bfloat16*)dz,
                  (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, kb_in);
       } else {
@@ -477,7 +477,7 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
       auto kern = bdrln_bwd_rg_kernel<__nv_bfloat16, CPW, STG, GW>;
       G = rg_grid(kern, rows, smem, thr);
       if (G > cap) G = cap;
-      launch_k(kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
+      launch_k(PDL_LN, kern, G, thr, smem, st, (const __nv_bfloat16*)dOut,
                (const __nv_bfloat16*)xhat, rstd, gamma, (__nv_bfloat16*)dz,
                (__nv_bfloat16*)dYpre, ws.partials, rows, I, g0, pk, kb_in);
     } else {

@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();   // the activations are the stream predecessor's outputs
 
   if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
@@ -592,22 +593,21 @@ cudaError_t launch_t(int grid, const CUtensorMap& a, const CUtensorMap& b, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (CG == 1) {
-    kern<<<grid, wg::kThreads, smem, st>>>(a, b, c, c2, x, p);
-    return cudaGetLastError();
-  }
+  if (CG == 1) return launch_k(PDL_WGEMM, kern, grid, wg::kThreads, smem, st, a, b, c, c2, x, p);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(wg::kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled(PDL_WGEMM) ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, kern, a, b, c, c2, x, p);
 }
 }  // namespace
