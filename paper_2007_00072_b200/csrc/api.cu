@@ -79,6 +79,8 @@ struct enc_ctx {
   int bdrln_variant = 0;   // ENC_OPT_BDRLN_VARIANT (kernel / warps per row of BDRLN, -bwd)
   int attn_dc = 1;         // ENC_OPT_ATTN_DC (fused BSB-bwd row term from C, R26)
   int mask_bytes = 1;      // ENC_OPT_MASK_BYTES (BDRLN / BAD keep bytes stored, R27)
+  int av_keep_gen = 0;     // ENC_OPT_AV_KEEP_GEN (attention keep words generated in A.V, R28;
+                           // measured +4 us at L: off)
   cudaEvent_t ev_kb_fork = nullptr, ev_kb_join = nullptr;
   // hand-written tcgen05 weight contractions (wgemm.cu) for bf16: ENC_OPT_GEMM_TC
   // weight contractions on the tcgen05 kernel: bit (1 << ENC_OP_GEMM_*) per contraction.
@@ -977,6 +979,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->mask_bytes = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_AV_KEEP_GEN) {
+    ctx->av_keep_gen = value ? 1 : 0;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_PDL) {
     if (value < 0 || value > 31) return ENC_EINVAL;
     pdl_set(value);
@@ -1199,13 +1205,18 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // fused + per-(b, h) path: A = dropout(P) is never stored -- the A V (and backward
   // A^T dC) contraction applies the stored keep bits to P while it is in shared memory
   const bool drop_on_load = fused_attn && use_bh(ctx, J, P);
+  // R28: on that path the A.V kernel's dropout-on-load warps generate the keep words from
+  // the Philox stream (FMA work beside a memory-bound stream) and store them for the
+  // backward; the score kernel runs no Philox (ENC_OPT_AV_KEEP_GEN, not with keep-ahead)
+  const bool av_gen = drop_on_load && ctx->av_keep_gen && !keep_ahead;
   if (fused_attn) {
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     if (keep_ahead) CK(cudaStreamWaitEvent(st, ctx->ev_kb_join, 0));
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
+    // (A.V generates the keep words on load, R28: the score kernel then writes P only)
     CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias, pk_attn, boff, Pm,
-                          drop_on_load ? nullptr : A, kbits, st, cfg->causal ? 1 : 0,
-                          keep_ahead ? 1 : 0));
+                          drop_on_load ? nullptr : A, av_gen ? nullptr : kbits, st,
+                          cfg->causal ? 1 : 0, keep_ahead ? 1 : 0));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {
@@ -1231,7 +1242,8 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
       // (+ the fp32 result's low bf16 word for the backward's row term, R26)
       CK(launch_attn_av_bh(B, H, J, P, Pm, V, ldqkv, C, I, kbits, pk_attn.scale, st,
                            dc_term_of(ctx, fused_attn, J, P) ? at(saved, SL.off[S_CLO])
-                                                             : nullptr));
+                                                             : nullptr,
+                           av_gen ? &pk_attn : nullptr, boff));
     } else if (tc_attn) {
       CK(attn_contract(ctx, ENC_AG_AV, B, H, J, P, A, 0, V, ldqkv, C, I, st));
     } else {

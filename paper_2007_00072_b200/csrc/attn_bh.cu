@@ -47,6 +47,12 @@ struct BhParams {
   // MMA, and the epilogue multiplies the fp32 accumulators by out_scale (= s)
   const uint32_t* keep;   // [B*H*J, K/32] ENC_KEEP_BITS words, or null (X used as is)
   float out_scale;
+  // keep_gen (A.V only, R28): the words are not read but generated from the Philox stream
+  // of the attention dropout site (key pk, chunk g0 of element (0,0,0,0)) by the
+  // dropout-on-load warps, applied, and written to `keep` for the backward
+  int keep_gen;
+  PhiloxKey pk;
+  int64_t g0;
   // optional (row output only): the rounding residual lo = bf16(acc - float(bf16(acc))) of
   // every stored element, same layout as the row output (the attention output's low word
   // for the backward's row term, R26)
@@ -203,17 +209,42 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
         return reinterpret_cast<const uint2*>(
             p.keep + ((int64_t)u * (nt * 128) + jt * 128 + row) * (nt * 4) + kt * 4 + bx * 2);
       };
+      const bool hiT = p.pk.T >= 0x8000u;
+      const uint32_t C2 = (hiT ? 0x10000u - p.pk.T : 0x8000u - p.pk.T) * 0x10001u;
+      const uint32_t Xm = hiT ? 0u : 0xFFFFFFFFu;
       int g = 0;
-      uint2 kw_next = blockIdx.x < p.units ? __ldg(kw_ptr(blockIdx.x, 0)) : make_uint2(0, 0);
+      uint2 kw_next = blockIdx.x < p.units && !p.keep_gen ? __ldg(kw_ptr(blockIdx.x, 0))
+                                                          : make_uint2(0, 0);
       for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
         for (int blk = 0; blk < nblk; ++blk, ++g) {
           const int s = g % STAGES;
-          const uint32_t kw[2] = {kw_next.x, kw_next.y};
-          // words of the next block, one block ahead (their latency hides behind this one)
-          if (blk + 1 < nblk)
+          uint32_t kw[2] = {kw_next.x, kw_next.y};
+          if (p.keep_gen) {
+            // this row's 64 columns of block blk: 8 Philox chunks, computed before the wait
+            // for the block's data (they do not depend on it); written for the backward
+            const int o = blk / nt, i = blk - (blk / nt) * nt;
+            const int jt = col_outer ? i : o, kt = col_outer ? o : i;
+            const int64_t grow = p.g0 + ((int64_t)u * (nt * 128) + jt * 128 + row) * (nt * 16) +
+                                 kt * 16 + bx * 8;
+            if (p.pk.T == 0) {
+              kw[0] = kw[1] = 0xFFFFFFFFu;
+            } else {
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                uint32_t f = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                  f |= keep_flags((uint64_t)(grow + 4 * c + j), p.pk, C2, Xm, 4 * j);
+                kw[c] = f;
+              }
+            }
+            __stcs(const_cast<uint2*>(kw_ptr(u, blk)), make_uint2(kw[0], kw[1]));
+          } else if (blk + 1 < nblk) {
+            // words of the next block, one block ahead (their latency hides behind this one)
             kw_next = __ldg(kw_ptr(u, blk + 1));
-          else if (u + (int)gridDim.x < p.units)
+          } else if (u + (int)gridDim.x < p.units) {
             kw_next = __ldg(kw_ptr(u + gridDim.x, 0));
+          }
           mbar_wait(&full[s], (g / STAGES) & 1);
           unsigned char* sx = base + s * stage_bytes + bx * 16384;
           // only 8-element chunks with a dropped element are rewritten (at p = 0.1, 43 % of
@@ -408,7 +439,8 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
                              int64_t ldyr, const void* Yc, int64_t ldyc, void* Or, int64_t ldor,
                              void* Oc, int64_t ldoc, float* ps_r, float* ps_c, int ps_ld,
                              const uint32_t* keep, float out_scale, cudaStream_t st,
-                             void* lo_r = nullptr) {
+                             void* lo_r = nullptr, const PhiloxKey* gen_pk = nullptr,
+                             int64_t gen_g0 = 0) {
   if (!attn_bh_supported(J, P)) return cudaErrorInvalidValue;
   if (lo_r && (((uintptr_t)lo_r & 15u) || ldor % 8)) return cudaErrorInvalidValue;
   BhParams p{};
@@ -425,6 +457,11 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
   p.ps_ld = ps_ld;
   p.keep = keep;
   p.out_scale = out_scale;
+  if (gen_pk != nullptr) {
+    p.keep_gen = 1;
+    p.pk = *gen_pk;
+    p.g0 = gen_g0;
+  }
   CUtensorMap m[5];
   int rd;
   bool ok = map_op(&m[0], X, false, B, H, J, J, 128, &rd);
@@ -448,9 +485,11 @@ static cudaError_t bh_launch(int B, int H, int J, int P, const void* X, const vo
 
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
                               int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
-                              float scale, cudaStream_t st, void* C_lo) {
+                              float scale, cudaStream_t st, void* C_lo, const PhiloxKey* gen_pk,
+                              int64_t batch_offset) {
   return bh_launch(B, H, J, P, A, V, ldv, nullptr, 0, C, ldc, nullptr, 0, nullptr, nullptr, 0,
-                   keep, keep ? scale : 1.f, st, C_lo);
+                   keep, keep ? scale : 1.f, st, C_lo, gen_pk,
+                   batch_offset * (int64_t)H * J * (J / 8));
 }
 
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,

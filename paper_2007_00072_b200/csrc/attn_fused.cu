@@ -108,28 +108,6 @@ __device__ __forceinline__ uint32_t sw64(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
 
-// Keep bits of the 8 elements of Philox chunk g (R5: element 2i <-> low 16-bit
-// lane of word i, 2i+1 <-> high lane; keep iff lane >= T), as a SWAR compare: with
-// C = per-lane (0x8000 - T) for T < 0x8000, x >= T  <=>  x >= 0x8000 or (x & 0x7FFF) + C has
-// bit 15 set (no carry leaves a lane), so bit 15 / 31 of ((w & 0x7FFF7FFF) + C) | w is
-// the keep bit of the low / high lane.  T >= 0x8000 (p >= 1/2): C = 0x10000 - T and AND.
-// The four words' flags are packed as: element u of the chunk -> bit (u odd ? 31 : 15)
-// - u/2, then shifted right by `sh`.
-// X = all ones for T < 0x8000 (OR), 0 for T >= 0x8000 (AND): (t & w) | ((t | w) & X) is
-// one LOP3; the flag bits are then masked as they are merged.
-__device__ __forceinline__ uint32_t keep_flags(uint64_t g, const PhiloxKey& pk, uint32_t C2,
-                                               uint32_t X, int sh) {
-  const uint4 w = philox4x32_10(g, pk);
-  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-  uint32_t f = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t t = (wv[i] & 0x7FFF7FFFu) + C2;
-    const uint32_t gi = (t & wv[i]) | ((t | wv[i]) & X);
-    f |= (gi >> (i + sh)) & (0x80008000u >> (i + sh));
-  }
-  return f;
-}
 // bit of element u (0..7) of chunk j (0..3) in a 32-element flag word
 __device__ __forceinline__ constexpr int flag_bit(int j, int u) {
   return ((u & 1) ? 31 : 15) - (u >> 1) - 4 * j;
@@ -280,7 +258,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       const uint2 w2 = __ldcs(reinterpret_cast<const uint2*>(kbw));
       kf[0] = w2.x;
       kf[1] = w2.y;
-    } else if (pk.T == 0) {   // p = 0: everything kept, no Philox stream
+    } else if (pk.T == 0 || (!kBwd && !kBits && !prm.write_a)) {
+      // p = 0: everything kept, no Philox stream.  Forward with neither A nor keep words
+      // stored (the layer's path: A.V generates the mask on load, R28): the flags are unused
       kf[0] = kf[1] = 0xFFFFFFFFu;
       if (!kBwd && kBits) __stcs(reinterpret_cast<uint2*>(kbw), make_uint2(kf[0], kf[1]));
     } else {

@@ -55,21 +55,7 @@ __device__ __forceinline__ uint4 pack8(const float* v) {
 __device__ __forceinline__ uint32_t sw64(int r, int c) {
   return (uint32_t)(r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
 }
-// keep flags of Philox chunk g packed ENC_KEEP_BITS-style (element u -> bit (u odd ? 31 :
-// 15) - u/2, shifted right by sh); SWAR compare as in attn_fused.cu
-__device__ __forceinline__ uint32_t keep_flags(uint64_t g, const PhiloxKey& pk, uint32_t C2,
-                                               uint32_t X, int sh) {
-  const uint4 w = philox4x32_10(g, pk);
-  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-  uint32_t f = 0;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t t = (wv[i] & 0x7FFF7FFFu) + C2;
-    const uint32_t gi = (t & wv[i]) | ((t | wv[i]) & X);
-    f |= (gi >> (i + sh)) & (0x80008000u >> (i + sh));
-  }
-  return f;
-}
+// keep_flags: common.cuh
 __device__ __forceinline__ constexpr int flag_bit(int j, int u) {
   return ((u & 1) ? 31 : 15) - (u >> 1) - 4 * j;
 }
@@ -188,6 +174,10 @@ __global__ void __launch_bounds__(kFThreads, 1) attn_qk_bsb_short_kernel(
       if (prm.keep_pre) {
         const uint4 kw = __ldcs(reinterpret_cast<const uint4*>(prm.keep_bits + rowi * 4));
         kf[0] = kw.x, kf[1] = kw.y, kf[2] = kw.z, kf[3] = kw.w;
+      } else if (!prm.keep_bits && !prm.write_a) {
+        // neither A nor keep words stored (the layer's path: A.V generates the mask on load,
+        // DESIGN.md R28): the flags are unused
+        kf[0] = kf[1] = kf[2] = kf[3] = 0xFFFFFFFFu;
       } else {
         row_flags(kf, prm.g0 + rowi * (kS / 8), pk, C2, X);
         if (prm.keep_bits)

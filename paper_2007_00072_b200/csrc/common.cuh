@@ -171,6 +171,28 @@ __device__ __forceinline__ void keep_mul8(uint64_t g, const PhiloxKey& pk, float
   }
 }
 
+// Keep bits of the 8 elements of Philox chunk g (R5: element 2i <-> low 16-bit
+// lane of word i, 2i+1 <-> high lane; keep iff lane >= T), as a SWAR compare: with
+// C = per-lane (0x8000 - T) for T < 0x8000, x >= T  <=>  x >= 0x8000 or (x & 0x7FFF) + C has
+// bit 15 set (no carry leaves a lane), so bit 15 / 31 of ((w & 0x7FFF7FFF) + C) | w is
+// the keep bit of the low / high lane.  T >= 0x8000 (p >= 1/2): C = 0x10000 - T and AND.
+// The four words' flags are packed as: element u of the chunk -> bit (u odd ? 31 : 15)
+// - u/2, then shifted right by `sh`.
+// X = all ones for T < 0x8000 (OR), 0 for T >= 0x8000 (AND): (t & w) | ((t | w) & X) is
+// one LOP3; the flag bits are then masked as they are merged.
+__device__ __forceinline__ uint32_t keep_flags(uint64_t g, const PhiloxKey& pk, uint32_t C2,
+                                               uint32_t X, int sh) {
+  const uint4 w = philox4x32_10(g, pk);
+  const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+  uint32_t f = 0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t t = (wv[i] & 0x7FFF7FFFu) + C2;
+    const uint32_t gi = (t & wv[i]) | ((t | wv[i]) & X);
+    f |= (gi >> (i + sh)) & (0x80008000u >> (i + sh));
+  }
+  return f;
+}
 // Keep bytes (R27): the 8 keep flags of chunk g as one byte, bit u = element u of
 // the chunk, stored by a forward site so its backward reads 1 byte per 8 elements instead
 // of re-running Philox.  keep_byte_mul8 also returns the multipliers of keep_mul8.

@@ -238,9 +238,13 @@ bool attn_bh_supported(int J, int P);
 // bias gradient, finished by launch_colsum_finalize over the B*4 partial rows).
 // keep (optional): dropout on load -- A is the stored P and the dropout is applied from the
 // ENC_KEEP_BITS words while the block is in shared memory; the result is scaled by `scale`.
+// gen_pk (R28): the keep words are generated from that Philox site (chunk index with
+// batch_offset, R5) by the dropout-on-load warps and written to `keep`, instead of
+// read from it
 cudaError_t launch_attn_av_bh(int B, int H, int J, int P, const void* A, const void* V,
                               int64_t ldv, void* C, int64_t ldc, const uint32_t* keep,
-                              float scale, cudaStream_t st, void* C_lo = nullptr);
+                              float scale, cudaStream_t st, void* C_lo = nullptr,
+                              const PhiloxKey* gen_pk = nullptr, int64_t batch_offset = 0);
 cudaError_t launch_attn_dv_bh(int B, int H, int J, int P, const void* A, const void* dC,
                               int64_t lddc, void* dV, int64_t lddv, float* ps_dv, int ps_ld,
                               const uint32_t* keep, float scale, cudaStream_t st);

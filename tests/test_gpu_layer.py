@@ -455,3 +455,34 @@ def test_mask_bytes_option_bitwise(dtype, dims, variant):
         out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu()))
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dims,causal", [
+    (Dims(B=2, J=512, H=4, P=64, U=1024), False),
+    (Dims(B=2, J=512, H=4, P=64, U=1024), True),
+    (Dims(B=3, J=128, H=4, P=64, U=512), False),   # short-row score kernels
+    (Dims(B=2, J=256, H=4, P=64, U=512), False),   # tiled score path (option inactive)
+])
+def test_av_keep_gen_option_bitwise(dims, causal):
+    """ENC_OPT_AV_KEEP_GEN (R28): the attention keep words generated by the A.V
+    kernel's dropout-on-load warps instead of the score kernel -- the stored words, Y, dX and
+    every gradient are bitwise those of the other placement."""
+    from paper_2007_00072_b200 import ops
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    prm = make_params(dims, "bf16", "parity", weight_std=0.05)
+    inp = make_inputs(dims, "bf16", key_padding=True)
+    X = torch.tensor(inp["X"], device="cuda").to(torch.bfloat16)
+    dY = torch.tensor(inp["dY"], device="cuda").to(torch.bfloat16)
+    M = torch.tensor(inp["mask_bias"], device="cuda")
+    out = []
+    for gen in (0, 1):
+        layer = EncoderLayer(dims, "bf16", LayerCfg(causal=causal))
+        ops.enc_set_option(layer.ctx, ops.OPT_AV_KEEP_GEN, gen)
+        layer.set_params(prm)
+        layer.saved.zero_()   # regions a path does not write compare equal
+        Y = layer.forward(X, M).clone()
+        dX = layer.backward(X, dY).clone()
+        torch.cuda.synchronize()
+        out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu(), layer.saved.cpu()))
+    for a, b in zip(out[0], out[1]):
+        assert torch.equal(a, b)
