@@ -55,11 +55,12 @@ def parse():
                          "full training step of BASELINE config 4)")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="e2e through encoder_layer_step_host (no cross-step input prefetch)")
-    ap.add_argument("--attn-overlap", action="store_true",
-                    help="dV contraction beside the fused dA + BSB-bwd kernel (ENC_OPT_ATTN_OVERLAP)")
-    ap.add_argument("--bwd-side", type=int, default=None, choices=[0, 1],
+    ap.add_argument("--attn-overlap", type=int, default=1, choices=[0, 1],
+                    help="dV contraction beside the fused dA + BSB-bwd kernel "
+                         "(ENC_OPT_ATTN_OVERLAP; default on: measured -6 us/step at L)")
+    ap.add_argument("--bwd-side", type=int, default=None, choices=[0, 1, 2],
                     help="weight-gradient contractions on a side stream (ENC_OPT_BWD_SIDE); "
-                         "default: on for config L (measured -6 us/step), off for Bb (+3 us)")
+                         "default off (with PDL measured +10 us at L, +4 us at Bb)")
     ap.add_argument("--no-qkv-direct", action="store_true",
                     help="separate AIB / AIB-bwd passes instead of the in-place QKV layout")
     ap.add_argument("--no-attn-bh", action="store_true",
@@ -209,7 +210,7 @@ def attention_desc(args, dims) -> str:
 def main():
     args = parse()
     if args.bwd_side is None:
-        args.bwd_side = 1 if args.config == "L" else 0
+        args.bwd_side = 0   # measured with PDL at L and Bb: the side stream costs 1-2 %
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

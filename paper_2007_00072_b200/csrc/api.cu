@@ -67,6 +67,9 @@ struct enc_ctx {
                              // the SMs it shares with dV)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // the backward's column-sum finalize beside the last weight contractions
+  cudaStream_t side2 = nullptr;
+  cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   void* side_ws = nullptr;
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
@@ -300,10 +303,12 @@ int enc_create(enc_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-  cudaEvent_t* evs[11] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking);
+  cudaEvent_t* evs[13] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
                           &c->ev_fork, &c->ev_join, &c->ev_pf,  &c->ev_pfs,
-                          &c->ev_bwd,  &c->ev_kb_fork, &c->ev_kb_join};
-  for (int i = 0; i < 11 && e == cudaSuccess; ++i)
+                          &c->ev_bwd,  &c->ev_kb_fork, &c->ev_kb_join, &c->ev_fork2,
+                          &c->ev_join2};
+  for (int i = 0; i < 13 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -344,9 +349,11 @@ void enc_destroy(enc_ctx* c) {
   }
   if (c->lt) lt_destroy(c->lt);
   for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join,
-                         c->ev_pf, c->ev_pfs, c->ev_bwd, c->ev_kb_fork, c->ev_kb_join})
+                         c->ev_pf, c->ev_pfs, c->ev_bwd, c->ev_kb_fork, c->ev_kb_join,
+                         c->ev_fork2, c->ev_join2})
     if (ev) cudaEventDestroy(ev);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->side_ws) cudaFree(c->side_ws);
   if (c->copy_in) cudaStreamDestroy(c->copy_in);
   if (c->copy_out) cudaStreamDestroy(c->copy_out);
@@ -934,7 +941,8 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   if (key == ENC_OPT_BWD_SIDE) {
-    ctx->bwd_side = value ? 1 : 0;
+    if (value < 0 || value > 2) return ENC_EINVAL;
+    ctx->bwd_side = value;   // 2: also the attention half's column-sum finalize on a 2nd stream
     return ENC_OK;
   }
   if (key == ENC_OPT_ATTN_OVERLAP) {
@@ -1603,6 +1611,34 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
     CK(launch_aib_bwd(dtype, B, J, H, P, dQ, dK, dV, dQKV, g->dbqkv, wa, st));
   }
+  // the attention half's column sums in one launch: BDRLN-bwd site 1 (dg1, dbe1, dbo), the
+  // QKV bias gradient from the per-(b,h) epilogues' B*4 partial rows (and, for the whole
+  // backward, the FFN half's).  Every input is final here: on the second side stream it
+  // overlaps the Q,K,V contractions instead of following them
+  auto finalize_att = [&](cudaStream_t fs) -> cudaError_t {
+    int nj = 1;
+    if (bgrad_epi) {
+      att_jobs[1].partials = bg;
+      att_jobs[1].R = B * 4;
+      att_jobs[1].ncols = att_jobs[1].nper = 3 * I;
+      att_jobs[1].out0 = g->dbqkv;
+      nj = 2;
+    }
+    if (ffn_deferred) {
+      att_jobs[nj++] = ffn_jobs[0];
+      att_jobs[nj++] = ffn_jobs[1];
+    }
+    return launch_colsum_finalize_jobs(att_jobs, nj, fs);
+  };
+  const bool early_fin = (bgrad_epi || !direct) && ctx->side2 && use_side && ctx->bwd_side == 2;
+  bool forked2 = false;
+  if (early_fin) {
+    CK(cudaEventRecord(ctx->ev_fork2, st));
+    CK(cudaStreamWaitEvent(ctx->side2, ctx->ev_fork2, 0));
+    forked2 = true;
+    OpTimer _t(ctx, bgrad_epi ? ENC_OP_AIB_BWD : ENC_OP_BDRLN_BWD1, ctx->side2, 1);
+    CK(finalize_att(ctx->side2));
+  }
   // Q,K,V dX (:593) accumulated onto dz1 (= BEI, :596), dW (:594)
   // (algebraic fusion, Table A.2: one dX / dW contraction per group of stacked blocks --
   // dX accumulates every group onto dz1, dW writes the group's rows of dWqkv)
@@ -1635,23 +1671,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     OpTimer _t(ctx, ENC_OP_AIB_BWD, st, 2);
     CK(launch_colsum(dtype, BJ, 3 * I, dQKV, g->dbqkv, wa, st));
   }
-  {
-    // the attention half's column sums in one launch: BDRLN-bwd site 1 (dg1, dbe1, dbo)
-    // and, on the per-(b,h) path, the QKV bias gradient from the B*4 epilogue partial rows
+  if (!early_fin) {
     OpTimer _t(ctx, bgrad_epi ? ENC_OP_AIB_BWD : ENC_OP_BDRLN_BWD1, st, 1);
-    int nj = 1;
-    if (bgrad_epi) {
-      att_jobs[1].partials = bg;
-      att_jobs[1].R = B * 4;
-      att_jobs[1].ncols = att_jobs[1].nper = 3 * I;
-      att_jobs[1].out0 = g->dbqkv;
-      nj = 2;
-    }
-    if (ffn_deferred) {
-      att_jobs[nj++] = ffn_jobs[0];
-      att_jobs[nj++] = ffn_jobs[1];
-    }
-    CK(launch_colsum_finalize_jobs(att_jobs, nj, st));
+    CK(finalize_att(st));
+  }
+  if (forked2) {
+    CK(cudaEventRecord(ctx->ev_join2, ctx->side2));
+    CK(cudaStreamWaitEvent(st, ctx->ev_join2, 0));
   }
   CK(join());
   return ENC_OK;
