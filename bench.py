@@ -58,9 +58,10 @@ def parse():
     ap.add_argument("--attn-overlap", type=int, default=1, choices=[0, 1],
                     help="dV contraction beside the fused dA + BSB-bwd kernel "
                          "(ENC_OPT_ATTN_OVERLAP; default on: measured -6 us/step at L)")
-    ap.add_argument("--bwd-side", type=int, default=None, choices=[0, 1, 2],
-                    help="weight-gradient contractions on a side stream (ENC_OPT_BWD_SIDE); "
-                         "default off (with PDL measured +10 us at L, +4 us at Bb)")
+    ap.add_argument("--bwd-side", type=int, default=None, choices=[0, 1, 2, 3],
+                    help="ENC_OPT_BWD_SIDE: 1 = weight-gradient contractions on a side stream, "
+                         "2 = and the column-sum finalize on a second one, 3 = only the "
+                         "finalize (default: measured fastest with PDL at L and Bb)")
     ap.add_argument("--no-qkv-direct", action="store_true",
                     help="separate AIB / AIB-bwd passes instead of the in-place QKV layout")
     ap.add_argument("--no-attn-bh", action="store_true",
@@ -210,7 +211,8 @@ def attention_desc(args, dims) -> str:
 def main():
     args = parse()
     if args.bwd_side is None:
-        args.bwd_side = 0   # measured with PDL at L and Bb: the side stream costs 1-2 %
+        args.bwd_side = 3   # with PDL: weight-gradient GEMMs on the main stream (a side stream
+        # measured 1-2 % slower at L and Bb), only the last column-sum finalize beside them
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

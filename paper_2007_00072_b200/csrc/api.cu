@@ -61,7 +61,8 @@ struct enc_ctx {
   cudaEvent_t ev_in = nullptr, ev_fwd = nullptr, ev_out = nullptr, ev_start = nullptr;
   // backward: weight-gradient contractions on a side stream (own cuBLASLt workspace),
   // forked after their inputs are ready and joined at the end of each backward part
-  int bwd_side = 0;          // ENC_OPT_BWD_SIDE (off: measured +1 % at L, -3 % at Bb)
+  int bwd_side = 3;          // ENC_OPT_BWD_SIDE (3: finalize beside the last contractions;
+                             // GEMMs on a side stream measured slower with PDL)
   int attn_overlap = 0;      // ENC_OPT_ATTN_OVERLAP: dV beside the fused dA + BSB-bwd (off:
                              // -7 us per step, but the fused kernel's own time then includes
                              // the SMs it shares with dV)
@@ -941,8 +942,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   if (key == ENC_OPT_BWD_SIDE) {
-    if (value < 0 || value > 2) return ENC_EINVAL;
-    ctx->bwd_side = value;   // 2: also the attention half's column-sum finalize on a 2nd stream
+    if (value < 0 || value > 3) return ENC_EINVAL;
+    // 1: weight-gradient contractions on the side stream; 2: and the attention half's
+    // column-sum finalize on a second one; 3: only the finalize on the second stream
+    ctx->bwd_side = value;
     return ENC_OK;
   }
   if (key == ENC_OPT_ATTN_OVERLAP) {
@@ -1398,7 +1401,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   ColsumJob ffn_jobs[2];
   // weight-gradient contractions go to the side stream: fork once the inputs exist, join
   // before returning (the next forward reuses the scratch they read)
-  const bool use_side = ctx->bwd_side && ctx->lt && ctx->use_lt && ctx->side;
+  const bool use_side = (ctx->bwd_side == 1 || ctx->bwd_side == 2) && ctx->lt && ctx->use_lt &&
+                        ctx->side;
   bool forked = false;
   auto fork = [&]() -> cudaStream_t {
     if (!use_side) return st;
@@ -1630,7 +1634,8 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     }
     return launch_colsum_finalize_jobs(att_jobs, nj, fs);
   };
-  const bool early_fin = (bgrad_epi || !direct) && ctx->side2 && use_side && ctx->bwd_side == 2;
+  const bool early_fin =
+      (bgrad_epi || !direct) && ctx->side2 && (ctx->bwd_side == 2 || ctx->bwd_side == 3);
   bool forked2 = false;
   if (early_fin) {
     CK(cudaEventRecord(ctx->ev_fork2, st));
