@@ -212,64 +212,74 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
       const bool hiT = p.pk.T >= 0x8000u;
       const uint32_t C2 = (hiT ? 0x10000u - p.pk.T : 0x8000u - p.pk.T) * 0x10001u;
       const uint32_t Xm = hiT ? 0u : 0xFFFFFFFFu;
-      int g = 0;
-      uint2 kw_next = blockIdx.x < p.units && !p.keep_gen ? __ldg(kw_ptr(blockIdx.x, 0))
-                                                          : make_uint2(0, 0);
-      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
-        for (int blk = 0; blk < nblk; ++blk, ++g) {
-          const int s = g % STAGES;
-          uint32_t kw[2] = {kw_next.x, kw_next.y};
-          if (p.keep_gen) {
-            // this row's 64 columns of block blk: 8 Philox chunks, computed before the wait
-            // for the block's data (they do not depend on it); written for the backward
-            const int o = blk / nt, i = blk - (blk / nt) * nt;
-            const int jt = col_outer ? i : o, kt = col_outer ? o : i;
-            const int64_t grow = p.g0 + ((int64_t)u * (nt * 128) + jt * 128 + row) * (nt * 16) +
-                                 kt * 16 + bx * 8;
-            if (p.pk.T == 0) {
-              kw[0] = kw[1] = 0xFFFFFFFFu;
-            } else {
+      // one block: its keep words kw (read or generated), the dropped elements of its X
+      // tile zeroed in shared memory, then handed to the MMA issuer
+      auto process = [&](int u, int blk, int g, uint2 kwv) {
+        const int s = g % STAGES;
+        uint32_t kw[2] = {kwv.x, kwv.y};
+        if (p.keep_gen) {
+          // this row's 64 columns of block blk: 8 Philox chunks, computed before the wait
+          // for the block's data (they do not depend on it); written for the backward
+          const int o = blk / nt, i = blk - (blk / nt) * nt;
+          const int jt = col_outer ? i : o, kt = col_outer ? o : i;
+          const int64_t grow = p.g0 + ((int64_t)u * (nt * 128) + jt * 128 + row) * (nt * 16) +
+                               kt * 16 + bx * 8;
+          if (p.pk.T == 0) {
+            kw[0] = kw[1] = 0xFFFFFFFFu;
+          } else {
 #pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                uint32_t f = 0;
+            for (int c = 0; c < 2; ++c) {
+              uint32_t f = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                  f |= keep_flags((uint64_t)(grow + 4 * c + j), p.pk, C2, Xm, 4 * j);
-                kw[c] = f;
-              }
-            }
-            __stcs(const_cast<uint2*>(kw_ptr(u, blk)), make_uint2(kw[0], kw[1]));
-          } else if (blk + 1 < nblk) {
-            // words of the next block, one block ahead (their latency hides behind this one)
-            kw_next = __ldg(kw_ptr(u, blk + 1));
-          } else if (u + (int)gridDim.x < p.units) {
-            kw_next = __ldg(kw_ptr(u + gridDim.x, 0));
-          }
-          mbar_wait(&full[s], (g / STAGES) & 1);
-          unsigned char* sx = base + s * stage_bytes + bx * 16384;
-          // only 8-element chunks with a dropped element are rewritten (at p = 0.1, 43 % of
-          // the chunks keep all 8)
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const uint32_t f = kw[c >> 2];
-            const int j = c & 3;
-            const uint32_t all = 0xF000F000u >> (4 * j);
-            if ((f & all) != all) {
-              uint4* loc = reinterpret_cast<uint4*>(sx + tc::sw128(row, c));
-              uint4 x = *loc;
-              x.x &= half_mask(f << (4 * j + 0));
-              x.y &= half_mask(f << (4 * j + 1));
-              x.z &= half_mask(f << (4 * j + 2));
-              x.w &= half_mask(f << (4 * j + 3));
-              *loc = x;
+              for (int j = 0; j < 4; ++j)
+                f |= keep_flags((uint64_t)(grow + 4 * c + j), p.pk, C2, Xm, 4 * j);
+              kw[c] = f;
             }
           }
-          fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
-          __syncwarp();
-          if (lane == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xf[s]))
-                         : "memory");
+          __stcs(const_cast<uint2*>(kw_ptr(u, blk)), make_uint2(kw[0], kw[1]));
         }
+        mbar_wait(&full[s], (g / STAGES) & 1);
+        unsigned char* sx = base + s * stage_bytes + bx * 16384;
+        // only 8-element chunks with a dropped element are rewritten (at p = 0.1, 43 % of
+        // the chunks keep all 8)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t f = kw[c >> 2];
+          const int j = c & 3;
+          const uint32_t all = 0xF000F000u >> (4 * j);
+          if ((f & all) != all) {
+            uint4* loc = reinterpret_cast<uint4*>(sx + tc::sw128(row, c));
+            uint4 x = *loc;
+            x.x &= half_mask(f << (4 * j + 0));
+            x.y &= half_mask(f << (4 * j + 1));
+            x.z &= half_mask(f << (4 * j + 2));
+            x.w &= half_mask(f << (4 * j + 3));
+            *loc = x;
+          }
+        }
+        fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&xf[s]))
+                       : "memory");
+      };
+      // read words: a two-register ring, each word pair loaded two blocks ahead of its use and
+      // never moved between registers (the load's latency hides behind a whole block)
+      auto load_kw = [&](int u, int blk) {
+        return (!p.keep_gen && blk < nblk) ? __ldg(kw_ptr(u, blk)) : make_uint2(0, 0);
+      };
+      int g = 0;
+      for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        uint2 kwa = load_kw(u, 0), kwb = load_kw(u, 1);
+        for (int blk = 0; blk < nblk; blk += 2, g += 2) {
+          process(u, blk, g, kwa);
+          kwa = load_kw(u, blk + 2);
+          if (blk + 1 < nblk) {
+            process(u, blk + 1, g + 1, kwb);
+            kwb = load_kw(u, blk + 3);
+          }
+        }
+        if (nblk & 1) --g;   // the loop counted one block past an odd block count
       }
     }
   } else {

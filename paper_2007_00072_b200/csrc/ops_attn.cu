@@ -612,6 +612,7 @@ cudaError_t launch_bias_rows(int dtype, int64_t rows, int cols, void* X, const f
 
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16* __restrict__ dst,
                                    int n) {
+  pdl_wait();   // src may be what the stream predecessor (an optimizer step) wrote
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = __float2bfloat16_rn(src[i]);
 }
@@ -619,8 +620,7 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ src, __nv_bfloat16*
 cudaError_t launch_f32_to_bf16(int n, const float* src, void* dst, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   const int grid = (n + 255) / 256 < 64 ? (n + 255) / 256 : 64;
-  f32_to_bf16_kernel<<<grid, 256, 0, st>>>(src, (__nv_bfloat16*)dst, n);
-  return cudaGetLastError();
+  return launch_k(PDL_LN, f32_to_bf16_kernel, grid, 256, 0, st, src, (__nv_bfloat16*)dst, n);
 }
 
 template <typename T>
