@@ -71,6 +71,9 @@ struct enc_ctx {
   // the backward's column-sum finalize beside the last weight contractions
   cudaStream_t side2 = nullptr;
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
+  // the FFN keep bytes drawn ahead beside the fused score kernel (R29)
+  cudaEvent_t ev_mk_fork = nullptr, ev_mk_join = nullptr;
+  int mask_ahead = 0;      // ENC_OPT_MASK_AHEAD (measured +7 us at L: off)
   void* side_ws = nullptr;
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
@@ -305,11 +308,11 @@ int enc_create(enc_ctx** out, int device) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking);
-  cudaEvent_t* evs[13] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
+  cudaEvent_t* evs[15] = {&c->ev_in,   &c->ev_fwd, &c->ev_out, &c->ev_start,
                           &c->ev_fork, &c->ev_join, &c->ev_pf,  &c->ev_pfs,
                           &c->ev_bwd,  &c->ev_kb_fork, &c->ev_kb_join, &c->ev_fork2,
-                          &c->ev_join2};
-  for (int i = 0; i < 13 && e == cudaSuccess; ++i)
+                          &c->ev_join2, &c->ev_mk_fork, &c->ev_mk_join};
+  for (int i = 0; i < 15 && e == cudaSuccess; ++i)
     e = cudaEventCreateWithFlags(evs[i], cudaEventDisableTiming);
   if (e != cudaSuccess) { enc_destroy(c); cudaSetDevice(prev); return cuda_fail(e); }
   c->lt = lt_create(c->blas_ws, c->blas_ws_bytes);  // optional: cuBLAS is the fallback
@@ -351,7 +354,7 @@ void enc_destroy(enc_ctx* c) {
   if (c->lt) lt_destroy(c->lt);
   for (cudaEvent_t ev : {c->ev_in, c->ev_fwd, c->ev_out, c->ev_start, c->ev_fork, c->ev_join,
                          c->ev_pf, c->ev_pfs, c->ev_bwd, c->ev_kb_fork, c->ev_kb_join,
-                         c->ev_fork2, c->ev_join2})
+                         c->ev_fork2, c->ev_join2, c->ev_mk_fork, c->ev_mk_join})
     if (ev) cudaEventDestroy(ev);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->side2) cudaStreamDestroy(c->side2);
@@ -990,6 +993,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->mask_bytes = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_MASK_AHEAD) {
+    ctx->mask_ahead = value ? 1 : 0;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_AV_KEEP_GEN) {
     ctx->av_keep_gen = value ? 1 : 0;
     return ENC_OK;
@@ -1213,6 +1220,20 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     else if (!bias_done)
       CK(launch_bias_rows(dtype, BJ, 3 * I, QKVs, prm->bqkv, st));
   }
+  // R29: the FFN site's keep bytes are drawn by a small kernel on the side stream, made
+  // ready together with the fused score kernel (launched at high priority): its CTAs take the
+  // SMs the score kernel's last wave leaves idle; Linear1 + BAD then reads the bytes
+  const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
+  const bool mask_ahead = ctx->mask_ahead && fused_attn && ctx->side &&
+                          bad_bytes_of(ctx, d, dtype) && ((size_t)BJ * (U / 8)) % 4 == 0;
+  if (mask_ahead) {
+    CK(cudaEventRecord(ctx->ev_mk_fork, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_mk_fork, 0));
+    CK(launch_keep_bytes((int64_t)BJ * (U / 8), boff * (int64_t)J * (U / 8), pk_ffn,
+                         (uint8_t*)at(saved, SL.off[S_KBF]), ctx->side));
+    ctx->launches += 1;
+    CK(cudaEventRecord(ctx->ev_mk_join, ctx->side));
+  }
   // fused + per-(b, h) path: A = dropout(P) is never stored -- the A V (and backward
   // A^T dC) contraction applies the stored keep bits to P while it is in shared memory
   const bool drop_on_load = fused_attn && use_bh(ctx, J, P);
@@ -1227,7 +1248,7 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     // (A.V generates the keep words on load, R28: the score kernel then writes P only)
     CK(launch_attn_qk_bsb(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, mask_bias, pk_attn, boff, Pm,
                           drop_on_load ? nullptr : A, av_gen ? nullptr : kbits, st,
-                          cfg->causal ? 1 : 0, keep_ahead ? 1 : 0));
+                          cfg->causal ? 1 : 0, keep_ahead ? 1 : 0, mask_ahead));
   } else {
     // QK^T (:551): S_bh[J,K] = Q_bh K_bh^T
     {
@@ -1280,9 +1301,13 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   }
   // Linear (:559) + BAD (:560-562).  The activation input h = X1 W1^T + b1 is kept for the
   // backward (saved.h); on the tcgen05 path BAD runs in the contraction's epilogue
-  const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
   WgemmArgs l1 = ffn_fwd_args(ctx, d, dtype, cfg, X1, prm->W1, prm->b1, pk_ffn, h, A1);
-  if (bad_bytes_of(ctx, d, dtype)) l1.kb_out = (uint8_t*)at(saved, SL.off[S_KBF]);
+  if (mask_ahead) {
+    CK(cudaStreamWaitEvent(st, ctx->ev_mk_join, 0));
+    l1.kb_in = (const uint8_t*)at(saved, SL.off[S_KBF]);
+  } else if (bad_bytes_of(ctx, d, dtype)) {
+    l1.kb_out = (uint8_t*)at(saved, SL.off[S_KBF]);
+  }
   if (wgemm_supported(l1)) {
     // (BAD has no launch of its own: no ENC_OP_BAD_FWD timing on this path)
     OpTimer _t(ctx, ENC_OP_GEMM_L1, st, 1);

@@ -408,10 +408,19 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       float fP[kNs];
 #pragma unroll
       for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
+      // A not stored (the layer's path): the warp's whole [32 x 64] P sub-tile is staged in
+      // its 4 KB region (128-B rows, SWIZZLE_128B) and leaves in ONE TMA store of full lines
+      const bool p_only = !prm.write_a;
+      if (p_only) {
+        if (lane == 0) tc::bulk_wait_read<0>();   // the previous tile's store has read it
+        __syncwarp();
+      }
 #pragma unroll
       for (int ch = 0; ch < kW / 32; ++ch) {
-        if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
-        __syncwarp();
+        if (!p_only) {
+          if (lane == 0) tc::bulk_wait_read<0>();   // staging free again
+          __syncwarp();
+        }
         tc::tmem_ld32(trow + ch * 32, v);
         if (ch + 1 == kW / 32) {   // last TMEM read of this tile by this warp
           tc::fence_before_sync();
@@ -425,6 +434,10 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
           const float fp = fP[(ch * 32 + 8 * j) / kSub], fa = fp * ds;
 #pragma unroll
           for (int u = 0; u < 8; ++u) x[u] = v[8 * j + u] * fp;
+          if (p_only) {
+            *reinterpret_cast<uint4*>(own + tc::sw128(lane, ch * 4 + j)) = pack8(x);
+            continue;
+          }
           *reinterpret_cast<uint4*>(own + sw64(lane, j)) = pack8(x);
           if (prm.write_a) {
 #pragma unroll
@@ -433,11 +446,20 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
             *reinterpret_cast<uint4*>(own + 2048 + sw64(lane, j)) = pack8(a);
           }
         }
+        if (p_only) continue;
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           tc::tma_store_4d(&mapO1, own, cb + ch * 32, m0 + q * 32, h, b);
           if (prm.write_a) tc::tma_store_4d(&mapO2, own + 2048, cb + ch * 32, m0 + q * 32, h, b);
+          tc::bulk_commit();
+        }
+      }
+      if (p_only) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_4d(&mapO2, own, cb, m0 + q * 32, h, b);   // P with 64-column boxes
           tc::bulk_commit();
         }
       }
@@ -671,7 +693,8 @@ bool attn_fused_supported(int J, int P) {
 cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const void* Q,
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
-                               uint32_t* keep_bits, cudaStream_t st, int causal, int keep_pre) {
+                               uint32_t* keep_bits, cudaStream_t st, int causal, int keep_pre,
+                               bool high_prio) {
   if (attn_short_supported(J, P))
     return launch_attn_qk_bsb_short(B, H, J, P, scale, Q, ldq, Kt, ldk, mask_bias, pk,
                                     batch_offset, Pout, Aout, keep_bits, st, causal, keep_pre);
@@ -679,7 +702,9 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   CUtensorMap mq, mk, mp, ma;
   bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
             map_bhrc(&mp, Pout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B) &&
-            map_bhrc(&ma, Aout ? Aout : Pout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B);
+            // A stored: A through 32-column boxes; else this map writes P in 64-column boxes
+            (Aout ? map_bhrc(&ma, Aout, B, H, J, K, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)
+                  : map_bhrc(&ma, Pout, B, H, J, K, 64, 32));
   if (!ok) return cudaErrorInvalidValue;
   const int tiles = (J / kRows) * B * H;
   FusedParams prm{H,         J,         tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8),
@@ -687,21 +712,21 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   if (causal) {   // the masking step: keys k > j of each query row j removed
     if (mask_bias)
       return keep_bits ? launch_persistent(attn_qk_bsb_kernel<true, true, true>, tiles, mq, mk, mp,
-                                           ma, prm, pk, st)
+                                           ma, prm, pk, st, high_prio)
                        : launch_persistent(attn_qk_bsb_kernel<true, false, true>, tiles, mq, mk,
-                                           mp, ma, prm, pk, st);
+                                           mp, ma, prm, pk, st, high_prio);
     return keep_bits ? launch_persistent(attn_qk_bsb_kernel<false, true, true>, tiles, mq, mk, mp,
-                                         ma, prm, pk, st)
+                                         ma, prm, pk, st, high_prio)
                      : launch_persistent(attn_qk_bsb_kernel<false, false, true>, tiles, mq, mk,
-                                         mp, ma, prm, pk, st);
+                                         mp, ma, prm, pk, st, high_prio);
   }
   if (mask_bias)
     return keep_bits
-               ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st)
-               : launch_persistent(attn_qk_bsb_kernel<true, false>, tiles, mq, mk, mp, ma, prm, pk, st);
+               ? launch_persistent(attn_qk_bsb_kernel<true, true>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio)
+               : launch_persistent(attn_qk_bsb_kernel<true, false>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio);
   return keep_bits
-             ? launch_persistent(attn_qk_bsb_kernel<false, true>, tiles, mq, mk, mp, ma, prm, pk, st)
-             : launch_persistent(attn_qk_bsb_kernel<false, false>, tiles, mq, mk, mp, ma, prm, pk, st);
+             ? launch_persistent(attn_qk_bsb_kernel<false, true>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio)
+             : launch_persistent(attn_qk_bsb_kernel<false, false>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio);
 }
 
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,

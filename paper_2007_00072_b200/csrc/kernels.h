@@ -157,6 +157,9 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
                                 const ReduceWs& ws, cudaStream_t st, int gw = 0,
                                 const uint8_t* kb_in = nullptr);
 
+// keep bytes of a whole dropout site (R27 layout) from Philox chunk g0 (nchunks % 4 == 0)
+cudaError_t launch_keep_bytes(int64_t nchunks, int64_t g0, const PhiloxKey& pk, uint8_t* out,
+                              cudaStream_t st);
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* h,
                            void* A1, cudaStream_t st);
@@ -202,8 +205,9 @@ struct WgemmArgs {
   int act = 0;
   PhiloxKey pk{};
   int64_t g0 = 0;                // Philox chunk index of element (0, 0)
-  // keep bytes ([M][N/8], R27): EPI_BAD_FWD stores them (kb_out), EPI_BAD_BWD reads
-  // them instead of evaluating Philox (kb_in)
+  // keep bytes ([M][N/8], R27): EPI_BAD_FWD stores them (kb_out), EPI_BAD_BWD --
+  // and EPI_BAD_FWD when they were drawn ahead (R29) -- reads them instead of evaluating
+  // Philox (kb_in)
   uint8_t* kb_out = nullptr;
   const uint8_t* kb_in = nullptr;
   void* ws = nullptr; size_t ws_bytes = 0;   // split-K slabs (fp32 EPI_STORE outputs)
@@ -277,7 +281,7 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
                                int64_t ldq, const void* Kt, int64_t ldk, const float* mask_bias,
                                const PhiloxKey& pk, int64_t batch_offset, void* Pout, void* Aout,
                                uint32_t* keep_bits, cudaStream_t st, int causal = 0,
-                               int keep_pre = 0);
+                               int keep_pre = 0, bool high_prio = false);
 // keep words of the attention dropout (ENC_KEEP_BITS layout) for [B,H,J,K], K % 64 == 0; the
 // fused forward reads them with keep_pre = 1
 cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& pk,

@@ -206,4 +206,36 @@ cudaError_t launch_bei(int dtype, int64_t n, const void* a, const void* b, void*
   return cudaGetLastError();
 }
 
+// Keep bytes (R27 layout: one byte per 8-element chunk, bit u = element u) of a whole dropout
+// site of `nchunks` chunks starting at Philox chunk g0: four independent Philox calls per
+// thread (one 32-bit word of bytes).  The layer launches it for the BAD site on a side stream
+// beside the fused score kernel, whose last wave leaves SMs idle (R29); the Linear1
+// + BAD epilogue then reads the bytes instead of running Philox.
+__global__ void __launch_bounds__(256) keep_bytes_kernel(uint32_t* __restrict__ out,
+                                                         int64_t nwords, int64_t g0,
+                                                         PhiloxKey pk) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t w = 0;
+    float m[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) w |= keep_byte_mul8((uint64_t)(g0 + 4 * i + j), pk, m) << (8 * j);
+    out[i] = w;
+  }
+}
+
+cudaError_t launch_keep_bytes(int64_t nchunks, int64_t g0, const PhiloxKey& pk, uint8_t* out,
+                              cudaStream_t st) {
+  if (nchunks <= 0) return cudaSuccess;
+  if (nchunks % 4 || ((uintptr_t)out & 3u)) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t nwords = nchunks / 4;
+  int64_t grid = (nwords + 255) / 256;
+  if (grid > 4 * sms) grid = 4 * sms;
+  keep_bytes_kernel<<<(int)grid, 256, 0, st>>>(reinterpret_cast<uint32_t*>(out), nwords, g0, pk);
+  return cudaGetLastError();
+}
+
 }  // namespace enc

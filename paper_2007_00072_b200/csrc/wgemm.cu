@@ -67,7 +67,8 @@ struct Params {
   int64_t g0;             // Philox chunk index of element (0, 0): batch_offset * J * N / 8
   float* partials;        // EPI_BAD_BWD: [ceil(M/128) * 4][N] column partial sums of dh
   uint8_t* kb_out;        // EPI_BAD_FWD: keep bytes [M][N/8] written (or null)
-  const uint8_t* kb_in;   // EPI_BAD_BWD: keep bytes [M][N/8] read instead of Philox (or null)
+  const uint8_t* kb_in;   // EPI_BAD_BWD / EPI_BAD_FWD: keep bytes [M][N/8] read instead of
+                          // Philox (or null)
 };
 
 // byte offset of 16-B chunk c (0..3) of row r in a [32 x 64 B] SWIZZLE_64B tile
@@ -375,6 +376,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = cidx & 1;
         unsigned char* sb = stg + buf * kStg;
         unsigned char* sb2 = stg + (buf ^ 1) * kStg;
+        // BAD epilogues with stored keep bytes: this lane's word (4 chunks of its row), loaded
+        // before the accumulator so its latency hides behind the TMEM load
+        uint32_t kw_pre = 0;
+        if ((EPI == EPI_BAD_FWD || EPI == EPI_BAD_BWD) && p.kb_in != nullptr && row < p.M &&
+            col < p.N) {
+          const int64_t ci0 = (int64_t)row * (p.N >> 3) + (col >> 3);
+          if ((p.N & 31) == 0) {
+            kw_pre = __ldg(reinterpret_cast<const uint32_t*>(p.kb_in + ci0));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              if (col + 8 * j < p.N) kw_pre |= (uint32_t)__ldg(p.kb_in + ci0 + j) << (8 * j);
+          }
+        }
         float v[CW];
         const uint32_t taddr =
             tmem + ((uint32_t)(q * 32) << 16) + as * kBN + chalf * kSliceCols + c * CW;
@@ -426,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           PhiloxKey pkh = p.pk;
           pkh.scale *= 0.5f;   // act_f2 returns 2 act(h)
           const int64_t ci0 = (int64_t)row * (p.N >> 3) + (col >> 3);   // first chunk
-          uint32_t kw = 0;                                              // its 4 keep bytes
+          uint32_t kw = kw_pre;   // its 4 keep bytes (given, R29; or formed below)
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float b[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, hb[8], m[8], a[8];
@@ -435,7 +450,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 8; ++i) hb[i] = v[8 * j + i] + b[i];
             o0[j] = pack_bf16x8(hb);
             unpack_bf16x8(o0[j], hb);
-            if (p.kb_out != nullptr)
+            if (p.kb_in != nullptr)
+              mul8_from_byte(kw >> (8 * j), pkh.scale, m);
+            else if (p.kb_out != nullptr)
               kw |= keep_byte_mul8((uint64_t)(p.g0 + ci0 + j), pkh, m) << (8 * j);
             else
               keep_mul8((uint64_t)(p.g0 + ci0 + j), pkh, m);
@@ -472,16 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {   // EPI_BAD_BWD
           // dh = keep ? acc * s * act'(h) : 0, written over h in the staging buffer
           const int64_t ci0 = (int64_t)row * (p.N >> 3) + (col >> 3);   // first chunk
-          uint32_t kw = 0;
-          if (p.kb_in != nullptr && row < p.M && col < p.N) {
-            if ((p.N & 31) == 0) {
-              kw = __ldg(reinterpret_cast<const uint32_t*>(p.kb_in + ci0));
-            } else {
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                if (col + 8 * j < p.N) kw |= (uint32_t)__ldg(p.kb_in + ci0 + j) << (8 * j);
-            }
-          }
+          const uint32_t kw = kw_pre;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             float h8[8], m[8];

@@ -444,17 +444,19 @@ def test_mask_bytes_option_bitwise(dtype, dims, variant):
     dY = torch.tensor(inp["dY"], device="cuda").to(tdt)
     M = torch.tensor(inp["mask_bias"], device="cuda")
     out = []
-    for mb in (0, 1):
+    for mb, ahead in ((0, 0), (1, 0), (1, 1)):   # (1, 1): FFN bytes drawn ahead (R29)
         layer = EncoderLayer(dims, dtype, LayerCfg())
         ops.enc_set_option(layer.ctx, ops.OPT_MASK_BYTES, mb)
+        ops.enc_set_option(layer.ctx, ops.OPT_MASK_AHEAD, ahead)
         ops.enc_set_option(layer.ctx, ops.OPT_BDRLN_VARIANT, variant)
         layer.set_params(prm)
         Y = layer.forward(X, M).clone()
         dX = layer.backward(X, dY).clone()
         torch.cuda.synchronize()
         out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu()))
-    for a, b in zip(out[0], out[1]):
-        assert torch.equal(a, b)
+    for other in out[1:]:
+        for a, b in zip(out[0], other):
+            assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("dims,causal", [
