@@ -35,6 +35,24 @@
 namespace enc {
 namespace wg {
 
+#ifdef ENC_WGEMM_TRACE
+// Debug-only timeline (tools/trace_wgemm.py builds a separate library with this on):
+// per CTA and tile index (< 8): [0] MMA warp starts the tile (accumulator free),
+// [1] its last MMA committed, [2] epilogue warp 2 has the accumulator, [3] it finished.
+__device__ unsigned long long g_wg_trace[148 * 8 * 4];
+__device__ __forceinline__ void wg_stamp(int it, int e) {
+  if (it < 8 && blockIdx.x < 148) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_wg_trace[(blockIdx.x * 8 + it) * 4 + e] = t;
+  }
+}
+#define WG_STAMP(it, e) wg_stamp((it), (e))
+#else
+#define WG_STAMP(it, e) ((void)0)
+#endif
+
+
 constexpr int kBM = 128, kBN = 256, kBK = 64;   // per-CTA accumulator tile 128 x 256
 constexpr int kEpiWarps = 16;                   // 4 per TMEM lane quarter
 constexpr int kSliceCols = kBN / (kEpiWarps / 4);  // accumulator columns per epilogue warp
@@ -294,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           mbar_wait(&tempty[as], ((it >> 1) & 1) ^ 1);
         tc::fence_after_sync();
+        if (lane == 0) WG_STAMP(it, 0);
         const uint32_t dacc = tmem + as * kBN;
         for (int kb = kb0; kb < kb1; ++kb, ++pc) {
           const uint32_t s = pc % kStages;
@@ -328,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_commit_pair(&tfull[as]);
           else
             tc::mma_commit(&tfull[as]);
+          WG_STAMP(it, 1);
         }
         __syncwarp();
       }
@@ -365,6 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int as = it & 1;
       mbar_wait_sleep(&tfull[as], (it >> 1) & 1, 20000u);
       tc::fence_after_sync();
+      if (ew == 0 && lane == 0) WG_STAMP(it, 2);
       const int row0 = mb * kBM * CG + rank * kBM + q * 32;
       const int row = row0 + lane;
       const int out_row0 = row0 + sp * p.M;   // split-K partial slab (EPI_STORE, fp32)
@@ -537,6 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
       }
+      if (ew == 0 && lane == 0) WG_STAMP(it, 3);
       (void)row;
     }
     if (lane == 0) tc::bulk_wait<0>();
@@ -765,5 +787,15 @@ cudaError_t launch_wgemm(const WgemmArgs& g, int num_sms, cudaStream_t st) {
 int wgemm_launches(const WgemmArgs& g, int num_sms) {
   return plan_of(g, num_sms).splits > 1 ? 2 : 1;
 }
+
+#ifdef ENC_WGEMM_TRACE
+extern "C" int enc_debug_wgemm_trace(void* host, size_t bytes) {
+  return (int)cudaMemcpyFromSymbol(host, wg::g_wg_trace, bytes);
+}
+extern "C" int enc_debug_wgemm_trace_clear() {
+  static unsigned long long zero[148 * 8 * 4];
+  return (int)cudaMemcpyToSymbol(wg::g_wg_trace, zero, sizeof(zero));
+}
+#endif
 
 }  // namespace enc
