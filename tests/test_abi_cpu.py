@@ -86,7 +86,7 @@ def test_bench_parses_its_flags():
     bench = importlib.import_module("bench")
     old = sys.argv
     try:
-        for argv in (["bench.py"], ["bench.py", "--config", "Bb", "--causal", "--attn-overlap"],
+        for argv in (["bench.py"], ["bench.py", "--config", "Bb", "--causal", "--attn-overlap", "0"],
                      ["bench.py", "--layers", "24", "--optimizer", "--no-prefetch"],
                      ["bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1"]):
             sys.argv = argv
