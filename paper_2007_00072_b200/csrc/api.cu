@@ -74,6 +74,9 @@ struct enc_ctx {
   // the FFN keep bytes drawn ahead beside the fused score kernel (R29)
   cudaEvent_t ev_mk_fork = nullptr, ev_mk_join = nullptr;
   int mask_ahead = 0;      // ENC_OPT_MASK_AHEAD (measured +7 us at L: off)
+  // ENC_OPT_SIDE_OPS (dW contractions on the side stream): Out-dW beside the fused BSB-bwd /
+  // dQdK stretch (measured -2..-6 us at L); the others measured neutral or slower
+  uint32_t side_ops = 1u << ENC_OP_GEMM_OUT_DW;
   void* side_ws = nullptr;
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
@@ -993,6 +996,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->mask_bytes = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_SIDE_OPS) {
+    ctx->side_ops = (uint32_t)value;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_MASK_AHEAD) {
     ctx->mask_ahead = value ? 1 : 0;
     return ENC_OK;
@@ -1429,14 +1436,18 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
   const bool use_side = (ctx->bwd_side == 1 || ctx->bwd_side == 2) && ctx->lt && ctx->use_lt &&
                         ctx->side;
   bool forked = false;
-  auto fork = [&]() -> cudaStream_t {
-    if (!use_side) return st;
+  // ENC_OPT_SIDE_OPS: a mask of weight-gradient contractions put on the side stream
+  // (overrides ENC_OPT_BWD_SIDE's all-or-none for those it names)
+  auto fork_op = [&](int op) -> bool {
+    return ctx->side && ctx->lt && ctx->use_lt && ((ctx->side_ops >> op) & 1u);
+  };
+  auto fork = [&](int op = -1) -> cudaStream_t {
+    if (!use_side && !(op >= 0 && fork_op(op))) return st;
     cudaEventRecord(ctx->ev_fork, st);
     cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0);
     forked = true;
     return ctx->side;
   };
-  void* const sws = use_side ? ctx->side_ws : nullptr;
   auto join = [&]() -> cudaError_t {
     if (!forked) return cudaSuccess;
     forked = false;
@@ -1472,10 +1483,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
         CK(launch_wgemm(l2, ctx->num_sms, st));
       }
       {
-        cudaStream_t ss = fork();
+        cudaStream_t ss = fork(ENC_OP_GEMM_L2_DW);
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
         if ((r = wcontract(ctx, ENC_OP_GEMM_L2_DW, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
-                           g->dW2, U, nullptr, sws)))
+                           g->dW2, U, nullptr, ss != st ? ctx->side_ws : nullptr)))
           return r;
       }
       // BAD-bwd has no launch of its own: db1's partials are finished with the half's
@@ -1493,10 +1504,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
           return r;
       }
       {
-        cudaStream_t ss = fork();
+        cudaStream_t ss = fork(ENC_OP_GEMM_L2_DW);
         OpTimer _t(ctx, ENC_OP_GEMM_L2_DW, ss, 0);
         if ((r = wcontract(ctx, ENC_OP_GEMM_L2_DW, ss, dtype, F32, true, false, I, U, BJ, dY2, I, A1, U, 0.f,
-                           g->dW2, U, nullptr, sws)))
+                           g->dW2, U, nullptr, ss != st ? ctx->side_ws : nullptr)))
           return r;
       }
       OpTimer _t(ctx, ENC_OP_BAD_BWD, st, ffn_deferred ? 1 : 2);
@@ -1513,10 +1524,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
       return r;
   }
   {
-    cudaStream_t ss = fork();
+    cudaStream_t ss = fork(ENC_OP_GEMM_L1_DW);
     OpTimer _t(ctx, ENC_OP_GEMM_L1_DW, ss, 0);
     if ((r = wcontract(ctx, ENC_OP_GEMM_L1_DW, ss, dtype, F32, true, false, U, I, BJ, dh, U, X1, I, 0.f, g->dW1, I,
-                       nullptr, sws)))
+                       nullptr, ss != st ? ctx->side_ws : nullptr)))
       return r;
   }
   if (!(parts & 2)) CK(join());   // the FFN bucket is complete when the FFN part returns
@@ -1543,10 +1554,10 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
       return r;
   }
   {
-    cudaStream_t ss = fork();
+    cudaStream_t ss = fork(ENC_OP_GEMM_OUT_DW);
     OpTimer _t(ctx, ENC_OP_GEMM_OUT_DW, ss, 0);
     if ((r = wcontract(ctx, ENC_OP_GEMM_OUT_DW, ss, dtype, F32, true, false, I, I, BJ, dYo, I, C, I, 0.f, g->dWo, I,
-                       nullptr, sws)))
+                       nullptr, ss != st ? ctx->side_ws : nullptr)))
       return r;
   }
   // Gamma dX1 (:588): dA_bh = dC_bh V_bh^T;  Gamma dX2 (:589): dV_bh = A_bh^T dC_bh
@@ -1685,13 +1696,13 @@ static int backward_impl(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_c
     }
   }
   {
-    cudaStream_t ss = fork();
+    cudaStream_t ss = fork(ENC_OP_GEMM_QKV_DW);
     OpTimer _t(ctx, ENC_OP_GEMM_QKV_DW, ss, 0);
     for (int gi = 0; gi < ngrp; ++gi) {
       const int s0 = gstart[gi], nI = gcount[gi] * I;
       if ((r = wcontract(ctx, ENC_OP_GEMM_QKV_DW, ss, dtype, F32, true, false, nI, I, BJ,
                          (const char*)dQKV + (size_t)s0 * I * es, 3 * I, X, I, 0.f,
-                         g->dWqkv + (size_t)s0 * I * I, I, nullptr, sws)))
+                         g->dWqkv + (size_t)s0 * I * I, I, nullptr, ss != st ? ctx->side_ws : nullptr)))
         return r;
     }
   }
