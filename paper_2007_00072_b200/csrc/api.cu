@@ -77,6 +77,7 @@ struct enc_ctx {
   // ENC_OPT_SIDE_OPS (dW contractions on the side stream): Out-dW beside the fused BSB-bwd /
   // dQdK stretch (measured -2..-6 us at L); the others measured neutral or slower
   uint32_t side_ops = 1u << ENC_OP_GEMM_OUT_DW;
+  int attn_fused_av = 1;   // ENC_OPT_ATTN_FUSED_AV (QK^T + BSB + A.V in one kernel, R30)
   void* side_ws = nullptr;
   // pipelined host steps: input copies done (ev_pf, on copy_in), fork point on the layer
   // stream (ev_pfs)
@@ -996,6 +997,10 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     ctx->mask_bytes = value ? 1 : 0;
     return ENC_OK;
   }
+  if (key == ENC_OPT_ATTN_FUSED_AV) {
+    ctx->attn_fused_av = value ? 1 : 0;
+    return ENC_OK;
+  }
   if (key == ENC_OPT_SIDE_OPS) {
     ctx->side_ops = (uint32_t)value;
     return ENC_OK;
@@ -1248,7 +1253,16 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // the Philox stream (FMA work beside a memory-bound stream) and store them for the
   // backward; the score kernel runs no Philox (ENC_OPT_AV_KEEP_GEN, not with keep-ahead)
   const bool av_gen = drop_on_load && ctx->av_keep_gen && !keep_ahead;
-  if (fused_attn) {
+  // R30: QK^T + BSB + A.V in one kernel (P aliased as the A operand in TMEM); C's low word
+  // is stored with C, so the backward's row term (R26) needs the same saved layout
+  const bool fused_av = drop_on_load && ctx->attn_fused_av && !keep_ahead && !av_gen &&
+                        attn_fused_av_supported(J, P) && dc_term_of(ctx, fused_attn, J, P);
+  if (fused_av) {
+    OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
+    CK(launch_attn_qk_bsb_av(B, H, J, P, scale, Q, ldqkv, Kt, ldqkv, V, ldqkv, mask_bias,
+                             pk_attn, boff, Pm, kbits, C, at(saved, SL.off[S_CLO]), I, st,
+                             cfg->causal ? 1 : 0));
+  } else if (fused_attn) {
     // QK^T (:551) + BSB (:552) in one tcgen05 kernel: S stays in TMEM
     if (keep_ahead) CK(cudaStreamWaitEvent(st, ctx->ev_kb_join, 0));
     OpTimer _t(ctx, ENC_OP_BSB_FWD, st, 1);
@@ -1276,8 +1290,10 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   }
   // Gamma (:553): C_bh[J,P] = A_bh V_bh, written into C[B,J,H,P]
   {
-    OpTimer _t(ctx, ENC_OP_GEMM_AV, st, 1);
-    if (drop_on_load) {
+    OpTimer _t(ctx, ENC_OP_GEMM_AV, st, fused_av ? 0 : 1, !fused_av);
+    if (fused_av) {
+      // computed by the score kernel above (R30)
+    } else if (drop_on_load) {
       // (+ the fp32 result's low bf16 word for the backward's row term, R26)
       CK(launch_attn_av_bh(B, H, J, P, Pm, V, ldqkv, C, I, kbits, pk_attn.scale, st,
                            dc_term_of(ctx, fused_attn, J, P) ? at(saved, SL.off[S_CLO])

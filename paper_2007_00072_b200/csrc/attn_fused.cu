@@ -547,6 +547,360 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
   if (warp == 0) tc::tmem_dealloc(tmem, kK);
 }
 
+// ------------------------------------------------------------------ score kernel + A.V
+// (R30) QK^T + BSB + A.V in one kernel: after the softmax the warp's P sub-tile is
+// staged in shared memory (and stored, the backward needs P), dropout is applied to the staged
+// values and the result A = keep * P (bf16) is written into TMEM over the consumed scores
+// (columns [0, 256): 32 per slice, two keys per column) -- the A operand of
+// C = A V (tcgen05.mma with A in TMEM), accumulated into columns [256, 320).  Warps 24-31
+// read C out (x dropout scale) and store C and its low bf16 word (R26).  P is never re-read
+// from HBM for the forward and the separate A.V launch disappears.
+//   shared memory: Q [128 x 64] | V [512 x 64] | per-warp 4 KB staging, whose first 64 KB
+//   (warps 0-15) also hold K [512 x 64] between its load and the score MMA | stats | barriers
+__device__ __forceinline__ uint32_t half_mask2(uint32_t g) {   // bits 15 / 31 -> half masks
+  uint32_t m;
+  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(g));
+  return m;
+}
+
+__device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+constexpr uint32_t kAvQ = 0, kAvV = 16384, kAvX = 81920;
+constexpr uint32_t kAvStats = kAvX + kWarps * 4096;
+constexpr uint32_t kAvBars = kAvStats + 2 * kSlices * kRows * 8;
+constexpr size_t kAvSmem = 1024 + kAvBars + 16 * 8 + 16;
+static_assert(kAvSmem <= 227 * 1024, "smem");
+
+template <bool kMask, bool kCausal>
+__global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
+    const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
+    const __grid_constant__ CUtensorMap mapV, const __grid_constant__ CUtensorMap mapP,
+    const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapClo,
+    FusedParams prm, PhiloxKey pk) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = tc::align1024(smem_raw);
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int q = warp & 3;
+  const int slice = warp >> 2;
+  const int r = q * 32 + lane;
+  const int cb = slice * kW;
+  const int mtiles = prm.J / kRows;
+  const bool leader = (warp == 0 && lane == 0);
+  const bool hiT = pk.T >= 0x8000u;
+  const uint32_t C2 = (hiT ? 0x10000u - pk.T : 0x8000u - pk.T) * 0x10001u;
+  const uint32_t X = hiT ? 0u : 0xFFFFFFFFu;
+
+  float2* stats = reinterpret_cast<float2*>(base + kAvStats);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + kAvBars);
+  uint64_t* op_full = bars + 0;    // Q + K landed
+  uint64_t* op_empty = bars + 1;   // score MMA done (Q, K slots free)
+  uint64_t* tm_full = bars + 2;    // S in TMEM
+  uint64_t* s_read = bars + 3;     // every warp read its S columns (count 32)
+  uint64_t* a_ready = bars + 4;    // every warp wrote its A columns (count 32)
+  uint64_t* v_full = bars + 5;     // V landed
+  uint64_t* c_full = bars + 6;     // C = A V in TMEM (also: V slot and A columns free)
+  uint64_t* c_done = bars + 7;     // C read out of TMEM (count 8)
+  uint64_t* stg_free = bars + 8;   // warps 0-15 staging free for the next K (count 16)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
+  unsigned char* own = base + kAvX + warp * 4096;
+
+  auto tile_coords = [&](int t, int& b, int& h, int& m0, int& bh) {
+    bh = t / mtiles;
+    m0 = (t - bh * mtiles) * kRows;
+    b = bh / prm.H;
+    h = bh - b * prm.H;
+  };
+  auto load_qk = [&](int t) {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    mbar_arrive_expect_tx(op_full, (uint32_t)(kRows + kK) * 128);
+    tc::tma_load_4d(base + kAvQ, &mapQ, op_full, 0, h, m0, b);
+    tc::tma_load_4d(base + kAvX, &mapK, op_full, 0, h, 0, b);
+    tc::tma_load_4d(base + kAvX + 256 * 128, &mapK, op_full, 0, h, 256, b);
+  };
+  auto load_v = [&](int t) {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    mbar_arrive_expect_tx(v_full, (uint32_t)kK * 128);
+    tc::tma_load_4d(base + kAvV, &mapV, v_full, 0, h, 0, b);
+    tc::tma_load_4d(base + kAvV + 256 * 128, &mapV, v_full, 0, h, 256, b);
+  };
+
+  if (leader) {
+    tc::prefetch_tmap(&mapQ);
+    tc::prefetch_tmap(&mapK);
+    tc::prefetch_tmap(&mapV);
+    tc::prefetch_tmap(&mapP);
+    tc::prefetch_tmap(&mapC);
+    tc::prefetch_tmap(&mapClo);
+    mbar_init(op_full, 1);
+    mbar_init(op_empty, 1);
+    mbar_init(tm_full, 1);
+    mbar_init(s_read, kWarps);
+    mbar_init(a_ready, kWarps);
+    mbar_init(v_full, 1);
+    mbar_init(c_full, 1);
+    mbar_init(c_done, 8);
+    mbar_init(stg_free, 16);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, kK);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + cb;
+  pdl_wait();   // operands are the stream predecessor's outputs
+
+  if (leader && blockIdx.x < prm.tiles) {
+    load_qk(blockIdx.x);
+    load_v(blockIdx.x);
+  }
+
+  int it = 0;
+  for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    const uint32_t ph = it & 1;
+    if (leader) {
+      // score MMA once the previous tile's C left TMEM and this tile's Q, K landed
+      if (it > 0) mbar_wait(c_done, ph ^ 1);
+      mbar_wait(op_full, ph);
+      tc::fence_after_sync();
+      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kRows, 256, false, false);
+      const uint32_t a0 = smem_u32(base + kAvQ), b0 = smem_u32(base + kAvX);
+#pragma unroll
+      for (int nh = 0; nh < 2; ++nh)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16(tmem + nh * 256, tc::smem_desc(a0 + k * 32, 16, 1024),
+                       tc::smem_desc(b0 + nh * 256 * 128 + k * 32, 16, 1024), idesc, k != 0);
+      tc::mma_commit(tm_full);
+      tc::mma_commit(op_empty);
+    }
+    __syncwarp();
+    // keep flags of this thread's 64 elements (needed: A = keep * P) and the keep words for
+    // the backward
+    const int64_t rowi = (int64_t)bh * prm.J + m0 + r;
+    uint32_t kf[2];
+    if (pk.T == 0) {
+      kf[0] = kf[1] = 0xFFFFFFFFu;
+    } else {
+      const int64_t grow = prm.g0 + rowi * (kK / 8) + cb / 8;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t f = 0;
+#pragma unroll 2
+        for (int j = 0; j < 4; ++j)
+          f |= keep_flags((uint64_t)(grow + 4 * c + j), pk, C2, X, 4 * j);
+        kf[c] = f;
+      }
+    }
+    __stcs(reinterpret_cast<uint2*>(prm.keep_bits + rowi * (kK / 32) + cb / 32),
+           make_uint2(kf[0], kf[1]));
+    mbar_wait_sleep(tm_full, ph);
+    tc::fence_after_sync();
+    float v[32];
+    // pass 1 (as fused_body): sub-chunk max, e = 2^(y - m_c) back into TMEM, sub-chunk sum
+    constexpr int kSub = kMask ? 16 : 32;
+    constexpr int kNs = kW / kSub;
+    const float c = prm.c;
+    float mc[kNs], lc[kNs];
+#pragma unroll
+    for (int ch = 0; ch < kNs; ++ch) {
+      float m;
+      if (kMask) {
+        tc::tmem_ld16(trow + ch * kSub, v);
+        const float4* mb4 =
+            reinterpret_cast<const float4*>(prm.mask_bias + (int64_t)b * kK + cb + ch * kSub);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 mm = ld_mask4(mb4 + i);
+          v[4 * i + 0] = fmaf(v[4 * i + 0], c, mm.x * kL2e);
+          v[4 * i + 1] = fmaf(v[4 * i + 1], c, mm.y * kL2e);
+          v[4 * i + 2] = fmaf(v[4 * i + 2], c, mm.z * kL2e);
+          v[4 * i + 3] = fmaf(v[4 * i + 3], c, mm.w * kL2e);
+        }
+        if (kCausal) {
+#pragma unroll
+          for (int i = 0; i < kSub; ++i)
+            if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
+        }
+        m = tree_max<kSub>(v);
+        const float mr = m == -INFINITY ? 0.f : m;
+#pragma unroll
+        for (int i = 0; i < kSub; ++i) v[i] = tc::ex2(v[i] - mr);
+        lc[ch] = tree_sum<kSub>(v);
+        tc::tmem_st16(trow + ch * kSub, v);
+      } else {
+        tc::tmem_ld32(trow + ch * kSub, v);
+        if (kCausal) {
+#pragma unroll
+          for (int i = 0; i < kSub; ++i)
+            if (cb + ch * kSub + i > m0 + r) v[i] = -INFINITY;
+        }
+        m = tree_max<kSub>(v) * c;
+        const float mz = (kCausal && m == -INFINITY) ? 0.f : m;
+#pragma unroll
+        for (int i = 0; i < kSub; ++i) v[i] = tc::ex2(fmaf(v[i], c, -mz));
+        lc[ch] = tree_sum<kSub>(v);
+        tc::tmem_st32(trow + ch * kSub, v);
+      }
+      mc[ch] = m;
+    }
+    float mt = mc[0];
+#pragma unroll
+    for (int ch = 1; ch < kNs; ++ch) mt = fmaxf(mt, mc[ch]);
+    const float mtr = mt == -INFINITY ? 0.f : mt;
+    float lt = 0.f;
+#pragma unroll
+    for (int ch = 0; ch < kNs; ++ch) lt += lc[ch] * tc::ex2(mc[ch] - mtr);
+    float2* st = stats + (it & 1) * (kSlices * kRows);
+    st[slice * kRows + r] = make_float2(mt, lt);
+    tc::tmem_wait_st();
+    qbar(q);
+    float M = st[r].x;
+#pragma unroll
+    for (int s2 = 1; s2 < kSlices; ++s2) M = fmaxf(M, st[s2 * kRows + r].x);
+    const float Mr = M == -INFINITY ? 0.f : M;
+    float L = 0.f;
+#pragma unroll
+    for (int s2 = 0; s2 < kSlices; ++s2) {
+      const float2 x2 = st[s2 * kRows + r];
+      L += x2.y * tc::ex2(x2.x - Mr);
+    }
+    const float invL = __fdividef(1.f, L);
+    float fP[kNs];
+#pragma unroll
+    for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
+    // pass 2: P staged as the warp's [32 x 64] SWIZZLE_128B tile (its previous contents --
+    // P / C of the last tile, or K -- have been read: see stg_free / bulk waits)
+    if (lane == 0) tc::bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int ch = 0; ch < kW / 32; ++ch) {
+      tc::tmem_ld32(trow + ch * 32, v);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float x[8];
+        const float fp = fP[(ch * 32 + 8 * j) / kSub];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = v[8 * j + u] * fp;
+        *reinterpret_cast<uint4*>(own + tc::sw128(lane, ch * 4 + j)) = pack8(x);
+      }
+    }
+    tc::fence_before_sync();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(s_read);   // this warp's S columns are consumed
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tc::tma_store_4d(&mapP, own, cb, m0 + q * 32, h, b);
+      tc::bulk_commit();
+    }
+    // A = keep * P into TMEM columns [32 * slice, +32) of this warp's lanes, once every warp
+    // has read its scores (the columns overlap other slices' S); 16 columns at a time
+    mbar_wait(s_read, ph);
+    tc::fence_after_sync();
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      float af[16];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int cc = half * 4 + c4;
+        uint4 x = *reinterpret_cast<const uint4*>(own + tc::sw128(lane, cc));
+        const uint32_t f = kf[half];
+        const int j = c4;
+        af[4 * c4 + 0] = __uint_as_float(x.x & half_mask2(f << (4 * j + 0)));
+        af[4 * c4 + 1] = __uint_as_float(x.y & half_mask2(f << (4 * j + 1)));
+        af[4 * c4 + 2] = __uint_as_float(x.z & half_mask2(f << (4 * j + 2)));
+        af[4 * c4 + 3] = __uint_as_float(x.w & half_mask2(f << (4 * j + 3)));
+      }
+      tc::tmem_st16(tmem + ((uint32_t)(q * 32) << 16) + 32 * slice + 16 * half, af);
+    }
+    tc::tmem_wait_st();
+    tc::fence_before_sync();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(a_ready);
+    if (warp < 16) {   // the next K lands in these warps' staging
+      if (lane == 0) {
+        tc::bulk_wait_read<0>();
+        mbar_arrive(stg_free);
+      }
+      __syncwarp();
+    }
+    if (leader) {
+      // C = A V: 32 k-steps of 16 keys, A from TMEM (8 columns each), V MN-major
+      mbar_wait(a_ready, ph);
+      mbar_wait(v_full, ph);
+      tc::fence_after_sync();
+      constexpr uint32_t idesc_av = tc::instr_desc_bf16_f32(kRows, 64, false, true);
+      const uint32_t v0 = smem_u32(base + kAvV);
+#pragma unroll 4
+      for (int ks = 0; ks < kK / 16; ++ks)
+        mma_bf16_ts(tmem + 256, tmem + 8 * ks, tc::smem_desc(v0 + ks * 2048, 8192, 1024),
+                    idesc_av, ks != 0);
+      tc::mma_commit(c_full);
+      // next tile's operands: Q + K once warps 0-15's staging is free, V once this MMA is done
+      if (t + (int)gridDim.x < prm.tiles) {
+        mbar_wait(op_empty, ph);
+        mbar_wait(stg_free, ph);
+        load_qk(t + gridDim.x);
+        mbar_wait(c_full, ph);
+        load_v(t + gridDim.x);
+      }
+    }
+    if (warp >= 24) {
+      // C (x dropout scale) or its low bf16 word, [32 rows x 64] per warp
+      mbar_wait_sleep(c_full, ph);
+      tc::fence_after_sync();
+      if (lane == 0) tc::bulk_wait_read<0>();   // this warp's P store has read the staging
+      __syncwarp();
+      const bool lo = warp >= 28;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        float cv[32];
+        tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + 256 + 32 * hh, cv);
+        if (hh == 1) {
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(c_done);   // C read out of TMEM
+        }
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+          float x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float y = cv[8 * c4 + u] * pk.scale;
+            x[u] = lo ? y - __bfloat162float(__float2bfloat16_rn(y)) : y;
+          }
+          *reinterpret_cast<uint4*>(own + tc::sw128(lane, hh * 4 + c4)) = pack8(x);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tc::tma_store_4d(lo ? &mapClo : &mapC, own, 0, h, m0 + q * 32, b);
+        tc::bulk_commit();
+      }
+    }
+  }
+  if (lane == 0) tc::bulk_wait<0>();
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, kK);
+}
+
 template <bool kMask, bool kBits, bool kCausal = false>
 __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_kernel(
     const __grid_constant__ CUtensorMap mapQ, const __grid_constant__ CUtensorMap mapK,
@@ -727,6 +1081,36 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
   return keep_bits
              ? launch_persistent(attn_qk_bsb_kernel<false, true>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio)
              : launch_persistent(attn_qk_bsb_kernel<false, false>, tiles, mq, mk, mp, ma, prm, pk, st, high_prio);
+}
+
+// QK^T + BSB + A.V in one kernel (R30): J = K = 512, P = 64; writes P, the keep words, C
+// ([B,J,H,P] rows, stride ldc) and C's low bf16 word (same layout)
+bool attn_fused_av_supported(int J, int P) { return P == 64 && J == kK; }
+
+cudaError_t launch_attn_qk_bsb_av(int B, int H, int J, int P, float scale, const void* Q,
+                                  int64_t ldq, const void* Kt, int64_t ldk, const void* V,
+                                  int64_t ldv, const float* mask_bias, const PhiloxKey& pk,
+                                  int64_t batch_offset, void* Pout, uint32_t* keep_bits,
+                                  void* C, void* C_lo, int64_t ldc, cudaStream_t st, int causal) {
+  if (!attn_fused_av_supported(J, P) || !keep_bits || !C || !C_lo)
+    return cudaErrorInvalidValue;
+  const int K = J;
+  CUtensorMap mq, mk, mv, mp, mc, ml;
+  bool ok = map_pop(&mq, Q, B, H, J, P, ldq, kRows) && map_pop(&mk, Kt, B, H, K, P, ldk, 256) &&
+            map_pop(&mv, V, B, H, K, P, ldv, 256) && map_bhrc(&mp, Pout, B, H, J, K, 64, 32) &&
+            map_pop(&mc, C, B, H, J, P, ldc, 32) && map_pop(&ml, C_lo, B, H, J, P, ldc, 32);
+  if (!ok) return cudaErrorInvalidValue;
+  const int tiles = (J / kRows) * B * H;
+  FusedParams prm{H,         J,         tiles, scale * kL2e, batch_offset * (int64_t)H * J * (K / 8),
+                  mask_bias, keep_bits, 0, 0};
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAvSmem);
+    return launch_k(PDL_ATTN_FUSED, kern, persistent_grid(tiles), kThreads, kAvSmem, st, mq, mk,
+                    mv, mp, mc, ml, prm, pk);
+  };
+  if (causal)
+    return mask_bias ? go(attn_qk_bsb_av_kernel<true, true>) : go(attn_qk_bsb_av_kernel<false, true>);
+  return mask_bias ? go(attn_qk_bsb_av_kernel<true, false>) : go(attn_qk_bsb_av_kernel<false, false>);
 }
 
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,

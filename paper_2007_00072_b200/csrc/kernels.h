@@ -286,6 +286,14 @@ cudaError_t launch_attn_qk_bsb(int B, int H, int J, int P, float scale, const vo
 // fused forward reads them with keep_pre = 1
 cudaError_t launch_attn_keep_bits(int B, int H, int J, int K, const PhiloxKey& pk,
                                   int64_t batch_offset, uint32_t* keep_bits, cudaStream_t st);
+// QK^T + BSB + A.V in one tcgen05 kernel (R30): P, keep words, C and C's low word
+bool attn_fused_av_supported(int J, int P);
+cudaError_t launch_attn_qk_bsb_av(int B, int H, int J, int P, float scale, const void* Q,
+                                  int64_t ldq, const void* Kt, int64_t ldk, const void* V,
+                                  int64_t ldv, const float* mask_bias, const PhiloxKey& pk,
+                                  int64_t batch_offset, void* Pout, uint32_t* keep_bits,
+                                  void* C, void* C_lo, int64_t ldc, cudaStream_t st,
+                                  int causal);
 cudaError_t launch_attn_da_bsbb(int B, int H, int J, int P, float scale, const void* dC,
                                 int64_t lddc, const void* V, int64_t ldv, const void* Pin,
                                 const PhiloxKey& pk, int64_t batch_offset,

@@ -130,7 +130,8 @@ def enc_set_option(ctx, key, value):
 (OPT_ATTN_TC, OPT_ATTN_FUSED, OPT_GEMM_LT, OPT_GEMM_AUTOTUNE, OPT_ATTN_BH, OPT_QKV_DIRECT,
  OPT_BWD_SIDE, OPT_ATTN_OVERLAP, OPT_GEMM_TC, OPT_GEMM_PAIR, OPT_GEMM_TC_MASK,
  OPT_KEEP_AHEAD, OPT_QKV_FUSION, OPT_QKV_FUSION_BWD, OPT_BDRLN_VARIANT, OPT_ATTN_DC,
- OPT_MASK_BYTES, OPT_PDL, OPT_AV_KEEP_GEN, OPT_MASK_AHEAD, OPT_SIDE_OPS) = range(21)
+ OPT_MASK_BYTES, OPT_PDL, OPT_AV_KEEP_GEN, OPT_MASK_AHEAD, OPT_SIDE_OPS,
+ OPT_ATTN_FUSED_AV) = range(22)
 QKV_SEPARATE, QKV_QK_STACKED, QKV_STACKED, QKV_KV_STACKED = range(4)
 
 

@@ -488,3 +488,45 @@ def test_av_keep_gen_option_bitwise(dims, causal):
         out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu(), layer.saved.cpu()))
     for a, b in zip(out[0], out[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("opts", [{21: 1}, {21: 0}])
+def test_layer_fused_av_stagewise(opts):
+    """ENC_OPT_ATTN_FUSED_AV (R30): QK^T + BSB + A.V in one kernel -- every stage
+    (P, keep words, C, ...) against the oracle fed the GPU's stored inputs, both settings."""
+    pairs, f32 = _stagewise(Dims(B=2, J=512, H=4, P=64, U=512), "bf16", "gelu", True,
+                            opts=opts, weight_std=0.06)
+    for n, g, o in pairs + f32:
+        assert_parity(n, g, o, "bf16")
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_layer_fused_av_matches_two_kernels(causal):
+    """The fused score + A.V kernel gives the two-kernel path's P and keep words bitwise, and
+    C / the gradients within bf16 accumulation-order noise."""
+    from paper_2007_00072_b200 import ops
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    dims = Dims(B=2, J=512, H=4, P=64, U=1024)
+    prm = make_params(dims, "bf16", "parity", weight_std=0.05)
+    inp = make_inputs(dims, "bf16", key_padding=True)
+    X = torch.tensor(inp["X"], device="cuda").to(torch.bfloat16)
+    dY = torch.tensor(inp["dY"], device="cuda").to(torch.bfloat16)
+    M = torch.tensor(inp["mask_bias"], device="cuda")
+    out = []
+    for fav in (0, 1):
+        layer = EncoderLayer(dims, "bf16", LayerCfg(causal=causal))
+        ops.enc_set_option(layer.ctx, ops.OPT_ATTN_FUSED_AV, fav)
+        layer.set_params(prm)
+        Y = layer.forward(X, M).clone()
+        dX = layer.backward(X, dY).clone()
+        torch.cuda.synchronize()
+        views = layer.saved_views()
+        out.append((Y.float().cpu(), dX.float().cpu(), layer.grad_flat.cpu(),
+                    views["P"].cpu(), views["keep_attn"].cpu(), views["C"].float().cpu()))
+    assert torch.equal(out[0][3], out[1][3])   # P
+    assert torch.equal(out[0][4], out[1][4])   # keep words
+    for i, name in ((0, "Y"), (1, "dX"), (2, "grads"), (5, "C")):
+        a, b = out[0][i], out[1][i]
+        err = (a - b).abs().max().item()
+        scale = a.abs().max().item()
+        assert err <= 2e-2 * scale + 1e-6, (name, err, scale)
