@@ -143,6 +143,10 @@ _SIGS = {
     "enc_attn_bwd_fused": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                    c_void_p, c_void_p, c_float, c_uint64, c_uint64, c_int64,
                                    c_void_p, c_void_p, c_void_p]),
+    "enc_attn_fwd_fused_av": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_float, c_uint64, c_uint64,
+                                      c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                                      c_void_p]),
     "enc_attn_bwd_fused_dc": (c_int, [c_void_p, c_int, c_int, c_int, c_int, c_float, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_float, c_uint64,
                                       c_uint64, c_int64, c_void_p, c_void_p, c_void_p]),

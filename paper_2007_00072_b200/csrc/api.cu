@@ -906,6 +906,26 @@ int enc_attn_bwd_fused(enc_ctx* ctx, int B, int H, int J, int P, float scale, co
   return ENC_OK;
 }
 
+int enc_attn_fwd_fused_av(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* Q,
+                          const void* Kt, const void* V, const float* mask_bias, float p,
+                          uint64_t seed, uint64_t subseq, int64_t batch_offset, void* Pout,
+                          uint32_t* keep_bits, void* C, void* C_lo, int causal,
+                          enc_stream_t stream) {
+  if (!ctx) return ENC_ENULL;
+  if (B < 0 || H <= 0 || !valid_p(p) || batch_offset < 0) return ENC_EINVAL;
+  if (!attn_fused_av_supported(J, P)) return ENC_EUNSUPPORTED;
+  CHECK_PTRS(Q, Kt, V, Pout, C, C_lo);
+  if (!keep_bits) return ENC_ENULL;
+  if (mask_bias && !aligned16(mask_bias)) return ENC_EALIGN;
+  if ((uintptr_t)keep_bits & 7u) return ENC_EALIGN;
+  if (B == 0) return ENC_OK;
+  OpTimer _t(ctx, ENC_OP_BSB_FWD, (cudaStream_t)stream, 1);
+  CK(launch_attn_qk_bsb_av(B, H, J, P, scale, Q, P, Kt, P, V, P, mask_bias,
+                           make_philox_key(p, seed, subseq), batch_offset, Pout, keep_bits, C,
+                           C_lo, (int64_t)H * P, (cudaStream_t)stream, causal ? 1 : 0));
+  return ENC_OK;
+}
+
 int enc_attn_bwd_fused_dc(enc_ctx* ctx, int B, int H, int J, int P, float scale, const void* dC,
                           const void* V, const void* Pin, const void* C_hi, const void* C_lo,
                           float p, uint64_t seed, uint64_t subseq, int64_t batch_offset,

@@ -672,6 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
     const uint32_t ph = it & 1;
+    TRACE(0);
     if (leader) {
       // score MMA once the previous tile's C left TMEM and this tile's Q, K landed
       if (it > 0) mbar_wait(c_done, ph ^ 1);
@@ -708,8 +709,10 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     }
     __stcs(reinterpret_cast<uint2*>(prm.keep_bits + rowi * (kK / 32) + cb / 32),
            make_uint2(kf[0], kf[1]));
+    TRACE(1);
     mbar_wait_sleep(tm_full, ph);
     tc::fence_after_sync();
+    TRACE(2);
     float v[32];
     // pass 1 (as fused_body): sub-chunk max, e = 2^(y - m_c) back into TMEM, sub-chunk sum
     constexpr int kSub = kMask ? 16 : 32;
@@ -769,6 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     st[slice * kRows + r] = make_float2(mt, lt);
     tc::tmem_wait_st();
     qbar(q);
+    TRACE(3);
     float M = st[r].x;
 #pragma unroll
     for (int s2 = 1; s2 < kSlices; ++s2) M = fmaxf(M, st[s2 * kRows + r].x);
@@ -801,6 +805,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     }
     tc::fence_before_sync();
     __syncwarp();
+    TRACE(4);
     if (lane == 0) mbar_arrive(s_read);   // this warp's S columns are consumed
     fence_proxy_async_smem();
     __syncwarp();
@@ -832,6 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     tc::fence_before_sync();
     __syncwarp();
     if (lane == 0) mbar_arrive(a_ready);
+    TRACE(5);
     if (warp < 16) {   // the next K lands in these warps' staging
       if (lane == 0) {
         tc::bulk_wait_read<0>();
@@ -894,6 +900,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
         tc::bulk_commit();
       }
     }
+    TRACE(6);
   }
   if (lane == 0) tc::bulk_wait<0>();
   tc::fence_before_sync();

@@ -149,6 +149,13 @@ def enc_attn_bwd_fused(ctx, B, H, J, P, scale, dC, V, Pin, p, seed, subseq, batc
         _p(keep_bits), _p(dS), _stream(stream)))
 
 
+def enc_attn_fwd_fused_av(ctx, B, H, J, P, scale, Q, K, V, mask_bias, p, seed, subseq,
+                          batch_offset, Pout, keep_bits, C, C_lo, stream=None, causal=False):
+    check("enc_attn_fwd_fused_av", _abi.load().enc_attn_fwd_fused_av(
+        ctx.ptr, B, H, J, P, scale, _p(Q), _p(K), _p(V), _p(mask_bias), p, seed, subseq,
+        batch_offset, _p(Pout), _p(keep_bits), _p(C), _p(C_lo), int(causal), _stream(stream)))
+
+
 def enc_attn_bwd_fused_dc(ctx, B, H, J, P, scale, dC, V, Pin, C_hi, C_lo, p, seed, subseq,
                           batch_offset, dS, keep_bits=None, stream=None):
     check("enc_attn_bwd_fused_dc", _abi.load().enc_attn_bwd_fused_dc(

@@ -147,6 +147,47 @@ def test_fused_backward_dc(ops, ctx, B, H, J, p, stored):
     assert_parity("dS", g, dSo, "bf16")
 
 
+@pytest.mark.parametrize("B,H", [(1, 1), (2, 3), (8, 16)])
+@pytest.mark.parametrize("p", [0.1, 0.0, 0.6])
+@pytest.mark.parametrize("masked,causal", [(False, False), (True, False), (False, True)])
+def test_fused_forward_av(ops, ctx, B, H, p, masked, causal):
+    """enc_attn_fwd_fused_av (R30): one kernel for S = Q K^T, BSB and C = A V --
+    P and C match the oracle (BSB then dropout(P) V in fp64), the keep words are exactly the
+    oracle's mask, and C_lo is C's rounding residual (C_hi + C_lo is the fp32 result)."""
+    J, P = 512, 64
+    Q = make_tensor((B, H, J, P), 51, "bf16", std=0.8)
+    K = make_tensor((B, H, J, P), 52, "bf16", std=0.8)
+    V = make_tensor((B, H, J, P), 53, "bf16")
+    M = None
+    if masked:
+        M = np.zeros((B, J), np.float32)
+        M[:, J - 48:] = -10000.0
+    boff, sub, scale = 3, 4, 0.125
+    Pm = torch.full((B, H, J, J), float("nan"), dtype=torch.bfloat16, device="cuda")
+    bits = torch.full((B, H, J, J // 32), -1, dtype=torch.int32, device="cuda")
+    C = torch.full((B, J, H, P), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Clo = torch.full_like(C, float("nan"))
+    Mt = None if M is None else torch.tensor(M, device="cuda")
+    ops.enc_attn_fwd_fused_av(ctx, B, H, J, P, scale, dev(Q), dev(K), dev(V), Mt, p, SEED, sub,
+                              boff, Pm, bits, C, Clo, causal=causal)
+    torch.cuda.synchronize()
+    S = Q.astype(np.float64) @ K.astype(np.float64).transpose(0, 1, 3, 2)
+    Po, _ = E.bsb_fwd(S, M, scale, p, SEED, sub, boff, causal=causal)
+    gP = host(Pm)
+    assert np.isfinite(gP).all()
+    assert_parity("P", gP, Po, "bf16")
+    keep = philox.keep_mask_tensor((B, H, J, J), boff, p, SEED, sub)
+    assert np.array_equal(decode(bits.cpu().numpy(), J), keep)
+    # C stage by stage: from the GPU's own P (the contraction's inputs as stored; the
+    # end-to-end path from S is covered by the layer tests)
+    Cg = host(C).transpose(0, 2, 1, 3)
+    A_gpu = gP * keep.astype(np.float64) * philox.dropout_scale(p)
+    assert_parity("C(gpu P)", Cg, A_gpu @ V.astype(np.float64), "bf16")
+    hi_lo = host(C) + host(Clo)
+    exact = (A_gpu @ V.astype(np.float64)).transpose(0, 2, 1, 3)
+    assert np.abs(hi_lo - exact).max() <= 1e-3 * (np.abs(exact).max() + 1e-30)
+
+
 @pytest.mark.parametrize("J,P", [(256, 64), (384, 64), (512, 32), (128, 32), (640, 64)])
 def test_fused_unsupported_shapes(ops, ctx, J, P):
     """The fused kernels hold a whole 512-key score row (or whole 128 x 128 score matrices)

@@ -58,6 +58,9 @@ def main():
         "bwd": (lambda: ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, args.p, seed, 0,
                                                0, dS, keep_bits=bits),
                 2 * x_bytes + 2 * s_bytes + k_bytes),
+        "fwd_av": (lambda: ops.enc_attn_fwd_fused_av(ctx, B, H, J, P, 0.125, Q, K, K, M, args.p,
+                                                     seed, 0, 0, Pm, bits, Cm, Cm),
+                   3 * x_bytes + s_bytes + k_bytes + 2 * x_bytes),
         "bwd_dc": (lambda: ops.enc_attn_bwd_fused_dc(ctx, B, H, J, P, 0.125, dC, K, Pm, Cm, Cm, args.p,
                                                      seed, 0, 0, dS, keep_bits=bits),
                    4 * x_bytes + 2 * s_bytes + k_bytes),

@@ -20,6 +20,7 @@ sys.path.insert(0, ROOT)
 
 FWD = ["philox", "mma_wait", "pass1", "qbar", "pass2+store", "next"]
 BWD = ["bits", "mma_wait", "p_wait", "pass1", "qbar", "pass2", "store+load", "next"]
+FAV = ["flags", "mma_wait", "pass1", "pass2", "A_write", "av/C", "next"]
 
 
 def build():
@@ -89,11 +90,19 @@ def run():
         ops.enc_attn_fwd_fused(ctx, B, H, J, P, 0.125, Q, K, None, 0.1, 2007000072, 0, 0, Pm, None,
                                keep_bits=bits)
 
+    V = torch.randn((B, H, J, P), device=dev, generator=g).to(bf)
+    Cm = torch.empty((B, J, H, P), device=dev, dtype=bf)
+    Clo = torch.empty_like(Cm)
+
+    def fav():
+        ops.enc_attn_fwd_fused_av(ctx, B, H, J, P, 0.125, Q, K, V, None, 0.1, 2007000072, 0, 0,
+                                  Pm, bits, Cm, Clo)
+
     def bwd():
         ops.enc_attn_bwd_fused(ctx, B, H, J, P, 0.125, dC, K, Pm, 0.1, 2007000072, 0, 0, dS,
                                keep_bits=bits)
 
-    for name, fn, labels in (("fwd", fwd, FWD), ("bwd", bwd, BWD)):
+    for name, fn, labels in (("fwd", fwd, FWD), ("fwd_av", fav, FAV), ("bwd", bwd, BWD)):
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
