@@ -363,9 +363,16 @@ def main():
     set_opt(6, int(args.bwd_side))
     set_opt(7, int(args.attn_overlap))
     tc_path = args.attn_backend in ("fused", "tc") and args.dtype == "bf16"
-    fused = tally.fused_bytes(dims, es, fused_attn=(args.attn_backend == "fused"
-                                                    and args.dtype == "bf16"),
-                              direct=tc_path and not args.no_qkv_direct)
+    # which kernels run (layer defaults; --opt overrides): A not stored with dropout on load,
+    # A.V inside the score kernel (R30) and the BSB-bwd row term from C (R26) at J = 512
+    opts = dict(tuple(int(x) for x in kv.split("=")) for kv in args.opt)
+    fa = args.attn_backend == "fused" and args.dtype == "bf16"
+    on_load = fa and not args.no_attn_bh
+    j512 = dims.J == 512 and dims.P == 64
+    dc = on_load and j512 and opts.get(15, 1) != 0
+    fused = tally.fused_bytes(dims, es, fused_attn=fa, direct=tc_path and not args.no_qkv_direct,
+                              a_stored=not on_load, dc_term=dc,
+                              fused_av=dc and opts.get(21, 1) != 0)
     flops = tally.gemm_flops(dims)
     dominant = max(per_op, key=per_op.get)
     dom_id = names.index(dominant)

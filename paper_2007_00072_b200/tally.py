@@ -15,20 +15,25 @@ def _d(d):
 
 
 def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = False,
-                direct: bool = False) -> dict:
+                direct: bool = False, a_stored: bool = True, fused_av: bool = False,
+                dc_term: bool = False) -> dict:
     """Algorithmic HBM bytes per launch of each fused operator (es = activation bytes).
     fused_attn: BSB / BSB-bwd run fused with their contraction (QK^T + BSB reads Q, K and
-    writes P, A and the keep bits; dC V^T + BSB-bwd reads dC, V, P and the keep bits and
-    writes dS).  direct: AIB / AIB-bwd are fused into the QKV contraction epilogue and the
-    attention kernels (no separate pass: 0 bytes).  BAD-fwd reads Y1 and writes A1 (the
-    activation input is recomputed by BAD-bwd from Y1 + b1)."""
+    writes P, the keep bits and -- a_stored -- A; dC V^T + BSB-bwd reads dC, V, P and the keep
+    bits and writes dS).  fused_av (R30): the score kernel also reads V and writes C and its
+    low word (the A.V launch disappears).  dc_term (R26): BSB-bwd also reads C_hi and C_lo.
+    direct: AIB / AIB-bwd are fused into the QKV contraction epilogue and the attention
+    kernels (no separate pass: 0 bytes).  BAD-fwd reads Y1 and writes A1."""
     B, J, H, P, I, U = _d(d)
     BJ, BJI, BJU, BHJK = B * J, B * J * I, B * J * U, B * H * J * J
     f = 4  # fp32
     if fused_attn:
         bits = BHJK // 8
-        bsb_f = 2 * BJI * es + 2 * BHJK * es + bits + (B * J * f if mask_bias else 0)
-        bsb_b = 2 * BJI * es + 2 * BHJK * es + bits
+        bsb_f = (2 * BJI * es + (2 if a_stored else 1) * BHJK * es + bits +
+                 (B * J * f if mask_bias else 0))
+        if fused_av:
+            bsb_f += 3 * BJI * es          # V in; C, C_lo out
+        bsb_b = 2 * BJI * es + 2 * BHJK * es + bits + (2 * BJI * es if dc_term else 0)
     else:
         bsb_f = 3 * BHJK * es + (B * J * f if mask_bias else 0)
         bsb_b = 3 * BHJK * es
@@ -49,7 +54,8 @@ def fused_bytes(d, es: int = 2, mask_bias: bool = False, fused_attn: bool = Fals
         # per-(b,h) streaming kernels read the [J x K] matrix once (P + keep words, dropout
         # applied on load; dS for dQ and dK together) and the P-wide operands
         bits = BHJK // 8
-        out["gemm_av"] = BHJK * es + bits + 2 * BJI * es
+        out["gemm_av"] = 0 if fused_av else BHJK * es + bits + 2 * BJI * es + (
+            BJI * es if dc_term else 0)
         out["gemm_av_dv"] = BHJK * es + bits + 2 * BJI * es
         out["gemm_qk_dq"] = BHJK * es + 4 * BJI * es
     return out
@@ -85,7 +91,8 @@ def step_kernel_bytes(d, es: int = 2) -> dict:
     Linear1 + BAD and Linear2-dX + BAD-bwd fused tcgen05 kernels, the other weight
     contractions plain), for the data-movement tally against the paper's Table A.1
     totals (DESIGN.md section 6).  Weights counted once per contraction that reads them;
-    fp32 gradient outputs 4 B; BDRLN / BAD masks regenerated, attention mask as 1-bit words."""
+    fp32 gradient outputs 4 B; attention mask as 1-bit words, (r2b) BDRLN / BAD masks as keep
+    bytes (R27), the score kernel fused with A.V (R30), the BSB-bwd row term from C (R26)."""
     B, J, H, P, I, U = _d(d)
     BJ = B * J
     x, xu, s = BJ * I * es, BJ * U * es, B * H * J * J * es     # [BJ,I], [BJ,U], [B,H,J,K]
@@ -95,24 +102,23 @@ def step_kernel_bytes(d, es: int = 2) -> dict:
     return {
         # forward
         "gemm_qkv+bias": x + wq + 3 * x,
-        "qk_bsb (fused)": 2 * x + s + bits,
-        "av (dropout on load)": s + bits + x + x,
+        "qk_bsb + av (fused, R30)": 3 * x + s + bits + 2 * x,
         "gemm_out": x + wo + x,
-        "bdrln_fwd1": 4 * x + BJ * f,
-        "gemm_l1 + BAD (fused)": x + w1 + 2 * xu,
+        "bdrln_fwd1": 4 * x + BJ * f + BJ * I // 8,
+        "gemm_l1 + BAD (fused)": x + w1 + 2 * xu + BJ * U // 8,
         "gemm_l2": xu + w1 + x,
-        "bdrln_fwd2": 4 * x + BJ * f,
+        "bdrln_fwd2": 4 * x + BJ * f + BJ * I // 8,
         # backward
-        "bdrln_bwd2": 4 * x + BJ * f,
-        "gemm_l2_dx + BAD-bwd (fused)": x + w1 + 2 * xu,
+        "bdrln_bwd2": 4 * x + BJ * f + BJ * I // 8,
+        "gemm_l2_dx + BAD-bwd (fused)": x + w1 + 2 * xu + BJ * U // 8,
         "gemm_l2_dw": x + xu + I * U * f,
         "gemm_l1_dx (+dz2)": xu + w1 + 2 * x,
         "gemm_l1_dw": xu + x + U * I * f,
-        "bdrln_bwd1": 4 * x + BJ * f,
+        "bdrln_bwd1": 4 * x + BJ * f + BJ * I // 8,
         "gemm_out_dx": x + wo + x,
         "gemm_out_dw": 2 * x + I * I * f,
         "dv (dropout on load)": s + bits + x + x,
-        "da_bsb_bwd (fused)": 2 * x + s + bits + s,
+        "da_bsb_bwd (fused, row term from C)": 2 * x + s + bits + s + 2 * x,
         "dq+dk": s + 2 * x + 2 * x,
         "gemm_qkv_dx (+dz1)": 3 * x + wq + 2 * x,
         "gemm_qkv_dw": 3 * x + x + 3 * I * I * f,
