@@ -73,7 +73,7 @@ struct enc_ctx {
   cudaEvent_t ev_fork2 = nullptr, ev_join2 = nullptr;
   // the FFN keep bytes drawn ahead beside the fused score kernel (R29)
   cudaEvent_t ev_mk_fork = nullptr, ev_mk_join = nullptr;
-  int mask_ahead = 0;      // ENC_OPT_MASK_AHEAD (measured +7 us at L: off)
+  int mask_ahead = 1;      // ENC_OPT_MASK_AHEAD (FFN bytes on the fused kernel's spare SMs, R31)
   // ENC_OPT_SIDE_OPS (dW contractions on the side stream): Out-dW beside the fused BSB-bwd /
   // dQdK stretch (measured -2..-6 us at L); the others measured neutral or slower
   uint32_t side_ops = 1u << ENC_OP_GEMM_OUT_DW;
@@ -1026,7 +1026,8 @@ int enc_set_option(enc_ctx* ctx, int key, int value) {
     return ENC_OK;
   }
   if (key == ENC_OPT_MASK_AHEAD) {
-    ctx->mask_ahead = value ? 1 : 0;
+    if (value < 0 || value > 2) return ENC_EINVAL;
+    ctx->mask_ahead = value;   // 2: the BDRLN sites' bytes too
     return ENC_OK;
   }
   if (key == ENC_OPT_AV_KEEP_GEN) {
@@ -1256,14 +1257,35 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // ready together with the fused score kernel (launched at high priority): its CTAs take the
   // SMs the score kernel's last wave leaves idle; Linear1 + BAD then reads the bytes
   const PhiloxKey pk_ffn = make_philox_key(cfg->p_ffn, cfg->seed, l4 + 2);
+  // (without the fused score + A.V kernel's spare SMs the side kernel measured slower: R29)
+  const int spare_sms = ctx->num_sms - balanced_grid((J / 128) * B * H);
   const bool mask_ahead = ctx->mask_ahead && fused_attn && ctx->side &&
-                          bad_bytes_of(ctx, d, dtype) && ((size_t)BJ * (U / 8)) % 4 == 0;
+                          bad_bytes_of(ctx, d, dtype) && ((size_t)BJ * (U / 8)) % 4 == 0 &&
+                          ctx->attn_fused_av && attn_fused_av_supported(J, P) && spare_sms > 0 &&
+                          dc_term_of(ctx, fused_attn, J, P) && use_bh(ctx, J, P) &&
+                          !ctx->keep_ahead && !ctx->av_keep_gen;
+  // R31: beside the fused score + A.V kernel, launched on a balanced grid (512 tiles: 128
+  // CTAs x 4), the keep bytes of the FFN site and of both BDRLN sites are drawn by 1024-thread
+  // CTAs on the SMs it leaves free (its CTAs hold every register of theirs, so the two never
+  // share an SM)
+  const bool spare_ahead = mask_ahead && ((size_t)BJ * (I / 8)) % 4 == 0;
+  const bool ln_ahead = spare_ahead && ctx->mask_ahead == 2;   // BDRLN sites too
   if (mask_ahead) {
     CK(cudaEventRecord(ctx->ev_mk_fork, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_mk_fork, 0));
+    const int cap = spare_ahead ? spare_sms : 0;
     CK(launch_keep_bytes((int64_t)BJ * (U / 8), boff * (int64_t)J * (U / 8), pk_ffn,
-                         (uint8_t*)at(saved, SL.off[S_KBF]), ctx->side));
+                         (uint8_t*)at(saved, SL.off[S_KBF]), ctx->side, cap));
     ctx->launches += 1;
+    if (spare_ahead && ctx->mask_ahead == 2) {   // (measured: does not fit the window)
+      for (int site = 0; site < 2; ++site) {
+        CK(launch_keep_bytes((int64_t)BJ * (I / 8), boff * (int64_t)J * (I / 8),
+                             make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1 + 2 * site),
+                             (uint8_t*)at(saved, SL.off[site ? S_KB2 : S_KB1]), ctx->side,
+                             cap));
+        ctx->launches += 1;
+      }
+    }
     CK(cudaEventRecord(ctx->ev_mk_join, ctx->side));
   }
   // fused + per-(b, h) path: A = dropout(P) is never stored -- the A V (and backward
@@ -1337,10 +1359,13 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
   // BDRLN site 1 (:555-558)
   {
     OpTimer _t(ctx, ENC_OP_BDRLN_FWD1, st, 1);
+    if (ln_ahead) CK(cudaStreamWaitEvent(st, ctx->ev_mk_join, 0));
     CK(launch_bdrln_fwd(dtype, B, J, I, Yo, prm->bo, X, prm->g1, prm->be1, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 1), boff, X1, xh1, r1, st,
                         ctx->bdrln_variant & 15,
-                        ctx->mask_bytes ? (uint8_t*)at(saved, SL.off[S_KB1]) : nullptr));
+                        ctx->mask_bytes && !ln_ahead ? (uint8_t*)at(saved, SL.off[S_KB1])
+                                                     : nullptr,
+                        ln_ahead ? (const uint8_t*)at(saved, SL.off[S_KB1]) : nullptr));
   }
   // Linear (:559) + BAD (:560-562).  The activation input h = X1 W1^T + b1 is kept for the
   // backward (saved.h); on the tcgen05 path BAD runs in the contraction's epilogue
@@ -1377,7 +1402,9 @@ int encoder_layer_forward(enc_ctx* ctx, const enc_dims* d, int dtype, const enc_
     CK(launch_bdrln_fwd(dtype, B, J, I, Y2, prm->b2, X1, prm->g2, prm->be2, cfg->ln_eps,
                         make_philox_key(cfg->p_hidden, cfg->seed, l4 + 3), boff, Y, xh2, r2, st,
                         (ctx->bdrln_variant >> 4) & 15,
-                        ctx->mask_bytes ? (uint8_t*)at(saved, SL.off[S_KB2]) : nullptr));
+                        ctx->mask_bytes && !ln_ahead ? (uint8_t*)at(saved, SL.off[S_KB2])
+                                                     : nullptr,
+                        ln_ahead ? (const uint8_t*)at(saved, SL.off[S_KB2]) : nullptr));
   }
   {
     std::lock_guard<std::mutex> lk(ctx->mu);

@@ -956,6 +956,18 @@ int persistent_grid(int tiles) {
   if (sms <= 0) sms = 148;
   return tiles < sms ? tiles : sms;
 }
+}  // namespace
+
+// the fewest CTAs that still finish `tiles` in the same number of waves as one CTA per SM
+// (512 tiles on 148 SMs: 128 CTAs x 4 tiles -- the 20 SMs left over take side work, R31)
+int balanced_grid(int tiles) {
+  const int sms = persistent_grid(1 << 30);
+  if (tiles <= 0) return 1;
+  const int waves = (tiles + sms - 1) / sms;
+  return (tiles + waves - 1) / waves;
+}
+
+namespace {
 
 template <typename Kern>
 cudaError_t launch_persistent(Kern kern, int tiles, const CUtensorMap& a, const CUtensorMap& b,
@@ -1112,7 +1124,7 @@ cudaError_t launch_attn_qk_bsb_av(int B, int H, int J, int P, float scale, const
                   mask_bias, keep_bits, 0, 0};
   auto go = [&](auto kern) -> cudaError_t {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kAvSmem);
-    return launch_k(PDL_ATTN_FUSED, kern, persistent_grid(tiles), kThreads, kAvSmem, st, mq, mk,
+    return launch_k(PDL_ATTN_FUSED, kern, balanced_grid(tiles), kThreads, kAvSmem, st, mq, mk,
                     mv, mp, mc, ml, prm, pk);
   };
   if (causal)

@@ -159,7 +159,8 @@ cudaError_t launch_bdrln_bwd_rg(int dtype, int B, int J, int I, const void* dOut
 
 // keep bytes of a whole dropout site (R27 layout) from Philox chunk g0 (nchunks % 4 == 0)
 cudaError_t launch_keep_bytes(int64_t nchunks, int64_t g0, const PhiloxKey& pk, uint8_t* out,
-                              cudaStream_t st);
+                              cudaStream_t st, int max_ctas = 0);
+int balanced_grid(int tiles);   // persistent CTAs for `tiles` in the fewest waves (attn_fused.cu)
 cudaError_t launch_bad_fwd(int dtype, int B, int J, int U, const void* Y1, const float* b1,
                            int act, const PhiloxKey& pk, int64_t batch_offset, void* h,
                            void* A1, cudaStream_t st);

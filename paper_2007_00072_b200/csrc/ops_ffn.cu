@@ -211,7 +211,7 @@ cudaError_t launch_bei(int dtype, int64_t n, const void* a, const void* b, void*
 // thread (one 32-bit word of bytes).  The layer launches it for the BAD site on a side stream
 // beside the fused score kernel, whose last wave leaves SMs idle (R29); the Linear1
 // + BAD epilogue then reads the bytes instead of running Philox.
-__global__ void __launch_bounds__(256) keep_bytes_kernel(uint32_t* __restrict__ out,
+__global__ void __launch_bounds__(1024) keep_bytes_kernel(uint32_t* __restrict__ out,
                                                          int64_t nwords, int64_t g0,
                                                          PhiloxKey pk) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nwords;
@@ -225,16 +225,20 @@ __global__ void __launch_bounds__(256) keep_bytes_kernel(uint32_t* __restrict__ 
 }
 
 cudaError_t launch_keep_bytes(int64_t nchunks, int64_t g0, const PhiloxKey& pk, uint8_t* out,
-                              cudaStream_t st) {
+                              cudaStream_t st, int max_ctas) {
   if (nchunks <= 0) return cudaSuccess;
   if (nchunks % 4 || ((uintptr_t)out & 3u)) return cudaErrorInvalidValue;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nwords = nchunks / 4;
-  int64_t grid = (nwords + 255) / 256;
-  if (grid > 4 * sms) grid = 4 * sms;
-  keep_bytes_kernel<<<(int)grid, 256, 0, st>>>(reinterpret_cast<uint32_t*>(out), nwords, g0, pk);
+  // 1024-thread CTAs: with max_ctas (the SMs a persistent kernel beside it leaves free) one
+  // per free SM, else up to two per SM
+  int64_t grid = (nwords + 1023) / 1024;
+  const int64_t cap = max_ctas > 0 ? max_ctas : 2 * sms;
+  if (grid > cap) grid = cap;
+  keep_bytes_kernel<<<(int)grid, 1024, 0, st>>>(reinterpret_cast<uint32_t*>(out), nwords, g0,
+                                                pk);
   return cudaGetLastError();
 }
 

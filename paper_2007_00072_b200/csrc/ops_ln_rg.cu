@@ -88,6 +88,12 @@ bdrln_fwd_rg_kernel(
   int k = 0;
   for (int row = first; row < rows; row += stride, ++k) {
     const int s = k % STG;
+    uint32_t kb[CPW];   // given keep bytes (R31), loaded before the row's data wait
+#pragma unroll
+    for (int i = 0; i < CPW; ++i)
+      kb[i] = (kb_in != nullptr && lane + 32 * i < ncq)
+                  ? (uint32_t)__ldg(kb_in + (int64_t)row * nc + w * ncq + lane + 32 * i)
+                  : 0u;
     mbar_wait(&bar[s], (uint32_t)(k / STG) & 1u);
     const T* sy = ring_row<T, 2, STG>(smem, I, g, s, 0);
     const T* sr = ring_row<T, 2, STG>(smem, I, g, s, 1);
@@ -101,7 +107,10 @@ bdrln_fwd_rg_kernel(
         float y[8], m[8];
         C::unpack(C::ld_smem(sy + ch * 8), y);
         C::unpack(C::ld_smem(sr + ch * 8), z[i]);
-        keep_mul8_io(g0, (int64_t)row * nc + ch, pk, kb_out, kb_in, m);
+        if (kb_in != nullptr)
+          mul8_from_byte(kb[i], pk.scale, m);
+        else
+          keep_mul8_io(g0, (int64_t)row * nc + ch, pk, kb_out, nullptr, m);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           z[i][j] = fmaf(y[j] + pb[i][j], m[j], z[i][j]);

@@ -444,7 +444,7 @@ def test_mask_bytes_option_bitwise(dtype, dims, variant):
     dY = torch.tensor(inp["dY"], device="cuda").to(tdt)
     M = torch.tensor(inp["mask_bias"], device="cuda")
     out = []
-    for mb, ahead in ((0, 0), (1, 0), (1, 1)):   # (1, 1): FFN bytes drawn ahead (R29)
+    for mb, ahead in ((0, 0), (1, 0), (1, 1)):   # (1, 1): bytes drawn ahead (R29 / R31)
         layer = EncoderLayer(dims, dtype, LayerCfg())
         ops.enc_set_option(layer.ctx, ops.OPT_MASK_BYTES, mb)
         ops.enc_set_option(layer.ctx, ops.OPT_MASK_AHEAD, ahead)
