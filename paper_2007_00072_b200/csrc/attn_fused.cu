@@ -862,14 +862,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
         mbar_wait(op_empty, ph);
         mbar_wait(stg_free, ph);
         load_qk(t + gridDim.x);
-        mbar_wait(c_full, ph);
-        load_v(t + gridDim.x);
       }
     }
     if (warp >= 24) {
       // C (x dropout scale) or its low bf16 word, [32 rows x 64] per warp
       mbar_wait_sleep(c_full, ph);
       tc::fence_after_sync();
+      // the V slot is free once the A.V MMA completed: the next tile's V, issued here so
+      // the MMA-issuing warp does not wait for it
+      if (warp == 24 && lane == 0 && t + (int)gridDim.x < prm.tiles) load_v(t + gridDim.x);
       if (lane == 0) tc::bulk_wait_read<0>();   // this warp's P store has read the staging
       __syncwarp();
       const bool lo = warp >= 28;
