@@ -200,6 +200,11 @@ def attention_desc(args, dims) -> str:
     backend = args.attn_backend
     if backend == "fused" and not (dims.J in (128, 512) and dims.P == 64 and args.dtype == "bf16"):
         backend = "tc" if args.dtype == "bf16" else "cublas"   # what the library selects
+    opts = dict(tuple(int(x) for x in kv.split("=")) for kv in args.opt)
+    if backend == "fused" and dims.J == 512 and opts.get(21, 1) and opts.get(15, 1):
+        return ("fused tcgen05 QK^T+BSB+A.V (S in TMEM, A = keep*P written over it as the A.V "
+                "operand) / dC.V^T+BSB-bwd (dA in TMEM, row term from C), dropout on load in "
+                "A^T.dC, dS.K + dS^T.Q per (b,h)")
     return {"fused": "fused tcgen05 QK^T+BSB / dA+BSB-bwd (S, dA in TMEM), dropout on load in "
                      "the per-(b,h) A.V / A^T.dC contractions",
             "tc": "tcgen05 QK^T / dA contractions + separate BSB kernels, per-(b,h) A.V, "
@@ -670,7 +675,8 @@ def main():
                        else f"CUDA graph replay (fwd+bwd, {len(parts)} graph(s) per step)",
                        "attention": attention_desc(args, dims),
                        "weight_contractions": gemm_desc(args),
-                       "bwd_side_stream": bool(args.bwd_side),
+                       "bwd_side_stream": {0: "none", 1: "dW", 2: "dW + finalize",
+                                           3: "finalize"}.get(args.bwd_side, args.bwd_side),
                        "options": args.opt or None},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "wall_s_timed_region": t_wall,
