@@ -530,3 +530,48 @@ def test_layer_fused_av_matches_two_kernels(causal):
         err = (a - b).abs().max().item()
         scale = a.abs().max().item()
         assert err <= 2e-2 * scale + 1e-6, (name, err, scale)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_pdl_mask_bitwise(graph):
+    """ENC_OPT_PDL (programmatic dependent launch) changes only when kernels start: with it
+    off, at the default mask and with every class on, Y, dX, every gradient and the saved
+    tensors are bitwise equal -- a kernel that read its predecessor's output before
+    griddepcontrol.wait would show up here as a difference."""
+    from paper_2007_00072_b200 import ops
+    from paper_2007_00072_b200.layer import EncoderLayer, LayerCfg
+    dims = Dims(B=2, J=512, H=4, P=64, U=1024)
+    prm = make_params(dims, "bf16", "parity", weight_std=0.05)
+    inp = make_inputs(dims, "bf16", key_padding=True)
+    X = torch.tensor(inp["X"], device="cuda").to(torch.bfloat16)
+    dY = torch.tensor(inp["dY"], device="cuda").to(torch.bfloat16)
+    M = torch.tensor(inp["mask_bias"], device="cuda")
+    out = []
+    layer = EncoderLayer(dims, "bf16", LayerCfg())
+    layer.set_params(prm)
+    try:
+        for mask in (0, 13, 31):
+            ops.enc_set_option(layer.ctx, ops.OPT_PDL, mask)
+            layer.saved.zero_()
+            layer.grad_flat.zero_()
+            if graph:
+                Y, dX = torch.empty_like(X), torch.empty_like(X)
+                layer.forward(X, M, Y)
+                layer.backward(X, dY, dX)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    layer.forward(X, M, Y)
+                    layer.backward(X, dY, dX)
+                layer.saved.zero_()
+                layer.grad_flat.zero_()
+                g.replay()
+            else:
+                Y = layer.forward(X, M).clone()
+                dX = layer.backward(X, dY).clone()
+            torch.cuda.synchronize()
+            out.append((Y.cpu(), dX.cpu(), layer.grad_flat.cpu(), layer.saved.cpu()))
+    finally:
+        ops.enc_set_option(layer.ctx, ops.OPT_PDL, 13)
+    for other in out[1:]:
+        for a, b in zip(out[0], other):
+            assert torch.equal(a, b)
