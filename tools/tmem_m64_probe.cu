@@ -45,7 +45,10 @@ __global__ void probe(float* out, int second_at_lane64) {
     for (int k = 0; k < 4; ++k)
       tc::mma_bf16(tmem, tc::smem_desc(smem_u32(A0) + k * 32, 16, 1024),
                    tc::smem_desc(smem_u32(Bm) + k * 32, 16, 1024), idesc, k != 0);
-    const uint32_t d2 = second_at_lane64 ? tmem + (64u << 16) : tmem + 256;
+    // mode 0: second D at column 256; 1: at lane 64; 2: at lane 16 (same columns)
+    const uint32_t d2 = second_at_lane64 == 1   ? tmem + (64u << 16)
+                        : second_at_lane64 == 2 ? tmem + (16u << 16)
+                                                : tmem + 256;
     for (int k = 0; k < 4; ++k)
       tc::mma_bf16(d2, tc::smem_desc(smem_u32(A1) + k * 32, 16, 1024),
                    tc::smem_desc(smem_u32(Bm) + k * 32, 16, 1024), idesc, k != 0);
@@ -71,13 +74,14 @@ __global__ void probe(float* out, int second_at_lane64) {
 int main() {
   float* d;
   cudaMalloc(&d, 128 * 4 * sizeof(float));
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 3; ++mode) {
     cudaMemset(d, 0, 128 * 4 * sizeof(float));
     probe<<<1, 128>>>(d, mode);
     cudaError_t e = cudaDeviceSynchronize();
     float h[512];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("mode %d (second MMA at %s): %s\n", mode, mode ? "lane 64" : "column 256",
+    printf("mode %d (second MMA at %s): %s\n", mode,
+           mode == 1 ? "lane 64" : mode == 2 ? "lane 16" : "column 256",
            cudaGetErrorString(e));
     for (int t = 0; t < 128; t += 4)
       printf("  lane %3d: col0 %6.1f col1 %6.1f | col256 %6.1f col257 %6.1f   lane %3d: %6.1f %6.1f | %6.1f %6.1f\n",
