@@ -174,21 +174,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_bh_kernel(
           uint32_t y0 = x0 + kXBytes;
           if (p.row_out) {
             // out_r[jt] += X(jt,kt) Yr(kt): X K-major (rows j), Yr MN-major (rows k)
+            const uint64_t xd = tc::smem_desc(x0, 16, 1024), yd = tc::smem_desc(y0, 8192, 1024);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              tc::mma_bf16(tmem + jt * 64,
-                           tc::smem_desc(x0 + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024),
-                           tc::smem_desc(y0 + ks * 2048, 8192, 1024), idesc_r,
-                           (kt | ks) != 0);
+              tc::mma_bf16(tmem + jt * 64, tc::desc_adv(xd, (ks >> 2) * 16384 + (ks & 3) * 32),
+                           tc::desc_adv(yd, ks * 2048), idesc_r, (kt | ks) != 0);
             y0 += kYBytes;
           }
           if (p.col_out) {
             // out_c[kt] += X(jt,kt)^T Yc(jt): X MN-major (M = k), Yc MN-major (rows j)
+            const uint64_t xd = tc::smem_desc(x0, 16384, 1024), yd = tc::smem_desc(y0, 8192, 1024);
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks)
-              tc::mma_bf16(tmem + col_off + kt * 64, tc::smem_desc(x0 + ks * 2048, 16384, 1024),
-                           tc::smem_desc(y0 + ks * 2048, 8192, 1024), idesc_c,
-                           (jt | ks) != 0);
+              tc::mma_bf16(tmem + col_off + kt * 64, tc::desc_adv(xd, ks * 2048),
+                           tc::desc_adv(yd, ks * 2048), idesc_c, (jt | ks) != 0);
           }
           tc::mma_commit(&empty[s]);
           if (i == nt - 1) tc::mma_commit(&tm_full[o]);   // outer tile o complete

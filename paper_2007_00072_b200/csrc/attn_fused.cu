@@ -238,13 +238,14 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
       mbar_wait(op_full, it & 1);
       tc::fence_after_sync();
       constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kRows, 256, false, false);
-      const uint32_t a0 = smem_u32(base + kOpA), b0 = smem_u32(base + kOpB);
+      const uint64_t ad = tc::smem_desc(smem_u32(base + kOpA), 16, 1024);
+      const uint64_t bd = tc::smem_desc(smem_u32(base + kOpB), 16, 1024);
 #pragma unroll
       for (int nh = 0; nh < 2; ++nh)
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          tc::mma_bf16(tmem + nh * 256, tc::smem_desc(a0 + k * 32, 16, 1024),
-                       tc::smem_desc(b0 + nh * 256 * 128 + k * 32, 16, 1024), idesc, k != 0);
+          tc::mma_bf16(tmem + nh * 256, tc::desc_adv(ad, k * 32),
+                       tc::desc_adv(bd, nh * 256 * 128 + k * 32), idesc, k != 0);
       tc::mma_commit(tm_full);
       tc::mma_commit(op_empty);
     }
@@ -673,23 +674,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     tile_coords(t, b, h, m0, bh);
     const uint32_t ph = it & 1;
     TRACE(0);
-    if (leader) {
-      // score MMA once the previous tile's C left TMEM and this tile's Q, K landed
-      if (it > 0) mbar_wait(c_done, ph ^ 1);
-      mbar_wait(op_full, ph);
-      tc::fence_after_sync();
-      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kRows, 256, false, false);
-      const uint32_t a0 = smem_u32(base + kAvQ), b0 = smem_u32(base + kAvX);
-#pragma unroll
-      for (int nh = 0; nh < 2; ++nh)
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tc::mma_bf16(tmem + nh * 256, tc::smem_desc(a0 + k * 32, 16, 1024),
-                       tc::smem_desc(b0 + nh * 256 * 128 + k * 32, 16, 1024), idesc, k != 0);
-      tc::mma_commit(tm_full);
-      tc::mma_commit(op_empty);
-    }
-    __syncwarp();
     // keep flags of this thread's 64 elements (needed: A = keep * P) and the keep words for
     // the backward
     const int64_t rowi = (int64_t)bh * prm.J + m0 + r;
@@ -710,6 +694,26 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     __stcs(reinterpret_cast<uint2*>(prm.keep_bits + rowi * (kK / 32) + cb / 32),
            make_uint2(kf[0], kf[1]));
     TRACE(1);
+    // (the MMA-issuing thread draws its flags first: issued earlier, its warp would enter
+    // pass 1 a flag phase late and hold back its quarter)
+    if (leader) {
+      // score MMA once the previous tile's C left TMEM and this tile's Q, K landed
+      if (it > 0) mbar_wait(c_done, ph ^ 1);
+      mbar_wait(op_full, ph);
+      tc::fence_after_sync();
+      constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kRows, 256, false, false);
+      const uint64_t ad = tc::smem_desc(smem_u32(base + kAvQ), 16, 1024);
+      const uint64_t bd = tc::smem_desc(smem_u32(base + kAvX), 16, 1024);
+#pragma unroll
+      for (int nh = 0; nh < 2; ++nh)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tc::mma_bf16(tmem + nh * 256, tc::desc_adv(ad, k * 32),
+                       tc::desc_adv(bd, nh * 256 * 128 + k * 32), idesc, k != 0);
+      tc::mma_commit(tm_full);
+      tc::mma_commit(op_empty);
+    }
+    __syncwarp();
     mbar_wait_sleep(tm_full, ph);
     tc::fence_after_sync();
     TRACE(2);
@@ -838,6 +842,21 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     __syncwarp();
     if (lane == 0) mbar_arrive(a_ready);
     TRACE(5);
+    if (leader) {
+      // C = A V: 32 k-steps of 16 keys, A from TMEM (8 columns each), V MN-major; issued
+      // before this warp waits for its P store to drain
+      mbar_wait(a_ready, ph);
+      mbar_wait(v_full, ph);
+      tc::fence_after_sync();
+      constexpr uint32_t idesc_av = tc::instr_desc_bf16_f32(kRows, 64, false, true);
+      const uint64_t vd = tc::smem_desc(smem_u32(base + kAvV), 8192, 1024);
+#pragma unroll
+      for (int ks = 0; ks < kK / 16; ++ks)
+        mma_bf16_ts(tmem + 256, tmem + 8 * ks, tc::desc_adv(vd, ks * 2048), idesc_av, ks != 0);
+      tc::mma_commit(c_full);
+      TRACE(7);
+    }
+    __syncwarp();
     if (warp < 16) {   // the next K lands in these warps' staging
       if (lane == 0) {
         tc::bulk_wait_read<0>();
@@ -846,17 +865,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       __syncwarp();
     }
     if (leader) {
-      // C = A V: 32 k-steps of 16 keys, A from TMEM (8 columns each), V MN-major
-      mbar_wait(a_ready, ph);
-      mbar_wait(v_full, ph);
-      tc::fence_after_sync();
-      constexpr uint32_t idesc_av = tc::instr_desc_bf16_f32(kRows, 64, false, true);
-      const uint32_t v0 = smem_u32(base + kAvV);
-#pragma unroll 4
-      for (int ks = 0; ks < kK / 16; ++ks)
-        mma_bf16_ts(tmem + 256, tmem + 8 * ks, tc::smem_desc(v0 + ks * 2048, 8192, 1024),
-                    idesc_av, ks != 0);
-      tc::mma_commit(c_full);
       // next tile's operands: Q + K once warps 0-15's staging is free, V once this MMA is done
       if (t + (int)gridDim.x < prm.tiles) {
         mbar_wait(op_empty, ph);
@@ -868,6 +876,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       // C (x dropout scale) or its low bf16 word, [32 rows x 64] per warp
       mbar_wait_sleep(c_full, ph);
       tc::fence_after_sync();
+      TRACE(7);
       // the V slot is free once the A.V MMA completed: the next tile's V, issued here so
       // the MMA-issuing warp does not wait for it
       if (warp == 24 && lane == 0 && t + (int)gridDim.x < prm.tiles) load_v(t + gridDim.x);

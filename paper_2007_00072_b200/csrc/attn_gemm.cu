@@ -123,15 +123,15 @@ __global__ void __launch_bounds__(kThreads, 1) attn_gemm_kernel(
       mbar_wait(&full[s], (kb / STAGES) & 1);
       tc::fence_after_sync();
       if (lane == 0) {
-        const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+        const uint64_t ad0 = p.a_mn ? tc::smem_desc(smem_u32(sA + s * kABytes), 8192, 1024)
+                                    : tc::smem_desc(smem_u32(sA + s * kABytes), 16, 1024);
+        const uint64_t bd0 = p.b_mn ? tc::smem_desc(smem_u32(sB + s * kBBytes), 8192, 1024)
+                                    : tc::smem_desc(smem_u32(sB + s * kBBytes), 16, 1024);
+        const uint32_t astep = p.a_mn ? 2048 : 32, bstep = p.b_mn ? 2048 : 32;
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {
-          const uint64_t ad = p.a_mn ? tc::smem_desc(a0 + k * 2048, 8192, 1024)
-                                     : tc::smem_desc(a0 + k * 32, 16, 1024);
-          const uint64_t bd = p.b_mn ? tc::smem_desc(b0 + k * 2048, 8192, 1024)
-                                     : tc::smem_desc(b0 + k * 32, 16, 1024);
-          tc::mma_bf16(tmem, ad, bd, idesc, (kb | k) != 0);
-        }
+        for (int k = 0; k < kBK / 16; ++k)
+          tc::mma_bf16(tmem, tc::desc_adv(ad0, k * astep), tc::desc_adv(bd0, k * bstep), idesc,
+                       (kb | k) != 0);
         tc::mma_commit(&empty[s]);
         if (kb == nk - 1) tc::mma_commit(tmem_full);
       }

@@ -138,11 +138,12 @@ __global__ void __launch_bounds__(kFThreads, 1) attn_qk_bsb_short_kernel(
         mbar_wait(&tm_empty[s], ph ^ 1u);
         mbar_wait(&op_full[s], ph);
         tc::fence_after_sync();
-        const uint32_t a0 = smem_u32(base + s * 2 * kOpBytes), b0 = a0 + kOpBytes;
+        const uint64_t ad = tc::smem_desc(smem_u32(base + s * 2 * kOpBytes), 16, 1024);
+        const uint64_t bd = tc::desc_adv(ad, kOpBytes);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          tc::mma_bf16(tmem + s * kS, tc::smem_desc(a0 + k * 32, 16, 1024),
-                       tc::smem_desc(b0 + k * 32, 16, 1024), idesc, k != 0);
+          tc::mma_bf16(tmem + s * kS, tc::desc_adv(ad, k * 32), tc::desc_adv(bd, k * 32), idesc,
+                       k != 0);
         tc::mma_commit(&tm_full[s]);
         tc::mma_commit(&op_empty[s]);
         const int tn = t + kFSlots * (int)gridDim.x;
@@ -350,11 +351,12 @@ __global__ void __launch_bounds__(kBThreads, 1) attn_da_bsbb_short_kernel(
         mbar_wait(&tm_empty[st], ((uint32_t)(i / kBSlots) & 1u) ^ 1u);
         mbar_wait(&op_full[so], (uint32_t)(i / kBOps) & 1u);
         tc::fence_after_sync();
-        const uint32_t a0 = smem_u32(base + kBOpOff + so * 2 * kOpBytes), b0 = a0 + kOpBytes;
+        const uint64_t ad = tc::smem_desc(smem_u32(base + kBOpOff + so * 2 * kOpBytes), 16, 1024);
+        const uint64_t bd = tc::desc_adv(ad, kOpBytes);
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          tc::mma_bf16(tmem + st * kS, tc::smem_desc(a0 + k * 32, 16, 1024),
-                       tc::smem_desc(b0 + k * 32, 16, 1024), idesc, k != 0);
+          tc::mma_bf16(tmem + st * kS, tc::desc_adv(ad, k * 32), tc::desc_adv(bd, k * 32), idesc,
+                       k != 0);
         tc::mma_commit(&tm_full[st]);
         tc::mma_commit(&op_empty[so]);
         if (i + kBOps < ntiles) {   // the stage is free once these MMAs have read it

@@ -33,6 +33,16 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// the descriptor of an operand `bytes` further on: the 14-bit start-address field holds
+// addr >> 4 and shared memory ends below 256 KB, so the addition never carries out of it.
+// Issue loops form the base descriptor once and step it with this (one 64-bit add per MMA
+// instead of rebuilding the fields: the MMA-issuing thread is otherwise the bottleneck of
+// short-N chains -- tools/mma_rate_probe.cu measured ~200 cycles per rebuilt-descriptor
+// MMA against ~55 for the stepped form at N = 64)
+__device__ __forceinline__ uint64_t desc_adv(uint64_t d, uint32_t bytes) {
+  return d + (uint64_t)(bytes >> 4);
+}
+
 __host__ __device__ constexpr uint32_t instr_desc_bf16_f32(int M, int N, bool a_mn_major,
                                                           bool b_mn_major) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn_major ? 1u : 0u) << 15) |

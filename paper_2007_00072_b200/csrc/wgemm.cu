@@ -322,13 +322,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&full[s], (pc / kStages) & 1);
           tc::fence_after_sync();
           if (lane == 0) {
-            const uint32_t a0 = smem_u32(sA + s * kABytes), b0 = smem_u32(sB + s * kBBytes);
+            const uint64_t ad0 = tc::smem_desc(smem_u32(sA + s * kABytes), AMN ? 8192 : 16, 1024);
+            const uint64_t bd0 = tc::smem_desc(smem_u32(sB + s * kBBytes), BMN ? 8192 : 16, 1024);
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t ad = AMN ? tc::smem_desc(a0 + k * 2048, 8192, 1024)
-                                      : tc::smem_desc(a0 + k * 32, 16, 1024);
-              const uint64_t bd = BMN ? tc::smem_desc(b0 + k * 2048, 8192, 1024)
-                                      : tc::smem_desc(b0 + k * 32, 16, 1024);
+              const uint64_t ad = tc::desc_adv(ad0, k * (AMN ? 2048 : 32));
+              const uint64_t bd = tc::desc_adv(bd0, k * (BMN ? 2048 : 32));
               const uint32_t acc = (kb != kb0 || k != 0) ? 1u : 0u;
               if (CG == 2)
                 mma_bf16_pair(dacc, ad, bd, idesc, acc);

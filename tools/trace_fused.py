@@ -56,11 +56,20 @@ def report(name, tr, labels, ntiles_cta):
                         cnt[e] += 1
         line = "  ".join(f"{labels[e]} {sums[e] / max(cnt[e], 1) / 1e3:6.2f}" for e in range(ne))
         print(f"  {wn} mean us per tile: {line}")
+    if ne == 7:   # the fused score + A.V kernel: stamp 7 sits between stamps 5 and 6
+        for w, wn in ((0, "warp0"), (1, "warp31")):
+            r = t[:, w, :ntiles_cta]
+            ok = (r[..., 5] > 0) & (r[..., 7] > 0) & (r[..., 6] > 0)
+            a = ((r[..., 7] - r[..., 5])[ok]).mean() / 1e3
+            b = ((r[..., 6] - r[..., 7])[ok]).mean() / 1e3
+            print(f"  {wn}: stamp5->7 {a:6.2f} us  stamp7->6 {b:6.2f} us")
     starts = np.sort(t[:, 0, 0, 0][t[:, 0, 0, 0] > 0] - t0) / 1e3
     print(f"  CTA first-tile start spread: {starts[0]:.2f} .. {starts[-1]:.2f} us")
     ends = []
     for c in range(148):
         row = t[c, 0]
+        if not (row > 0).any():
+            continue
         ends.append((row[row > 0].max() - t0) / 1e3)
     ends = np.sort(np.array(ends))
     print(f"  CTA last-stamp: min {ends[0]:.2f} median {np.median(ends):.2f} max {ends[-1]:.2f} us")
@@ -118,6 +127,8 @@ def run():
             lib.enc_debug_fused_trace(buf.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(buf.nbytes))
             print(f"{name} rep {rep}: event time {e0.elapsed_time(e1) * 1e3:.2f} us")
         report(name, buf, labels, 8)
+        if os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+            np.save(os.path.join(ROOT, "gpurun_out", f"trace_{name}.npy"), buf)
 
 
 if __name__ == "__main__":
