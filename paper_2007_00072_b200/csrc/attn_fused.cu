@@ -556,8 +556,9 @@ __device__ __forceinline__ void fused_body(const CUtensorMap& mapA, const CUtens
 // C = A V (tcgen05.mma with A in TMEM), accumulated into columns [256, 320).  Warps 24-31
 // read C out (x dropout scale) and store C and its low bf16 word (R26).  P is never re-read
 // from HBM for the forward and the separate A.V launch disappears.
-//   shared memory: Q [128 x 64] | V [512 x 64] | per-warp 4 KB staging, whose first 64 KB
-//   (warps 0-15) also hold K [512 x 64] between its load and the score MMA | stats | barriers
+//   shared memory: Q [128 x 64] | K or V slot [512 x 64] | per-warp 4 KB staging | stats |
+//   barriers.  The slot holds K from the previous tile's C = A V (c_full) to this tile's score
+//   MMA (op_empty), then V: the next K never waits for this tile's P stores to drain.
 __device__ __forceinline__ uint32_t half_mask2(uint32_t g) {   // bits 15 / 31 -> half masks
   uint32_t m;
   asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(m) : "r"(g));
@@ -603,15 +604,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
 
   float2* stats = reinterpret_cast<float2*>(base + kAvStats);
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + kAvBars);
-  uint64_t* op_full = bars + 0;    // Q + K landed
-  uint64_t* op_empty = bars + 1;   // score MMA done (Q, K slots free)
+  uint64_t* op_full = bars + 0;    // Q + K landed (count 2: Q and K are issued separately)
+  uint64_t* op_empty = bars + 1;   // score MMA done (Q slot free, the K in the V slot read)
   uint64_t* tm_full = bars + 2;    // S in TMEM
   uint64_t* s_read = bars + 3;     // every warp read its S columns (count 32)
   uint64_t* a_ready = bars + 4;    // every warp wrote its A columns (count 32)
   uint64_t* v_full = bars + 5;     // V landed
   uint64_t* c_full = bars + 6;     // C = A V in TMEM (also: V slot and A columns free)
   uint64_t* c_done = bars + 7;     // C read out of TMEM (count 8)
-  uint64_t* stg_free = bars + 8;   // warps 0-15 staging free for the next K (count 16)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 9);
   unsigned char* own = base + kAvX + warp * 4096;
 
@@ -621,13 +621,20 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     b = bh / prm.H;
     h = bh - b * prm.H;
   };
-  auto load_qk = [&](int t) {
+  // the V slot holds K from the previous tile's C = A V until this tile's score MMA, then V:
+  // K never waits for the P stores to drain out of the staging
+  auto load_q = [&](int t) {
     int b, h, m0, bh;
     tile_coords(t, b, h, m0, bh);
-    mbar_arrive_expect_tx(op_full, (uint32_t)(kRows + kK) * 128);
+    mbar_arrive_expect_tx(op_full, (uint32_t)kRows * 128);
     tc::tma_load_4d(base + kAvQ, &mapQ, op_full, 0, h, m0, b);
-    tc::tma_load_4d(base + kAvX, &mapK, op_full, 0, h, 0, b);
-    tc::tma_load_4d(base + kAvX + 256 * 128, &mapK, op_full, 0, h, 256, b);
+  };
+  auto load_k = [&](int t) {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    mbar_arrive_expect_tx(op_full, (uint32_t)kK * 128);
+    tc::tma_load_4d(base + kAvV, &mapK, op_full, 0, h, 0, b);
+    tc::tma_load_4d(base + kAvV + 256 * 128, &mapK, op_full, 0, h, 256, b);
   };
   auto load_v = [&](int t) {
     int b, h, m0, bh;
@@ -644,7 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     tc::prefetch_tmap(&mapP);
     tc::prefetch_tmap(&mapC);
     tc::prefetch_tmap(&mapClo);
-    mbar_init(op_full, 1);
+    mbar_init(op_full, 2);
     mbar_init(op_empty, 1);
     mbar_init(tm_full, 1);
     mbar_init(s_read, kWarps);
@@ -652,7 +659,6 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     mbar_init(v_full, 1);
     mbar_init(c_full, 1);
     mbar_init(c_done, 8);
-    mbar_init(stg_free, 16);
     fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, kK);
@@ -664,8 +670,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
   pdl_wait();   // operands are the stream predecessor's outputs
 
   if (leader && blockIdx.x < prm.tiles) {
-    load_qk(blockIdx.x);
-    load_v(blockIdx.x);
+    load_q(blockIdx.x);
+    load_k(blockIdx.x);
   }
 
   int it = 0;
@@ -703,7 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       tc::fence_after_sync();
       constexpr uint32_t idesc = tc::instr_desc_bf16_f32(kRows, 256, false, false);
       const uint64_t ad = tc::smem_desc(smem_u32(base + kAvQ), 16, 1024);
-      const uint64_t bd = tc::smem_desc(smem_u32(base + kAvX), 16, 1024);
+      const uint64_t bd = tc::smem_desc(smem_u32(base + kAvV), 16, 1024);
 #pragma unroll
       for (int nh = 0; nh < 2; ++nh)
 #pragma unroll
@@ -716,6 +722,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     __syncwarp();
     mbar_wait_sleep(tm_full, ph);
     tc::fence_after_sync();
+    if (warp == 24 && lane == 0) {
+      // the score MMA has read Q and K: this tile's V into the V slot, the next tile's Q
+      mbar_wait(op_empty, ph);
+      load_v(t);
+      if (t + (int)gridDim.x < prm.tiles) load_q(t + gridDim.x);
+    }
     TRACE(2);
     float v[32];
     // pass 1 (as fused_body): sub-chunk max, e = 2^(y - m_c) back into TMEM, sub-chunk sum
@@ -792,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
 #pragma unroll
     for (int ch = 0; ch < kNs; ++ch) fP[ch] = tc::ex2(mc[ch] - Mr) * invL;
     // pass 2: P staged as the warp's [32 x 64] SWIZZLE_128B tile (its previous contents --
-    // P / C of the last tile, or K -- have been read: see stg_free / bulk waits)
+    // P / C of the last tile -- have been read: see the bulk waits)
     if (lane == 0) tc::bulk_wait_read<0>();
     __syncwarp();
 #pragma unroll
@@ -848,6 +860,9 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       mbar_wait(a_ready, ph);
       mbar_wait(v_full, ph);
       tc::fence_after_sync();
+#ifdef ENC_FUSED_TRACE_AV_ISSUE
+      TRACE(6);   // (debug: the issuing thread's stamp 6 = A ready, V landed)
+#endif
       constexpr uint32_t idesc_av = tc::instr_desc_bf16_f32(kRows, 64, false, true);
       const uint64_t vd = tc::smem_desc(smem_u32(base + kAvV), 8192, 1024);
 #pragma unroll
@@ -857,29 +872,14 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       TRACE(7);
     }
     __syncwarp();
-    if (warp < 16) {   // the next K lands in these warps' staging
-      if (lane == 0) {
-        tc::bulk_wait_read<0>();
-        mbar_arrive(stg_free);
-      }
-      __syncwarp();
-    }
-    if (leader) {
-      // next tile's operands: Q + K once warps 0-15's staging is free, V once this MMA is done
-      if (t + (int)gridDim.x < prm.tiles) {
-        mbar_wait(op_empty, ph);
-        mbar_wait(stg_free, ph);
-        load_qk(t + gridDim.x);
-      }
-    }
     if (warp >= 24) {
       // C (x dropout scale) or its low bf16 word, [32 rows x 64] per warp
       mbar_wait_sleep(c_full, ph);
       tc::fence_after_sync();
       TRACE(7);
-      // the V slot is free once the A.V MMA completed: the next tile's V, issued here so
+      // the V slot is free once the A.V MMA completed: the next tile's K, issued here so
       // the MMA-issuing warp does not wait for it
-      if (warp == 24 && lane == 0 && t + (int)gridDim.x < prm.tiles) load_v(t + gridDim.x);
+      if (warp == 24 && lane == 0 && t + (int)gridDim.x < prm.tiles) load_k(t + gridDim.x);
       if (lane == 0) tc::bulk_wait_read<0>();   // this warp's P store has read the staging
       __syncwarp();
       const bool lo = warp >= 28;
@@ -910,7 +910,11 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
         tc::bulk_commit();
       }
     }
+#ifdef ENC_FUSED_TRACE_AV_ISSUE
+    if (!leader) TRACE(6);
+#else
     TRACE(6);
+#endif
   }
   if (lane == 0) tc::bulk_wait<0>();
   tc::fence_before_sync();

@@ -23,10 +23,10 @@ BWD = ["bits", "mma_wait", "p_wait", "pass1", "qbar", "pass2", "store+load", "ne
 FAV = ["flags", "mma_wait", "pass1", "pass2", "A_write", "av/C", "next"]
 
 
-def build():
+def build(extra=()):
     import __graft_entry__ as g
     srcs = sorted(glob.glob(os.path.join(ROOT, "paper_2007_00072_b200", "csrc", "*.cu")))
-    cmd = [g.NVCC, *g.NVCC_FLAGS, "-DENC_FUSED_TRACE", "-o", LIB, *srcs, "-lcublasLt", "-lcublas",
+    cmd = [g.NVCC, *g.NVCC_FLAGS, "-DENC_FUSED_TRACE", *extra, "-o", LIB, *srcs, "-lcublasLt", "-lcublas",
            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
     subprocess.run(cmd, check=True)
 
@@ -134,5 +134,7 @@ def run():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--build", action="store_true")
+    ap.add_argument("--av-issue", action="store_true",
+                    help="fwd_av: the issuing thread's stamp 6 marks A ready (not the tile end)")
     a = ap.parse_args()
-    build() if a.build else run()
+    build(["-DENC_FUSED_TRACE_AV_ISSUE"] if a.av_issue else []) if a.build else run()
