@@ -674,16 +674,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     load_k(blockIdx.x);
   }
 
-  int it = 0;
-  for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
-    int b, h, m0, bh;
-    tile_coords(t, b, h, m0, bh);
-    const uint32_t ph = it & 1;
-    TRACE(0);
-    // keep flags of this thread's 64 elements (needed: A = keep * P) and the keep words for
-    // the backward
-    const int64_t rowi = (int64_t)bh * prm.J + m0 + r;
-    uint32_t kf[2];
+  // keep flags of this thread's 64 elements of tile tt (needed: A = keep * P) and the keep
+  // words for the backward
+  auto draw_flags = [&](int tt, uint32_t kf[2]) {
+    int b2, h2, m2, bh2;
+    tile_coords(tt, b2, h2, m2, bh2);
+    const int64_t rowi = (int64_t)bh2 * prm.J + m2 + r;
     if (pk.T == 0) {
       kf[0] = kf[1] = 0xFFFFFFFFu;
     } else {
@@ -699,6 +695,19 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     }
     __stcs(reinterpret_cast<uint2*>(prm.keep_bits + rowi * (kK / 32) + cb / 32),
            make_uint2(kf[0], kf[1]));
+  };
+  // C = A V is issued by a C read-out warp (idle until C is ready anyway): warp 0, which
+  // issues the score MMAs, goes on to the next tile's flags as soon as its A is written
+  const bool av_issuer = warp == 24 && lane == 0;
+
+  int it = 0;
+  uint32_t kf[2];
+  for (int t = blockIdx.x; t < prm.tiles; t += gridDim.x, ++it) {
+    int b, h, m0, bh;
+    tile_coords(t, b, h, m0, bh);
+    const uint32_t ph = it & 1;
+    TRACE(0);
+    draw_flags(t, kf);
     TRACE(1);
     // (the MMA-issuing thread draws its flags first: issued earlier, its warp would enter
     // pass 1 a flag phase late and hold back its quarter)
@@ -854,9 +863,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
     __syncwarp();
     if (lane == 0) mbar_arrive(a_ready);
     TRACE(5);
-    if (leader) {
-      // C = A V: 32 k-steps of 16 keys, A from TMEM (8 columns each), V MN-major; issued
-      // before this warp waits for its P store to drain
+    if (av_issuer) {
+      // C = A V: 32 k-steps of 16 keys, A from TMEM (8 columns each), V MN-major
       mbar_wait(a_ready, ph);
       mbar_wait(v_full, ph);
       tc::fence_after_sync();
