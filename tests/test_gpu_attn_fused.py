@@ -154,6 +154,18 @@ def test_fused_forward_av(ops, ctx, B, H, p, masked, causal):
     """enc_attn_fwd_fused_av (R30): one kernel for S = Q K^T, BSB and C = A V --
     P and C match the oracle (BSB then dropout(P) V in fp64), the keep words are exactly the
     oracle's mask, and C_lo is C's rounding residual (C_hi + C_lo is the fp32 result)."""
+    _check_forward_av(ops, ctx, B, H, p, masked, causal)
+
+
+@pytest.mark.parametrize("masked", [False, True])
+def test_fused_forward_av_ragged_schedule(ops, ctx, masked):
+    """B 5 x H 16 = 320 tiles on the balanced persistent grid (107 CTAs of 3 tiles but one of
+    2): the K / V slot hand-over, the next tile's Q, K loads and the score MMA issued across
+    tiles stop at each CTA's own last tile."""
+    _check_forward_av(ops, ctx, 5, 16, 0.1, masked, False)
+
+
+def _check_forward_av(ops, ctx, B, H, p, masked, causal):
     J, P = 512, 64
     Q = make_tensor((B, H, J, P), 51, "bf16", std=0.8)
     K = make_tensor((B, H, J, P), 52, "bf16", std=0.8)
