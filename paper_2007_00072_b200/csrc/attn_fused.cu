@@ -868,16 +868,12 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       mbar_wait(a_ready, ph);
       mbar_wait(v_full, ph);
       tc::fence_after_sync();
-#ifdef ENC_FUSED_TRACE_AV_ISSUE
-      TRACE(6);   // (debug: the issuing thread's stamp 6 = A ready, V landed)
-#endif
       constexpr uint32_t idesc_av = tc::instr_desc_bf16_f32(kRows, 64, false, true);
       const uint64_t vd = tc::smem_desc(smem_u32(base + kAvV), 8192, 1024);
 #pragma unroll
       for (int ks = 0; ks < kK / 16; ++ks)
         mma_bf16_ts(tmem + 256, tmem + 8 * ks, tc::desc_adv(vd, ks * 2048), idesc_av, ks != 0);
       tc::mma_commit(c_full);
-      TRACE(7);
     }
     __syncwarp();
     if (warp >= 24) {
@@ -885,8 +881,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
       mbar_wait_sleep(c_full, ph);
       tc::fence_after_sync();
       TRACE(7);
-      // the V slot is free once the A.V MMA completed: the next tile's K, issued here so
-      // the MMA-issuing warp does not wait for it
+      // the V slot is free once the A.V MMA completed: the next tile's K
       if (warp == 24 && lane == 0 && t + (int)gridDim.x < prm.tiles) load_k(t + gridDim.x);
       if (lane == 0) tc::bulk_wait_read<0>();   // this warp's P store has read the staging
       __syncwarp();
@@ -918,11 +913,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_qk_bsb_av_kernel(
         tc::bulk_commit();
       }
     }
-#ifdef ENC_FUSED_TRACE_AV_ISSUE
-    if (!leader) TRACE(6);
-#else
     TRACE(6);
-#endif
   }
   if (lane == 0) tc::bulk_wait<0>();
   tc::fence_before_sync();

@@ -56,13 +56,13 @@ def report(name, tr, labels, ntiles_cta):
                         cnt[e] += 1
         line = "  ".join(f"{labels[e]} {sums[e] / max(cnt[e], 1) / 1e3:6.2f}" for e in range(ne))
         print(f"  {wn} mean us per tile: {line}")
-    if ne == 7:   # the fused score + A.V kernel: stamp 7 sits between stamps 5 and 6
-        for w, wn in ((0, "warp0"), (1, "warp31")):
-            r = t[:, w, :ntiles_cta]
-            ok = (r[..., 5] > 0) & (r[..., 7] > 0) & (r[..., 6] > 0)
+    if ne == 7:   # the fused score + A.V kernel: warp 31 stamps 7 (C ready) between 5 and 6
+        r = t[:, 1, :ntiles_cta]
+        ok = (r[..., 5] > 0) & (r[..., 7] > 0) & (r[..., 6] > 0)
+        if ok.any():
             a = ((r[..., 7] - r[..., 5])[ok]).mean() / 1e3
             b = ((r[..., 6] - r[..., 7])[ok]).mean() / 1e3
-            print(f"  {wn}: stamp5->7 {a:6.2f} us  stamp7->6 {b:6.2f} us")
+            print(f"  warp31: A written -> C ready {a:6.2f} us  C read-out + store {b:6.2f} us")
     starts = np.sort(t[:, 0, 0, 0][t[:, 0, 0, 0] > 0] - t0) / 1e3
     print(f"  CTA first-tile start spread: {starts[0]:.2f} .. {starts[-1]:.2f} us")
     ends = []
@@ -134,7 +134,5 @@ def run():
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--build", action="store_true")
-    ap.add_argument("--av-issue", action="store_true",
-                    help="fwd_av: the issuing thread's stamp 6 marks A ready (not the tile end)")
     a = ap.parse_args()
-    build(["-DENC_FUSED_TRACE_AV_ISSUE"] if a.av_issue else []) if a.build else run()
+    build() if a.build else run()
