@@ -1,7 +1,8 @@
 #!/usr/bin/env python
-"""Median CUDA-event time of one fused score + A.V launch at config L (B=8, H=16, J=512,
-P=64, dropout 0.1), L2 flushed before each launch.  ENC_LIB_PATH selects the library build,
-so two builds can be compared on one box:  python tools/time_fused_av.py [reps]"""
+"""Median CUDA-event time of one fused score + A.V launch and one fused BSB-bwd (row term
+from C) launch at config L (B=8, H=16, J=512, P=64, dropout 0.1), L2 flushed before each
+launch.  ENC_LIB_PATH selects the library build, so two builds can be compared on one box:
+  python tools/time_fused_av.py [reps]"""
 import os
 import statistics
 import sys
@@ -25,21 +26,32 @@ def main():
     Cm = torch.empty((B, J, H, P), device=dev, dtype=bf)
     Clo = torch.empty_like(Cm)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    ts = []
-    for i in range(reps + 5):
-        flush.fill_(i & 255)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
+    dC = torch.randn((B, J, H, P), device=dev, generator=g).to(bf)
+    dS = torch.empty_like(Pm)
+
+    def fwd():
         ops.enc_attn_fwd_fused_av(ctx, B, H, J, P, 0.125, Q, K, V, None, 0.1, 2007000072, 0, 0,
                                   Pm, bits, Cm, Clo)
-        e1.record()
-        torch.cuda.synchronize()
-        if i >= 5:
-            ts.append(e0.elapsed_time(e1) * 1e3)
-    ts.sort()
-    print(f"{os.path.basename(os.environ.get('ENC_LIB_PATH', 'libencoder.so'))}: fused A.V "
-          f"median {statistics.median(ts):.2f} us  p10 {ts[len(ts) // 10]:.2f}  "
-          f"p90 {ts[9 * len(ts) // 10]:.2f}")
+
+    def bwd():
+        ops.enc_attn_bwd_fused_dc(ctx, B, H, J, P, 0.125, dC, V, Pm, Cm, Clo, 0.1, 2007000072,
+                                  0, 0, dS, keep_bits=bits)
+
+    lib = os.path.basename(os.environ.get("ENC_LIB_PATH", "libencoder.so"))
+    for name, fn in (("fused A.V", fwd), ("fused BSB-bwd (C)", bwd)):
+        ts = []
+        for i in range(reps + 5):
+            flush.fill_(i & 255)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            if i >= 5:
+                ts.append(e0.elapsed_time(e1) * 1e3)
+        ts.sort()
+        print(f"{lib}: {name} median {statistics.median(ts):.2f} us  p10 {ts[len(ts) // 10]:.2f}"
+              f"  p90 {ts[9 * len(ts) // 10]:.2f}")
 
 
 if __name__ == "__main__":
