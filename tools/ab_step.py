@@ -52,9 +52,9 @@ def main():
         for kv in filter(None, kvs.split(",")):
             k, val = (int(x, 0) for x in kv.split("="))
             opts[k] = val
-        if 17 not in opts:   # the process-wide PDL mask: keep the library default
+        if 17 not in opts:   # the process-wide PDL mask: the library default (kPdlDefault)
             if pdl0 is None:
-                pdl0 = int(os.environ.get("ENC_PDL", "1"), 0)
+                pdl0 = int(os.environ.get("ENC_PDL", "13"), 0)
             opts[17] = pdl0
         for k, val in opts.items():
             ops.enc_set_option(layer.ctx, k, val)
